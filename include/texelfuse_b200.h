@@ -1,0 +1,142 @@
+/*
+ * texelfuse_b200 — C ABI of the B200-native label-fusion hot path.
+ *
+ * Drop-in boundary for the reference package texelfuse
+ * (/root/reference/pkg/src/texelfuse).  Each entry point replaces the
+ * reference function cited beside it; the Python host layer
+ * (paper_2111_11103_b200/) keeps the reference's Python API and binds these
+ * symbols with ctypes.
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers (CUDA global memory, allocated
+ *    by the caller; the library never allocates or frees on the hot path).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *    Every call is stream-ordered and asynchronous; no call synchronizes.
+ *  - Return value: TFB_OK or one of the TFB_ERR_* codes; tfb_last_error()
+ *    returns the message of the last failing call on the calling thread.
+ *    The host layer maps codes onto the reference's exception types
+ *    (errors.py:4-17): DATA→DataError, CAPACITY→CapacityError,
+ *    STATE/CUDA→RuntimeError, VALUE→ValueError.
+ *  - Camera packing, 16 float64 per frame: R (3x3 row-major world→camera,
+ *    x right / y down / z forward, geometry.py:110-116), t (3), fx, fy, cx, cy.
+ *  - A "row" is the global texel index offsets[t] + texel (fusion.py:167);
+ *    per-pixel row images use -1 (rasterizer.NONE) for uncovered pixels.
+ */
+#ifndef TEXELFUSE_B200_H
+#define TEXELFUSE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TFB_OK 0
+#define TFB_ERR_DATA 1     /* DataError     (shape / id / layout mismatch)   */
+#define TFB_ERR_CAPACITY 2 /* CapacityError (workspace or smem budget)       */
+#define TFB_ERR_STATE 3    /* RuntimeError  (state guard)                    */
+#define TFB_ERR_CUDA 4     /* RuntimeError  (CUDA launch / runtime failure)  */
+#define TFB_ERR_VALUE 5    /* ValueError    (bad aggregator / mode / alpha)  */
+
+/* fusion.py:34 AGGREGATORS, fusion.py:35 WEIGHT_MODES */
+#define TFB_AGG_SUM 0
+#define TFB_AGG_MAXSUM 1
+#define TFB_AGG_MUL 2
+#define TFB_W_PIXELS_IID 0
+#define TFB_W_IMAGES_IID 1
+#define TFB_W_BLEND 2
+#define TFB_W_EXPLICIT 3 /* caller-provided per-pixel weights (fusion.py:145 `weights`) */
+
+/* Mesh + texel layout resident on the device (geometry.py:31-77, 208-232). */
+typedef struct tfb_scene {
+  const double *vertices;   /* (num_vertices, 3) float64, world metres     */
+  const int32_t *triangles; /* (num_triangles, 3) int32                   */
+  const int32_t *steps;     /* (num_triangles,) subdivision steps s_t      */
+  const int8_t *origins;    /* (num_triangles,) uv-origin vertex 0..2       */
+  const int64_t *offsets;   /* (num_triangles,) first global texel row     */
+  int64_t num_vertices;
+  int64_t num_triangles;
+  int64_t total_texels;
+} tfb_scene;
+
+const char *tfb_last_error(void);
+int tfb_version(void);
+
+/* Bytes of scratch tfb_rasterize needs for up to `max_frames` frames of
+ * width x height; `pair_capacity` = triangle/tile pairs budgeted per frame
+ * (0 = default).  Tiles whose lists overflow it stay exact (slow path). */
+size_t tfb_raster_workspace_bytes(int64_t num_triangles, int width, int height, int max_frames,
+                                  int64_t pair_capacity);
+
+/* rasterizer.py:93-202 (rasterize) for `nframes` cameras of one size.
+ * Bit-exact with the reference: ascending-triangle sequential depth fold
+ * with the 1e-9 tie rule, top-left-style edge ownership, near-plane clip +
+ * fan, perspective-correct (u, v) → texel id.
+ * Outputs (device, nframes*H*W each): rows_out (required).  Optional (NULL
+ * to skip): tri_out / texel_out (IdImage.triangle / .texel), depth_out / u_out
+ * / v_out (IdImage.depth / .u / .v).  texel_hits (nframes*total_texels u32,
+ * zeroed by the caller, may be NULL) receives per-frame per-row pixel counts
+ * (the np.unique count of fusion.py:135-136). */
+int tfb_rasterize(const tfb_scene *scene, const double *cams, int nframes, int width, int height,
+                  void *workspace, size_t workspace_bytes, int64_t pair_capacity, int32_t *rows_out,
+                  uint32_t *texel_hits, int32_t *tri_out, int32_t *texel_out, double *depth_out,
+                  double *u_out, double *v_out, void *stream);
+
+/* rows = offsets[tri] + texel for host-built IdImages (fusion.py:167);
+ * -1 where tri == -1.  Out-of-range ids set *bad_flag (device int) to 1. */
+int tfb_rows_from_ids(const int32_t *tri, const int32_t *texel, int64_t npix, const tfb_scene *scene,
+                      int32_t *rows_out, int32_t *bad_flag, void *stream);
+
+/* Per-frame per-row pixel counts from row images (fusion.py:135-136). */
+int tfb_count_hits(const int32_t *rows, int64_t hw, int nframes, int64_t total_texels, uint32_t *hits,
+                   void *stream);
+
+/* Zero the hit counters touched by `rows` (leaves the array all-zero again). */
+int tfb_clear_hits(const int32_t *rows, int64_t hw, int nframes, int64_t total_texels, uint32_t *hits,
+                   void *stream);
+
+/* compute_pixel_weights (fusion.py:114-142) as an (nframes, H*W) float64 image. */
+int tfb_pixel_weights(const int32_t *rows, int64_t hw, int nframes, const uint32_t *hits,
+                      int64_t total_texels, int weight_mode, double alpha, double *out, void *stream);
+
+/* accumulate_frame (fusion.py:145-183) for `nframes` frames in one launch.
+ * probs: device array of nframes device pointers, each an (H*W, c) float32
+ * image (16-byte aligned).  weight_mode TFB_W_EXPLICIT reads `weights`
+ * (nframes*H*W float64), the other modes derive w from `texel_hits`.
+ * accum: (total_texels, accum_stride) float32 (accum_is_f64 = 0; stride a
+ * multiple of 4) or float64 (accum_is_f64 = 1); log-space for TFB_AGG_MUL.
+ * counts: (total_texels,) u32 observation counts.  fallback_out (optional,
+ * nframes*H*W int32): the per-pixel network argmax probs.argmax(axis=2)
+ * (cli.py:293, bindings/__init__.py:112), fused into the same pass. */
+int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const float *const *probs, int num_classes,
+             const uint32_t *texel_hits, const double *weights, int64_t total_texels, int aggregator,
+             int weight_mode, double alpha, void *accum, int accum_is_f64, int64_t accum_stride,
+             uint32_t *counts, int32_t *fallback_out, void *stream);
+
+/* finalize + texel_argmax (fusion.py:186-222).  rows_out (total_texels*c
+ * float32), unobserved_out (u8) and labels_out (int32, UNKNOWN = -1) are each
+ * optional. */
+int tfb_finalize(const void *accum, int accum_is_f64, int64_t accum_stride, const uint32_t *counts,
+                 int64_t total_texels, int num_classes, int aggregator, float *rows_out,
+                 uint8_t *unobserved_out, int32_t *labels_out, void *stream);
+
+/* render_labels (renderback.py:28-56): out = labels[row] or -1, then holes
+ * filled from `fallback` (nframes*H*W int32, optional). */
+int tfb_render(const int32_t *rows, int64_t hw, int nframes, const int32_t *texel_labels,
+               int64_t total_texels, const int32_t *fallback, int32_t *out, void *stream);
+
+/* compute_worst_case_areas (geometry.py:360-380): per-triangle maximum
+ * projected pixel area over `nframes` cameras, max-folded into areas_inout
+ * (num_triangles float64, caller-initialised, normally zeros).  sizes holds
+ * (width, height) int32 per frame. */
+int tfb_worst_case_areas(const tfb_scene *scene, const double *cams, const int32_t *sizes, int nframes,
+                         double *areas_inout, void *stream);
+
+/* probs.argmax(axis=2) (cli.py:293): first maximum, NaN-first like NumPy. */
+int tfb_probs_argmax(const float *probs, int64_t npix, int num_classes, int32_t *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TEXELFUSE_B200_H */

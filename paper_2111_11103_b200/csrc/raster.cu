@@ -1,0 +1,631 @@
+// Tile-binned z-buffer rasterizer, bit-exact with rasterizer.py:93-202.
+//
+// Per batch of frames (one launch per stage, all frames at once):
+//   k_setup  one thread per (frame, triangle): FMA-ordered world→camera
+//            transform (geometry.py:161), near-plane clip + fan
+//            (rasterizer.py:62-82, 113-122), projection, bbox, signed area,
+//            CCW reorder and edge setup (rasterizer.py:136-164).  Surviving
+//            (sub)triangles become 128-byte records at slot 2t+sub; their
+//            tile coverage is counted.
+//   k_scan   per-frame exclusive scan of tile counts.
+//   k_fill   record ids into per-tile lists (unordered).
+//   k_raster one CTA per 16x16 tile, one thread per pixel.  Each pixel keeps
+//            the K smallest (triangle, sub) keys of the records that cover it
+//            (edge test in float64, ownership rule rasterizer.py:85-90), then
+//            folds them in ascending key order with the reference's exact
+//            test `z > 0 && z < depth - 1e-9` (rasterizer.py:171).  Pixels
+//            covered by more than K records run further passes over keys
+//            above the last folded one, so the fold always equals the
+//            reference's sequential ascending-index loop — including the
+//            non-transitive tie chains a packed atomicMin cannot reproduce.
+//            The winner's perspective-correct barycentrics, (u, v) and texel
+//            id (rasterizer.py:177-196) are evaluated once, in the epilogue.
+//
+// Exactness: every float64 operation of the reference expression is issued
+// as an explicit round-to-nearest intrinsic in the reference's order and this
+// translation unit is compiled with -fmad=false, so no contraction changes a
+// rounding.  Only the camera transform uses FMA, in the order OpenBLAS dgemm
+// evaluates `points @ R.T + t`.
+#include <math.h>
+
+#include "common.cuh"
+
+namespace tfb {
+namespace {
+
+constexpr int kTile = 16;
+constexpr int kThreads = 256;
+constexpr int kCand = 8;
+constexpr uint32_t kNoKey = 0xffffffffu;
+
+struct __align__(16) RecGeom {
+  double xs[3], ys[3], zs[3], dX[3], dY[3], area2;
+};
+static_assert(sizeof(RecGeom) == 128, "record geometry is one 128-byte line");
+
+struct __align__(16) RecMeta {
+  int16_t x0, x1, y0, y1;  // clamped pixel bbox (rasterizer.py:141-146)
+  int32_t t;               // triangle index
+  uint32_t flags;          // bits 0-2 edge accept, 3 reordered, 4 clipped
+};
+static_assert(sizeof(RecMeta) == 16, "record meta is 16 bytes");
+
+struct Cam {
+  double R[9], T[3], fx, fy, cx, cy;
+};
+
+struct Work {
+  RecGeom *geom;
+  RecMeta *meta;
+  uint32_t *vis;
+  uint32_t *fcnt;       // per frame: [0] visible records
+  uint32_t *tile_count; // per frame per tile
+  uint32_t *tile_cursor;
+  uint64_t *tile_off;
+  uint32_t *list;
+  int64_t rs;   // record slots per frame (2m)
+  int64_t cap;  // list capacity per frame
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+bool carve(void *ws, size_t ws_bytes, int64_t m, int nframes, int ntiles, int64_t cap, Work &w,
+           size_t *need_out) {
+  const int64_t rs = 2 * (m > 0 ? m : 1);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align256(off + bytes);
+    return o;
+  };
+  size_t o_geom = take(sizeof(RecGeom) * rs * nframes);
+  size_t o_meta = take(sizeof(RecMeta) * rs * nframes);
+  size_t o_vis = take(sizeof(uint32_t) * rs * nframes);
+  size_t o_fcnt = take(sizeof(uint32_t) * 4 * nframes);
+  size_t o_tc = take(sizeof(uint32_t) * ntiles * nframes);
+  size_t o_cur = take(sizeof(uint32_t) * ntiles * nframes);
+  size_t o_off = take(sizeof(uint64_t) * ntiles * nframes);
+  size_t o_list = take(sizeof(uint32_t) * cap * nframes);
+  if (need_out) *need_out = off;
+  if (!ws || ws_bytes < off) return false;
+  char *b = static_cast<char *>(ws);
+  w.geom = reinterpret_cast<RecGeom *>(b + o_geom);
+  w.meta = reinterpret_cast<RecMeta *>(b + o_meta);
+  w.vis = reinterpret_cast<uint32_t *>(b + o_vis);
+  w.fcnt = reinterpret_cast<uint32_t *>(b + o_fcnt);
+  w.tile_count = reinterpret_cast<uint32_t *>(b + o_tc);
+  w.tile_cursor = reinterpret_cast<uint32_t *>(b + o_cur);
+  w.tile_off = reinterpret_cast<uint64_t *>(b + o_off);
+  w.list = reinterpret_cast<uint32_t *>(b + o_list);
+  w.rs = rs;
+  w.cap = cap;
+  return true;
+}
+
+int64_t default_cap(int64_t m, int ntiles) {
+  int64_t c = 4 * m;
+  if (c < (int64_t)16 * ntiles) c = (int64_t)16 * ntiles;
+  if (c < 65536) c = 65536;
+  if (c > 0xffffffffLL) c = 0xffffffffLL;
+  return c;
+}
+
+__device__ __forceinline__ void load_cam(Cam &cam, const double *cams, int f) {
+  double *d = reinterpret_cast<double *>(&cam);
+  if (threadIdx.x < 16) d[threadIdx.x] = cams[(int64_t)f * 16 + threadIdx.x];
+}
+
+// geometry.py:159-161 through OpenBLAS dgemm: fma(z,R2,fma(y,R1,x*R0)) + t
+__device__ __forceinline__ void xform(const Cam &c, const double *__restrict__ v, double out[3]) {
+  const double x = __ldg(v), y = __ldg(v + 1), z = __ldg(v + 2);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    out[r] = __dadd_rn(__fma_rn(z, c.R[3 * r + 2], __fma_rn(y, c.R[3 * r + 1], __dmul_rn(x, c.R[3 * r]))),
+                       c.T[r]);
+}
+
+__device__ __forceinline__ void tri_cam(const tfb_scene &sc, const Cam &cam, int64_t t, double P[3][3]) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int64_t vi = __ldg(sc.triangles + 3 * t + k);
+    xform(cam, sc.vertices + 3 * vi, P[k]);
+  }
+}
+
+// rasterizer.py:62-82 (Sutherland–Hodgman against z >= NEAR_PLANE).
+__device__ int clip_near(const double P[3][3], double op[4][3], double ob[4][3]) {
+  int n = 0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int k1 = (k + 1) % 3;
+    const double *a = P[k], *b = P[k1];
+    const bool ina = a[2] >= kNearPlane, inb = b[2] >= kNearPlane;
+    if (ina) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        op[n][q] = a[q];
+        ob[n][q] = (q == k) ? 1.0 : 0.0;
+      }
+      ++n;
+    }
+    if (ina != inb) {
+      const double tt = __ddiv_rn(__dsub_rn(kNearPlane, a[2]), __dsub_rn(b[2], a[2]));
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        op[n][q] = __dadd_rn(a[q], __dmul_rn(tt, __dsub_rn(b[q], a[q])));
+        const double ba = (q == k) ? 1.0 : 0.0, bb = (q == k1) ? 1.0 : 0.0;
+        ob[n][q] = __dadd_rn(ba, __dmul_rn(tt, __dsub_rn(bb, ba)));
+      }
+      ++n;
+    }
+  }
+  return n;
+}
+
+__device__ __forceinline__ bool boundary_accept(double ax, double ay, double bx, double by) {
+  // rasterizer.py:85-90
+  const double dy = __dsub_rn(by, ay), dx = __dsub_rn(bx, ax);
+  return dy > 0.0 || (dy == 0.0 && dx < 0.0);
+}
+
+// rasterizer.py:136-164 up to the per-pixel loop.  Returns false when the
+// reference would return early (empty bbox, zero or non-finite area).
+__device__ bool build_record(const Cam &cam, int W, int H, const double P[3][3], int t, bool clipped,
+                             RecGeom &g, RecMeta &mt) {
+  double xs0[3], ys0[3], zs0[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    zs0[k] = P[k][2];
+    xs0[k] = __dadd_rn(__dmul_rn(__ddiv_rn(P[k][0], zs0[k]), cam.fx), cam.cx);  // :138
+    ys0[k] = __dadd_rn(__dmul_rn(__ddiv_rn(P[k][1], zs0[k]), cam.fy), cam.cy);  // :139
+  }
+  const double xmin = fmin(fmin(xs0[0], xs0[1]), xs0[2]), xmax = fmax(fmax(xs0[0], xs0[1]), xs0[2]);
+  const double ymin = fmin(fmin(ys0[0], ys0[1]), ys0[2]), ymax = fmax(fmax(ys0[0], ys0[1]), ys0[2]);
+  const double x0d = fmax(ceil(__dsub_rn(xmin, 0.5)), 0.0);
+  const double x1d = fmin(floor(__dsub_rn(xmax, 0.5)), (double)(W - 1));
+  const double y0d = fmax(ceil(__dsub_rn(ymin, 0.5)), 0.0);
+  const double y1d = fmin(floor(__dsub_rn(ymax, 0.5)), (double)(H - 1));
+  if (!(x0d <= x1d) || !(y0d <= y1d)) return false;  // :145
+  double area2 = __dsub_rn(__dmul_rn(__dsub_rn(xs0[1], xs0[0]), __dsub_rn(ys0[2], ys0[0])),
+                           __dmul_rn(__dsub_rn(ys0[1], ys0[0]), __dsub_rn(xs0[2], xs0[0])));  // :148
+  if (area2 == 0.0 || !isfinite(area2)) return false;                                           // :149
+  const bool re = !(area2 > 0.0);                                                             // :151
+  const int o1 = re ? 2 : 1, o2 = re ? 1 : 2;
+  g.xs[0] = xs0[0]; g.xs[1] = xs0[o1]; g.xs[2] = xs0[o2];
+  g.ys[0] = ys0[0]; g.ys[1] = ys0[o1]; g.ys[2] = ys0[o2];
+  g.zs[0] = zs0[0]; g.zs[1] = zs0[o1]; g.zs[2] = zs0[o2];
+  g.area2 = fabs(area2);
+  uint32_t flags = (re ? 8u : 0u) | (clipped ? 16u : 0u);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int a = (k + 1) % 3, b = (k + 2) % 3;
+    g.dX[k] = __dsub_rn(g.xs[b], g.xs[a]);
+    g.dY[k] = __dsub_rn(g.ys[b], g.ys[a]);
+    if (boundary_accept(g.xs[a], g.ys[a], g.xs[b], g.ys[b])) flags |= 1u << k;
+  }
+  mt.x0 = (int16_t)x0d;
+  mt.x1 = (int16_t)x1d;
+  mt.y0 = (int16_t)y0d;
+  mt.y1 = (int16_t)y1d;
+  mt.t = t;
+  mt.flags = flags;
+  return true;
+}
+
+__device__ __forceinline__ void store_record(const Work &w, int f, int64_t slot, const RecGeom &g,
+                                             const RecMeta &mt, int ntiles, int TX) {
+  const int64_t idx = (int64_t)f * w.rs + slot;
+  const double2 *src = reinterpret_cast<const double2 *>(&g);
+  double2 *dst = reinterpret_cast<double2 *>(w.geom + idx);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) dst[q] = src[q];
+  w.meta[idx] = mt;
+  uint32_t *tc = w.tile_count + (int64_t)f * ntiles;
+  for (int ty = mt.y0 / kTile; ty <= mt.y1 / kTile; ++ty)
+    for (int tx = mt.x0 / kTile; tx <= mt.x1 / kTile; ++tx) atomicAdd(tc + ty * TX + tx, 1u);
+}
+
+__global__ void __launch_bounds__(kThreads) k_setup(tfb_scene sc, const double *__restrict__ cams, int W,
+                                                    int H, int TX, int ntiles, Work w) {
+  const int f = blockIdx.y;
+  __shared__ Cam cam;
+  __shared__ uint32_t warp_tot[kThreads / 32];
+  __shared__ uint32_t base;
+  load_cam(cam, cams, f);
+  __syncthreads();
+  const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  uint32_t mask = 0;
+  if (t < sc.num_triangles) {
+    double P[3][3];
+    tri_cam(sc, cam, t, P);
+    const double zmax = fmax(fmax(P[0][2], P[1][2]), P[2][2]);
+    const double zmin = fmin(fmin(P[0][2], P[1][2]), P[2][2]);
+    if (!(zmax < kNearPlane)) {  // rasterizer.py:111
+      RecGeom g;
+      RecMeta mt;
+      if (zmin >= kNearPlane) {
+        if (build_record(cam, W, H, P, (int)t, false, g, mt)) {
+          store_record(w, f, 2 * t, g, mt, ntiles, TX);
+          mask = 1;
+        }
+      } else {
+        double op[4][3], ob[4][3];
+        const int n = clip_near(P, op, ob);
+        for (int k = 1; k + 1 < n; ++k) {  // fan (0, k, k+1), rasterizer.py:119-122
+          double S[3][3];
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            S[0][q] = op[0][q];
+            S[1][q] = op[k][q];
+            S[2][q] = op[k + 1][q];
+          }
+          if (build_record(cam, W, H, S, (int)t, true, g, mt)) {
+            store_record(w, f, 2 * t + (k - 1), g, mt, ntiles, TX);
+            mask |= 1u << (k - 1);
+          }
+        }
+      }
+    }
+  }
+  // block-aggregated append of visible record ids (one global atomic per block)
+  const uint32_t nrec = __popc(mask);
+  uint32_t incl = nrec;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t s = 0;
+    for (int i = 0; i < kThreads / 32; ++i) {
+      const uint32_t v = warp_tot[i];
+      warp_tot[i] = s;
+      s += v;
+    }
+    base = s ? atomicAdd(w.fcnt + 4 * f, s) : 0;
+  }
+  __syncthreads();
+  uint32_t pos = base + warp_tot[warp] + incl - nrec;
+  uint32_t *vis = w.vis + (int64_t)f * w.rs;
+  if (mask & 1u) vis[pos++] = (uint32_t)(2 * t);
+  if (mask & 2u) vis[pos++] = (uint32_t)(2 * t + 1);
+}
+
+__global__ void __launch_bounds__(1024) k_scan(Work w, int ntiles) {
+  const int f = blockIdx.x;
+  const uint32_t *cnt = w.tile_count + (int64_t)f * ntiles;
+  uint64_t *off = w.tile_off + (int64_t)f * ntiles;
+  __shared__ uint64_t warp_tot[32];
+  __shared__ uint64_t running;
+  if (threadIdx.x == 0) running = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int b0 = 0; b0 < ntiles; b0 += 1024) {
+    const int i = b0 + threadIdx.x;
+    const uint64_t v = i < ntiles ? cnt[i] : 0;
+    uint64_t incl = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t u = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += u;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      uint64_t s = warp_tot[lane];
+      uint64_t x = s;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t u = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += u;
+      }
+      warp_tot[lane] = x - s;  // exclusive warp prefix
+    }
+    __syncthreads();
+    const uint64_t r0 = running;
+    if (i < ntiles) off[i] = r0 + warp_tot[warp] + incl - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) running = r0 + warp_tot[warp] + incl;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_fill(Work w, int ntiles, int TX) {
+  const int f = blockIdx.y;
+  const uint32_t nvis = w.fcnt[4 * f];
+  const uint32_t *vis = w.vis + (int64_t)f * w.rs;
+  const RecMeta *meta = w.meta + (int64_t)f * w.rs;
+  const uint64_t *toff = w.tile_off + (int64_t)f * ntiles;
+  uint32_t *cur = w.tile_cursor + (int64_t)f * ntiles;
+  uint32_t *list = w.list + (int64_t)f * w.cap;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nvis; i += gridDim.x * blockDim.x) {
+    const uint32_t r = vis[i];
+    const RecMeta mt = meta[r];
+    for (int ty = mt.y0 / kTile; ty <= mt.y1 / kTile; ++ty)
+      for (int tx = mt.x0 / kTile; tx <= mt.x1 / kTile; ++tx) {
+        const int tile = ty * TX + tx;
+        const uint64_t pos = toff[tile] + atomicAdd(cur + tile, 1u);
+        if (pos < (uint64_t)w.cap) list[pos] = r;
+      }
+  }
+}
+
+struct Outs {
+  int32_t *rows;
+  uint32_t *hits;
+  int32_t *tri;
+  int32_t *texel;
+  double *depth;
+  double *u;
+  double *v;
+};
+
+// edge functions at one pixel centre, rasterizer.py:161-162
+__device__ __forceinline__ bool edges_at(const RecGeom &g, uint32_t flags, double px, double py, double e[3]) {
+  bool inside = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int a = (k + 1) % 3;
+    e[k] = __dsub_rn(__dmul_rn(g.dX[k], __dsub_rn(py, g.ys[a])), __dmul_rn(g.dY[k], __dsub_rn(px, g.xs[a])));
+    inside = inside && (e[k] > 0.0 || (e[k] == 0.0 && ((flags >> k) & 1u)));
+  }
+  return inside;
+}
+
+__device__ __forceinline__ double np_max(double a, double b) { return isnan(a) ? a : (a > b ? a : b); }
+__device__ __forceinline__ double np_min(double a, double b) { return isnan(a) ? a : (a < b ? a : b); }
+
+__global__ void __launch_bounds__(kThreads, 2) k_raster(tfb_scene sc, const double *__restrict__ cams, int W,
+                                                        int H, int TX, int ntiles, Work w, Outs o) {
+  const int f = blockIdx.y;
+  const int tile = blockIdx.x;
+  const int tx = tile % TX, ty = tile / TX;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
+  const int px_i = wx0 + (lane & 7), py_i = wy0 + (lane >> 3);
+  const bool in_img = px_i < W && py_i < H;
+  const double px = (double)px_i + 0.5, py = (double)py_i + 0.5;
+
+  __shared__ RecGeom sgeom[kThreads];
+  __shared__ RecMeta smeta[kThreads];
+  __shared__ uint32_t skey[kThreads];
+  __shared__ Cam cam;
+  load_cam(cam, cams, f);
+
+  const uint32_t tcount = w.tile_count[(int64_t)f * ntiles + tile];
+  const uint64_t toff = w.tile_off[(int64_t)f * ntiles + tile];
+  const bool ovf = toff + tcount > (uint64_t)w.cap;
+  const uint32_t *src = ovf ? w.vis + (int64_t)f * w.rs : w.list + (int64_t)f * w.cap + toff;
+  const uint32_t nsrc = ovf ? w.fcnt[4 * f] : tcount;
+  const bool single = nsrc <= (uint32_t)kThreads;
+  const RecGeom *geom = w.geom + (int64_t)f * w.rs;
+  const RecMeta *meta = w.meta + (int64_t)f * w.rs;
+
+  double depth = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+  uint32_t win = kNoKey;
+  double ww0 = 0.0, ww1 = 0.0, ww2 = 0.0;
+  uint32_t lo = 0;          // next key to consider
+  bool need = in_img;       // this pixel still has unfolded candidates
+
+  for (;;) {
+    uint32_t ck[kCand], cs[kCand];
+#pragma unroll
+    for (int i = 0; i < kCand; ++i) {
+      ck[i] = kNoKey;
+      cs[i] = 0;
+    }
+    uint32_t ncand = 0;
+    for (uint32_t b0 = 0; b0 < nsrc; b0 += kThreads) {
+      const uint32_t n = min((uint32_t)kThreads, nsrc - b0);
+      __syncthreads();
+      if (threadIdx.x < n) {
+        const uint32_t r = src[b0 + threadIdx.x];
+        skey[threadIdx.x] = r;
+        smeta[threadIdx.x] = meta[r];
+        const double2 *gs = reinterpret_cast<const double2 *>(geom + r);
+        double2 *gd = reinterpret_cast<double2 *>(sgeom + threadIdx.x);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) gd[q] = gs[q];
+      }
+      __syncthreads();
+      for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        bool rel = false;
+        if (j < n) {
+          const RecMeta mt = smeta[j];
+          rel = mt.x0 <= wx0 + 7 && mt.x1 >= wx0 && mt.y0 <= wy0 + 3 && mt.y1 >= wy0;
+        }
+        uint32_t m = __ballot_sync(0xffffffffu, rel);
+        if (!__any_sync(0xffffffffu, need)) m = 0;
+        while (m) {
+          const uint32_t jj = j0 + __ffs(m) - 1;
+          m &= m - 1;
+          const RecMeta mt = smeta[jj];
+          if (need && px_i >= mt.x0 && px_i <= mt.x1 && py_i >= mt.y0 && py_i <= mt.y1) {
+            const uint32_t key = skey[jj];
+            if (key >= lo) {
+              double e[3];
+              if (edges_at(sgeom[jj], mt.flags, px, py, e)) {
+                ++ncand;
+                uint32_t k = key, s = jj;
+#pragma unroll
+                for (int i = 0; i < kCand; ++i) {
+                  if (k < ck[i]) {
+                    const uint32_t tk = ck[i], ts = cs[i];
+                    ck[i] = k;
+                    cs[i] = s;
+                    k = tk;
+                    s = ts;
+                  }
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+    // ascending sequential fold over this pass's candidates (rasterizer.py:108, 170-171)
+    const uint32_t nf = min(ncand, (uint32_t)kCand);
+#pragma unroll
+    for (int i = 0; i < kCand; ++i) {
+      if ((uint32_t)i < nf) {
+        const RecGeom &g = single ? sgeom[cs[i]] : geom[ck[i]];
+        const uint32_t flags = single ? smeta[cs[i]].flags : meta[ck[i]].flags;
+        double e[3];
+        edges_at(g, flags, px, py, e);
+        const double w0 = __ddiv_rn(e[0], g.zs[0]), w1 = __ddiv_rn(e[1], g.zs[1]), w2 = __ddiv_rn(e[2], g.zs[2]);
+        const double z = __ddiv_rn(g.area2, __dadd_rn(__dadd_rn(w0, w1), w2));
+        if (z > 0.0 && z < __dsub_rn(depth, kDepthTie)) {
+          depth = z;
+          win = ck[i];
+          ww0 = w0;
+          ww1 = w1;
+          ww2 = w2;
+        }
+      }
+    }
+    const bool more = need && ncand > (uint32_t)kCand;
+    if (more) lo = ck[kCand - 1] + 1;
+    need = more;
+    if (!__syncthreads_or(more)) break;
+  }
+
+  if (!in_img) return;
+  const int64_t pix = (int64_t)f * W * H + (int64_t)py_i * W + px_i;
+  int32_t row = -1;
+  if (win != kNoKey) {
+    const int64_t t = win >> 1;
+    const int sub = (int)(win & 1u);
+    const uint32_t flags = meta[win].flags;
+    // barycentric rows of the (sub)triangle vertices in the original triangle
+    double B[3][3];
+    if (flags & 16u) {
+      double P[3][3], op[4][3], ob[4][3];
+      tri_cam(sc, cam, t, P);
+      clip_near(P, op, ob);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        B[0][q] = ob[0][q];
+        B[1][q] = ob[sub + 1][q];
+        B[2][q] = ob[sub + 2][q];
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) B[r][q] = (r == q) ? 1.0 : 0.0;
+    }
+    if (flags & 8u) {  // reorder (0, 2, 1), rasterizer.py:151-152
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const double tmp = B[1][q];
+        B[1][q] = B[2][q];
+        B[2][q] = tmp;
+      }
+    }
+    // rasterizer.py:177-188
+    const double wsum = __dadd_rn(__dadd_rn(ww0, ww1), ww2);
+    double b[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      b[k] = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(ww0, B[0][k]), __dmul_rn(ww1, B[1][k])), __dmul_rn(ww2, B[2][k])),
+                       wsum);
+      if (b[k] < 0.0) b[k] = 0.0;
+    }
+    const double bs = __dadd_rn(__dadd_rn(b[0], b[1]), b[2]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) b[k] = __ddiv_rn(b[k], bs);
+    // rasterizer.py:190-196
+    const int origin = __ldg(sc.origins + t);
+    const int s = __ldg(sc.steps + t);
+    double u = __dsub_rn(1.0, b[origin]);
+    double v = b[(origin + 2) % 3];
+    u = np_min(np_max(u, 0.0), 1.0);
+    v = np_min(np_max(v, 0.0), u);
+    long long i = (long long)__dmul_rn((double)s, u);
+    if (i > s - 1) i = s - 1;
+    long long j = (long long)__dmul_rn((double)s, v);
+    if (j > i) j = i;
+    const int32_t texel = (int32_t)((i * i + i) / 2 + j);
+    row = (int32_t)(__ldg(sc.offsets + t) + texel);
+    if (o.tri) o.tri[pix] = (int32_t)t;
+    if (o.texel) o.texel[pix] = texel;
+    if (o.depth) o.depth[pix] = depth;
+    if (o.u) o.u[pix] = u;
+    if (o.v) o.v[pix] = v;
+  } else {
+    if (o.tri) o.tri[pix] = -1;
+    if (o.texel) o.texel[pix] = 0;
+    if (o.depth) o.depth[pix] = depth;
+    if (o.u) o.u[pix] = 0.0;
+    if (o.v) o.v[pix] = 0.0;
+  }
+  o.rows[pix] = row;
+  if (o.hits && row >= 0) {
+    // warp-aggregated per-frame texel hit count (fusion.py:135-136)
+    const unsigned act = __activemask();
+    const unsigned peers = __match_any_sync(act, row);
+    if ((int)(__ffs(peers) - 1) == lane)
+      atomicAdd(o.hits + (int64_t)f * sc.total_texels + row, (uint32_t)__popc(peers));
+  }
+}
+
+}  // namespace
+}  // namespace tfb
+
+using namespace tfb;
+
+extern "C" size_t tfb_raster_workspace_bytes(int64_t num_triangles, int width, int height, int max_frames,
+                                             int64_t pair_capacity) {
+  const int TX = (width + kTile - 1) / kTile, TY = (height + kTile - 1) / kTile;
+  const int ntiles = TX * TY;
+  const int64_t cap = pair_capacity > 0 ? pair_capacity : default_cap(num_triangles, ntiles);
+  Work w;
+  size_t need = 0;
+  carve(nullptr, 0, num_triangles, max_frames, ntiles, cap, w, &need);
+  return need;
+}
+
+extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nframes, int width, int height,
+                             void *workspace, size_t workspace_bytes, int64_t pair_capacity, int32_t *rows_out,
+                             uint32_t *texel_hits, int32_t *tri_out, int32_t *texel_out, double *depth_out,
+                             double *u_out, double *v_out, void *stream) {
+  TFB_REQUIRE(scene && cams && rows_out, TFB_ERR_DATA, "tfb_rasterize: null scene, cameras or output");
+  TFB_REQUIRE(width > 0 && height > 0 && width < 32768 && height < 32768, TFB_ERR_DATA,
+              "tfb_rasterize: image size %dx%d outside 1..32767", width, height);
+  TFB_REQUIRE(nframes >= 0, TFB_ERR_DATA, "tfb_rasterize: negative frame count");
+  TFB_REQUIRE(scene->num_triangles < (1LL << 30), TFB_ERR_CAPACITY,
+              "tfb_rasterize: %lld triangles exceed the 2^30 record-key range", (long long)scene->num_triangles);
+  TFB_REQUIRE(scene->total_texels < (1LL << 31), TFB_ERR_CAPACITY,
+              "tfb_rasterize: %lld texels exceed int32 row ids", (long long)scene->total_texels);
+  if (nframes == 0) return TFB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int TX = (width + kTile - 1) / kTile, TY = (height + kTile - 1) / kTile;
+  const int ntiles = TX * TY;
+  const int64_t m = scene->num_triangles;
+  const int64_t cap = pair_capacity > 0 ? pair_capacity : default_cap(m, ntiles);
+  Work w;
+  size_t need = 0;
+  if (!carve(workspace, workspace_bytes, m, nframes, ntiles, cap, w, &need)) {
+    set_error("tfb_rasterize: workspace of %zu bytes is smaller than the %zu required", workspace_bytes, need);
+    return TFB_ERR_CAPACITY;
+  }
+  cudaMemsetAsync(w.fcnt, 0, sizeof(uint32_t) * 4 * nframes, st);
+  cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ntiles * nframes, st);
+  cudaMemsetAsync(w.tile_cursor, 0, sizeof(uint32_t) * ntiles * nframes, st);
+  tfb_scene sc = *scene;
+  if (m > 0) {
+    dim3 g1((unsigned)((m + kThreads - 1) / kThreads), nframes);
+    k_setup<<<g1, kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w);
+    k_scan<<<nframes, 1024, 0, st>>>(w, ntiles);
+    int64_t fb = (2 * m + 255) / 256;
+    const int fill_blocks = (int)(fb < 1184 ? fb : 1184);
+    k_fill<<<dim3(fill_blocks, nframes), 256, 0, st>>>(w, ntiles, TX);
+  }
+  Outs o{rows_out, texel_hits, tri_out, texel_out, depth_out, u_out, v_out};
+  k_raster<<<dim3(ntiles, nframes), kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
+  return check_launch("tfb_rasterize");
+}
