@@ -101,8 +101,10 @@ int tfb_pixel_weights(const int32_t *rows, int64_t hw, int nframes, const uint32
                       int64_t total_texels, int weight_mode, double alpha, double *out, void *stream);
 
 /* accumulate_frame (fusion.py:145-183) for `nframes` frames in one launch.
- * probs: device array of nframes device pointers, each an (H*W, c) float32
- * image (16-byte aligned).  weight_mode TFB_W_EXPLICIT reads `weights`
+ * probs: HOST array of nframes device pointers, each an (H*W, c) float32
+ * image (16-byte aligned); they travel in the kernel parameters (up to 32
+ * frames per launch), so no pointer table is copied and the call is CUDA-graph
+ * capturable.  weight_mode TFB_W_EXPLICIT reads `weights`
  * (nframes*H*W float64), the other modes derive w from `texel_hits`.
  * accum: (total_texels, accum_stride) float32 (accum_is_f64 = 0; stride a
  * multiple of 4) or float64 (accum_is_f64 = 1); log-space for TFB_AGG_MUL.

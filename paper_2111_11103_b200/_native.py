@@ -102,6 +102,12 @@ def ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def ptr_array(addrs):
+    """Host array of device pointers (tfb_fuse's per-frame probability maps)."""
+    arr = (ctypes.c_void_p * max(len(addrs), 1))(*[int(a) for a in addrs])
+    return ctypes.cast(arr, ctypes.c_void_p), arr
+
+
 def stream_handle(stream=None):
     import torch
 

@@ -1,0 +1,180 @@
+"""MeshAnnotation-style fusion: ``add(probs, camera)`` / ``get()`` / ``render(camera)``.
+
+The batched, device-resident front end of the hot path (BASELINE north star):
+for each batch of up to ``max_batch`` frames of one size it issues exactly
+four stream-ordered launches — rasterize (tfb_rasterize: setup, scan, fill,
+tile raster with the per-frame texel hit counts fused into its epilogue),
+scatter-add (tfb_fuse), and the hit-counter reset (tfb_clear_hits) — and
+never synchronizes with the host.  ``get()`` finalizes once (tfb_finalize)
+and returns the per-texel rows; ``render`` rasterizes the requested cameras
+and gathers labels (tfb_render).  Multi-GPU: each rank adds its own frames,
+then ``allreduce()`` sums accumulators and counts over NCCL before ``get()``.
+
+It is a thin layer over the same ProbabilityTexture the reference-compatible
+functions use (fusion.py / session.py), so textures and results interchange.
+"""
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .device import scene_for
+from .fusion import init_texture, parse_weight_mode
+from .geometry import pack_camera, uniform_layout
+from .renderback import render_labels_device
+
+
+def _cams_array(cameras):
+    if isinstance(cameras, torch.Tensor):
+        return cameras.detach().to(torch.float64).reshape(-1, 16)
+    if isinstance(cameras, np.ndarray) and cameras.ndim == 2 and cameras.shape[1] == 16:
+        return torch.as_tensor(np.ascontiguousarray(cameras, dtype=np.float64))
+    if not isinstance(cameras, (list, tuple)):
+        cameras = [cameras]
+    return torch.as_tensor(np.stack([pack_camera(c) for c in cameras]))
+
+
+def _sizes(cameras, width, height):
+    if width is not None and height is not None:
+        return int(width), int(height)
+    cam0 = cameras[0] if isinstance(cameras, (list, tuple)) else cameras
+    return int(cam0.width), int(cam0.height)
+
+
+class MeshAnnotation:
+    """Fuse per-frame class probabilities onto a mesh's texels on the GPU."""
+
+    def __init__(self, mesh, layout=None, num_classes=None, aggregator="mul", weight_mode="images_iid",
+                 accum_dtype="float32", max_batch=8, device=None, memory_budget=None):
+        if num_classes is None:
+            raise ValueError("num_classes is required")
+        self.mesh = mesh
+        self.layout = layout if layout is not None else uniform_layout(mesh, 1)
+        self.num_classes = int(num_classes)
+        self.weight_mode, self.alpha = parse_weight_mode(weight_mode)
+        budget = memory_budget if memory_budget is not None else float("inf")
+        self.texture = init_texture(self.layout, self.num_classes, aggregator, budget, accum_dtype, device)
+        self.scene = scene_for(mesh, self.layout, self.texture.device)
+        self.device = self.scene.device
+        self.max_batch = int(max_batch)
+        self._staging = None
+        self.frames_added = 0
+
+    # -- accumulation ------------------------------------------------------------------
+    def _probs_batch(self, probs, b, H, W):
+        """Per-frame device pointers for b frames (device tensors used in place)."""
+        c = self.num_classes
+        if isinstance(probs, (list, tuple)):
+            items = list(probs)
+        else:
+            items = [probs[i] for i in range(b)] if probs.ndim == 4 else [probs]
+        out, keep = [], []
+        need_stage = [i for i, p in enumerate(items) if not (isinstance(p, torch.Tensor) and p.is_cuda
+                                                             and p.dtype == torch.float32 and p.is_contiguous()
+                                                             and p.data_ptr() % 16 == 0)]
+        if need_stage:
+            shape = (self.max_batch, H, W, c)
+            if self._staging is None or tuple(self._staging.shape) != shape:
+                self._staging = torch.empty(shape, dtype=torch.float32, device=self.device)
+        for i, p in enumerate(items):
+            if tuple(p.shape) != (H, W, c):
+                from .errors import DataError
+
+                raise DataError("probability array shape %s does not match expected %s"
+                                % (tuple(p.shape), (H, W, c)))
+            if i in need_stage:
+                dst = self._staging[i]
+                if isinstance(p, torch.Tensor):
+                    dst.copy_(p, non_blocking=True)
+                else:
+                    dst.copy_(torch.from_numpy(np.ascontiguousarray(p, dtype=np.float32)), non_blocking=True)
+                p = dst
+            out.append(p.data_ptr())
+            keep.append(p)
+        return out, keep
+
+    def add_batch(self, probs, cameras, width=None, height=None, fallback_out=None, stream=None):
+        """Fold B frames: probs (B, H, W, c) tensor/array or a list of (H, W, c);
+        cameras a list of CameraFrame or a (B, 16) camera array/tensor.
+        fallback_out (optional (B, H*W) int32 device tensor) receives each
+        frame's network argmax."""
+        tex = self.texture
+        if tex.finalized:
+            raise RuntimeError("texture is already finalized")
+        W, H = _sizes(cameras, width, height)
+        cams_all = _cams_array(cameras).to(self.device, non_blocking=True)
+        B = int(cams_all.shape[0])
+        hw = H * W
+        tex._push_host()
+        needs_hits = self.weight_mode != "pixels_iid"
+        for b0 in range(0, B, self.max_batch):
+            b = min(self.max_batch, B - b0)
+            chunk = probs[b0:b0 + b]
+            ptrs, keep = self._probs_batch(chunk, b, H, W)
+            rows = self.scene.buffer("rows", (self.max_batch, hw), torch.int32)[:b]
+            hits = self.scene.hits(self.max_batch)[:b] if needs_hits else None
+            self.scene.rasterize(cams_all[b0:b0 + b], W, H, rows, hits=hits, stream=stream)
+            parr, _k = N.ptr_array(ptrs)
+            fb = fallback_out[b0:b0 + b] if fallback_out is not None else None
+            N.call("tfb_fuse", N.ptr(rows), hw, b, parr, self.num_classes, N.ptr(hits), None, tex.total_texels,
+                   N.AGG_IDS[tex.aggregator], N.WMODE_IDS[self.weight_mode], float(self.alpha or 0.0),
+                   N.ptr(tex._accum), int(tex.is_f64), tex.stride, N.ptr(tex._counts), N.ptr(fb),
+                   N.stream_handle(stream))
+            if needs_hits:
+                N.call("tfb_clear_hits", N.ptr(rows), hw, b, tex.total_texels, N.ptr(hits),
+                       N.stream_handle(stream))
+            del keep
+        tex._h_accum = tex._h_counts = None
+        self.frames_added += B
+
+    def add(self, probs, camera, **kw):
+        """Fold one (H, W, c) probability map seen from ``camera``."""
+        self.add_batch([probs], [camera] if not isinstance(camera, (list, tuple)) else camera, **kw)
+
+    # -- exchange ------------------------------------------------------------------------
+    def allreduce(self, group=None):
+        """Sum accumulators and counts over all ranks (one NCCL all-reduce each)."""
+        import torch.distributed as dist
+
+        tex = self.texture
+        tex._push_host()
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            dist.all_reduce(tex._accum, op=dist.ReduceOp.SUM, group=group)
+            dist.all_reduce(tex._counts, op=dist.ReduceOp.SUM, group=group)
+        tex._h_accum = tex._h_counts = None
+
+    # -- results -------------------------------------------------------------------------
+    def _finalize(self):
+        from .fusion import finalize
+
+        if not self.texture.finalized:
+            finalize(self.texture)
+
+    def get(self, host=False):
+        """Finalize once; per-texel class distributions (n_x, c) float32."""
+        self._finalize()
+        return self.texture.rows if host else self.texture.rows_device
+
+    def labels(self, host=False):
+        self._finalize()
+        return self.texture.labels_device.cpu().numpy() if host else self.texture.labels_device
+
+    def render(self, cameras, width=None, height=None, fallback=None, host=False, stream=None):
+        """Label images (B, H, W) int32 for the given cameras (renderback.py:28-56)."""
+        self._finalize()
+        W, H = _sizes(cameras, width, height)
+        cams = _cams_array(cameras).to(self.device, non_blocking=True)
+        B = int(cams.shape[0])
+        hw = H * W
+        out = torch.empty((B, hw), dtype=torch.int32, device=self.device)
+        labels = self.texture.labels_device
+        for b0 in range(0, B, self.max_batch):
+            b = min(self.max_batch, B - b0)
+            rows = self.scene.buffer("rows", (self.max_batch, hw), torch.int32)[:b]
+            self.scene.rasterize(cams[b0:b0 + b], W, H, rows, stream=stream)
+            fb = None
+            if fallback is not None:
+                fb = torch.as_tensor(fallback).to(self.device, torch.int32).reshape(B, hw)[b0:b0 + b].contiguous()
+            render_labels_device(labels, rows, hw, b, fb, out[b0:b0 + b], stream)
+        out = out.view(B, H, W)
+        return out.cpu().numpy() if host else out

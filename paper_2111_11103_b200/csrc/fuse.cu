@@ -27,12 +27,13 @@ namespace tfb {
 namespace {
 
 constexpr int kFuseThreads = 256;
+constexpr int kMaxFrames = 32;  // frames per launch (pointers travel in the kernel parameters)
 
 struct FuseParams {
+  const float *probs[kMaxFrames];
   const int32_t *rows;
   int64_t hw;
   int nframes;
-  const float *const *probs;
   int c;
   const uint32_t *hits;
   const double *weights;
@@ -142,7 +143,7 @@ __device__ __forceinline__ bool tma_ok(const float *src, int npix, int c) {
 }
 
 template <typename AccT, int AGG>
-__global__ void __launch_bounds__(kFuseThreads) k_fuse(FuseParams p) {
+__global__ void __launch_bounds__(kFuseThreads) k_fuse(const __grid_constant__ FuseParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int P = p.P, c = p.c, NS = p.NS;
   const Smem L = smem_layout(P, c, NS, (int)sizeof(AccT));
@@ -331,7 +332,7 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse(FuseParams p) {
 }
 
 template <typename AccT, int AGG>
-int launch_fuse(FuseParams &p, cudaStream_t st) {
+int launch_fuse(const FuseParams &p, cudaStream_t st) {
   const Smem L = smem_layout(p.P, p.c, p.NS, (int)sizeof(AccT));
   auto kern = k_fuse<AccT, AGG>;
   static int configured_bytes = -1;
@@ -449,10 +450,7 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
   if (NS > 4) NS = 4;
   if (NS < 2) NS = 2;
   FuseParams p;
-  p.rows = rows;
   p.hw = hw;
-  p.nframes = nframes;
-  p.probs = probs;
   p.c = num_classes;
   p.hits = texel_hits;
   p.weights = weights;
@@ -462,24 +460,38 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
   p.accum = accum;
   p.stride = accum_stride;
   p.counts = counts;
-  p.fallback = fallback_out;
   p.P = P;
   p.NS = NS;
   p.cpf = (hw + P - 1) / P;
-  p.nitems = p.cpf * nframes;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (accum_is_f64) {
-    switch (aggregator) {
-      case TFB_AGG_SUM: return launch_fuse<double, TFB_AGG_SUM>(p, st);
-      case TFB_AGG_MAXSUM: return launch_fuse<double, TFB_AGG_MAXSUM>(p, st);
-      default: return launch_fuse<double, TFB_AGG_MUL>(p, st);
+  for (int f0 = 0; f0 < nframes; f0 += kMaxFrames) {
+    const int nf = nframes - f0 < kMaxFrames ? nframes - f0 : kMaxFrames;
+    for (int i = 0; i < kMaxFrames; ++i) p.probs[i] = i < nf ? probs[f0 + i] : nullptr;
+    for (int i = 0; i < nf; ++i)
+      TFB_REQUIRE(p.probs[i], TFB_ERR_DATA, "tfb_fuse: null probability pointer for frame %d", f0 + i);
+    p.rows = rows + (int64_t)f0 * hw;
+    p.weights = weights ? weights + (int64_t)f0 * hw : nullptr;
+    p.hits = texel_hits ? texel_hits + (int64_t)f0 * total_texels : nullptr;
+    p.fallback = fallback_out ? fallback_out + (int64_t)f0 * hw : nullptr;
+    p.nframes = nf;
+    p.nitems = p.cpf * nf;
+    int rc;
+    if (accum_is_f64) {
+      switch (aggregator) {
+        case TFB_AGG_SUM: rc = launch_fuse<double, TFB_AGG_SUM>(p, st); break;
+        case TFB_AGG_MAXSUM: rc = launch_fuse<double, TFB_AGG_MAXSUM>(p, st); break;
+        default: rc = launch_fuse<double, TFB_AGG_MUL>(p, st); break;
+      }
+    } else {
+      switch (aggregator) {
+        case TFB_AGG_SUM: rc = launch_fuse<float, TFB_AGG_SUM>(p, st); break;
+        case TFB_AGG_MAXSUM: rc = launch_fuse<float, TFB_AGG_MAXSUM>(p, st); break;
+        default: rc = launch_fuse<float, TFB_AGG_MUL>(p, st); break;
+      }
     }
+    if (rc != TFB_OK) return rc;
   }
-  switch (aggregator) {
-    case TFB_AGG_SUM: return launch_fuse<float, TFB_AGG_SUM>(p, st);
-    case TFB_AGG_MAXSUM: return launch_fuse<float, TFB_AGG_MAXSUM>(p, st);
-    default: return launch_fuse<float, TFB_AGG_MUL>(p, st);
-  }
+  return TFB_OK;
 }
 
 extern "C" int tfb_rows_from_ids(const int32_t *tri, const int32_t *texel, int64_t npix, const tfb_scene *scene,

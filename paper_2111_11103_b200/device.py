@@ -1,0 +1,161 @@
+"""Device residency of the mesh + texel layout, and thin launch wrappers.
+
+A DeviceScene holds the float64 vertices, int32 triangles and the layout
+arrays in HBM (uploaded once) plus per-(width, height, batch) scratch, and
+launches the C-ABI kernels on the caller's CUDA stream.  All buffers are
+torch tensors (PyTorch is the allocator); the library never allocates.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .geometry import pack_camera
+
+_CACHE_ATTR = "_tfb_device_scene"
+
+
+def _dev(device):
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+class DeviceScene:
+    """Mesh + layout in device memory (geometry.py:31-77, 208-232)."""
+
+    def __init__(self, mesh, layout, device=None):
+        """``mesh`` may be None for a layout-only scene (texel rows and fusion,
+        no rasterization)."""
+        N.require_cuda()
+        if mesh is not None and layout.num_triangles != mesh.num_triangles:
+            from .errors import DataError
+
+            raise DataError("layout covers %d triangles but mesh has %d" % (layout.num_triangles, mesh.num_triangles))
+        self.device = _dev(device)
+        self.mesh = mesh
+        self.layout = layout
+        d = self.device
+        verts = mesh.vertices if mesh is not None else np.zeros((0, 3))
+        tris = mesh.triangles if mesh is not None else np.zeros((0, 3), np.int32)
+        self.vertices = torch.as_tensor(np.ascontiguousarray(verts, np.float64), device=d)
+        self.triangles = torch.as_tensor(np.ascontiguousarray(tris, np.int32), device=d)
+        self.steps = torch.as_tensor(np.ascontiguousarray(layout.steps, np.int32), device=d)
+        self.origins = torch.as_tensor(np.ascontiguousarray(layout.origins, np.int8), device=d)
+        self.offsets = torch.as_tensor(np.ascontiguousarray(layout.offsets, np.int64), device=d)
+        self.num_triangles = int(layout.num_triangles)
+        self.total_texels = int(layout.total_texels)
+        self.struct = N.TfbScene(
+            self.vertices.data_ptr(), self.triangles.data_ptr(), self.steps.data_ptr(), self.origins.data_ptr(),
+            self.offsets.data_ptr(), len(verts), self.num_triangles, self.total_texels)
+        self._sig = _signature(mesh, layout)
+        self._ws = {}
+        self._bufs = {}
+
+    def matches(self, mesh, layout):
+        return self._sig == _signature(mesh, layout)
+
+    def same_layout(self, layout):
+        return self.layout is layout or self._sig[4:] == _signature(None, layout)[4:]
+
+    @property
+    def sref(self):
+        return ctypes.byref(self.struct)
+
+    # -- scratch ---------------------------------------------------------------
+    def workspace(self, width, height, nframes):
+        key = (width, height)
+        ws = self._ws.get(key)
+        if ws is None or ws[0] < nframes:
+            nbytes = N.load().tfb_raster_workspace_bytes(self.num_triangles, width, height, nframes, 0)
+            ws = (nframes, torch.empty(nbytes, dtype=torch.uint8, device=self.device))
+            self._ws[key] = ws
+        return ws[1]
+
+    def buffer(self, name, shape, dtype, zero=False):
+        """Named persistent scratch (grown on demand, never shrunk)."""
+        n = int(np.prod(shape))
+        t = self._bufs.get(name)
+        if t is None or t.numel() < n or t.dtype != dtype:
+            t = (torch.zeros if zero else torch.empty)(max(n, 1), dtype=dtype, device=self.device)
+            self._bufs[name] = t
+        return t[:n].view(*shape)
+
+    def hits(self, nframes):
+        """Per-frame texel hit counters; kept all-zero between uses by tfb_clear_hits."""
+        return self.buffer("hits", (nframes, max(self.total_texels, 1)), torch.int32, zero=True)
+
+    # -- launches --------------------------------------------------------------
+    def rasterize(self, cams, width, height, rows, hits=None, tri=None, texel=None, depth=None, u=None, v=None,
+                  stream=None):
+        """cams: (B, 16) float64 device tensor; rows: (B, H*W) int32 device tensor."""
+        B = int(cams.shape[0])
+        if B == 0:
+            return
+        if self.mesh is None:
+            raise RuntimeError("layout-only scene cannot rasterize")
+        ws = self.workspace(width, height, B)
+        N.call("tfb_rasterize", self.sref, N.ptr(cams), B, int(width), int(height), N.ptr(ws), ws.numel(), 0,
+               N.ptr(rows), N.ptr(hits), N.ptr(tri), N.ptr(texel), N.ptr(depth), N.ptr(u), N.ptr(v),
+               N.stream_handle(stream))
+
+    def cams_tensor(self, frames):
+        arr = np.stack([pack_camera(f) for f in frames]) if frames else np.zeros((0, 16))
+        return torch.as_tensor(arr, dtype=torch.float64).to(self.device, non_blocking=False)
+
+
+def _signature(mesh, layout):
+    mv = (id(mesh.vertices), id(mesh.triangles), mesh.vertices.shape, mesh.triangles.shape) if mesh is not None \
+        else (None, None, None, None)
+    return mv + (id(layout.steps), id(layout.origins), id(layout.offsets), int(layout.total_texels))
+
+
+def scene_for(mesh, layout, device=None):
+    """Cached DeviceScene for (mesh, layout), keyed on array identity."""
+    cached = getattr(layout, _CACHE_ATTR, None)
+    if cached is not None and cached.matches(mesh, layout) and (device is None or cached.device == _dev(device)):
+        return cached
+    sc = DeviceScene(mesh, layout, device)
+    try:
+        object.__setattr__(layout, _CACHE_ATTR, sc)
+    except Exception:  # pragma: no cover
+        pass
+    return sc
+
+
+def layout_scene(layout, device=None):
+    """Cached layout-only DeviceScene (offsets/steps for fusion of host IdImages)."""
+    cached = getattr(layout, "_tfb_layout_scene", None)
+    if cached is not None and cached.same_layout(layout) and (device is None or cached.device == _dev(device)):
+        return cached
+    full = getattr(layout, _CACHE_ATTR, None)
+    if full is not None and full.same_layout(layout) and (device is None or full.device == _dev(device)):
+        return full
+    sc = DeviceScene(None, layout, device)
+    object.__setattr__(layout, "_tfb_layout_scene", sc)
+    return sc
+
+
+class _MeshOnly:
+    """Layout stand-in for kernels that only read the mesh (area pass)."""
+
+    def __init__(self, m):
+        self.steps = np.ones(m, np.int32)
+        self.origins = np.zeros(m, np.int8)
+        self.offsets = np.arange(m, dtype=np.int64)
+        self.total_texels = m
+        self.num_triangles = m
+
+
+def worst_case_areas(mesh, frames, device=None):
+    """compute_worst_case_areas (geometry.py:360-380) on the GPU; returns host float64 (m,)."""
+    N.require_cuda()
+    sc = DeviceScene(mesh, _MeshOnly(mesh.num_triangles), device)
+    cams = sc.cams_tensor(frames)
+    sizes = torch.as_tensor(np.array([[f.width, f.height] for f in frames], dtype=np.int32)).to(sc.device)
+    areas = torch.zeros(mesh.num_triangles, dtype=torch.float64, device=sc.device)
+    N.call("tfb_worst_case_areas", sc.sref, N.ptr(cams), N.ptr(sizes), len(frames), N.ptr(areas),
+           N.stream_handle())
+    return areas.cpu().numpy()

@@ -1,0 +1,144 @@
+"""Per-frame correspondences (rasterizer.py:93-202) on the GPU.
+
+``rasterize`` returns an IdImage whose planes live in device memory; the
+host views ``triangle``/``texel``/``depth``/``u``/``v`` are materialized on
+first access (depth/u/v by a second, bit-identical rasterization that also
+writes those float64 planes — only tests and debugging read them).
+IdImages can also be built on the host from arrays, as the reference's test
+helpers do (tests/helpers.py:45-61); they are uploaded when first used.
+"""
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .device import scene_for
+from .errors import DataError
+
+DEPTH_TIE = 1e-9  # rasterizer.py:18
+NONE = -1  # rasterizer.py:20
+
+
+class IdImage:
+    """Per-pixel (triangle, texel) correspondence of one frame (rasterizer.py:23-43)."""
+
+    def __init__(self, frame_id, width, height, triangle=None, texel=None, depth=None, u=None, v=None):
+        self.frame_id = frame_id
+        self.width = int(width)
+        self.height = int(height)
+        self._host = {}
+        for name, arr in (("triangle", triangle), ("texel", texel), ("depth", depth), ("u", u), ("v", v)):
+            if arr is not None:
+                if isinstance(arr, torch.Tensor):
+                    arr = arr.detach().cpu().numpy()
+                self._host[name] = np.asarray(arr)
+        self._rows = None  # (H*W,) int32 device rows for _rows_scene
+        self._rows_scene = None
+        self._dev_tri = None
+        self._dev_texel = None
+        self._source = None  # (scene, camera record) for lazily re-rendered planes
+
+    # -- construction from the device path -------------------------------------
+    @classmethod
+    def _from_device(cls, frame_id, width, height, scene, cam, rows, tri=None, texel=None):
+        ids = cls(frame_id, width, height)
+        ids._rows = rows
+        ids._rows_scene = scene
+        ids._dev_tri = tri
+        ids._dev_texel = texel
+        ids._source = (scene, cam)
+        return ids
+
+    # -- reference field access ---------------------------------------------------
+    def _materialize(self, name):
+        if name in self._host:
+            return self._host[name]
+        H, W = self.height, self.width
+        if name in ("triangle", "texel") and self._dev_tri is not None:
+            self._host["triangle"] = self._dev_tri.view(H, W).cpu().numpy()
+            self._host["texel"] = self._dev_texel.view(H, W).cpu().numpy()
+            return self._host[name]
+        if self._source is None:
+            raise AttributeError("IdImage has no %s plane" % name)
+        scene, cam = self._source
+        d = scene.device
+        rows = torch.empty((1, H * W), dtype=torch.int32, device=d)
+        tri = torch.empty((1, H * W), dtype=torch.int32, device=d)
+        tex = torch.empty((1, H * W), dtype=torch.int32, device=d)
+        dep = torch.empty((1, H * W), dtype=torch.float64, device=d)
+        uu = torch.empty((1, H * W), dtype=torch.float64, device=d)
+        vv = torch.empty((1, H * W), dtype=torch.float64, device=d)
+        scene.rasterize(cam, W, H, rows, tri=tri, texel=tex, depth=dep, u=uu, v=vv)
+        for key, t in (("triangle", tri), ("texel", tex), ("depth", dep), ("u", uu), ("v", vv)):
+            self._host.setdefault(key, t.view(H, W).cpu().numpy())
+        return self._host[name]
+
+    triangle = property(lambda self: self._materialize("triangle"))
+    texel = property(lambda self: self._materialize("texel"))
+    depth = property(lambda self: self._materialize("depth"))
+    u = property(lambda self: self._materialize("u"))
+    v = property(lambda self: self._materialize("v"))
+
+    @property
+    def covered(self):
+        return self.triangle != NONE
+
+    # -- device rows ----------------------------------------------------------------
+    def rows_on(self, scene):
+        """(H*W,) int32 device tensor of global texel rows (offsets[t] + texel, -1 uncovered)."""
+        if self._rows is not None and self._rows_scene is not None and (
+                self._rows_scene is scene or self._rows_scene.same_layout(scene.layout)):
+            return self._rows
+        tri = np.ascontiguousarray(self.triangle, dtype=np.int32).reshape(-1)
+        tex = np.ascontiguousarray(self.texel, dtype=np.int32).reshape(-1)
+        if tri.size != self.width * self.height:
+            raise DataError("IdImage planes do not match its %dx%d size" % (self.width, self.height))
+        d = scene.device
+        t_tri = torch.as_tensor(tri).to(d)
+        t_tex = torch.as_tensor(tex).to(d)
+        rows = torch.empty(tri.size, dtype=torch.int32, device=d)
+        bad = torch.zeros(1, dtype=torch.int32, device=d)
+        N.call("tfb_rows_from_ids", N.ptr(t_tri), N.ptr(t_tex), tri.size, scene.sref, N.ptr(rows), N.ptr(bad),
+               N.stream_handle())
+        if int(bad.item()):
+            raise DataError("IdImage references triangles or texels outside the layout")
+        self._rows, self._rows_scene = rows, scene
+        return rows
+
+
+def rasterize(mesh, layout, frame, device=None):
+    """Render triangle/texel correspondences for one frame (rasterizer.py:93-132)."""
+    if layout.num_triangles != mesh.num_triangles:
+        raise DataError("layout covers %d triangles but mesh has %d" % (layout.num_triangles, mesh.num_triangles))
+    scene = scene_for(mesh, layout, device)
+    W, H = int(frame.width), int(frame.height)
+    cam = scene.cams_tensor([frame])
+    d = scene.device
+    rows = torch.empty((1, H * W), dtype=torch.int32, device=d)
+    tri = torch.empty((1, H * W), dtype=torch.int32, device=d)
+    tex = torch.empty((1, H * W), dtype=torch.int32, device=d)
+    scene.rasterize(cam, W, H, rows, tri=tri, texel=tex)
+    return IdImage._from_device(frame.frame_id, W, H, scene, cam, rows.view(-1), tri.view(-1), tex.view(-1))
+
+
+def project_point(frame, point):
+    """Project one world point → (x_px, y_px, depth) (rasterizer.py:46-59)."""
+    p = np.asarray(point, dtype=np.float64).reshape(1, 3) @ frame.rotation.T + frame.translation
+    z = float(p[0, 2])
+    if z == 0.0:
+        return float("nan"), float("nan"), 0.0
+    return float(p[0, 0] / z * frame.fx + frame.cx), float(p[0, 1] / z * frame.fy + frame.cy), z
+
+
+def pixel_world_points(mesh, layout, ids):
+    """World position of every covered pixel from its (u, v) (rasterizer.py:205-224)."""
+    cov = ids.covered
+    tri = ids.triangle[cov].astype(np.int64)
+    u, v = ids.u[cov], ids.v[cov]
+    o = layout.origins[tri].astype(np.int64)
+    w = np.empty((len(tri), 3))
+    r = np.arange(len(tri))
+    w[r, o] = 1.0 - u
+    w[r, (o + 1) % 3] = u - v
+    w[r, (o + 2) % 3] = v
+    return np.einsum("nk,nkd->nd", w, mesh.vertices[mesh.triangles[tri]])
