@@ -59,6 +59,23 @@ class MeshAnnotation:
         self.max_batch = int(max_batch)
         self._staging = None
         self.frames_added = 0
+        # optional list receiving (frames, ev_start, ev_after_raster, ev_after_fuse) per batch
+        self.profile = None
+
+    def _event(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream(self.device))
+        return e
+
+    def reset(self):
+        """Zero the accumulator and counts for a new fusion job (same layout)."""
+        tex = self.texture
+        tex._accum.zero_()
+        tex._counts.zero_()
+        tex.finalized = False
+        tex._rows = tex._unobs = tex._labels = None
+        tex._h_accum = tex._h_counts = tex._h_rows = tex._h_unobs = None
+        self.frames_added = 0
 
     # -- accumulation ------------------------------------------------------------------
     def _probs_batch(self, probs, b, H, W):
@@ -113,13 +130,21 @@ class MeshAnnotation:
             ptrs, keep = self._probs_batch(chunk, b, H, W)
             rows = self.scene.buffer("rows", (self.max_batch, hw), torch.int32)[:b]
             hits = self.scene.hits(self.max_batch)[:b] if needs_hits else None
+            prof = self.profile
+            if prof is not None:
+                e0 = self._event()
             self.scene.rasterize(cams_all[b0:b0 + b], W, H, rows, hits=hits, stream=stream)
+            if prof is not None:
+                e1 = self._event()
             parr, _k = N.ptr_array(ptrs)
             fb = fallback_out[b0:b0 + b] if fallback_out is not None else None
             N.call("tfb_fuse", N.ptr(rows), hw, b, parr, self.num_classes, N.ptr(hits), None, tex.total_texels,
                    N.AGG_IDS[tex.aggregator], N.WMODE_IDS[self.weight_mode], float(self.alpha or 0.0),
                    N.ptr(tex._accum), int(tex.is_f64), tex.stride, N.ptr(tex._counts), N.ptr(fb),
                    N.stream_handle(stream))
+            if prof is not None:
+                e2 = self._event()
+                prof.append((b, e0, e1, e2))
             if needs_hits:
                 N.call("tfb_clear_hits", N.ptr(rows), hw, b, tex.total_texels, N.ptr(hits),
                        N.stream_handle(stream))

@@ -1,24 +1,28 @@
 // Fusion scatter-add (fusion.py:114-183) and its per-frame helpers.
 //
-// k_fuse is the HBM-bound hot kernel.  It is persistent (grid = resident CTAs
-// across the 148 SMs) and walks (frame, chunk) work items, a chunk being P
-// consecutive pixels whose (P, c) float32 probability rows are one
-// contiguous span of the (H, W, c) map.  One elected thread streams each
-// chunk into a shared-memory ring of NS stages with the Blackwell bulk-copy
-// engine (cp.async.bulk … mbarrier::complete_tx, L2 evict_first hint: each
-// probability byte is read exactly once and must not evict the accumulator,
-// which stays L2-resident at the BASELINE sizes).  While later chunks are in
-// flight the CTA:
-//   1. gathers each pixel's texel row and weight (pixels_iid / images_iid /
-//      blend from the per-frame texel hit counts, or explicit weights);
-//   2. finds runs of consecutive pixels on the same texel (segments; at the
-//      BASELINE scene ~2.5 pixels per run along a scanline);
-//   3. gives every thread (segment, 4-class quad) items: the run's weighted
-//      transformed probabilities (w·p, w·p·[p==max], w·log clip(p)) are summed
-//      from shared memory and land with ONE vector reduction
+// k_fuse is the HBM-bound hot kernel.  Work item = (frame, 32-pixel chunk):
+// the chunk's (32, c) float32 probability rows are one contiguous span of the
+// (H, W, c) map.  Every warp is an independent pipeline (no CTA barriers):
+// lane 0 streams its items into a private shared-memory ring of NS stages
+// with the Blackwell bulk-copy engine (cp.async.bulk … mbarrier::complete_tx,
+// L2 evict_first: each probability byte is read once and must not evict the
+// accumulator, which stays L2-resident at the BASELINE sizes), while the
+// warp's lanes
+//   1. hold the chunk's texel rows and weights in registers, prefetched one
+//      and two items ahead (rows, then the dependent hit-count gather);
+//   2. find runs of consecutive pixels on the same texel with two ballots
+//      (segments; ~2.5 pixels per run at the BASELINE scene);
+//   3. take (segment, 4-class quad) items: the run's transformed probabilities
+//      are reduced from shared memory and land with ONE vector reduction
 //      red.global.add.v4.f32 per quad, plus one u32 count add per run.
-// The per-pixel network argmax used as the render fallback (cli.py:293,
-// bindings/__init__.py:112) is emitted from the same staged bytes when asked.
+// Weights derived from the hit counts (pixels_iid / images_iid / blend) are
+// equal inside a run, so w is applied once per item, and for the product
+// rule sum_i w*log(p_i) is evaluated as w*log(prod_i p_i) over up to four
+// pixels with a streamlined log (range reduction to [sqrt(1/2), sqrt(2)) and
+// an atanh series; ~15 instructions, relative accuracy kept near p = 1).
+// The float64 parity mode instead follows the reference arithmetic pixel by
+// pixel (w*log(p) in double, fusion.py:177).  The per-pixel network argmax
+// (render fallback, cli.py:293) is emitted from the same staged bytes.
 #include <math.h>
 
 #include "common.cuh"
@@ -26,8 +30,9 @@
 namespace tfb {
 namespace {
 
-constexpr int kFuseThreads = 256;
-constexpr int kMaxFrames = 32;  // frames per launch (pointers travel in the kernel parameters)
+constexpr int kWarps = 4;        // warps per CTA (independent pipelines)
+constexpr int kChunk = 32;       // pixels per work item = one per lane
+constexpr int kMaxFrames = 32;   // frames per launch (pointers travel in the kernel parameters)
 
 struct FuseParams {
   const float *probs[kMaxFrames];
@@ -44,37 +49,34 @@ struct FuseParams {
   int64_t stride;
   uint32_t *counts;
   int32_t *fallback;
-  int P;
   int NS;
   int64_t cpf;     // chunks per frame
   int64_t nitems;  // nframes * cpf
 };
 
-struct Smem {
+struct WarpSmem {
   size_t stage_floats;  // per stage, multiple of 4
-  size_t o_row, o_w, o_max, o_head, o_len, o_bar, o_misc, total;
+  size_t o_w, o_row, o_max, o_head, o_len, o_bar, total;
 };
 
 __host__ __device__ inline size_t al(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-__host__ __device__ inline Smem smem_layout(int P, int c, int NS, int accbytes) {
-  Smem s;
-  s.stage_floats = al((size_t)P * c, 4);
+__host__ __device__ inline WarpSmem warp_layout(int c, int NS, int accbytes) {
+  WarpSmem s;
+  s.stage_floats = al((size_t)kChunk * c, 4);
   size_t o = (size_t)NS * s.stage_floats * 4;
   s.o_w = o = al(o, 16);
-  o += (size_t)P * accbytes;
+  o += (size_t)kChunk * accbytes;
   s.o_row = o = al(o, 16);
-  o += (size_t)P * 4;
-  s.o_max = o = al(o, 16);
-  o += (size_t)P * 4;
-  s.o_head = o = al(o, 16);
-  o += (size_t)P * 4;
-  s.o_len = o = al(o, 16);
-  o += (size_t)P * 4;
+  o += kChunk * 4;
+  s.o_max = o;
+  o += kChunk * 4;
+  s.o_head = o;
+  o += kChunk * 4;
+  s.o_len = o;
+  o += kChunk * 4;
   s.o_bar = o = al(o, 16);
   o += (size_t)NS * 8;
-  s.o_misc = o = al(o, 16);
-  o += 64;
   s.total = al(o, 128);
   return s;
 }
@@ -123,18 +125,18 @@ __device__ __forceinline__ double np_clip(double x, double lo, double hi) {
   return x < hi ? x : hi;
 }
 
-template <int AGG>
-__device__ __forceinline__ float xf_f(float v, float mx) {
-  if (AGG == TFB_AGG_SUM) return v;
-  if (AGG == TFB_AGG_MAXSUM) return v == mx ? v : 0.0f;  // fusion.py:174-175 (ties kept)
-  return logf(np_clipf(v, kMulClampF, 1.0f));            // fusion.py:177
-}
-
-template <int AGG>
-__device__ __forceinline__ double xf_d(float v, float mx) {
-  if (AGG == TFB_AGG_SUM) return (double)v;
-  if (AGG == TFB_AGG_MAXSUM) return v == mx ? (double)v : 0.0;
-  return log(np_clip((double)v, kMulClamp, 1.0));
+// log(x) for normal positive finite x: x = m * 2^e with m in [sqrt(1/2), sqrt(2)),
+// log(m) = 2 atanh(s), s = (m-1)/(m+1), |s| <= 0.1716, series to s^9.
+// m - 1 is exact (Sterbenz), so the relative error stays ~3 ulp even as x → 1.
+__device__ __forceinline__ float fast_logf(float x) {
+  const int bits = __float_as_int(x);
+  const int e = (bits - 0x3f3504f3) >> 23;
+  const float m = __int_as_float(bits - (e << 23));
+  const float s = __fdividef(m - 1.0f, m + 1.0f);
+  const float z = s * s;
+  const float poly = fmaf(fmaf(fmaf(z, 1.0f / 9.0f, 1.0f / 7.0f), z, 1.0f / 5.0f), z, 1.0f / 3.0f);
+  const float s2 = s + s;
+  return fmaf((float)e, 0.693147180559945f, fmaf(s2 * z, poly, s2));
 }
 
 __device__ __forceinline__ bool tma_ok(const float *src, int npix, int c) {
@@ -142,34 +144,52 @@ __device__ __forceinline__ bool tma_ok(const float *src, int npix, int c) {
   return (bytes % 16 == 0) && (((uintptr_t)src & 15) == 0) && bytes > 0;
 }
 
-template <typename AccT, int AGG>
-__global__ void __launch_bounds__(kFuseThreads) k_fuse(const __grid_constant__ FuseParams p) {
+__device__ __forceinline__ int32_t row_of(const FuseParams &p, int64_t item, int lane) {
+  if (item >= p.nitems) return -1;
+  const int64_t f = item / p.cpf;
+  const int64_t pix = (item - f * p.cpf) * kChunk + lane;
+  return pix < p.hw ? __ldg(p.rows + f * p.hw + pix) : -1;
+}
+
+// fusion.py:132-141 (mode weights) or the caller's explicit weights
+__device__ __forceinline__ double weight_of(const FuseParams &p, int64_t item, int lane, int32_t r) {
+  if (r < 0 || item >= p.nitems) return 0.0;
+  const int64_t f = item / p.cpf;
+  if (p.wmode == TFB_W_EXPLICIT) return __ldg(p.weights + f * p.hw + (item - f * p.cpf) * kChunk + lane);
+  if (p.wmode == TFB_W_PIXELS_IID) return 1.0;
+  const double per_image = 1.0 / (double)__ldg(p.hits + f * p.n_x + r);
+  return p.wmode == TFB_W_IMAGES_IID ? per_image : (1.0 - p.alpha) + p.alpha * per_image;
+}
+
+template <typename AccT, int AGG, bool EQW>
+__global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ FuseParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const int P = p.P, c = p.c, NS = p.NS;
-  const Smem L = smem_layout(P, c, NS, (int)sizeof(AccT));
-  float *stages = reinterpret_cast<float *>(smem);
-  AccT *sw = reinterpret_cast<AccT *>(smem + L.o_w);
-  int32_t *srow = reinterpret_cast<int32_t *>(smem + L.o_row);
-  float *smax = reinterpret_cast<float *>(smem + L.o_max);
-  int32_t *shead = reinterpret_cast<int32_t *>(smem + L.o_head);
-  int32_t *slen = reinterpret_cast<int32_t *>(smem + L.o_len);
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + L.o_bar);
-  int32_t *misc = reinterpret_cast<int32_t *>(smem + L.o_misc);  // [0..7] warp counts, [8] nseg
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t G = gridDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = p.c, NS = p.NS;
+  const WarpSmem L = warp_layout(c, NS, (int)sizeof(AccT));
+  unsigned char *ws = smem + (size_t)warp * L.total;
+  float *stages = reinterpret_cast<float *>(ws);
+  AccT *sw = reinterpret_cast<AccT *>(ws + L.o_w);
+  int32_t *srow = reinterpret_cast<int32_t *>(ws + L.o_row);
+  float *smax = reinterpret_cast<float *>(ws + L.o_max);
+  int32_t *shead = reinterpret_cast<int32_t *>(ws + L.o_head);
+  int32_t *slen = reinterpret_cast<int32_t *>(ws + L.o_len);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(ws + L.o_bar);
+  const int64_t GW = (int64_t)gridDim.x * kWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
 
   uint64_t policy = 0;
-  if (tid == 0) {
+  if (lane == 0) {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
     for (int s = 0; s < NS; ++s) mbar_init(bar + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
+  __syncwarp();
 
   auto issue = [&](int64_t item, int s) {
-    const int64_t f = item / p.cpf, ch = item - f * p.cpf;
-    const int64_t start = ch * P;
-    const int npix = (int)min((int64_t)P, p.hw - start);
+    const int64_t f = item / p.cpf;
+    const int64_t start = (item - f * p.cpf) * kChunk;
+    const int npix = (int)min((int64_t)kChunk, p.hw - start);
     const float *src = p.probs[f] + start * c;
     if (tma_ok(src, npix, c)) {
       const uint32_t bytes = (uint32_t)((size_t)npix * c * 4);
@@ -177,56 +197,42 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse(const __grid_constant__ F
       bulk_g2s(stages + (size_t)s * L.stage_floats, src, bytes, bar + s, policy);
     }
   };
-  if (tid == 0) {
-    for (int s = 0; s < NS; ++s) {
-      const int64_t item = blockIdx.x + (int64_t)s * G;
-      if (item < p.nitems) issue(item, s);
-    }
-  }
+  if (lane == 0)
+    for (int s = 0; s < NS; ++s)
+      if (gw + s * GW < p.nitems) issue(gw + s * GW, s);
 
   const int nq = (c + 3) >> 2;
+  const float inv_nq = 1.0f / (float)nq;
   const bool vec_ok = (c & 3) == 0;
+  const unsigned lt_mask = (1u << lane) - 1u;
+
+  int32_t r_cur = row_of(p, gw, lane);
+  double w_cur = weight_of(p, gw, lane, r_cur);
+  int32_t r_nxt = row_of(p, gw + GW, lane);
   uint32_t phase = 0;
   int64_t it = 0;
-  for (int64_t item = blockIdx.x; item < p.nitems; item += G, ++it) {
+  for (int64_t item = gw; item < p.nitems; item += GW, ++it) {
+    // software prefetch: weights one item ahead, rows two items ahead
+    const double w_nxt = weight_of(p, item + GW, lane, r_nxt);
+    const int32_t r_nn = row_of(p, item + 2 * GW, lane);
+
     const int s = (int)(it % NS);
-    const int64_t f = item / p.cpf, ch = item - f * p.cpf;
-    const int64_t start = ch * P;
-    const int npix = (int)min((int64_t)P, p.hw - start);
+    const int64_t f = item / p.cpf;
+    const int64_t start = (item - f * p.cpf) * kChunk;
+    const int npix = (int)min((int64_t)kChunk, p.hw - start);
     const float *src = p.probs[f] + start * c;
     float *st = stages + (size_t)s * L.stage_floats;
-
-    // (1) per-pixel texel row and weight (fusion.py:114-142, 167-169)
-    if (tid < P) {
-      int32_t r = -1;
-      double w = 0.0;
-      if (tid < npix) {
-        r = p.rows[f * p.hw + start + tid];
-        if (r >= 0) {
-          if (p.wmode == TFB_W_EXPLICIT) {
-            w = p.weights[f * p.hw + start + tid];
-          } else if (p.wmode == TFB_W_PIXELS_IID) {
-            w = 1.0;
-          } else {
-            const double per_image = 1.0 / (double)p.hits[f * p.n_x + r];
-            w = p.wmode == TFB_W_IMAGES_IID ? per_image : (1.0 - p.alpha) + p.alpha * per_image;
-          }
-        }
-      }
-      srow[tid] = r;
-      sw[tid] = (AccT)w;
-    }
     if (tma_ok(src, npix, c)) {
       mbar_wait(bar + s, (phase >> s) & 1u);
       phase ^= 1u << s;
     } else {
-      for (int i = tid; i < npix * c; i += kFuseThreads) st[i] = src[i];
+      for (int i = lane; i < npix * c; i += 32) st[i] = src[i];
+      __syncwarp();
     }
-    __syncthreads();
 
-    // (2) per-pixel maximum (maxsum) and network argmax fallback
-    if ((AGG == TFB_AGG_MAXSUM || p.fallback) && tid < npix) {
-      const float *pp = st + (size_t)tid * c;
+    // per-pixel maximum (maxsum, fusion.py:174) and network argmax fallback
+    if ((AGG == TFB_AGG_MAXSUM || p.fallback) && lane < npix) {
+      const float *pp = st + (size_t)lane * c;
       float best = pp[0];
       int bi = 0;
       for (int k = 1; k < c; ++k) {
@@ -236,48 +242,39 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse(const __grid_constant__ F
           bi = k;
         }
       }
-      smax[tid] = best;
-      if (p.fallback) p.fallback[f * p.hw + start + tid] = bi;
+      smax[lane] = best;
+      if (p.fallback) p.fallback[f * p.hw + start + lane] = bi;
     }
-    // (3) segment heads: runs of equal rows
-    bool head = false;
-    if (tid < npix) {
-      const int32_t r = srow[tid];
-      head = r >= 0 && (tid == 0 || srow[tid - 1] != r);
-    }
-    const uint32_t hb = __ballot_sync(0xffffffffu, head);
-    if (lane == 0) misc[warp] = __popc(hb);
-    __syncthreads();
-    if (head) {
-      int base = 0;
-      for (int w2 = 0; w2 < warp; ++w2) base += misc[w2];
-      const int idx = base + __popc(hb & ((1u << lane) - 1u));
-      const int32_t r = srow[tid];
-      int len = 1;
-      while (tid + len < npix && srow[tid + len] == r) ++len;
-      shead[idx] = tid;
-      slen[idx] = len;
-    }
-    if (tid == 0) {
-      int n = 0;
-      for (int w2 = 0; w2 < kFuseThreads / 32; ++w2) n += misc[w2];
-      misc[8] = n;
-    }
-    __syncthreads();
 
-    // (4) one vector reduction per (segment, class quad)
-    const int nseg = misc[8];
-    for (int q2 = tid; q2 < nseg * nq; q2 += kFuseThreads) {
-      const int sg = q2 / nq;
+    // runs of equal rows: two ballots give run heads and run boundaries
+    const int32_t prev = __shfl_up_sync(0xffffffffu, r_cur, 1);
+    const bool change = lane == 0 || prev != r_cur;
+    const bool head = change && r_cur >= 0;
+    const unsigned cmask = __ballot_sync(0xffffffffu, change);
+    const unsigned hmask = __ballot_sync(0xffffffffu, head);
+    if (head) {
+      const int idx = __popc(hmask & lt_mask);
+      const unsigned above = cmask & ~((2u << lane) - 1u);
+      const int nxt = above ? __ffs(above) - 1 : 32;
+      shead[idx] = lane;
+      slen[idx] = nxt - lane;
+    }
+    srow[lane] = r_cur;
+    sw[lane] = (AccT)w_cur;
+    __syncwarp();
+
+    const int nseg = __popc(hmask);
+    const int total = nseg * nq;
+    for (int q2 = lane; q2 < total; q2 += 32) {
+      const int sg = (int)(((float)q2 + 0.5f) * inv_nq);
       const int q = q2 - sg * nq;
       const int h = shead[sg], len = slen[sg];
       const int32_t r = srow[h];
       const int k0 = q * 4;
       if (sizeof(AccT) == 4) {
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        float m0 = 1.f, m1 = 1.f, m2 = 1.f, m3 = 1.f;  // running products (mul, EQW)
         for (int i = h; i < h + len; ++i) {
-          const float wv = (float)sw[i];
-          const float mx = AGG == TFB_AGG_MAXSUM ? smax[i] : 0.f;
           const float *pp = st + (size_t)i * c + k0;
           float v0, v1, v2, v3;
           if (vec_ok) {
@@ -289,10 +286,40 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse(const __grid_constant__ F
             v2 = k0 + 2 < c ? pp[2] : 1.0f;
             v3 = k0 + 3 < c ? pp[3] : 1.0f;
           }
-          a0 += wv * xf_f<AGG>(v0, mx);
-          a1 += wv * xf_f<AGG>(v1, mx);
-          a2 += wv * xf_f<AGG>(v2, mx);
-          a3 += wv * xf_f<AGG>(v3, mx);
+          const float wi = EQW ? 1.0f : (float)sw[i];
+          if (AGG == TFB_AGG_SUM) {
+            a0 = fmaf(wi, v0, a0); a1 = fmaf(wi, v1, a1); a2 = fmaf(wi, v2, a2); a3 = fmaf(wi, v3, a3);
+          } else if (AGG == TFB_AGG_MAXSUM) {
+            const float mx = smax[i];
+            a0 = fmaf(wi, v0 == mx ? v0 : 0.f, a0);
+            a1 = fmaf(wi, v1 == mx ? v1 : 0.f, a1);
+            a2 = fmaf(wi, v2 == mx ? v2 : 0.f, a2);
+            a3 = fmaf(wi, v3 == mx ? v3 : 0.f, a3);
+          } else {
+            v0 = np_clipf(v0, kMulClampF, 1.0f);
+            v1 = np_clipf(v1, kMulClampF, 1.0f);
+            v2 = np_clipf(v2, kMulClampF, 1.0f);
+            v3 = np_clipf(v3, kMulClampF, 1.0f);
+            if (EQW) {  // w * sum log p = w * log prod p, folded four pixels at a time (>= 1e-28, normal)
+              m0 *= v0; m1 *= v1; m2 *= v2; m3 *= v3;
+              if (((i - h) & 3) == 3) {
+                a0 += fast_logf(m0); a1 += fast_logf(m1); a2 += fast_logf(m2); a3 += fast_logf(m3);
+                m0 = m1 = m2 = m3 = 1.f;
+              }
+            } else {
+              a0 = fmaf(wi, fast_logf(v0), a0);
+              a1 = fmaf(wi, fast_logf(v1), a1);
+              a2 = fmaf(wi, fast_logf(v2), a2);
+              a3 = fmaf(wi, fast_logf(v3), a3);
+            }
+          }
+        }
+        if (AGG == TFB_AGG_MUL && EQW && (len & 3)) {
+          a0 += fast_logf(m0); a1 += fast_logf(m1); a2 += fast_logf(m2); a3 += fast_logf(m3);
+        }
+        if (EQW) {
+          const float w = (float)sw[h];
+          a0 *= w; a1 *= w; a2 *= w; a3 *= w;
         }
         if (!vec_ok) {  // padding columns receive exact zeros
           if (k0 + 1 >= c) a1 = 0.f;
@@ -304,14 +331,22 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse(const __grid_constant__ F
                      "f"(a3)
                      : "memory");
       } else {
+        // float64 parity mode: the reference's per-pixel contribution w * f(p) (fusion.py:171-177)
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         for (int i = h; i < h + len; ++i) {
           const double wv = (double)sw[i];
-          const float mx = AGG == TFB_AGG_MAXSUM ? smax[i] : 0.f;
           const float *pp = st + (size_t)i * c + k0;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (k0 + k < c) acc[k] += wv * xf_d<AGG>(pp[k], mx);
+          for (int k = 0; k < 4; ++k) {
+            if (k0 + k < c) {
+              const float v = pp[k];
+              double t;
+              if (AGG == TFB_AGG_SUM) t = (double)v;
+              else if (AGG == TFB_AGG_MAXSUM) t = v == smax[i] ? (double)v : 0.0;
+              else t = log(np_clip((double)v, kMulClamp, 1.0));
+              acc[k] += wv * t;
+            }
+          }
         }
         double *dst = reinterpret_cast<double *>(p.accum) + (int64_t)r * p.stride + k0;
 #pragma unroll
@@ -320,39 +355,50 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse(const __grid_constant__ F
       }
       if (q == 0) atomicAdd(p.counts + r, (uint32_t)len);
     }
-    __syncthreads();  // stage s and the side arrays are free again
-    if (tid == 0) {
-      const int64_t nxt = item + (int64_t)NS * G;
-      if (nxt < p.nitems) {
+    __syncwarp();  // stage s and the side arrays are free again
+    if (lane == 0) {
+      const int64_t nx = item + (int64_t)NS * GW;
+      if (nx < p.nitems) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(nxt, s);
+        issue(nx, s);
       }
     }
+    r_cur = r_nxt;
+    w_cur = w_nxt;
+    r_nxt = r_nn;
   }
 }
 
-template <typename AccT, int AGG>
+template <typename AccT, int AGG, bool EQW>
 int launch_fuse(const FuseParams &p, cudaStream_t st) {
-  const Smem L = smem_layout(p.P, p.c, p.NS, (int)sizeof(AccT));
-  auto kern = k_fuse<AccT, AGG>;
-  static int configured_bytes = -1;
+  const WarpSmem L = warp_layout(p.c, p.NS, (int)sizeof(AccT));
+  const size_t bytes = L.total * kWarps;
+  auto kern = k_fuse<AccT, AGG, EQW>;
+  static size_t configured_bytes = 0;
   static int blocks_per_sm = 0;
   static int num_sms = 0;
-  if (configured_bytes != (int)L.total) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total) != cudaSuccess)
+  if (configured_bytes != bytes) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
       return check_launch("tfb_fuse: shared memory configuration");
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kFuseThreads, L.total);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kWarps * 32, bytes);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
-    configured_bytes = (int)L.total;
+    configured_bytes = bytes;
   }
+  const int64_t warps_needed = (p.nitems + 0) / 1;
   int64_t grid = (int64_t)num_sms * blocks_per_sm;
-  if (grid > p.nitems) grid = p.nitems;
+  const int64_t need = (warps_needed + kWarps - 1) / kWarps;
+  if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, kFuseThreads, L.total, st>>>(p);
+  kern<<<(unsigned)grid, kWarps * 32, bytes, st>>>(p);
   return check_launch("tfb_fuse");
+}
+
+template <typename AccT, int AGG>
+int launch_fuse_w(const FuseParams &p, cudaStream_t st) {
+  return p.wmode == TFB_W_EXPLICIT ? launch_fuse<AccT, AGG, false>(p, st) : launch_fuse<AccT, AGG, true>(p, st);
 }
 
 __global__ void k_rows_from_ids(const int32_t *tri, const int32_t *texel, int64_t npix, tfb_scene sc, int32_t *rows,
@@ -441,14 +487,10 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
   TFB_REQUIRE(accum_is_f64 || (accum_stride % 4 == 0 && ((uintptr_t)accum & 15) == 0), TFB_ERR_DATA,
               "tfb_fuse: float32 accumulator rows must be 16-byte aligned (stride multiple of 4)");
   if (nframes <= 0 || hw <= 0) return TFB_OK;
-  int P = 128;
-  while (P > 8 && (size_t)P * num_classes * 4 > 48 * 1024) P >>= 1;
-  TFB_REQUIRE((size_t)P * num_classes * 4 <= 96 * 1024, TFB_ERR_CAPACITY,
+  const size_t stage = (size_t)kChunk * num_classes * 4;
+  TFB_REQUIRE(stage * 2 * kWarps <= 200 * 1024, TFB_ERR_CAPACITY,
               "tfb_fuse: %d classes exceed the shared-memory staging budget", num_classes);
-  const size_t stage = (size_t)P * num_classes * 4;
-  int NS = (int)((96 * 1024) / (stage ? stage : 1));
-  if (NS > 4) NS = 4;
-  if (NS < 2) NS = 2;
+  const int NS = stage <= 2048 ? 4 : 2;
   FuseParams p;
   p.hw = hw;
   p.c = num_classes;
@@ -460,9 +502,8 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
   p.accum = accum;
   p.stride = accum_stride;
   p.counts = counts;
-  p.P = P;
   p.NS = NS;
-  p.cpf = (hw + P - 1) / P;
+  p.cpf = (hw + kChunk - 1) / kChunk;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   for (int f0 = 0; f0 < nframes; f0 += kMaxFrames) {
     const int nf = nframes - f0 < kMaxFrames ? nframes - f0 : kMaxFrames;
@@ -478,15 +519,15 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
     int rc;
     if (accum_is_f64) {
       switch (aggregator) {
-        case TFB_AGG_SUM: rc = launch_fuse<double, TFB_AGG_SUM>(p, st); break;
-        case TFB_AGG_MAXSUM: rc = launch_fuse<double, TFB_AGG_MAXSUM>(p, st); break;
-        default: rc = launch_fuse<double, TFB_AGG_MUL>(p, st); break;
+        case TFB_AGG_SUM: rc = launch_fuse_w<double, TFB_AGG_SUM>(p, st); break;
+        case TFB_AGG_MAXSUM: rc = launch_fuse_w<double, TFB_AGG_MAXSUM>(p, st); break;
+        default: rc = launch_fuse_w<double, TFB_AGG_MUL>(p, st); break;
       }
     } else {
       switch (aggregator) {
-        case TFB_AGG_SUM: rc = launch_fuse<float, TFB_AGG_SUM>(p, st); break;
-        case TFB_AGG_MAXSUM: rc = launch_fuse<float, TFB_AGG_MAXSUM>(p, st); break;
-        default: rc = launch_fuse<float, TFB_AGG_MUL>(p, st); break;
+        case TFB_AGG_SUM: rc = launch_fuse_w<float, TFB_AGG_SUM>(p, st); break;
+        case TFB_AGG_MAXSUM: rc = launch_fuse_w<float, TFB_AGG_MAXSUM>(p, st); break;
+        default: rc = launch_fuse_w<float, TFB_AGG_MUL>(p, st); break;
       }
     }
     if (rc != TFB_OK) return rc;

@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path against the reference goldens and the CPU oracle.
+
+Bars: triangle / texel ids bit-exact (depth, u, v too);
+counts exact; float64 accumulators within 1e-12 relative (atomic order),
+float32 accumulators within 1e-5 relative (log space for mul); labels
+identical except where the reference's top-2 margin is below 1e-5.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2111_11103_b200 import (
+    MeshAnnotation, Mesh, TexelLayout, accumulate_frame, build_texel_layout, compute_pixel_weights,
+    compute_worst_case_areas, finalize, init_texture, rasterize, render_labels, texel_argmax, uniform_layout)
+from paper_2111_11103_b200.geometry import CameraFrame, Intrinsics, pack_camera
+from paper_2111_11103_b200.rasterizer import IdImage
+from paper_2111_11103_b200.synth import (NoiseModel, corrupt, make_room, random_room_trajectory,
+                                         scannet_intrinsics)
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _frame(cam, W, H, fid=0):
+    return CameraFrame(fid, Intrinsics(cam[12], cam[13], cam[14], cam[15], W, H), cam[:9].reshape(3, 3), cam[9:12])
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    z = np.load(os.path.join(GOLD, "cfg1.npz"))
+    d = {k: z[k] for k in z.files}
+    mesh = Mesh(d["verts"], d["tris"])
+    layout = TexelLayout(d["steps"], d["origins"], d["offsets"], int(d["total_texels"]))
+    W, H = (int(x) for x in d["wh"])
+    frames = [_frame(c, W, H, i) for i, c in enumerate(d["cams"])]
+    c = int(d["num_classes"])
+    model = NoiseModel("flip", epsilon=0.3, q=0.8, seed=1)
+    probs = [corrupt(d["gt"][f].astype(np.int32), model, c, f) for f in range(len(frames))]
+    return d, mesh, layout, frames, probs
+
+
+def test_raster_golden_cases_bitexact():
+    z = np.load(os.path.join(GOLD, "raster_cases.npz"))
+    for name in [str(n) for n in z["names"]]:
+        mesh = Mesh(z[name + "/verts"], z[name + "/tris"])
+        steps = z[name + "/steps"]
+        layout = TexelLayout(steps, z[name + "/origins"], z[name + "/offsets"],
+                             int(((steps.astype(np.int64) ** 2 + steps) // 2).sum()))
+        W, H = (int(x) for x in z[name + "/wh"])
+        for f, cam in enumerate(z[name + "/cams"]):
+            ids = rasterize(mesh, layout, _frame(cam, W, H))
+            np.testing.assert_array_equal(ids.triangle, z[name + "/tri"][f], err_msg=name)
+            np.testing.assert_array_equal(ids.texel, z[name + "/texel"][f], err_msg=name)
+            np.testing.assert_array_equal(ids.depth, z[name + "/depth"][f], err_msg=name)
+            cov = ids.triangle >= 0
+            np.testing.assert_array_equal(ids.u[cov], z[name + "/u"][f][cov], err_msg=name)
+            np.testing.assert_array_equal(ids.v[cov], z[name + "/v"][f][cov], err_msg=name)
+
+
+def test_raster_cfg1_all_frames_bitexact(cfg1):
+    d, mesh, layout, frames, _ = cfg1
+    for f, fr in enumerate(frames):
+        ids = rasterize(mesh, layout, fr)
+        np.testing.assert_array_equal(ids.triangle, d["tri"][f])
+        np.testing.assert_array_equal(ids.texel, d["texel"][f])
+
+
+def test_raster_cfg2_full_frame_bitexact():
+    z = np.load(os.path.join(GOLD, "cfg2_frame.npz"))
+    v, t = make_room((6.0, 5.0, 3.0), 158)
+    mesh = Mesh.from_arrays(v, t)
+    layout = uniform_layout(mesh, 1)
+    ids = rasterize(mesh, layout, _frame(z["cam"], 640, 480))
+    np.testing.assert_array_equal(ids.triangle, z["tri"])
+    np.testing.assert_array_equal(ids.texel, z["texel"])
+    assert float(ids.depth[ids.covered].sum()) == float(z["depth_sum"])
+
+
+def test_raster_cfg2_batched_random_cameras_vs_oracle():
+    """Full BASELINE size, batched launch (B=6), fine layout (steps=3): rows bit-exact."""
+    v, t = make_room((6.0, 5.0, 3.0), 158)
+    mesh = Mesh.from_arrays(v, t)
+    layout = uniform_layout(mesh, 3)
+    frames = random_room_trajectory(6, scannet_intrinsics(), seed=11)
+    ann = MeshAnnotation(mesh, layout, num_classes=4, max_batch=6)
+    cams = ann.scene.cams_tensor(frames)
+    rows = torch.empty((6, 640 * 480), dtype=torch.int32, device=ann.device)
+    ann.scene.rasterize(cams, 640, 480, rows)
+    rows = rows.cpu().numpy()
+    for k, fr in enumerate(frames):
+        ref = O.rasterize(mesh.vertices, mesh.triangles, layout.steps, layout.origins, pack_camera(fr), 640, 480,
+                          want_uv=False)
+        np.testing.assert_array_equal(rows[k], O.pixel_rows(layout.offsets, ref["triangle"], ref["texel"]).ravel())
+
+
+def test_raster_overflow_fallback_exact():
+    """A pair capacity far too small forces every tile through the exact slow path."""
+    from paper_2111_11103_b200 import _native as N
+
+    v, t = make_room((6.0, 5.0, 3.0), 24)
+    mesh = Mesh.from_arrays(v, t)
+    layout = uniform_layout(mesh, 2)
+    frames = random_room_trajectory(2, Intrinsics(100.0, 100.0, 63.5, 47.5, 128, 96), seed=5)
+    ann = MeshAnnotation(mesh, layout, num_classes=4, max_batch=2)
+    sc = ann.scene
+    cams = sc.cams_tensor(frames)
+    nbytes = N.load().tfb_raster_workspace_bytes(mesh.num_triangles, 128, 96, 2, 16)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=ann.device)
+    rows = torch.empty((2, 128 * 96), dtype=torch.int32, device=ann.device)
+    N.call("tfb_rasterize", sc.sref, N.ptr(cams), 2, 128, 96, N.ptr(ws), nbytes, 16, N.ptr(rows), None, None, None,
+           None, None, None, N.stream_handle())
+    rows = rows.cpu().numpy()
+    for k, fr in enumerate(frames):
+        ref = O.rasterize(mesh.vertices, mesh.triangles, layout.steps, layout.origins, pack_camera(fr), 128, 96,
+                          want_uv=False)
+        np.testing.assert_array_equal(rows[k], O.pixel_rows(layout.offsets, ref["triangle"], ref["texel"]).ravel())
+
+
+def test_worst_case_areas_and_layout_cfg1(cfg1):
+    d, mesh, _, frames, _ = cfg1
+    areas = compute_worst_case_areas(mesh, frames)
+    np.testing.assert_array_equal(areas, d["areas"])
+    layout = build_texel_layout(mesh, areas, 0.2)
+    np.testing.assert_array_equal(layout.steps, d["steps"])
+    np.testing.assert_array_equal(layout.offsets, d["offsets"])
+    np.testing.assert_array_equal(layout.origins, d["origins"])
+
+
+def _margin_ok(rows_ref, unobs_ref, labels_ref, labels, agg, accum_ref):
+    top2 = np.sort(rows_ref.astype(np.float64), axis=1)[:, -2:]
+    if agg == "mul":
+        scale = np.abs(accum_ref).max(axis=1)
+        gap = (np.sort(accum_ref, axis=1)[:, -1] - np.sort(accum_ref, axis=1)[:, -2])
+        decided = gap >= 1e-5 * np.maximum(scale, 1e-30)
+    else:
+        decided = (top2[:, 1] - top2[:, 0]) >= 1e-5
+    decided &= top2[:, 1] != top2[:, 0]
+    decided |= unobs_ref
+    np.testing.assert_array_equal(labels[decided], labels_ref[decided])
+    return decided
+
+
+@pytest.mark.parametrize("agg", ["sum", "mul", "maxsum"])
+@pytest.mark.parametrize("wm", ["images_iid", "pixels_iid"])
+def test_fusion_cfg1_float64_library_api(cfg1, agg, wm):
+    d, mesh, layout, frames, probs = cfg1
+    key = "%s_%s" % (agg, wm)
+    tex = init_texture(layout, int(d["num_classes"]), agg, accum_dtype="float64")
+    for fr, p in zip(frames, probs):
+        ids = rasterize(mesh, layout, fr)
+        accumulate_frame(tex, ids, p, compute_pixel_weights(ids, wm))
+    np.testing.assert_array_equal(tex.counts, d[key + "/counts"])
+    ref = d[key + "/accum"]
+    np.testing.assert_allclose(tex.accum, ref, rtol=1e-12, atol=1e-12)
+    finalize(tex)
+    np.testing.assert_array_equal(tex.unobserved, d[key + "/unobserved"])
+    np.testing.assert_allclose(tex.rows, d[key + "/rows"], atol=1e-6)
+    labels = texel_argmax(tex)
+    _margin_ok(d[key + "/rows"], d[key + "/unobserved"], d[key + "/labels"], labels, agg, ref)
+    if key + "/rendered" in d:
+        for f, (fr, p) in enumerate(zip(frames, probs)):
+            ids = rasterize(mesh, layout, fr)
+            out = render_labels(d[key + "/labels"], layout, ids, fallback=p.argmax(axis=2).astype(np.int32))
+            np.testing.assert_array_equal(out, d[key + "/rendered"][f])
+
+
+@pytest.mark.parametrize("agg", ["sum", "mul", "maxsum"])
+def test_fusion_cfg1_float32_batched(cfg1, agg):
+    d, mesh, layout, frames, probs = cfg1
+    key = "%s_images_iid" % agg
+    ann = MeshAnnotation(mesh, layout, num_classes=int(d["num_classes"]), aggregator=agg,
+                         weight_mode="images_iid", accum_dtype="float32", max_batch=7)
+    ann.add_batch(torch.as_tensor(np.stack(probs)).cuda(), frames)
+    np.testing.assert_array_equal(ann.texture.counts, d[key + "/counts"])
+    ref = d[key + "/accum"]
+    got = ann.texture.accum
+    err = np.abs(got - ref) / np.maximum(np.abs(ref), 1e-3)
+    assert err.max() < 1e-5, err.max()
+    labels = ann.labels(host=True)
+    _margin_ok(d[key + "/rows"], d[key + "/unobserved"], d[key + "/labels"], labels, agg, ref)
+
+
+def test_fusion_cfg2_float32_mul_vs_oracle():
+    """BASELINE size: 6 frames, c=40 softmax maps, mul + images_iid, vs the float64 oracle."""
+    v, t = make_room((6.0, 5.0, 3.0), 158)
+    mesh = Mesh.from_arrays(v, t)
+    layout = uniform_layout(mesh, 1)
+    frames = random_room_trajectory(6, scannet_intrinsics(), seed=2)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    probs = torch.softmax(torch.randn((6, 480, 640, 40), generator=g, device="cuda") * 2, dim=-1)
+    ann = MeshAnnotation(mesh, layout, num_classes=40, aggregator="mul", weight_mode="images_iid", max_batch=4)
+    fb = torch.empty((6, 480 * 640), dtype=torch.int32, device="cuda")
+    ann.add_batch(probs, frames, fallback_out=fb)
+    acc = np.zeros((layout.total_texels, 40))
+    cnt = np.zeros(layout.total_texels, np.int64)
+    ph = probs.cpu().numpy()
+    for k, fr in enumerate(frames):
+        ref = O.rasterize(mesh.vertices, mesh.triangles, layout.steps, layout.origins, pack_camera(fr), 640, 480,
+                          want_uv=False)
+        w = O.compute_pixel_weights(ref["triangle"], ref["texel"], "images_iid")
+        O.accumulate_frame(acc, cnt, layout.offsets, ref["triangle"], ref["texel"], ph[k], w, "mul")
+        np.testing.assert_array_equal(fb[k].cpu().numpy(), ph[k].argmax(axis=2).ravel())
+    np.testing.assert_array_equal(ann.texture.counts, cnt)
+    got = ann.texture.accum
+    seen = cnt > 0
+    err = np.abs(got[seen] - acc[seen]) / np.maximum(np.abs(acc[seen]), 1e-3)
+    assert err.max() < 1e-5, err.max()
+    rows, unobs = O.finalize(acc, cnt, "mul")
+    _margin_ok(rows, unobs, O.texel_argmax(rows, unobs), ann.labels(host=True), "mul", acc)
+
+
+def test_render_batched_matches_oracle(cfg1):
+    d, mesh, layout, frames, probs = cfg1
+    key = "sum_images_iid"
+    ann = MeshAnnotation(mesh, layout, num_classes=int(d["num_classes"]), aggregator="sum",
+                         accum_dtype="float64", max_batch=8)
+    ann.add_batch(probs, frames)
+    labels = ann.labels(host=True)
+    imgs = ann.render(frames, host=True)
+    for f in range(len(frames)):
+        ref = O.render_labels(labels, layout.offsets, d["tri"][f], d["texel"][f])
+        np.testing.assert_array_equal(imgs[f], ref)
+    _margin_ok(d[key + "/rows"], d[key + "/unobserved"], d[key + "/labels"], labels, "sum", d[key + "/accum"])
+
+
+def test_host_ids_rows_and_weights():
+    mesh = Mesh.from_arrays(np.array([[0, 0, 1], [1, 0, 1], [0, 1, 1.0]]), np.array([[0, 1, 2]]))
+    layout = uniform_layout(mesh, 3)
+    ids = IdImage(0, 4, 1, triangle=np.array([[0, 0, -1, 0]]), texel=np.array([[1, 1, 0, 5]]))
+    w = compute_pixel_weights(ids, "images_iid")
+    np.testing.assert_allclose(np.asarray(w), [[0.5, 0.5, 0.0, 1.0]])
+    tex = init_texture(layout, 2, "sum")
+    accumulate_frame(tex, ids, np.full((1, 4, 2), 0.5, np.float32), w)
+    assert tex.counts.tolist() == [0, 2, 0, 0, 0, 1]
