@@ -54,26 +54,48 @@ struct FuseParams {
   int64_t nitems;  // nframes * cpf
 };
 
+struct Geo {
+  int nq;    // class quads
+  int QW;    // quads handled per pass (<= 32)
+  int G;     // pixel groups per warp (lanes = G x QW)
+  int span;  // pixels per group
+};
+
+__host__ __device__ inline Geo geo_of(int c) {
+  Geo g;
+  g.nq = (c + 3) >> 2;
+  g.QW = g.nq < 32 ? g.nq : 32;
+  g.G = 32 / g.QW;
+  g.span = (kChunk + g.G - 1) / g.G;
+  return g;
+}
+
+// at most one piece per pixel
+constexpr int kMaxPieces = kChunk;
+
 struct WarpSmem {
   size_t stage_floats;  // per stage, multiple of 4
-  size_t o_w, o_row, o_max, o_head, o_len, o_bar, total;
+  size_t o_tab, o_pw, o_prow, o_plen, o_w, o_max, o_bar, total;
 };
 
 __host__ __device__ inline size_t al(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 __host__ __device__ inline WarpSmem warp_layout(int c, int NS, int accbytes) {
+  const Geo g = geo_of(c);
   WarpSmem s;
   s.stage_floats = al((size_t)kChunk * c, 4);
   size_t o = (size_t)NS * s.stage_floats * 4;
+  s.o_tab = o = al(o, 32);
+  o += (size_t)kMaxPieces * g.QW * 4 * accbytes;
+  s.o_pw = o = al(o, 16);
+  o += (size_t)kMaxPieces * accbytes;
+  s.o_prow = o;
+  o += (size_t)kMaxPieces * 4;
+  s.o_plen = o;
+  o += (size_t)kMaxPieces * 4;
   s.o_w = o = al(o, 16);
   o += (size_t)kChunk * accbytes;
-  s.o_row = o = al(o, 16);
-  o += kChunk * 4;
   s.o_max = o;
-  o += kChunk * 4;
-  s.o_head = o;
-  o += kChunk * 4;
-  s.o_len = o;
   o += kChunk * 4;
   s.o_bar = o = al(o, 16);
   o += (size_t)NS * 8;
@@ -112,11 +134,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
-__device__ __forceinline__ float np_clipf(float x, float lo, float hi) {
-  // NumPy clip kernel semantics: MIN(MAX(x, lo), hi), NaN passes through
-  if (isnan(x)) return x;
-  x = x > lo ? x : lo;
-  return x < hi ? x : hi;
+// np.clip(p, 1e-7, 1) with NaN passing through (fusion.py:177): NaN-propagating min/max
+__device__ __forceinline__ float clip_mul(float x) {
+  float y;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(y) : "f"(x), "f"(kMulClampF));
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(y) : "f"(y), "f"(1.0f));
+  return y;
 }
 
 __device__ __forceinline__ double np_clip(double x, double lo, double hi) {
@@ -125,14 +148,16 @@ __device__ __forceinline__ double np_clip(double x, double lo, double hi) {
   return x < hi ? x : hi;
 }
 
-// log(x) for normal positive finite x: x = m * 2^e with m in [sqrt(1/2), sqrt(2)),
-// log(m) = 2 atanh(s), s = (m-1)/(m+1), |s| <= 0.1716, series to s^9.
-// m - 1 is exact (Sterbenz), so the relative error stays ~3 ulp even as x → 1.
+// log(x) for positive normal x: x = m * 2^e, m in [sqrt(1/2), sqrt(2)),
+// log(m) = 2 atanh(s), s = (m-1)/(m+1), |s| <= 0.1716, series to s^9.  m - 1
+// is exact (Sterbenz), so the relative error stays a few ulp even as x → 1.
 __device__ __forceinline__ float fast_logf(float x) {
   const int bits = __float_as_int(x);
   const int e = (bits - 0x3f3504f3) >> 23;
   const float m = __int_as_float(bits - (e << 23));
-  const float s = __fdividef(m - 1.0f, m + 1.0f);
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(m + 1.0f));
+  const float s = (m - 1.0f) * r;
   const float z = s * s;
   const float poly = fmaf(fmaf(fmaf(z, 1.0f / 9.0f, 1.0f / 7.0f), z, 1.0f / 5.0f), z, 1.0f / 3.0f);
   const float s2 = s + s;
@@ -144,39 +169,64 @@ __device__ __forceinline__ bool tma_ok(const float *src, int npix, int c) {
   return (bytes % 16 == 0) && (((uintptr_t)src & 15) == 0) && bytes > 0;
 }
 
-__device__ __forceinline__ int32_t row_of(const FuseParams &p, int64_t item, int lane) {
-  if (item >= p.nitems) return -1;
-  const int64_t f = item / p.cpf;
-  const int64_t pix = (item - f * p.cpf) * kChunk + lane;
-  return pix < p.hw ? __ldg(p.rows + f * p.hw + pix) : -1;
+// (frame, chunk) of a work item, advanced by the warp-grid stride without divisions
+struct Pos {
+  int64_t f, ch;
+};
+
+__device__ __forceinline__ void advance(Pos &q, int64_t dF, int64_t dC, int64_t cpf) {
+  q.ch += dC;
+  q.f += dF;
+  if (q.ch >= cpf) {
+    q.ch -= cpf;
+    ++q.f;
+  }
 }
 
-// fusion.py:132-141 (mode weights) or the caller's explicit weights
-__device__ __forceinline__ double weight_of(const FuseParams &p, int64_t item, int lane, int32_t r) {
-  if (r < 0 || item >= p.nitems) return 0.0;
-  const int64_t f = item / p.cpf;
-  if (p.wmode == TFB_W_EXPLICIT) return __ldg(p.weights + f * p.hw + (item - f * p.cpf) * kChunk + lane);
+__device__ __forceinline__ int32_t row_at(const FuseParams &p, Pos q, int lane) {
+  if (q.f >= p.nframes) return -1;
+  const int64_t pix = q.ch * kChunk + lane;
+  return pix < p.hw ? __ldg(p.rows + q.f * p.hw + pix) : -1;
+}
+
+// raw weight source, loaded one item ahead and converted only when used so the
+// gather latency overlaps a whole item (fusion.py:132-141)
+__device__ __forceinline__ double wsrc_at(const FuseParams &p, Pos q, int lane, int32_t r) {
+  if (r < 0 || q.f >= p.nframes) return 0.0;
+  if (p.wmode == TFB_W_EXPLICIT) return __ldg(p.weights + q.f * p.hw + q.ch * kChunk + lane);
   if (p.wmode == TFB_W_PIXELS_IID) return 1.0;
-  const double per_image = 1.0 / (double)__ldg(p.hits + f * p.n_x + r);
-  return p.wmode == TFB_W_IMAGES_IID ? per_image : (1.0 - p.alpha) + p.alpha * per_image;
+  return (double)__ldg(p.hits + q.f * p.n_x + r);
+}
+
+template <typename AccT>
+__device__ __forceinline__ AccT weight_from(const FuseParams &p, double src, int32_t r) {
+  if (r < 0) return (AccT)0;
+  if (p.wmode == TFB_W_EXPLICIT || p.wmode == TFB_W_PIXELS_IID) return (AccT)src;
+  const AccT per_image = (AccT)1 / (AccT)src;
+  return p.wmode == TFB_W_IMAGES_IID ? per_image : ((AccT)1 - (AccT)p.alpha) + (AccT)p.alpha * per_image;
 }
 
 template <typename AccT, int AGG, bool EQW>
 __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ FuseParams p) {
+  // product rule in float32 with weights constant per run: fold w*log(prod p)
+  constexpr bool kProd = (AGG == TFB_AGG_MUL) && EQW && sizeof(AccT) == 4;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = p.c, NS = p.NS;
+  const Geo geo = geo_of(c);
   const WarpSmem L = warp_layout(c, NS, (int)sizeof(AccT));
   unsigned char *ws = smem + (size_t)warp * L.total;
   float *stages = reinterpret_cast<float *>(ws);
+  AccT *tab = reinterpret_cast<AccT *>(ws + L.o_tab);
+  AccT *pw = reinterpret_cast<AccT *>(ws + L.o_pw);
+  int32_t *prow = reinterpret_cast<int32_t *>(ws + L.o_prow);
+  int32_t *plen = reinterpret_cast<int32_t *>(ws + L.o_plen);
   AccT *sw = reinterpret_cast<AccT *>(ws + L.o_w);
-  int32_t *srow = reinterpret_cast<int32_t *>(ws + L.o_row);
   float *smax = reinterpret_cast<float *>(ws + L.o_max);
-  int32_t *shead = reinterpret_cast<int32_t *>(ws + L.o_head);
-  int32_t *slen = reinterpret_cast<int32_t *>(ws + L.o_len);
   uint64_t *bar = reinterpret_cast<uint64_t *>(ws + L.o_bar);
   const int64_t GW = (int64_t)gridDim.x * kWarps;
   const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t dF = GW / p.cpf, dC = GW - dF * p.cpf;
 
   uint64_t policy = 0;
   if (lane == 0) {
@@ -186,186 +236,223 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
   }
   __syncwarp();
 
-  auto issue = [&](int64_t item, int s) {
-    const int64_t f = item / p.cpf;
-    const int64_t start = (item - f * p.cpf) * kChunk;
+  auto issue = [&](Pos q, int s) {
+    const int64_t start = q.ch * kChunk;
     const int npix = (int)min((int64_t)kChunk, p.hw - start);
-    const float *src = p.probs[f] + start * c;
+    const float *src = p.probs[q.f] + start * c;
     if (tma_ok(src, npix, c)) {
       const uint32_t bytes = (uint32_t)((size_t)npix * c * 4);
       mbar_expect_tx(bar + s, bytes);
       bulk_g2s(stages + (size_t)s * L.stage_floats, src, bytes, bar + s, policy);
     }
   };
-  if (lane == 0)
-    for (int s = 0; s < NS; ++s)
-      if (gw + s * GW < p.nitems) issue(gw + s * GW, s);
+  Pos cur{gw / p.cpf, gw % p.cpf};
+  if (lane == 0) {
+    Pos q = cur;
+    for (int s = 0; s < NS && q.f < p.nframes; ++s) {
+      issue(q, s);
+      advance(q, dF, dC, p.cpf);
+    }
+  }
+  Pos nxt = cur, nn = cur;
+  advance(nxt, dF, dC, p.cpf);
+  advance(nn, dF, dC, p.cpf);
+  advance(nn, dF, dC, p.cpf);
 
-  const int nq = (c + 3) >> 2;
-  const float inv_nq = 1.0f / (float)nq;
   const bool vec_ok = (c & 3) == 0;
-  const unsigned lt_mask = (1u << lane) - 1u;
+  const unsigned upto = (2u << lane) - 1u;  // lanes <= this one
+  // lane -> (pixel group g, class quad qi) for phase A
+  const int g = lane / geo.QW, qi0 = lane - g * geo.QW;
+  const int i0 = g * geo.span;
+  const int i1 = min(i0 + geo.span, kChunk);
+  const bool grp_start = (lane % geo.span) == 0;  // lane as a pixel: first pixel of its group
+  const float inv_qw = 1.0f / (float)geo.QW;
 
-  int32_t r_cur = row_of(p, gw, lane);
-  double w_cur = weight_of(p, gw, lane, r_cur);
-  int32_t r_nxt = row_of(p, gw + GW, lane);
+  int32_t r_cur = row_at(p, cur, lane);
+  double ws_cur = wsrc_at(p, cur, lane, r_cur);
+  int32_t r_nxt = row_at(p, nxt, lane);
   uint32_t phase = 0;
-  int64_t it = 0;
-  for (int64_t item = gw; item < p.nitems; item += GW, ++it) {
-    // software prefetch: weights one item ahead, rows two items ahead
-    const double w_nxt = weight_of(p, item + GW, lane, r_nxt);
-    const int32_t r_nn = row_of(p, item + 2 * GW, lane);
+  int s = 0;
+  while (cur.f < p.nframes) {
+    // software prefetch: weight sources one item ahead, rows two items ahead
+    const double ws_nxt = wsrc_at(p, nxt, lane, r_nxt);
+    const int32_t r_nn = row_at(p, nn, lane);
 
-    const int s = (int)(it % NS);
-    const int64_t f = item / p.cpf;
-    const int64_t start = (item - f * p.cpf) * kChunk;
+    const int64_t start = cur.ch * kChunk;
     const int npix = (int)min((int64_t)kChunk, p.hw - start);
-    const float *src = p.probs[f] + start * c;
+    const float *src = p.probs[cur.f] + start * c;
     float *st = stages + (size_t)s * L.stage_floats;
+
+    // pieces: runs of equal rows, split at group starts (and every 4 pixels for the product rule)
+    const AccT w = weight_from<AccT>(p, ws_cur, r_cur);
+    const int32_t prev = __shfl_up_sync(0xffffffffu, r_cur, 1);
+    const bool chg = lane == 0 || prev != r_cur || grp_start;
+    const unsigned cmask = __ballot_sync(0xffffffffu, chg);
+    bool pstart = chg;
+    if (kProd) {
+      const int rs = 31 - __clz(cmask & upto);
+      pstart = ((lane - rs) & 3) == 0;
+    }
+    const unsigned smask = __ballot_sync(0xffffffffu, pstart);
+    const int npieces = __popc(smask);
+    if (pstart) {
+      const int idx = __popc(smask & upto) - 1;
+      const unsigned above = smask & ~upto;
+      prow[idx] = r_cur;
+      plen[idx] = (above ? __ffs(above) - 1 : kChunk) - lane;
+      pw[idx] = w;
+    }
+    sw[lane] = w;
+
     if (tma_ok(src, npix, c)) {
       mbar_wait(bar + s, (phase >> s) & 1u);
       phase ^= 1u << s;
     } else {
       for (int i = lane; i < npix * c; i += 32) st[i] = src[i];
+    }
+    __syncwarp();
+
+    // per-pixel maximum (maxsum, fusion.py:174) and network argmax fallback (cli.py:293)
+    if (AGG == TFB_AGG_MAXSUM || p.fallback) {
+      if (lane < npix) {
+        const float *pp = st + (size_t)lane * c;
+        float best = pp[0];
+        int bi = 0;
+        for (int k = 1; k < c; ++k) {
+          const float v = pp[k];
+          if (!isnan(best) && (isnan(v) || v > best)) {
+            best = v;
+            bi = k;
+          }
+        }
+        smax[lane] = best;
+        if (p.fallback) p.fallback[cur.f * p.hw + start + lane] = bi;
+      }
       __syncwarp();
     }
 
-    // per-pixel maximum (maxsum, fusion.py:174) and network argmax fallback
-    if ((AGG == TFB_AGG_MAXSUM || p.fallback) && lane < npix) {
-      const float *pp = st + (size_t)lane * c;
-      float best = pp[0];
-      int bi = 0;
-      for (int k = 1; k < c; ++k) {
-        const float v = pp[k];
-        if (!isnan(best) && (isnan(v) || v > best)) {
-          best = v;
-          bi = k;
-        }
-      }
-      smax[lane] = best;
-      if (p.fallback) p.fallback[f * p.hw + start + lane] = bi;
-    }
-
-    // runs of equal rows: two ballots give run heads and run boundaries
-    const int32_t prev = __shfl_up_sync(0xffffffffu, r_cur, 1);
-    const bool change = lane == 0 || prev != r_cur;
-    const bool head = change && r_cur >= 0;
-    const unsigned cmask = __ballot_sync(0xffffffffu, change);
-    const unsigned hmask = __ballot_sync(0xffffffffu, head);
-    if (head) {
-      const int idx = __popc(hmask & lt_mask);
-      const unsigned above = cmask & ~((2u << lane) - 1u);
-      const int nxt = above ? __ffs(above) - 1 : 32;
-      shead[idx] = lane;
-      slen[idx] = nxt - lane;
-    }
-    srow[lane] = r_cur;
-    sw[lane] = (AccT)w_cur;
-    __syncwarp();
-
-    const int nseg = __popc(hmask);
-    const int total = nseg * nq;
-    for (int q2 = lane; q2 < total; q2 += 32) {
-      const int sg = (int)(((float)q2 + 0.5f) * inv_nq);
-      const int q = q2 - sg * nq;
-      const int h = shead[sg], len = slen[sg];
-      const int32_t r = srow[h];
-      const int k0 = q * 4;
-      if (sizeof(AccT) == 4) {
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-        float m0 = 1.f, m1 = 1.f, m2 = 1.f, m3 = 1.f;  // running products (mul, EQW)
-        for (int i = h; i < h + len; ++i) {
-          const float *pp = st + (size_t)i * c + k0;
+    for (int qb = 0; qb < geo.nq; qb += geo.QW) {
+      // ---- phase A (branch-free): lanes = (group g, quad qi) scan their pixels in order;
+      //      each pixel folds into its piece's running value, stored to the piece's table slot
+      const int q = qb + qi0;
+      if (g < geo.G && q < geo.nq) {
+        const int k0 = q * 4;
+        const float *pp = st + (size_t)i0 * c + k0;
+        AccT a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        const float pad = AGG == TFB_AGG_MUL ? 1.0f : 0.0f;
+        for (int i = i0; i < i1; ++i, pp += c) {
+          const bool ps = (smask >> i) & 1u;
           float v0, v1, v2, v3;
           if (vec_ok) {
             const float4 v = *reinterpret_cast<const float4 *>(pp);
             v0 = v.x; v1 = v.y; v2 = v.z; v3 = v.w;
           } else {
             v0 = pp[0];
-            v1 = k0 + 1 < c ? pp[1] : 1.0f;
-            v2 = k0 + 2 < c ? pp[2] : 1.0f;
-            v3 = k0 + 3 < c ? pp[3] : 1.0f;
+            v1 = k0 + 1 < c ? pp[1] : pad;
+            v2 = k0 + 2 < c ? pp[2] : pad;
+            v3 = k0 + 3 < c ? pp[3] : pad;
           }
-          const float wi = EQW ? 1.0f : (float)sw[i];
-          if (AGG == TFB_AGG_SUM) {
-            a0 = fmaf(wi, v0, a0); a1 = fmaf(wi, v1, a1); a2 = fmaf(wi, v2, a2); a3 = fmaf(wi, v3, a3);
-          } else if (AGG == TFB_AGG_MAXSUM) {
-            const float mx = smax[i];
-            a0 = fmaf(wi, v0 == mx ? v0 : 0.f, a0);
-            a1 = fmaf(wi, v1 == mx ? v1 : 0.f, a1);
-            a2 = fmaf(wi, v2 == mx ? v2 : 0.f, a2);
-            a3 = fmaf(wi, v3 == mx ? v3 : 0.f, a3);
+          if (kProd) {
+            a0 = (ps ? 1.0f : (float)a0) * clip_mul(v0);
+            a1 = (ps ? 1.0f : (float)a1) * clip_mul(v1);
+            a2 = (ps ? 1.0f : (float)a2) * clip_mul(v2);
+            a3 = (ps ? 1.0f : (float)a3) * clip_mul(v3);
+          } else if (sizeof(AccT) == 4) {
+            const float wi = EQW ? 1.0f : (float)sw[i];
+            float t0 = v0, t1 = v1, t2 = v2, t3 = v3;
+            if (AGG == TFB_AGG_MAXSUM) {
+              const float mx = smax[i];
+              t0 = v0 == mx ? v0 : 0.f; t1 = v1 == mx ? v1 : 0.f; t2 = v2 == mx ? v2 : 0.f; t3 = v3 == mx ? v3 : 0.f;
+            } else if (AGG == TFB_AGG_MUL) {
+              t0 = fast_logf(clip_mul(v0)); t1 = fast_logf(clip_mul(v1));
+              t2 = fast_logf(clip_mul(v2)); t3 = fast_logf(clip_mul(v3));
+            }
+            a0 = fmaf(wi, t0, ps ? 0.f : (float)a0);
+            a1 = fmaf(wi, t1, ps ? 0.f : (float)a1);
+            a2 = fmaf(wi, t2, ps ? 0.f : (float)a2);
+            a3 = fmaf(wi, t3, ps ? 0.f : (float)a3);
           } else {
-            v0 = np_clipf(v0, kMulClampF, 1.0f);
-            v1 = np_clipf(v1, kMulClampF, 1.0f);
-            v2 = np_clipf(v2, kMulClampF, 1.0f);
-            v3 = np_clipf(v3, kMulClampF, 1.0f);
-            if (EQW) {  // w * sum log p = w * log prod p, folded four pixels at a time (>= 1e-28, normal)
-              m0 *= v0; m1 *= v1; m2 *= v2; m3 *= v3;
-              if (((i - h) & 3) == 3) {
-                a0 += fast_logf(m0); a1 += fast_logf(m1); a2 += fast_logf(m2); a3 += fast_logf(m3);
-                m0 = m1 = m2 = m3 = 1.f;
-              }
-            } else {
-              a0 = fmaf(wi, fast_logf(v0), a0);
-              a1 = fmaf(wi, fast_logf(v1), a1);
-              a2 = fmaf(wi, fast_logf(v2), a2);
-              a3 = fmaf(wi, fast_logf(v3), a3);
+            // float64 parity mode: the reference's per-pixel w * f(p) (fusion.py:171-177)
+            const double wi = (double)sw[i];
+            const float vv[4] = {v0, v1, v2, v3};
+            double t[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              if (AGG == TFB_AGG_SUM) t[k] = (double)vv[k];
+              else if (AGG == TFB_AGG_MAXSUM) t[k] = vv[k] == smax[i] ? (double)vv[k] : 0.0;
+              else t[k] = log(np_clip((double)vv[k], kMulClamp, 1.0));
             }
+            a0 = (ps ? 0.0 : (double)a0) + wi * t[0];
+            a1 = (ps ? 0.0 : (double)a1) + wi * t[1];
+            a2 = (ps ? 0.0 : (double)a2) + wi * t[2];
+            a3 = (ps ? 0.0 : (double)a3) + wi * t[3];
+          }
+          const int idx = __popc(smask & ((2u << i) - 1u)) - 1;
+          AccT *t = tab + ((size_t)idx * geo.QW + qi0) * 4;
+          if (sizeof(AccT) == 4) {
+            *reinterpret_cast<float4 *>(t) = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
+          } else {
+            t[0] = a0; t[1] = a1; t[2] = a2; t[3] = a3;
           }
         }
-        if (AGG == TFB_AGG_MUL && EQW && (len & 3)) {
-          a0 += fast_logf(m0); a1 += fast_logf(m1); a2 += fast_logf(m2); a3 += fast_logf(m3);
-        }
-        if (EQW) {
-          const float w = (float)sw[h];
-          a0 *= w; a1 *= w; a2 *= w; a3 *= w;
-        }
-        if (!vec_ok) {  // padding columns receive exact zeros
-          if (k0 + 1 >= c) a1 = 0.f;
-          if (k0 + 2 >= c) a2 = 0.f;
-          if (k0 + 3 >= c) a3 = 0.f;
-        }
-        float *dst = reinterpret_cast<float *>(p.accum) + (int64_t)r * p.stride + k0;
-        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a0), "f"(a1), "f"(a2),
-                     "f"(a3)
-                     : "memory");
-      } else {
-        // float64 parity mode: the reference's per-pixel contribution w * f(p) (fusion.py:171-177)
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int i = h; i < h + len; ++i) {
-          const double wv = (double)sw[i];
-          const float *pp = st + (size_t)i * c + k0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (k0 + k < c) {
-              const float v = pp[k];
-              double t;
-              if (AGG == TFB_AGG_SUM) t = (double)v;
-              else if (AGG == TFB_AGG_MAXSUM) t = v == smax[i] ? (double)v : 0.0;
-              else t = log(np_clip((double)v, kMulClamp, 1.0));
-              acc[k] += wv * t;
-            }
-          }
-        }
-        double *dst = reinterpret_cast<double *>(p.accum) + (int64_t)r * p.stride + k0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (k0 + k < c) atomicAdd(dst + k, acc[k]);
       }
-      if (q == 0) atomicAdd(p.counts + r, (uint32_t)len);
+      __syncwarp();
+
+      // ---- phase B (converged): log / weight / one vector reduction per (piece, quad)
+      for (int e = lane; e < npieces * geo.QW; e += 32) {
+        const int pc = (int)(((float)e + 0.5f) * inv_qw);
+        const int qi = e - pc * geo.QW;
+        const int q2 = qb + qi;
+        const int32_t r = prow[pc];
+        if (r < 0 || q2 >= geo.nq) continue;
+        const int k0 = q2 * 4;
+        const AccT *t = tab + (size_t)e * 4;
+        if (sizeof(AccT) == 4) {
+          const float4 v = *reinterpret_cast<const float4 *>(t);
+          float a0 = v.x, a1 = v.y, a2 = v.z, a3 = v.w;
+          if (kProd) {
+            a0 = fast_logf(a0); a1 = fast_logf(a1); a2 = fast_logf(a2); a3 = fast_logf(a3);
+          }
+          if (EQW) {
+            const float wv = (float)pw[pc];
+            a0 *= wv; a1 *= wv; a2 *= wv; a3 *= wv;
+          }
+          if (!vec_ok) {  // padding columns receive exact zeros
+            if (k0 + 1 >= c) a1 = 0.f;
+            if (k0 + 2 >= c) a2 = 0.f;
+            if (k0 + 3 >= c) a3 = 0.f;
+          }
+          float *dst = reinterpret_cast<float *>(p.accum) + (int64_t)r * p.stride + k0;
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a0), "f"(a1), "f"(a2),
+                       "f"(a3)
+                       : "memory");
+        } else {
+          double *dst = reinterpret_cast<double *>(p.accum) + (int64_t)r * p.stride + k0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (k0 + k < c) atomicAdd(dst + k, (double)t[k]);
+        }
+        if (q2 == 0) atomicAdd(p.counts + r, (uint32_t)plen[pc]);
+      }
+      __syncwarp();
     }
-    __syncwarp();  // stage s and the side arrays are free again
+
+    // stage s, table and side arrays are free again
     if (lane == 0) {
-      const int64_t nx = item + (int64_t)NS * GW;
-      if (nx < p.nitems) {
+      Pos ahead = cur;
+      for (int k = 0; k < NS; ++k) advance(ahead, dF, dC, p.cpf);
+      if (ahead.f < p.nframes) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(nx, s);
+        issue(ahead, s);
       }
     }
+    cur = nxt;
+    nxt = nn;
+    advance(nn, dF, dC, p.cpf);
     r_cur = r_nxt;
-    w_cur = w_nxt;
+    ws_cur = ws_nxt;
     r_nxt = r_nn;
+    s = (s + 1 == NS) ? 0 : s + 1;
   }
 }
 
@@ -387,9 +474,8 @@ int launch_fuse(const FuseParams &p, cudaStream_t st) {
     if (blocks_per_sm < 1) blocks_per_sm = 1;
     configured_bytes = bytes;
   }
-  const int64_t warps_needed = (p.nitems + 0) / 1;
   int64_t grid = (int64_t)num_sms * blocks_per_sm;
-  const int64_t need = (warps_needed + kWarps - 1) / kWarps;
+  const int64_t need = (p.nitems + kWarps - 1) / kWarps;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
   kern<<<(unsigned)grid, kWarps * 32, bytes, st>>>(p);
@@ -488,9 +574,9 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
               "tfb_fuse: float32 accumulator rows must be 16-byte aligned (stride multiple of 4)");
   if (nframes <= 0 || hw <= 0) return TFB_OK;
   const size_t stage = (size_t)kChunk * num_classes * 4;
-  TFB_REQUIRE(stage * 2 * kWarps <= 200 * 1024, TFB_ERR_CAPACITY,
-              "tfb_fuse: %d classes exceed the shared-memory staging budget", num_classes);
   const int NS = stage <= 2048 ? 4 : 2;
+  TFB_REQUIRE(warp_layout(num_classes, NS, accum_is_f64 ? 8 : 4).total * kWarps <= 227 * 1024, TFB_ERR_CAPACITY,
+              "tfb_fuse: %d classes exceed the shared-memory staging budget", num_classes);
   FuseParams p;
   p.hw = hw;
   p.c = num_classes;
