@@ -18,8 +18,8 @@
 // Weights derived from the hit counts (pixels_iid / images_iid / blend) are
 // equal inside a run, so w is applied once per item, and for the product
 // rule sum_i w*log(p_i) is evaluated as w*log(prod_i p_i) over up to four
-// pixels with a streamlined log (range reduction to [sqrt(1/2), sqrt(2)) and
-// an atanh series; ~15 instructions, relative accuracy kept near p = 1).
+// pixels, with a MUFU lg2 log that switches to a log1p series above 0.9 so the
+// relative accuracy holds as p -> 1.
 // The float64 parity mode instead follows the reference arithmetic pixel by
 // pixel (w*log(p) in double, fusion.py:177).  The per-pixel network argmax
 // (render fallback, cli.py:293) is emitted from the same staged bytes.
@@ -75,7 +75,7 @@ constexpr int kMaxPieces = kChunk;
 
 struct WarpSmem {
   size_t stage_floats;  // per stage, multiple of 4
-  size_t o_tab, o_pw, o_prow, o_plen, o_w, o_max, o_bar, total;
+  size_t o_tab, o_pw, o_prow, o_w, o_max, o_bar, total;
 };
 
 __host__ __device__ inline size_t al(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -90,8 +90,6 @@ __host__ __device__ inline WarpSmem warp_layout(int c, int NS, int accbytes) {
   s.o_pw = o = al(o, 16);
   o += (size_t)kMaxPieces * accbytes;
   s.o_prow = o;
-  o += (size_t)kMaxPieces * 4;
-  s.o_plen = o;
   o += (size_t)kMaxPieces * 4;
   s.o_w = o = al(o, 16);
   o += (size_t)kChunk * accbytes;
@@ -148,22 +146,6 @@ __device__ __forceinline__ double np_clip(double x, double lo, double hi) {
   return x < hi ? x : hi;
 }
 
-// log(x) for positive normal x: x = m * 2^e, m in [sqrt(1/2), sqrt(2)),
-// log(m) = 2 atanh(s), s = (m-1)/(m+1), |s| <= 0.1716, series to s^9.  m - 1
-// is exact (Sterbenz), so the relative error stays a few ulp even as x → 1.
-__device__ __forceinline__ float fast_logf(float x) {
-  const int bits = __float_as_int(x);
-  const int e = (bits - 0x3f3504f3) >> 23;
-  const float m = __int_as_float(bits - (e << 23));
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(m + 1.0f));
-  const float s = (m - 1.0f) * r;
-  const float z = s * s;
-  const float poly = fmaf(fmaf(fmaf(z, 1.0f / 9.0f, 1.0f / 7.0f), z, 1.0f / 5.0f), z, 1.0f / 3.0f);
-  const float s2 = s + s;
-  return fmaf((float)e, 0.693147180559945f, fmaf(s2 * z, poly, s2));
-}
-
 __device__ __forceinline__ bool tma_ok(const float *src, int npix, int c) {
   const size_t bytes = (size_t)npix * c * 4;
   return (bytes % 16 == 0) && (((uintptr_t)src & 15) == 0) && bytes > 0;
@@ -171,10 +153,10 @@ __device__ __forceinline__ bool tma_ok(const float *src, int npix, int c) {
 
 // (frame, chunk) of a work item, advanced by the warp-grid stride without divisions
 struct Pos {
-  int64_t f, ch;
+  int f, ch;
 };
 
-__device__ __forceinline__ void advance(Pos &q, int64_t dF, int64_t dC, int64_t cpf) {
+__device__ __forceinline__ void advance(Pos &q, int dF, int dC, int cpf) {
   q.ch += dC;
   q.f += dF;
   if (q.ch >= cpf) {
@@ -185,25 +167,41 @@ __device__ __forceinline__ void advance(Pos &q, int64_t dF, int64_t dC, int64_t 
 
 __device__ __forceinline__ int32_t row_at(const FuseParams &p, Pos q, int lane) {
   if (q.f >= p.nframes) return -1;
-  const int64_t pix = q.ch * kChunk + lane;
-  return pix < p.hw ? __ldg(p.rows + q.f * p.hw + pix) : -1;
+  const int pix = q.ch * kChunk + lane;
+  return pix < (int)p.hw ? __ldg(p.rows + (q.f * (int)p.hw + pix)) : -1;
 }
 
-// raw weight source, loaded one item ahead and converted only when used so the
-// gather latency overlaps a whole item (fusion.py:132-141)
+// raw weight source (hit count bits or explicit weight), loaded one item ahead
+// and converted only when used, so the gather latency overlaps a whole item
 __device__ __forceinline__ double wsrc_at(const FuseParams &p, Pos q, int lane, int32_t r) {
-  if (r < 0 || q.f >= p.nframes) return 0.0;
-  if (p.wmode == TFB_W_EXPLICIT) return __ldg(p.weights + q.f * p.hw + q.ch * kChunk + lane);
-  if (p.wmode == TFB_W_PIXELS_IID) return 1.0;
-  return (double)__ldg(p.hits + q.f * p.n_x + r);
+  if (r < 0 || q.f >= p.nframes || p.wmode == TFB_W_PIXELS_IID) return 0.0;
+  if (p.wmode == TFB_W_EXPLICIT) return __ldg(p.weights + (q.f * (int)p.hw + q.ch * kChunk + lane));
+  return __longlong_as_double((long long)__ldg(p.hits + ((int64_t)q.f * p.n_x + r)));
 }
 
+// fusion.py:132-141
 template <typename AccT>
 __device__ __forceinline__ AccT weight_from(const FuseParams &p, double src, int32_t r) {
   if (r < 0) return (AccT)0;
-  if (p.wmode == TFB_W_EXPLICIT || p.wmode == TFB_W_PIXELS_IID) return (AccT)src;
-  const AccT per_image = (AccT)1 / (AccT)src;
+  if (p.wmode == TFB_W_PIXELS_IID) return (AccT)1;
+  if (p.wmode == TFB_W_EXPLICIT) return (AccT)src;
+  const AccT per_image = (AccT)1 / (AccT)(uint32_t)__double_as_longlong(src);
   return p.wmode == TFB_W_IMAGES_IID ? per_image : ((AccT)1 - (AccT)p.alpha) + (AccT)p.alpha * per_image;
+}
+
+// log of a (product of) clipped probabilities, x in [1e-28, 1]: MUFU lg2 (2 ulp
+// below 1/2, 2^-22.6 absolute above) and, where that absolute error would be
+// large relative to |log x| (x > 0.9), the log1p series in t = x - 1 (exact),
+// truncation t^7/7, i.e. < 1.5e-7 relative.
+__device__ __forceinline__ float log_prob(float x) {
+  float l;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(x));
+  float y = l * 0.693147180559945f;
+  if (x > 0.9f) {
+    const float t = x - 1.0f;
+    y = t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, fmaf(t, -1.0f / 6.0f, 1.0f / 5.0f), -0.25f), 1.0f / 3.0f), -0.5f), 1.0f);
+  }
+  return y;
 }
 
 template <typename AccT, int AGG, bool EQW>
@@ -220,13 +218,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
   AccT *tab = reinterpret_cast<AccT *>(ws + L.o_tab);
   AccT *pw = reinterpret_cast<AccT *>(ws + L.o_pw);
   int32_t *prow = reinterpret_cast<int32_t *>(ws + L.o_prow);
-  int32_t *plen = reinterpret_cast<int32_t *>(ws + L.o_plen);
   AccT *sw = reinterpret_cast<AccT *>(ws + L.o_w);
   float *smax = reinterpret_cast<float *>(ws + L.o_max);
   uint64_t *bar = reinterpret_cast<uint64_t *>(ws + L.o_bar);
-  const int64_t GW = (int64_t)gridDim.x * kWarps;
-  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
-  const int64_t dF = GW / p.cpf, dC = GW - dF * p.cpf;
+  const int GW = gridDim.x * kWarps;
+  const int gw = blockIdx.x * kWarps + warp;
+  const int cpf = (int)p.cpf;
+  const int dF = GW / cpf, dC = GW - dF * cpf;
 
   uint64_t policy = 0;
   if (lane == 0) {
@@ -237,7 +235,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
   __syncwarp();
 
   auto issue = [&](Pos q, int s) {
-    const int64_t start = q.ch * kChunk;
+    const int64_t start = (int64_t)q.ch * kChunk;
     const int npix = (int)min((int64_t)kChunk, p.hw - start);
     const float *src = p.probs[q.f] + start * c;
     if (tma_ok(src, npix, c)) {
@@ -246,18 +244,18 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
       bulk_g2s(stages + (size_t)s * L.stage_floats, src, bytes, bar + s, policy);
     }
   };
-  Pos cur{gw / p.cpf, gw % p.cpf};
+  Pos cur{gw / cpf, gw % cpf};
   if (lane == 0) {
     Pos q = cur;
     for (int s = 0; s < NS && q.f < p.nframes; ++s) {
       issue(q, s);
-      advance(q, dF, dC, p.cpf);
+      advance(q, dF, dC, cpf);
     }
   }
   Pos nxt = cur, nn = cur;
-  advance(nxt, dF, dC, p.cpf);
-  advance(nn, dF, dC, p.cpf);
-  advance(nn, dF, dC, p.cpf);
+  advance(nxt, dF, dC, cpf);
+  advance(nn, dF, dC, cpf);
+  advance(nn, dF, dC, cpf);
 
   const bool vec_ok = (c & 3) == 0;
   const unsigned upto = (2u << lane) - 1u;  // lanes <= this one
@@ -278,7 +276,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
     const double ws_nxt = wsrc_at(p, nxt, lane, r_nxt);
     const int32_t r_nn = row_at(p, nn, lane);
 
-    const int64_t start = cur.ch * kChunk;
+    const int64_t start = (int64_t)cur.ch * kChunk;
     const int npix = (int)min((int64_t)kChunk, p.hw - start);
     const float *src = p.probs[cur.f] + start * c;
     float *st = stages + (size_t)s * L.stage_floats;
@@ -298,9 +296,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
     if (pstart) {
       const int idx = __popc(smask & upto) - 1;
       const unsigned above = smask & ~upto;
+      const int len = (above ? __ffs(above) - 1 : kChunk) - lane;
       prow[idx] = r_cur;
-      plen[idx] = (above ? __ffs(above) - 1 : kChunk) - lane;
       pw[idx] = w;
+      if (r_cur >= 0) atomicAdd(p.counts + r_cur, (uint32_t)len);  // fusion.py:182
     }
     sw[lane] = w;
 
@@ -326,7 +325,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
           }
         }
         smax[lane] = best;
-        if (p.fallback) p.fallback[cur.f * p.hw + start + lane] = bi;
+        if (p.fallback) p.fallback[(int64_t)cur.f * p.hw + start + lane] = bi;
       }
       __syncwarp();
     }
@@ -340,8 +339,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
         const float *pp = st + (size_t)i0 * c + k0;
         AccT a0 = 0, a1 = 0, a2 = 0, a3 = 0;
         const float pad = AGG == TFB_AGG_MUL ? 1.0f : 0.0f;
+        int idx = __popc(smask & ((1u << i0) - 1u)) - 1;
         for (int i = i0; i < i1; ++i, pp += c) {
           const bool ps = (smask >> i) & 1u;
+          idx += ps ? 1 : 0;
           float v0, v1, v2, v3;
           if (vec_ok) {
             const float4 v = *reinterpret_cast<const float4 *>(pp);
@@ -364,8 +365,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
               const float mx = smax[i];
               t0 = v0 == mx ? v0 : 0.f; t1 = v1 == mx ? v1 : 0.f; t2 = v2 == mx ? v2 : 0.f; t3 = v3 == mx ? v3 : 0.f;
             } else if (AGG == TFB_AGG_MUL) {
-              t0 = fast_logf(clip_mul(v0)); t1 = fast_logf(clip_mul(v1));
-              t2 = fast_logf(clip_mul(v2)); t3 = fast_logf(clip_mul(v3));
+              t0 = log_prob(clip_mul(v0)); t1 = log_prob(clip_mul(v1));
+              t2 = log_prob(clip_mul(v2)); t3 = log_prob(clip_mul(v3));
             }
             a0 = fmaf(wi, t0, ps ? 0.f : (float)a0);
             a1 = fmaf(wi, t1, ps ? 0.f : (float)a1);
@@ -387,7 +388,6 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
             a2 = (ps ? 0.0 : (double)a2) + wi * t[2];
             a3 = (ps ? 0.0 : (double)a3) + wi * t[3];
           }
-          const int idx = __popc(smask & ((2u << i) - 1u)) - 1;
           AccT *t = tab + ((size_t)idx * geo.QW + qi0) * 4;
           if (sizeof(AccT) == 4) {
             *reinterpret_cast<float4 *>(t) = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
           const float4 v = *reinterpret_cast<const float4 *>(t);
           float a0 = v.x, a1 = v.y, a2 = v.z, a3 = v.w;
           if (kProd) {
-            a0 = fast_logf(a0); a1 = fast_logf(a1); a2 = fast_logf(a2); a3 = fast_logf(a3);
+            a0 = log_prob(a0); a1 = log_prob(a1); a2 = log_prob(a2); a3 = log_prob(a3);
           }
           if (EQW) {
             const float wv = (float)pw[pc];
@@ -432,7 +432,6 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
           for (int k = 0; k < 4; ++k)
             if (k0 + k < c) atomicAdd(dst + k, (double)t[k]);
         }
-        if (q2 == 0) atomicAdd(p.counts + r, (uint32_t)plen[pc]);
       }
       __syncwarp();
     }
@@ -440,7 +439,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
     // stage s, table and side arrays are free again
     if (lane == 0) {
       Pos ahead = cur;
-      for (int k = 0; k < NS; ++k) advance(ahead, dF, dC, p.cpf);
+      for (int k = 0; k < NS; ++k) advance(ahead, dF, dC, cpf);
       if (ahead.f < p.nframes) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue(ahead, s);
@@ -448,7 +447,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
     }
     cur = nxt;
     nxt = nn;
-    advance(nn, dF, dC, p.cpf);
+    advance(nn, dF, dC, cpf);
     r_cur = r_nxt;
     ws_cur = ws_nxt;
     r_nxt = r_nn;
@@ -573,6 +572,8 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
   TFB_REQUIRE(accum_is_f64 || (accum_stride % 4 == 0 && ((uintptr_t)accum & 15) == 0), TFB_ERR_DATA,
               "tfb_fuse: float32 accumulator rows must be 16-byte aligned (stride multiple of 4)");
   if (nframes <= 0 || hw <= 0) return TFB_OK;
+  TFB_REQUIRE(hw * kMaxFrames < (1LL << 31), TFB_ERR_CAPACITY, "tfb_fuse: %lld pixels per frame is too many",
+              (long long)hw);
   const size_t stage = (size_t)kChunk * num_classes * 4;
   const int NS = stage <= 2048 ? 4 : 2;
   TFB_REQUIRE(warp_layout(num_classes, NS, accum_is_f64 ? 8 : 4).total * kWarps <= 227 * 1024, TFB_ERR_CAPACITY,
