@@ -46,7 +46,8 @@ static_assert(sizeof(RecGeom) == 128, "record geometry is one 128-byte line");
 struct __align__(16) RecMeta {
   int16_t x0, x1, y0, y1;  // clamped pixel bbox (rasterizer.py:141-146)
   int32_t t;               // triangle index
-  uint32_t flags;          // bits 0-2 edge accept, 3 reordered, 4 clipped
+  uint32_t flags;          // bits 0-2 edge accept, 3 reordered, 4 clipped, 5-6 uv origin,
+                           // 7 fan sub-triangle, 16-31 subdivision steps
 };
 static_assert(sizeof(RecMeta) == 16, "record meta is 16 bytes");
 
@@ -58,11 +59,12 @@ struct Work {
   RecGeom *geom;
   RecMeta *meta;
   uint32_t *vis;
-  uint32_t *fcnt;       // per frame: [0] visible records
+  uint32_t *fcnt;       // per frame: [0] visible records; fcnt[1] of frame 0: big-tile count
   uint32_t *tile_count; // per frame per tile
   uint32_t *tile_cursor;
   uint64_t *tile_off;
   uint32_t *list;
+  uint32_t *big;  // (frame, tile) codes handed to k_raster_big; count in fcnt[1]
   int64_t rs;   // record slots per frame (2m)
   int64_t cap;  // list capacity per frame
 };
@@ -86,6 +88,7 @@ bool carve(void *ws, size_t ws_bytes, int64_t m, int nframes, int ntiles, int64_
   size_t o_cur = take(sizeof(uint32_t) * ntiles * nframes);
   size_t o_off = take(sizeof(uint64_t) * ntiles * nframes);
   size_t o_list = take(sizeof(uint32_t) * cap * nframes);
+  size_t o_big = take(sizeof(uint32_t) * ntiles * nframes);
   if (need_out) *need_out = off;
   if (!ws || ws_bytes < off) return false;
   char *b = static_cast<char *>(ws);
@@ -97,6 +100,7 @@ bool carve(void *ws, size_t ws_bytes, int64_t m, int nframes, int ntiles, int64_
   w.tile_cursor = reinterpret_cast<uint32_t *>(b + o_cur);
   w.tile_off = reinterpret_cast<uint64_t *>(b + o_off);
   w.list = reinterpret_cast<uint32_t *>(b + o_list);
+  w.big = reinterpret_cast<uint32_t *>(b + o_big);
   w.rs = rs;
   w.cap = cap;
   return true;
@@ -170,8 +174,8 @@ __device__ __forceinline__ bool boundary_accept(double ax, double ay, double bx,
 
 // rasterizer.py:136-164 up to the per-pixel loop.  Returns false when the
 // reference would return early (empty bbox, zero or non-finite area).
-__device__ bool build_record(const Cam &cam, int W, int H, const double P[3][3], int t, bool clipped,
-                             RecGeom &g, RecMeta &mt) {
+__device__ bool build_record(const Cam &cam, int W, int H, const double P[3][3], int t, bool clipped, int sub,
+                             uint32_t tflags, RecGeom &g, RecMeta &mt) {
   double xs0[3], ys0[3], zs0[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -195,7 +199,7 @@ __device__ bool build_record(const Cam &cam, int W, int H, const double P[3][3],
   g.ys[0] = ys0[0]; g.ys[1] = ys0[o1]; g.ys[2] = ys0[o2];
   g.zs[0] = zs0[0]; g.zs[1] = zs0[o1]; g.zs[2] = zs0[o2];
   g.area2 = fabs(area2);
-  uint32_t flags = (re ? 8u : 0u) | (clipped ? 16u : 0u);
+  uint32_t flags = tflags | (re ? 8u : 0u) | (clipped ? 16u : 0u) | ((uint32_t)sub << 7);
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     const int a = (k + 1) % 3, b = (k + 2) % 3;
@@ -240,11 +244,29 @@ __global__ void __launch_bounds__(kThreads) k_setup(tfb_scene sc, const double *
     tri_cam(sc, cam, t, P);
     const double zmax = fmax(fmax(P[0][2], P[1][2]), P[2][2]);
     const double zmin = fmin(fmin(P[0][2], P[1][2]), P[2][2]);
-    if (!(zmax < kNearPlane)) {  // rasterizer.py:111
+    bool live = !(zmax < kNearPlane);  // rasterizer.py:111
+    if (live && zmin >= kNearPlane) {
+      // Conservative frustum cull without divisions: a triangle whose vertices
+      // all project more than 1/4 pixel beyond one image edge has an empty
+      // bbox in the reference (rasterizer.py:141-146); the 1/4 px margin dwarfs
+      // the rounding of these products, so no visible triangle is dropped.
+      bool l = true, r = true, u = true, d = true;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double z = P[k][2];
+        l = l && (P[k][0] * cam.fx + (cam.cx - 0.25) * z < 0.0);
+        r = r && (P[k][0] * cam.fx + (cam.cx - ((double)W - 0.25)) * z > 0.0);
+        u = u && (P[k][1] * cam.fy + (cam.cy - 0.25) * z < 0.0);
+        d = d && (P[k][1] * cam.fy + (cam.cy - ((double)H - 0.25)) * z > 0.0);
+      }
+      live = !(l || r || u || d);
+    }
+    if (live) {
       RecGeom g;
       RecMeta mt;
+      const uint32_t tflags = ((uint32_t)__ldg(sc.origins + t) << 5) | ((uint32_t)__ldg(sc.steps + t) << 16);
       if (zmin >= kNearPlane) {
-        if (build_record(cam, W, H, P, (int)t, false, g, mt)) {
+        if (build_record(cam, W, H, P, (int)t, false, 0, tflags, g, mt)) {
           store_record(w, f, 2 * t, g, mt, ntiles, TX);
           mask = 1;
         }
@@ -259,7 +281,7 @@ __global__ void __launch_bounds__(kThreads) k_setup(tfb_scene sc, const double *
             S[1][q] = op[k][q];
             S[2][q] = op[k + 1][q];
           }
-          if (build_record(cam, W, H, S, (int)t, true, g, mt)) {
+          if (build_record(cam, W, H, S, (int)t, true, k - 1, tflags, g, mt)) {
             store_record(w, f, 2 * t + (k - 1), g, mt, ntiles, TX);
             mask |= 1u << (k - 1);
           }
@@ -378,139 +400,49 @@ __device__ __forceinline__ bool edges_at(const RecGeom &g, uint32_t flags, doubl
 __device__ __forceinline__ double np_max(double a, double b) { return isnan(a) ? a : (a > b ? a : b); }
 __device__ __forceinline__ double np_min(double a, double b) { return isnan(a) ? a : (a < b ? a : b); }
 
-__global__ void __launch_bounds__(kThreads, 2) k_raster(tfb_scene sc, const double *__restrict__ cams, int W,
-                                                        int H, int TX, int ntiles, Work w, Outs o) {
-  const int f = blockIdx.y;
-  const int tile = blockIdx.x;
-  const int tx = tile % TX, ty = tile / TX;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
-  const int px_i = wx0 + (lane & 7), py_i = wy0 + (lane >> 3);
-  const bool in_img = px_i < W && py_i < H;
-  const double px = (double)px_i + 0.5, py = (double)py_i + 0.5;
-
-  __shared__ RecGeom sgeom[kThreads];
-  __shared__ RecMeta smeta[kThreads];
-  __shared__ uint32_t skey[kThreads];
-  __shared__ Cam cam;
-  load_cam(cam, cams, f);
-
-  const uint32_t tcount = w.tile_count[(int64_t)f * ntiles + tile];
-  const uint64_t toff = w.tile_off[(int64_t)f * ntiles + tile];
-  const bool ovf = toff + tcount > (uint64_t)w.cap;
-  const uint32_t *src = ovf ? w.vis + (int64_t)f * w.rs : w.list + (int64_t)f * w.cap + toff;
-  const uint32_t nsrc = ovf ? w.fcnt[4 * f] : tcount;
-  const bool single = nsrc <= (uint32_t)kThreads;
-  const RecGeom *geom = w.geom + (int64_t)f * w.rs;
-  const RecMeta *meta = w.meta + (int64_t)f * w.rs;
-
-  double depth = __longlong_as_double(0x7ff0000000000000LL);  // +inf
-  uint32_t win = kNoKey;
-  double ww0 = 0.0, ww1 = 0.0, ww2 = 0.0;
-  uint32_t lo = 0;          // next key to consider
-  bool need = in_img;       // this pixel still has unfolded candidates
-
-  for (;;) {
-    uint32_t ck[kCand], cs[kCand];
-#pragma unroll
-    for (int i = 0; i < kCand; ++i) {
-      ck[i] = kNoKey;
-      cs[i] = 0;
-    }
-    uint32_t ncand = 0;
-    for (uint32_t b0 = 0; b0 < nsrc; b0 += kThreads) {
-      const uint32_t n = min((uint32_t)kThreads, nsrc - b0);
-      __syncthreads();
-      if (threadIdx.x < n) {
-        const uint32_t r = src[b0 + threadIdx.x];
-        skey[threadIdx.x] = r;
-        smeta[threadIdx.x] = meta[r];
-        const double2 *gs = reinterpret_cast<const double2 *>(geom + r);
-        double2 *gd = reinterpret_cast<double2 *>(sgeom + threadIdx.x);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) gd[q] = gs[q];
-      }
-      __syncthreads();
-      for (uint32_t j0 = 0; j0 < n; j0 += 32) {
-        const uint32_t j = j0 + lane;
-        bool rel = false;
-        if (j < n) {
-          const RecMeta mt = smeta[j];
-          rel = mt.x0 <= wx0 + 7 && mt.x1 >= wx0 && mt.y0 <= wy0 + 3 && mt.y1 >= wy0;
-        }
-        uint32_t m = __ballot_sync(0xffffffffu, rel);
-        if (!__any_sync(0xffffffffu, need)) m = 0;
-        while (m) {
-          const uint32_t jj = j0 + __ffs(m) - 1;
-          m &= m - 1;
-          const RecMeta mt = smeta[jj];
-          if (need && px_i >= mt.x0 && px_i <= mt.x1 && py_i >= mt.y0 && py_i <= mt.y1) {
-            const uint32_t key = skey[jj];
-            if (key >= lo) {
-              double e[3];
-              if (edges_at(sgeom[jj], mt.flags, px, py, e)) {
-                ++ncand;
-                uint32_t k = key, s = jj;
-#pragma unroll
-                for (int i = 0; i < kCand; ++i) {
-                  if (k < ck[i]) {
-                    const uint32_t tk = ck[i], ts = cs[i];
-                    ck[i] = k;
-                    cs[i] = s;
-                    k = tk;
-                    s = ts;
-                  }
-                }
-              }
-            }
-          }
-        }
-      }
-    }
-    // ascending sequential fold over this pass's candidates (rasterizer.py:108, 170-171)
-    const uint32_t nf = min(ncand, (uint32_t)kCand);
-#pragma unroll
-    for (int i = 0; i < kCand; ++i) {
-      if ((uint32_t)i < nf) {
-        const RecGeom &g = single ? sgeom[cs[i]] : geom[ck[i]];
-        const uint32_t flags = single ? smeta[cs[i]].flags : meta[ck[i]].flags;
-        double e[3];
-        edges_at(g, flags, px, py, e);
-        const double w0 = __ddiv_rn(e[0], g.zs[0]), w1 = __ddiv_rn(e[1], g.zs[1]), w2 = __ddiv_rn(e[2], g.zs[2]);
-        const double z = __ddiv_rn(g.area2, __dadd_rn(__dadd_rn(w0, w1), w2));
-        if (z > 0.0 && z < __dsub_rn(depth, kDepthTie)) {
-          depth = z;
-          win = ck[i];
-          ww0 = w0;
-          ww1 = w1;
-          ww2 = w2;
-        }
-      }
-    }
-    const bool more = need && ncand > (uint32_t)kCand;
-    if (more) lo = ck[kCand - 1] + 1;
-    need = more;
-    if (!__syncthreads_or(more)) break;
+// Sequential-fold step for one covering record (rasterizer.py:170-171): the
+// reference's exact `z > 0 && z < depth - 1e-9` in float64.
+struct Fold {
+  double depth, w0, w1, w2;
+  int32_t win;  // record slot (smem index or global key), -1 = none
+  __device__ __forceinline__ void init() {
+    depth = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    w0 = w1 = w2 = 0.0;
+    win = -1;
   }
+  __device__ __forceinline__ void step(const RecGeom &g, uint32_t flags, double px, double py, int32_t id) {
+    double e[3];
+    edges_at(g, flags, px, py, e);
+    const double a = __ddiv_rn(e[0], g.zs[0]), b = __ddiv_rn(e[1], g.zs[1]), c = __ddiv_rn(e[2], g.zs[2]);
+    const double z = __ddiv_rn(g.area2, __dadd_rn(__dadd_rn(a, b), c));
+    if (z > 0.0 && z < __dsub_rn(depth, kDepthTie)) {
+      depth = z;
+      win = id;
+      w0 = a;
+      w1 = b;
+      w2 = c;
+    }
+  }
+};
 
-  if (!in_img) return;
+// Winner epilogue, rasterizer.py:177-202: perspective-correct barycentrics of
+// the original triangle → (u, v) → texel id → global row; optional planes.
+__device__ __forceinline__ void write_pixel(const tfb_scene &sc, const Cam &cam, const Outs &o, int f, int W, int H,
+                                            int px_i, int py_i, const Fold &fd, uint32_t flags, int32_t t) {
   const int64_t pix = (int64_t)f * W * H + (int64_t)py_i * W + px_i;
   int32_t row = -1;
-  if (win != kNoKey) {
-    const int64_t t = win >> 1;
-    const int sub = (int)(win & 1u);
-    const uint32_t flags = meta[win].flags;
-    // barycentric rows of the (sub)triangle vertices in the original triangle
+  if (fd.win >= 0) {
+    const int sub = (flags >> 7) & 1u;
     double B[3][3];
-    if (flags & 16u) {
+    if (flags & 16u) {  // clipped: barycentric rows of the fan vertices (rasterizer.py:62-82, 119-122)
       double P[3][3], op[4][3], ob[4][3];
       tri_cam(sc, cam, t, P);
       clip_near(P, op, ob);
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         B[0][q] = ob[0][q];
-        B[1][q] = ob[sub + 1][q];
-        B[2][q] = ob[sub + 2][q];
+        B[1][q] = sub ? ob[2][q] : ob[1][q];
+        B[2][q] = sub ? ob[3][q] : ob[2][q];
       }
     } else {
 #pragma unroll
@@ -526,23 +458,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster(tfb_scene sc, const doub
         B[2][q] = tmp;
       }
     }
-    // rasterizer.py:177-188
-    const double wsum = __dadd_rn(__dadd_rn(ww0, ww1), ww2);
+    const double wsum = __dadd_rn(__dadd_rn(fd.w0, fd.w1), fd.w2);
     double b[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      b[k] = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(ww0, B[0][k]), __dmul_rn(ww1, B[1][k])), __dmul_rn(ww2, B[2][k])),
+      b[k] = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(fd.w0, B[0][k]), __dmul_rn(fd.w1, B[1][k])),
+                                 __dmul_rn(fd.w2, B[2][k])),
                        wsum);
       if (b[k] < 0.0) b[k] = 0.0;
     }
     const double bs = __dadd_rn(__dadd_rn(b[0], b[1]), b[2]);
 #pragma unroll
     for (int k = 0; k < 3; ++k) b[k] = __ddiv_rn(b[k], bs);
-    // rasterizer.py:190-196
-    const int origin = __ldg(sc.origins + t);
-    const int s = __ldg(sc.steps + t);
-    double u = __dsub_rn(1.0, b[origin]);
-    double v = b[(origin + 2) % 3];
+    const int origin = (flags >> 5) & 3u;
+    const int s = (int)(flags >> 16);
+    const double bo = origin == 0 ? b[0] : (origin == 1 ? b[1] : b[2]);
+    const double bv = origin == 0 ? b[2] : (origin == 1 ? b[0] : b[1]);
+    double u = __dsub_rn(1.0, bo);
+    double v = bv;
     u = np_min(np_max(u, 0.0), 1.0);
     v = np_min(np_max(v, 0.0), u);
     long long i = (long long)__dmul_rn((double)s, u);
@@ -551,15 +484,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster(tfb_scene sc, const doub
     if (j > i) j = i;
     const int32_t texel = (int32_t)((i * i + i) / 2 + j);
     row = (int32_t)(__ldg(sc.offsets + t) + texel);
-    if (o.tri) o.tri[pix] = (int32_t)t;
+    if (o.tri) o.tri[pix] = t;
     if (o.texel) o.texel[pix] = texel;
-    if (o.depth) o.depth[pix] = depth;
+    if (o.depth) o.depth[pix] = fd.depth;
     if (o.u) o.u[pix] = u;
     if (o.v) o.v[pix] = v;
   } else {
     if (o.tri) o.tri[pix] = -1;
     if (o.texel) o.texel[pix] = 0;
-    if (o.depth) o.depth[pix] = depth;
+    if (o.depth) o.depth[pix] = fd.depth;
     if (o.u) o.u[pix] = 0.0;
     if (o.v) o.v[pix] = 0.0;
   }
@@ -568,13 +501,193 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster(tfb_scene sc, const doub
     // warp-aggregated per-frame texel hit count (fusion.py:135-136)
     const unsigned act = __activemask();
     const unsigned peers = __match_any_sync(act, row);
-    if ((int)(__ffs(peers) - 1) == lane)
+    if ((int)(__ffs(peers) - 1) == (int)(threadIdx.x & 31))
       atomicAdd(o.hits + (int64_t)f * sc.total_texels + row, (uint32_t)__popc(peers));
+  }
+}
+
+// One CTA per 16x16 tile with at most kThreads records.  The tile's record
+// list arrives unordered from k_fill; a rank sort in shared memory restores
+// ascending (triangle, fan) order, so each pixel can fold its covering
+// records in exactly the reference's order while streaming through them,
+// with the float64 divisions deferred to one pending record.  Larger or
+// overflowed tiles are handed to k_raster_big.
+__global__ void __launch_bounds__(kThreads, 3) k_raster(tfb_scene sc, const double *__restrict__ cams, int W, int H,
+                                                        int TX, int ntiles, Work w, Outs o) {
+  const int f = blockIdx.y;
+  const int tile = blockIdx.x;
+  const int tx = tile % TX, ty = tile / TX;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
+  const int px_i = wx0 + (lane & 7), py_i = wy0 + (lane >> 3);
+  const bool in_img = px_i < W && py_i < H;
+  const double px = (double)px_i + 0.5, py = (double)py_i + 0.5;
+
+  const uint32_t n = w.tile_count[(int64_t)f * ntiles + tile];
+  const uint64_t toff = w.tile_off[(int64_t)f * ntiles + tile];
+  if (toff + n > (uint64_t)w.cap || n > (uint32_t)kThreads) {
+    if (threadIdx.x == 0) w.big[atomicAdd(w.fcnt + 1, 1u)] = (uint32_t)(f * ntiles + tile);
+    return;
+  }
+  __shared__ RecGeom sgeom[kThreads];
+  __shared__ RecMeta smeta[kThreads];
+  __shared__ uint32_t skey[kThreads];
+  __shared__ Cam cam;
+  load_cam(cam, cams, f);
+  const uint32_t *src = w.list + (int64_t)f * w.cap + toff;
+  if (threadIdx.x < n) skey[threadIdx.x] = src[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < n) {
+    const uint32_t key = skey[threadIdx.x];
+    uint32_t rank = 0;
+    for (uint32_t j = 0; j < n; ++j) rank += skey[j] < key ? 1u : 0u;
+    const int64_t r = (int64_t)f * w.rs + key;
+    smeta[rank] = w.meta[r];
+    const double2 *gs = reinterpret_cast<const double2 *>(w.geom + r);
+    double2 *gd = reinterpret_cast<double2 *>(sgeom + rank);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) gd[q] = gs[q];
+  }
+  __syncthreads();
+
+  Fold fd;
+  fd.init();
+  int32_t pend = -1;
+  for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+    const uint32_t j = j0 + lane;
+    bool rel = false;
+    if (j < n) {
+      const RecMeta mt = smeta[j];
+      rel = mt.x0 <= wx0 + 7 && mt.x1 >= wx0 && mt.y0 <= wy0 + 3 && mt.y1 >= wy0;
+    }
+    uint32_t m = __ballot_sync(0xffffffffu, rel);
+    while (m) {
+      const int jj = (int)j0 + __ffs(m) - 1;
+      m &= m - 1;
+      const RecMeta mt = smeta[jj];
+      if (in_img && px_i >= mt.x0 && px_i <= mt.x1 && py_i >= mt.y0 && py_i <= mt.y1) {
+        double e[3];
+        if (edges_at(sgeom[jj], mt.flags, px, py, e)) {
+          if (pend >= 0) fd.step(sgeom[pend], smeta[pend].flags, px, py, pend);
+          pend = jj;
+        }
+      }
+    }
+  }
+  if (pend >= 0) fd.step(sgeom[pend], smeta[pend].flags, px, py, pend);
+  if (!in_img) return;
+  const uint32_t flags = fd.win >= 0 ? smeta[fd.win].flags : 0u;
+  const int32_t t = fd.win >= 0 ? smeta[fd.win].t : -1;
+  write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t);
+}
+
+// Tiles with more than kThreads records, or whose list overflowed the pair
+// budget (then every visible record of the frame is scanned and filtered by
+// bbox).  Records stream through shared memory in chunks in arbitrary order;
+// each pixel keeps the kCand smallest covering keys above `lo`, folds them in
+// ascending order and repeats with `lo` past the last folded key until no
+// covering record is left — the same sequential fold, in any list order.
+__global__ void __launch_bounds__(kThreads, 2) k_raster_big(tfb_scene sc, const double *__restrict__ cams, int W,
+                                                            int H, int TX, int ntiles, Work w, Outs o) {
+  __shared__ RecGeom sgeom[kThreads];
+  __shared__ RecMeta smeta[kThreads];
+  __shared__ uint32_t skey[kThreads];
+  __shared__ Cam cam;
+  const uint32_t nbig = w.fcnt[1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+    const uint32_t code = w.big[bi];
+    const int f = (int)(code / ntiles), tile = (int)(code % ntiles);
+    const int tx = tile % TX, ty = tile / TX;
+    const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
+    const int px_i = wx0 + (lane & 7), py_i = wy0 + (lane >> 3);
+    const bool in_img = px_i < W && py_i < H;
+    const double px = (double)px_i + 0.5, py = (double)py_i + 0.5;
+    __syncthreads();
+    load_cam(cam, cams, f);
+    const uint32_t tcount = w.tile_count[(int64_t)f * ntiles + tile];
+    const uint64_t toff = w.tile_off[(int64_t)f * ntiles + tile];
+    const bool ovf = toff + tcount > (uint64_t)w.cap;
+    const uint32_t *src = ovf ? w.vis + (int64_t)f * w.rs : w.list + (int64_t)f * w.cap + toff;
+    const uint32_t nsrc = ovf ? w.fcnt[4 * f] : tcount;
+    const RecGeom *geom = w.geom + (int64_t)f * w.rs;
+    const RecMeta *meta = w.meta + (int64_t)f * w.rs;
+
+    Fold fd;
+    fd.init();
+    uint32_t lo = 0;     // next key to consider
+    bool need = in_img;  // this pixel still has unfolded candidates
+    for (;;) {
+      uint32_t ck[kCand];
+#pragma unroll
+      for (int i = 0; i < kCand; ++i) ck[i] = kNoKey;
+      uint32_t ncand = 0;
+      for (uint32_t b0 = 0; b0 < nsrc; b0 += kThreads) {
+        const uint32_t n = min((uint32_t)kThreads, nsrc - b0);
+        __syncthreads();
+        if (threadIdx.x < n) {
+          const uint32_t r = src[b0 + threadIdx.x];
+          skey[threadIdx.x] = r;
+          smeta[threadIdx.x] = meta[r];
+          const double2 *gs = reinterpret_cast<const double2 *>(geom + r);
+          double2 *gd = reinterpret_cast<double2 *>(sgeom + threadIdx.x);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) gd[q] = gs[q];
+        }
+        __syncthreads();
+        for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+          const uint32_t j = j0 + lane;
+          bool rel = false;
+          if (j < n) {
+            const RecMeta mt = smeta[j];
+            rel = mt.x0 <= wx0 + 7 && mt.x1 >= wx0 && mt.y0 <= wy0 + 3 && mt.y1 >= wy0;
+          }
+          uint32_t m = __ballot_sync(0xffffffffu, rel);
+          if (!__any_sync(0xffffffffu, need)) m = 0;
+          while (m) {
+            const uint32_t jj = j0 + __ffs(m) - 1;
+            m &= m - 1;
+            const RecMeta mt = smeta[jj];
+            if (need && px_i >= mt.x0 && px_i <= mt.x1 && py_i >= mt.y0 && py_i <= mt.y1) {
+              const uint32_t key = skey[jj];
+              double e[3];
+              if (key >= lo && edges_at(sgeom[jj], mt.flags, px, py, e)) {
+                ++ncand;
+                uint32_t k = key;
+#pragma unroll
+                for (int i = 0; i < kCand; ++i) {
+                  if (k < ck[i]) {
+                    const uint32_t tk = ck[i];
+                    ck[i] = k;
+                    k = tk;
+                  }
+                }
+              }
+            }
+          }
+        }
+      }
+      const uint32_t nf = min(ncand, (uint32_t)kCand);
+      for (uint32_t i = 0; i < nf; ++i) {
+        const uint32_t key = ck[i];
+        fd.step(geom[key], meta[key].flags, px, py, (int32_t)key);
+      }
+      const bool more = need && ncand > (uint32_t)kCand;
+      if (more) lo = ck[kCand - 1] + 1;
+      need = more;
+      if (!__syncthreads_or(more)) break;
+    }
+    if (in_img) {
+      const uint32_t flags = fd.win >= 0 ? meta[fd.win].flags : 0u;
+      const int32_t t = fd.win >= 0 ? meta[fd.win].t : -1;
+      write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t);
+    }
   }
 }
 
 }  // namespace
 }  // namespace tfb
+
 
 using namespace tfb;
 
@@ -627,5 +740,6 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
   }
   Outs o{rows_out, texel_hits, tri_out, texel_out, depth_out, u_out, v_out};
   k_raster<<<dim3(ntiles, nframes), kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
+  k_raster_big<<<148, kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
   return check_launch("tfb_rasterize");
 }
