@@ -58,8 +58,8 @@ struct Cam {
 struct Work {
   RecGeom *geom;
   RecMeta *meta;
-  uint32_t *vis;
-  uint32_t *fcnt;       // per frame: [0] visible records; fcnt[1] of frame 0: big-tile count
+  uint8_t *vmask;       // per frame per triangle: bit k = fan sub-triangle k has a record
+  uint32_t *fcnt;       // fcnt[1]: big-tile count
   uint32_t *tile_count; // per frame per tile
   uint32_t *tile_cursor;
   uint64_t *tile_off;
@@ -82,7 +82,7 @@ bool carve(void *ws, size_t ws_bytes, int64_t m, int nframes, int ntiles, int64_
   };
   size_t o_geom = take(sizeof(RecGeom) * rs * nframes);
   size_t o_meta = take(sizeof(RecMeta) * rs * nframes);
-  size_t o_vis = take(sizeof(uint32_t) * rs * nframes);
+  size_t o_vis = take((size_t)(rs / 2) * nframes);
   size_t o_fcnt = take(sizeof(uint32_t) * 4 * nframes);
   size_t o_tc = take(sizeof(uint32_t) * ntiles * nframes);
   size_t o_cur = take(sizeof(uint32_t) * ntiles * nframes);
@@ -94,7 +94,7 @@ bool carve(void *ws, size_t ws_bytes, int64_t m, int nframes, int ntiles, int64_
   char *b = static_cast<char *>(ws);
   w.geom = reinterpret_cast<RecGeom *>(b + o_geom);
   w.meta = reinterpret_cast<RecMeta *>(b + o_meta);
-  w.vis = reinterpret_cast<uint32_t *>(b + o_vis);
+  w.vmask = reinterpret_cast<uint8_t *>(b + o_vis);
   w.fcnt = reinterpret_cast<uint32_t *>(b + o_fcnt);
   w.tile_count = reinterpret_cast<uint32_t *>(b + o_tc);
   w.tile_cursor = reinterpret_cast<uint32_t *>(b + o_cur);
@@ -233,8 +233,6 @@ __global__ void __launch_bounds__(kThreads) k_setup(tfb_scene sc, const double *
                                                     int H, int TX, int ntiles, Work w) {
   const int f = blockIdx.y;
   __shared__ Cam cam;
-  __shared__ uint32_t warp_tot[kThreads / 32];
-  __shared__ uint32_t base;
   load_cam(cam, cams, f);
   __syncthreads();
   const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
@@ -289,31 +287,7 @@ __global__ void __launch_bounds__(kThreads) k_setup(tfb_scene sc, const double *
       }
     }
   }
-  // block-aggregated append of visible record ids (one global atomic per block)
-  const uint32_t nrec = __popc(mask);
-  uint32_t incl = nrec;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += v;
-  }
-  if (lane == 31) warp_tot[warp] = incl;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t s = 0;
-    for (int i = 0; i < kThreads / 32; ++i) {
-      const uint32_t v = warp_tot[i];
-      warp_tot[i] = s;
-      s += v;
-    }
-    base = s ? atomicAdd(w.fcnt + 4 * f, s) : 0;
-  }
-  __syncthreads();
-  uint32_t pos = base + warp_tot[warp] + incl - nrec;
-  uint32_t *vis = w.vis + (int64_t)f * w.rs;
-  if (mask & 1u) vis[pos++] = (uint32_t)(2 * t);
-  if (mask & 2u) vis[pos++] = (uint32_t)(2 * t + 1);
+  if (t < sc.num_triangles) w.vmask[(int64_t)f * (w.rs / 2) + t] = (uint8_t)mask;
 }
 
 __global__ void __launch_bounds__(1024) k_scan(Work w, int ntiles) {
@@ -355,23 +329,26 @@ __global__ void __launch_bounds__(1024) k_scan(Work w, int ntiles) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_fill(Work w, int ntiles, int TX) {
+__global__ void __launch_bounds__(256) k_fill(Work w, int64_t m, int ntiles, int TX) {
   const int f = blockIdx.y;
-  const uint32_t nvis = w.fcnt[4 * f];
-  const uint32_t *vis = w.vis + (int64_t)f * w.rs;
+  const uint8_t *vm = w.vmask + (int64_t)f * m;
   const RecMeta *meta = w.meta + (int64_t)f * w.rs;
   const uint64_t *toff = w.tile_off + (int64_t)f * ntiles;
   uint32_t *cur = w.tile_cursor + (int64_t)f * ntiles;
   uint32_t *list = w.list + (int64_t)f * w.cap;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nvis; i += gridDim.x * blockDim.x) {
-    const uint32_t r = vis[i];
-    const RecMeta mt = meta[r];
-    for (int ty = mt.y0 / kTile; ty <= mt.y1 / kTile; ++ty)
-      for (int tx = mt.x0 / kTile; tx <= mt.x1 / kTile; ++tx) {
-        const int tile = ty * TX + tx;
-        const uint64_t pos = toff[tile] + atomicAdd(cur + tile, 1u);
-        if (pos < (uint64_t)w.cap) list[pos] = r;
-      }
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t mask = vm[t];
+    for (int sub = 0; sub < 2; ++sub) {
+      if (!((mask >> sub) & 1u)) continue;
+      const uint32_t r = (uint32_t)(2 * t + sub);
+      const RecMeta mt = meta[r];
+      for (int ty = mt.y0 / kTile; ty <= mt.y1 / kTile; ++ty)
+        for (int tx = mt.x0 / kTile; tx <= mt.x1 / kTile; ++tx) {
+          const int tile = ty * TX + tx;
+          const uint64_t pos = toff[tile] + atomicAdd(cur + tile, 1u);
+          if (pos < (uint64_t)w.cap) list[pos] = r;
+        }
+    }
   }
 }
 
@@ -506,87 +483,157 @@ __device__ __forceinline__ void write_pixel(const tfb_scene &sc, const Cam &cam,
   }
 }
 
-// One CTA per 16x16 tile with at most kThreads records.  The tile's record
-// list arrives unordered from k_fill; a rank sort in shared memory restores
-// ascending (triangle, fan) order, so each pixel can fold its covering
-// records in exactly the reference's order while streaming through them,
-// with the float64 divisions deferred to one pending record.  Larger or
-// overflowed tiles are handed to k_raster_big.
-__global__ void __launch_bounds__(kThreads, 3) k_raster(tfb_scene sc, const double *__restrict__ cams, int W, int H,
+// One CTA per 16x16 tile with at most kThreads records (the common case).
+//  1. The tile's record ids (unordered from k_fill) are rank-sorted in shared
+//     memory, restoring the reference's ascending (triangle, fan) order, and
+//     the 128-byte records are staged in that order.
+//  2. Pair-parallel edge tests: every (record, pixel of its bbox in the tile)
+//     pair gets its own thread (prefix sum of bbox areas + one binary search
+//     per thread-run), so float64 lanes are not wasted on pixels outside a
+//     small triangle's bbox.  Covering pairs bump the pixel's candidate count
+//     and atomicMin its first (smallest-key) record.
+//  3. One thread per pixel: a single candidate is folded directly; pixels with
+//     several run the exact ascending sequential fold over the tile's records
+//     (rasterizer.py:108, 170-171), so depth ties resolve as in the reference.
+//  Larger or overflowed tiles are handed to k_raster_big.
+__global__ void __launch_bounds__(kThreads, 2) k_raster(tfb_scene sc, const double *__restrict__ cams, int W, int H,
                                                         int TX, int ntiles, Work w, Outs o) {
   const int f = blockIdx.y;
   const int tile = blockIdx.x;
-  const int tx = tile % TX, ty = tile / TX;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
-  const int px_i = wx0 + (lane & 7), py_i = wy0 + (lane >> 3);
-  const bool in_img = px_i < W && py_i < H;
-  const double px = (double)px_i + 0.5, py = (double)py_i + 0.5;
-
+  const int tx0 = (tile % TX) * kTile, ty0 = (tile / TX) * kTile;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t n = w.tile_count[(int64_t)f * ntiles + tile];
   const uint64_t toff = w.tile_off[(int64_t)f * ntiles + tile];
   if (toff + n > (uint64_t)w.cap || n > (uint32_t)kThreads) {
-    if (threadIdx.x == 0) w.big[atomicAdd(w.fcnt + 1, 1u)] = (uint32_t)(f * ntiles + tile);
+    if (tid == 0) w.big[atomicAdd(w.fcnt + 1, 1u)] = (uint32_t)(f * ntiles + tile);
     return;
   }
   __shared__ RecGeom sgeom[kThreads];
   __shared__ RecMeta smeta[kThreads];
   __shared__ uint32_t skey[kThreads];
+  __shared__ uint32_t sbox[kThreads];  // tile-relative bbox: x0 | y0 << 8 | w << 16 | h << 24
+  __shared__ uint32_t spre[kThreads];  // exclusive prefix of bbox areas
+  __shared__ uint32_t pfirst[kTile * kTile];
+  __shared__ uint32_t pcnt[kTile * kTile];
+  __shared__ uint32_t wtot[kThreads / 32];
   __shared__ Cam cam;
   load_cam(cam, cams, f);
+  pfirst[tid] = 0xffffffffu;
+  pcnt[tid] = 0u;
   const uint32_t *src = w.list + (int64_t)f * w.cap + toff;
-  if (threadIdx.x < n) skey[threadIdx.x] = src[threadIdx.x];
+  if (tid < n) skey[tid] = src[tid];
   __syncthreads();
-  if (threadIdx.x < n) {
-    const uint32_t key = skey[threadIdx.x];
+  if (tid < n) {
+    const uint32_t key = skey[tid];
     uint32_t rank = 0;
     for (uint32_t j = 0; j < n; ++j) rank += skey[j] < key ? 1u : 0u;
     const int64_t r = (int64_t)f * w.rs + key;
-    smeta[rank] = w.meta[r];
+    const RecMeta mt = w.meta[r];
+    smeta[rank] = mt;
     const double2 *gs = reinterpret_cast<const double2 *>(w.geom + r);
     double2 *gd = reinterpret_cast<double2 *>(sgeom + rank);
 #pragma unroll
     for (int q = 0; q < 8; ++q) gd[q] = gs[q];
+    const int bx0 = max((int)mt.x0, tx0) - tx0, bx1 = min((int)mt.x1, tx0 + kTile - 1) - tx0;
+    const int by0 = max((int)mt.y0, ty0) - ty0, by1 = min((int)mt.y1, ty0 + kTile - 1) - ty0;
+    sbox[rank] = (uint32_t)bx0 | ((uint32_t)by0 << 8) | ((uint32_t)(bx1 - bx0 + 1) << 16) |
+                 ((uint32_t)(by1 - by0 + 1) << 24);
   }
   __syncthreads();
+  // exclusive block scan of bbox areas (in sorted order)
+  uint32_t area = 0;
+  if (tid < n) {
+    const uint32_t b = sbox[tid];
+    area = ((b >> 16) & 0xffu) * (b >> 24);
+  }
+  uint32_t incl = area;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  if (lane == 31) wtot[warp] = incl;
+  __syncthreads();
+  uint32_t wbase = 0, total = 0;
+#pragma unroll
+  for (int i = 0; i < kThreads / 32; ++i) {
+    const uint32_t v = wtot[i];
+    wbase += i < warp ? v : 0u;
+    total += v;
+  }
+  spre[tid] = wbase + incl - area;
+  __syncthreads();
 
-  Fold fd;
-  fd.init();
-  int32_t pend = -1;
-  for (uint32_t j0 = 0; j0 < n; j0 += 32) {
-    const uint32_t j = j0 + lane;
-    bool rel = false;
-    if (j < n) {
-      const RecMeta mt = smeta[j];
-      rel = mt.x0 <= wx0 + 7 && mt.x1 >= wx0 && mt.y0 <= wy0 + 3 && mt.y1 >= wy0;
+  // pair-parallel edge tests: thread handles pairs [p0, p1)
+  const uint32_t ppt = (total + kThreads - 1) / kThreads;
+  const uint32_t p0 = tid * ppt, p1 = min(p0 + ppt, total);
+  if (p0 < p1) {
+    int lo = 0, hi = (int)n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (spre[mid] <= p0) lo = mid;
+      else hi = mid - 1;
     }
-    uint32_t m = __ballot_sync(0xffffffffu, rel);
-    while (m) {
-      const int jj = (int)j0 + __ffs(m) - 1;
-      m &= m - 1;
-      const RecMeta mt = smeta[jj];
-      if (in_img && px_i >= mt.x0 && px_i <= mt.x1 && py_i >= mt.y0 && py_i <= mt.y1) {
-        double e[3];
-        if (edges_at(sgeom[jj], mt.flags, px, py, e)) {
-          if (pend >= 0) fd.step(sgeom[pend], smeta[pend].flags, px, py, pend);
-          pend = jj;
+    int j = lo;
+    uint32_t b = sbox[j];
+    int bw = (b >> 16) & 0xff, bh = b >> 24;
+    const int local = (int)(p0 - spre[j]);
+    int ly = local / bw, lx = local - ly * bw;
+    for (uint32_t p = p0; p < p1; ++p) {
+      const int pxl = (int)(b & 0xffu) + lx, pyl = (int)((b >> 8) & 0xffu) + ly;
+      double e[3];
+      if (edges_at(sgeom[j], smeta[j].flags, (double)(tx0 + pxl) + 0.5, (double)(ty0 + pyl) + 0.5, e)) {
+        const int pix = pyl * kTile + pxl;
+        atomicMin(pfirst + pix, (uint32_t)j);
+        atomicAdd(pcnt + pix, 1u);
+      }
+      if (++lx == bw) {
+        lx = 0;
+        if (++ly == bh) {
+          ly = 0;
+          ++j;
+          if (j < (int)n) {
+            b = sbox[j];
+            bw = (b >> 16) & 0xff;
+            bh = b >> 24;
+          }
         }
       }
     }
   }
-  if (pend >= 0) fd.step(sgeom[pend], smeta[pend].flags, px, py, pend);
-  if (!in_img) return;
+  __syncthreads();
+
+  // one thread per pixel: fold its covering records in ascending order
+  const int pxl = tid & (kTile - 1), pyl = tid / kTile;
+  const int px_i = tx0 + pxl, py_i = ty0 + pyl;
+  if (px_i >= W || py_i >= H) return;
+  const double px = (double)px_i + 0.5, py = (double)py_i + 0.5;
+  const uint32_t cnt = pcnt[tid];
+  Fold fd;
+  fd.init();
+  if (cnt == 1u) {
+    const int j = (int)pfirst[tid];
+    fd.step(sgeom[j], smeta[j].flags, px, py, j);
+  } else if (cnt > 1u) {
+    for (int j = (int)pfirst[tid]; j < (int)n; ++j) {
+      const uint32_t b = sbox[j];
+      const int bx = b & 0xff, by = (b >> 8) & 0xff;
+      if (pxl < bx || pxl >= bx + (int)((b >> 16) & 0xff) || pyl < by || pyl >= by + (int)(b >> 24)) continue;
+      double e[3];
+      if (edges_at(sgeom[j], smeta[j].flags, px, py, e)) fd.step(sgeom[j], smeta[j].flags, px, py, j);
+    }
+  }
   const uint32_t flags = fd.win >= 0 ? smeta[fd.win].flags : 0u;
   const int32_t t = fd.win >= 0 ? smeta[fd.win].t : -1;
   write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t);
 }
 
 // Tiles with more than kThreads records, or whose list overflowed the pair
-// budget (then every visible record of the frame is scanned and filtered by
-// bbox).  Records stream through shared memory in chunks in arbitrary order;
-// each pixel keeps the kCand smallest covering keys above `lo`, folds them in
-// ascending order and repeats with `lo` past the last folded key until no
-// covering record is left — the same sequential fold, in any list order.
+// budget (then every record slot of the frame is scanned, invalid slots
+// masked out by vmask).  Records stream through shared memory in chunks in
+// arbitrary order; each pixel keeps the kCand smallest covering keys above
+// `lo`, folds them in ascending order and repeats with `lo` past the last
+// folded key until no covering record is left — the same sequential fold.
 __global__ void __launch_bounds__(kThreads, 2) k_raster_big(tfb_scene sc, const double *__restrict__ cams, int W,
                                                             int H, int TX, int ntiles, Work w, Outs o) {
   __shared__ RecGeom sgeom[kThreads];
@@ -608,8 +655,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster_big(tfb_scene sc, const 
     const uint32_t tcount = w.tile_count[(int64_t)f * ntiles + tile];
     const uint64_t toff = w.tile_off[(int64_t)f * ntiles + tile];
     const bool ovf = toff + tcount > (uint64_t)w.cap;
-    const uint32_t *src = ovf ? w.vis + (int64_t)f * w.rs : w.list + (int64_t)f * w.cap + toff;
-    const uint32_t nsrc = ovf ? w.fcnt[4 * f] : tcount;
+    const uint32_t *list = w.list + (int64_t)f * w.cap + toff;
+    const uint8_t *vm = w.vmask + (int64_t)f * (w.rs / 2);
+    const uint32_t nsrc = ovf ? (uint32_t)w.rs : tcount;
     const RecGeom *geom = w.geom + (int64_t)f * w.rs;
     const RecMeta *meta = w.meta + (int64_t)f * w.rs;
 
@@ -626,13 +674,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster_big(tfb_scene sc, const 
         const uint32_t n = min((uint32_t)kThreads, nsrc - b0);
         __syncthreads();
         if (threadIdx.x < n) {
-          const uint32_t r = src[b0 + threadIdx.x];
+          const uint32_t i = b0 + threadIdx.x;
+          const uint32_t r = ovf ? i : list[i];
           skey[threadIdx.x] = r;
-          smeta[threadIdx.x] = meta[r];
-          const double2 *gs = reinterpret_cast<const double2 *>(geom + r);
-          double2 *gd = reinterpret_cast<double2 *>(sgeom + threadIdx.x);
+          if (!ovf || ((vm[r >> 1] >> (r & 1u)) & 1u)) {
+            smeta[threadIdx.x] = meta[r];
+            const double2 *gs = reinterpret_cast<const double2 *>(geom + r);
+            double2 *gd = reinterpret_cast<double2 *>(sgeom + threadIdx.x);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) gd[q] = gs[q];
+            for (int q = 0; q < 8; ++q) gd[q] = gs[q];
+          } else {
+            RecMeta empty;
+            empty.x0 = 1;
+            empty.x1 = 0;
+            empty.y0 = 1;
+            empty.y1 = 0;
+            empty.t = -1;
+            empty.flags = 0;
+            smeta[threadIdx.x] = empty;
+          }
         }
         __syncthreads();
         for (uint32_t j0 = 0; j0 < n; j0 += 32) {
@@ -689,6 +749,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster_big(tfb_scene sc, const 
 }  // namespace tfb
 
 
+
 using namespace tfb;
 
 extern "C" size_t tfb_raster_workspace_bytes(int64_t num_triangles, int width, int height, int max_frames,
@@ -734,9 +795,9 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
     dim3 g1((unsigned)((m + kThreads - 1) / kThreads), nframes);
     k_setup<<<g1, kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w);
     k_scan<<<nframes, 1024, 0, st>>>(w, ntiles);
-    int64_t fb = (2 * m + 255) / 256;
+    int64_t fb = (m + 255) / 256;
     const int fill_blocks = (int)(fb < 1184 ? fb : 1184);
-    k_fill<<<dim3(fill_blocks, nframes), 256, 0, st>>>(w, ntiles, TX);
+    k_fill<<<dim3(fill_blocks, nframes), 256, 0, st>>>(w, m, ntiles, TX);
   }
   Outs o{rows_out, texel_hits, tri_out, texel_out, depth_out, u_out, v_out};
   k_raster<<<dim3(ntiles, nframes), kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
