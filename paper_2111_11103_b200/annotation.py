@@ -146,8 +146,11 @@ class MeshAnnotation:
                 e2 = self._event()
                 prof.append((b, e0, e1, e2))
             if needs_hits:
-                N.call("tfb_clear_hits", N.ptr(rows), hw, b, tex.total_texels, N.ptr(hits),
-                       N.stream_handle(stream))
+                if tex.total_texels <= 4 * hw:  # a dense memset is cheaper than the scattered reset
+                    hits.zero_()
+                else:
+                    N.call("tfb_clear_hits", N.ptr(rows), hw, b, tex.total_texels, N.ptr(hits),
+                           N.stream_handle(stream))
             del keep
         tex._h_accum = tex._h_counts = None
         self.frames_added += B

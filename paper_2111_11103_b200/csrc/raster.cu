@@ -229,7 +229,7 @@ __device__ __forceinline__ void store_record(const Work &w, int f, int64_t slot,
     for (int tx = mt.x0 / kTile; tx <= mt.x1 / kTile; ++tx) atomicAdd(tc + ty * TX + tx, 1u);
 }
 
-__global__ void __launch_bounds__(kThreads) k_setup(tfb_scene sc, const double *__restrict__ cams, int W,
+__global__ void __launch_bounds__(kThreads, 4) k_setup(tfb_scene sc, const double *__restrict__ cams, int W,
                                                     int H, int TX, int ntiles, Work w) {
   const int f = blockIdx.y;
   __shared__ Cam cam;
@@ -390,6 +390,9 @@ struct Fold {
   __device__ __forceinline__ void step(const RecGeom &g, uint32_t flags, double px, double py, int32_t id) {
     double e[3];
     edges_at(g, flags, px, py, e);
+    step_e(g, e, id);
+  }
+  __device__ __forceinline__ void step_e(const RecGeom &g, const double e[3], int32_t id) {
     const double a = __ddiv_rn(e[0], g.zs[0]), b = __ddiv_rn(e[1], g.zs[1]), c = __ddiv_rn(e[2], g.zs[2]);
     const double z = __ddiv_rn(g.area2, __dadd_rn(__dadd_rn(a, b), c));
     if (z > 0.0 && z < __dsub_rn(depth, kDepthTie)) {
@@ -404,74 +407,90 @@ struct Fold {
 
 // Winner epilogue, rasterizer.py:177-202: perspective-correct barycentrics of
 // the original triangle → (u, v) → texel id → global row; optional planes.
+// For an unclipped triangle the barycentric rows are a permutation of the
+// identity, so (w0*B0k + w1*B1k) + w2*B2k is exactly w_perm(k) (x*1 = x,
+// x*0 = 0, x + 0 = x for the finite w's of a covering record) and the
+// products are skipped; of the final normalization b /= b.sum() only the two
+// components (u, v) read are divided.
 __device__ __forceinline__ void write_pixel(const tfb_scene &sc, const Cam &cam, const Outs &o, int f, int W, int H,
                                             int px_i, int py_i, const Fold &fd, uint32_t flags, int32_t t) {
-  const int64_t pix = (int64_t)f * W * H + (int64_t)py_i * W + px_i;
+  const int64_t pix = (int64_t)f * W * H + (int64_t)(py_i * W + px_i);
   int32_t row = -1;
   if (fd.win >= 0) {
-    const int sub = (flags >> 7) & 1u;
-    double B[3][3];
+    const double wsum = __dadd_rn(__dadd_rn(fd.w0, fd.w1), fd.w2);
+    double b0, b1, b2;
     if (flags & 16u) {  // clipped: barycentric rows of the fan vertices (rasterizer.py:62-82, 119-122)
+      const int sub = (flags >> 7) & 1u;
       double P[3][3], op[4][3], ob[4][3];
       tri_cam(sc, cam, t, P);
       clip_near(P, op, ob);
+      double B[3][3];
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         B[0][q] = ob[0][q];
         B[1][q] = sub ? ob[2][q] : ob[1][q];
         B[2][q] = sub ? ob[3][q] : ob[2][q];
       }
-    } else {
+      if (flags & 8u) {  // reorder (0, 2, 1), rasterizer.py:151-152
 #pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) B[r][q] = (r == q) ? 1.0 : 0.0;
-    }
-    if (flags & 8u) {  // reorder (0, 2, 1), rasterizer.py:151-152
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const double tmp = B[1][q];
-        B[1][q] = B[2][q];
-        B[2][q] = tmp;
+        for (int q = 0; q < 3; ++q) {
+          const double tmp = B[1][q];
+          B[1][q] = B[2][q];
+          B[2][q] = tmp;
+        }
       }
-    }
-    const double wsum = __dadd_rn(__dadd_rn(fd.w0, fd.w1), fd.w2);
-    double b[3];
+      double bb[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      b[k] = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(fd.w0, B[0][k]), __dmul_rn(fd.w1, B[1][k])),
-                                 __dmul_rn(fd.w2, B[2][k])),
-                       wsum);
-      if (b[k] < 0.0) b[k] = 0.0;
+      for (int k = 0; k < 3; ++k)
+        bb[k] = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(fd.w0, B[0][k]), __dmul_rn(fd.w1, B[1][k])),
+                                    __dmul_rn(fd.w2, B[2][k])),
+                          wsum);
+      b0 = bb[0];
+      b1 = bb[1];
+      b2 = bb[2];
+    } else {
+      // rows = identity reordered by (0, 1, 2) or (0, 2, 1): b_k = w_perm(k) / wsum
+      b0 = __ddiv_rn(fd.w0, wsum);
+      b1 = __ddiv_rn((flags & 8u) ? fd.w2 : fd.w1, wsum);
+      b2 = __ddiv_rn((flags & 8u) ? fd.w1 : fd.w2, wsum);
     }
-    const double bs = __dadd_rn(__dadd_rn(b[0], b[1]), b[2]);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) b[k] = __ddiv_rn(b[k], bs);
+    if (b0 < 0.0) b0 = 0.0;  // np.clip(b, 0, None)
+    if (b1 < 0.0) b1 = 0.0;
+    if (b2 < 0.0) b2 = 0.0;
+    const double bs = __dadd_rn(__dadd_rn(b0, b1), b2);
     const int origin = (flags >> 5) & 3u;
     const int s = (int)(flags >> 16);
-    const double bo = origin == 0 ? b[0] : (origin == 1 ? b[1] : b[2]);
-    const double bv = origin == 0 ? b[2] : (origin == 1 ? b[0] : b[1]);
-    double u = __dsub_rn(1.0, bo);
-    double v = bv;
+    const double bo = origin == 0 ? b0 : (origin == 1 ? b1 : b2);
+    const double bv = origin == 0 ? b2 : (origin == 1 ? b0 : b1);
+    double u = __dsub_rn(1.0, __ddiv_rn(bo, bs));
+    double v = __ddiv_rn(bv, bs);
     u = np_min(np_max(u, 0.0), 1.0);
     v = np_min(np_max(v, 0.0), u);
-    long long i = (long long)__dmul_rn((double)s, u);
+    int i = (int)__dmul_rn((double)s, u);
     if (i > s - 1) i = s - 1;
-    long long j = (long long)__dmul_rn((double)s, v);
+    int j = (int)__dmul_rn((double)s, v);
     if (j > i) j = i;
-    const int32_t texel = (int32_t)((i * i + i) / 2 + j);
+    const int32_t texel = (i * i + i) / 2 + j;
     row = (int32_t)(__ldg(sc.offsets + t) + texel);
-    if (o.tri) o.tri[pix] = t;
-    if (o.texel) o.texel[pix] = texel;
-    if (o.depth) o.depth[pix] = fd.depth;
-    if (o.u) o.u[pix] = u;
-    if (o.v) o.v[pix] = v;
+    if (o.tri) {
+      o.tri[pix] = t;
+      o.texel[pix] = texel;
+    }
+    if (o.depth) {
+      o.depth[pix] = fd.depth;
+      o.u[pix] = u;
+      o.v[pix] = v;
+    }
   } else {
-    if (o.tri) o.tri[pix] = -1;
-    if (o.texel) o.texel[pix] = 0;
-    if (o.depth) o.depth[pix] = fd.depth;
-    if (o.u) o.u[pix] = 0.0;
-    if (o.v) o.v[pix] = 0.0;
+    if (o.tri) {
+      o.tri[pix] = -1;
+      o.texel[pix] = 0;
+    }
+    if (o.depth) {
+      o.depth[pix] = fd.depth;
+      o.u[pix] = 0.0;
+      o.v[pix] = 0.0;
+    }
   }
   o.rows[pix] = row;
   if (o.hits && row >= 0) {
@@ -498,9 +517,9 @@ __device__ __forceinline__ void write_pixel(const tfb_scene &sc, const Cam &cam,
 //  Larger or overflowed tiles are handed to k_raster_big.
 __global__ void __launch_bounds__(kThreads, 2) k_raster(tfb_scene sc, const double *__restrict__ cams, int W, int H,
                                                         int TX, int ntiles, Work w, Outs o) {
-  const int f = blockIdx.y;
-  const int tile = blockIdx.x;
-  const int tx0 = (tile % TX) * kTile, ty0 = (tile / TX) * kTile;
+  const int f = blockIdx.z;
+  const int tile = blockIdx.y * TX + blockIdx.x;
+  const int tx0 = blockIdx.x * kTile, ty0 = blockIdx.y * kTile;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t n = w.tile_count[(int64_t)f * ntiles + tile];
   const uint64_t toff = w.tile_off[(int64_t)f * ntiles + tile];
@@ -515,6 +534,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster(tfb_scene sc, const doub
   __shared__ uint32_t spre[kThreads];  // exclusive prefix of bbox areas
   __shared__ uint32_t pfirst[kTile * kTile];
   __shared__ uint32_t pcnt[kTile * kTile];
+  __shared__ double pe[kTile * kTile][3];  // edge values of a pixel's (single) covering pair
   __shared__ uint32_t wtot[kThreads / 32];
   __shared__ Cam cam;
   load_cam(cam, cams, f);
@@ -586,6 +606,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster(tfb_scene sc, const doub
         const int pix = pyl * kTile + pxl;
         atomicMin(pfirst + pix, (uint32_t)j);
         atomicAdd(pcnt + pix, 1u);
+        pe[pix][0] = e[0];  // meaningful only when this is the pixel's sole candidate
+        pe[pix][1] = e[1];
+        pe[pix][2] = e[2];
       }
       if (++lx == bw) {
         lx = 0;
@@ -613,7 +636,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster(tfb_scene sc, const doub
   fd.init();
   if (cnt == 1u) {
     const int j = (int)pfirst[tid];
-    fd.step(sgeom[j], smeta[j].flags, px, py, j);
+    const double e[3] = {pe[tid][0], pe[tid][1], pe[tid][2]};
+    fd.step_e(sgeom[j], e, j);
   } else if (cnt > 1u) {
     for (int j = (int)pfirst[tid]; j < (int)n; ++j) {
       const uint32_t b = sbox[j];
@@ -800,7 +824,7 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
     k_fill<<<dim3(fill_blocks, nframes), 256, 0, st>>>(w, m, ntiles, TX);
   }
   Outs o{rows_out, texel_hits, tri_out, texel_out, depth_out, u_out, v_out};
-  k_raster<<<dim3(ntiles, nframes), kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
+  k_raster<<<dim3(TX, TY, nframes), kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
   k_raster_big<<<148, kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
   return check_launch("tfb_rasterize");
 }
