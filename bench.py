@@ -158,9 +158,9 @@ def run_reference(args):
     if rank != 0:
         return
     threads = min(len(os.sched_getaffinity(0)), 64)
-    sample = 2 * threads
+    sample = 8 * threads
     for _ in range(args.warmup):
-        cpu_reference(args, min(sample, threads), threads)
+        cpu_reference(args, threads, threads)
     vals = []
     t_total = 0.0
     for _ in range(args.steps):
@@ -289,7 +289,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and not args.no_cpu:
         threads = min(len(os.sched_getaffinity(0)), 64)
-        sample = 8 * threads
+        sample = 64 * threads
         val, dt = cpu_reference(args, sample, threads, scene=(mesh, layout))
         cpu = {"value": val, "unit": "frames/s", "cores": threads, "kind": "port",
                "sample": "%d cfg2 frames (rasterize+images_iid+mul accumulate+finalize), oracle C port, "

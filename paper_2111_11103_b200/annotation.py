@@ -162,13 +162,11 @@ class MeshAnnotation:
     # -- exchange ------------------------------------------------------------------------
     def allreduce(self, group=None):
         """Sum accumulators and counts over all ranks (one NCCL all-reduce each)."""
-        import torch.distributed as dist
+        from .dist import allreduce_sum_
 
         tex = self.texture
         tex._push_host()
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-            dist.all_reduce(tex._accum, op=dist.ReduceOp.SUM, group=group)
-            dist.all_reduce(tex._counts, op=dist.ReduceOp.SUM, group=group)
+        allreduce_sum_([tex._accum, tex._counts], group)
         tex._h_accum = tex._h_counts = None
 
     # -- results -------------------------------------------------------------------------

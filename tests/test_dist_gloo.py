@@ -1,0 +1,93 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): frame sharding plus ONE sum
+all-reduce of (accumulator, counts) reproduces the single-rank texture.  The
+per-rank fold here is the CPU oracle (the GPU fold is covered by the parity
+tests); what is under test is paper_2111_11103_b200.dist."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _scene():
+    z = np.load(os.path.join(GOLD, "cfg1.npz"))
+    from paper_2111_11103_b200.synth import NoiseModel, corrupt
+
+    c = int(z["num_classes"])
+    model = NoiseModel("flip", epsilon=0.3, q=0.8, seed=1)
+    probs = [corrupt(z["gt"][f].astype(np.int32), model, c, f) for f in range(len(z["cams"]))]
+    return z, probs
+
+
+def _fold(z, probs, frames, agg):
+    import oracle as O
+
+    n_x, c = int(z["total_texels"]), int(z["num_classes"])
+    acc = np.zeros((n_x, c))
+    cnt = np.zeros(n_x, np.int64)
+    for f in frames:
+        w = O.compute_pixel_weights(z["tri"][f], z["texel"][f], "images_iid")
+        O.accumulate_frame(acc, cnt, z["offsets"], z["tri"][f], z["texel"][f], probs[f], w, agg)
+    return acc, cnt
+
+
+def _worker(rank, world, port, agg, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    from paper_2111_11103_b200 import dist as D
+
+    r, w, _ = D.init_from_env("gloo")
+    assert (r, w) == (rank, world)
+    z, probs = _scene()
+    mine = D.shard_frames(list(range(len(z["cams"]))))
+    acc, cnt = _fold(z, probs, mine, agg)
+    ta, tc = torch.from_numpy(acc), torch.from_numpy(cnt)
+    D.allreduce_sum_([ta, tc])
+    if rank == 0:
+        np.save(out + "_acc.npy", ta.numpy())
+        np.save(out + "_cnt.npy", tc.numpy())
+        np.save(out + "_mine.npy", np.array(mine))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("agg", ["sum", "mul"])
+def test_two_rank_shards_plus_allreduce_equal_single_rank(tmp_path, agg):
+    out = str(tmp_path / "r")
+    mp.spawn(_worker, args=(2, _free_port(), agg, out), nprocs=2, join=True)
+    z, probs = _scene()
+    acc1, cnt1 = _fold(z, probs, range(len(z["cams"])), agg)
+    np.testing.assert_array_equal(np.load(out + "_cnt.npy"), cnt1)
+    np.testing.assert_allclose(np.load(out + "_acc.npy"), acc1, rtol=1e-12, atol=1e-12)
+    np.testing.assert_array_equal(np.load(out + "_mine.npy"), np.arange(10))
+    import oracle as O
+
+    rows, unobs = O.finalize(np.load(out + "_acc.npy"), cnt1, agg)
+    ref_rows, ref_unobs = O.finalize(acc1, cnt1, agg)
+    np.testing.assert_array_equal(O.texel_argmax(rows, unobs), O.texel_argmax(ref_rows, ref_unobs))
+
+
+def test_shard_bounds_partition():
+    from paper_2111_11103_b200.dist import shard_bounds
+
+    for n in (0, 1, 7, 2000):
+        for p in (1, 2, 3, 8):
+            got = [shard_bounds(n, r, p) for r in range(p)]
+            assert got[0][0] == 0 and got[-1][1] == n
+            assert all(got[i][1] == got[i + 1][0] for i in range(p - 1))
+    with pytest.raises(ValueError):
+        shard_bounds(10, 2, 2)
