@@ -413,7 +413,8 @@ struct Fold {
 // products are skipped; of the final normalization b /= b.sum() only the two
 // components (u, v) read are divided.
 __device__ __forceinline__ void write_pixel(const tfb_scene &sc, const Cam &cam, const Outs &o, int f, int W, int H,
-                                            int px_i, int py_i, const Fold &fd, uint32_t flags, int32_t t) {
+                                            int px_i, int py_i, const Fold &fd, uint32_t flags, int32_t t,
+                                            int64_t offset) {
   const int64_t pix = (int64_t)f * W * H + (int64_t)(py_i * W + px_i);
   int32_t row = -1;
   if (fd.win >= 0) {
@@ -471,7 +472,7 @@ __device__ __forceinline__ void write_pixel(const tfb_scene &sc, const Cam &cam,
     int j = (int)__dmul_rn((double)s, v);
     if (j > i) j = i;
     const int32_t texel = (i * i + i) / 2 + j;
-    row = (int32_t)(__ldg(sc.offsets + t) + texel);
+    row = (int32_t)(offset + texel);
     if (o.tri) {
       o.tri[pix] = t;
       o.texel[pix] = texel;
@@ -502,20 +503,35 @@ __device__ __forceinline__ void write_pixel(const tfb_scene &sc, const Cam &cam,
   }
 }
 
+struct TileSmem {
+  RecGeom geom[kThreads];
+  RecMeta meta[kThreads];
+  int64_t off[kThreads];              // offsets[t] of the record's triangle
+  unsigned long long pmin[kTile * kTile];  // per pixel: min (key << 32 | slot) of covering records
+  double pe[kTile * kTile][3];        // edge values of a pixel's (single) covering pair
+  Cam cam;
+  uint32_t key[kThreads];
+  uint32_t box[kThreads];             // tile-relative bbox: x0 | y0 << 8 | w << 16 | h << 24
+  uint32_t pre[kThreads];             // exclusive prefix of bbox areas
+  uint32_t pcnt[kTile * kTile];
+  uint32_t wtot[kThreads / 32];
+};
+
 // One CTA per 16x16 tile with at most kThreads records (the common case).
-//  1. The tile's record ids (unordered from k_fill) are rank-sorted in shared
-//     memory, restoring the reference's ascending (triangle, fan) order, and
-//     the 128-byte records are staged in that order.
+//  1. The tile's records are staged in shared memory in list order (all
+//     threads cooperate on the 128-byte copies); bbox-in-tile and area per
+//     record, exclusive scan of areas.
 //  2. Pair-parallel edge tests: every (record, pixel of its bbox in the tile)
-//     pair gets its own thread (prefix sum of bbox areas + one binary search
-//     per thread-run), so float64 lanes are not wasted on pixels outside a
-//     small triangle's bbox.  Covering pairs bump the pixel's candidate count
-//     and atomicMin its first (smallest-key) record.
-//  3. One thread per pixel: a single candidate is folded directly; pixels with
-//     several run the exact ascending sequential fold over the tile's records
-//     (rasterizer.py:108, 170-171), so depth ties resolve as in the reference.
+//     pair gets its own thread (one binary search per thread-run), so float64
+//     lanes are not wasted on pixels outside a small triangle's bbox.  A
+//     covering pair bumps the pixel's candidate count and atomicMin's its
+//     (record key, slot).
+//  3. One thread per pixel: a single candidate is folded directly; with
+//     several, the pixel repeatedly selects the smallest covering key above
+//     the last folded one — the reference's ascending sequential fold
+//     (rasterizer.py:108, 170-171) without sorting the list.
 //  Larger or overflowed tiles are handed to k_raster_big.
-__global__ void __launch_bounds__(kThreads, 2) k_raster(tfb_scene sc, const double *__restrict__ cams, int W, int H,
+__global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const double *__restrict__ cams, int W, int H,
                                                         int TX, int ntiles, Work w, Outs o) {
   const int f = blockIdx.z;
   const int tile = blockIdx.y * TX + blockIdx.x;
@@ -527,44 +543,36 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster(tfb_scene sc, const doub
     if (tid == 0) w.big[atomicAdd(w.fcnt + 1, 1u)] = (uint32_t)(f * ntiles + tile);
     return;
   }
-  __shared__ RecGeom sgeom[kThreads];
-  __shared__ RecMeta smeta[kThreads];
-  __shared__ uint32_t skey[kThreads];
-  __shared__ uint32_t sbox[kThreads];  // tile-relative bbox: x0 | y0 << 8 | w << 16 | h << 24
-  __shared__ uint32_t spre[kThreads];  // exclusive prefix of bbox areas
-  __shared__ uint32_t pfirst[kTile * kTile];
-  __shared__ uint32_t pcnt[kTile * kTile];
-  __shared__ double pe[kTile * kTile][3];  // edge values of a pixel's (single) covering pair
-  __shared__ uint32_t wtot[kThreads / 32];
-  __shared__ Cam cam;
+  extern __shared__ __align__(16) unsigned char raster_smem[];
+  TileSmem &S = *reinterpret_cast<TileSmem *>(raster_smem);
+  RecGeom *sgeom = S.geom;
+  RecMeta *smeta = S.meta;
+  int64_t *soff = S.off;
+  uint32_t *skey = S.key, *sbox = S.box, *spre = S.pre, *pcnt = S.pcnt, *wtot = S.wtot;
+  unsigned long long *pmin = S.pmin;
+  double(*pe)[3] = S.pe;
+  Cam &cam = S.cam;
   load_cam(cam, cams, f);
-  pfirst[tid] = 0xffffffffu;
+  pmin[tid] = ~0ull;
   pcnt[tid] = 0u;
   const uint32_t *src = w.list + (int64_t)f * w.cap + toff;
-  if (tid < n) skey[tid] = src[tid];
-  __syncthreads();
-  if (tid < n) {
-    const uint32_t key = skey[tid];
-    uint32_t rank = 0;
-    for (uint32_t j = 0; j < n; ++j) rank += skey[j] < key ? 1u : 0u;
-    const int64_t r = (int64_t)f * w.rs + key;
-    const RecMeta mt = w.meta[r];
-    smeta[rank] = mt;
-    const double2 *gs = reinterpret_cast<const double2 *>(w.geom + r);
-    double2 *gd = reinterpret_cast<double2 *>(sgeom + rank);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) gd[q] = gs[q];
-    const int bx0 = max((int)mt.x0, tx0) - tx0, bx1 = min((int)mt.x1, tx0 + kTile - 1) - tx0;
-    const int by0 = max((int)mt.y0, ty0) - ty0, by1 = min((int)mt.y1, ty0 + kTile - 1) - ty0;
-    sbox[rank] = (uint32_t)bx0 | ((uint32_t)by0 << 8) | ((uint32_t)(bx1 - bx0 + 1) << 16) |
-                 ((uint32_t)(by1 - by0 + 1) << 24);
-  }
-  __syncthreads();
-  // exclusive block scan of bbox areas (in sorted order)
+  const RecGeom *geom = w.geom + (int64_t)f * w.rs;
   uint32_t area = 0;
   if (tid < n) {
-    const uint32_t b = sbox[tid];
-    area = ((b >> 16) & 0xffu) * (b >> 24);
+    const uint32_t key = src[tid];
+    const RecMeta mt = w.meta[(int64_t)f * w.rs + key];
+    skey[tid] = key;
+    smeta[tid] = mt;
+    soff[tid] = __ldg(sc.offsets + mt.t);
+    const int bx0 = max((int)mt.x0, tx0) - tx0, bx1 = min((int)mt.x1, tx0 + kTile - 1) - tx0;
+    const int by0 = max((int)mt.y0, ty0) - ty0, by1 = min((int)mt.y1, ty0 + kTile - 1) - ty0;
+    const uint32_t bw = (uint32_t)(bx1 - bx0 + 1), bh = (uint32_t)(by1 - by0 + 1);
+    sbox[tid] = (uint32_t)bx0 | ((uint32_t)by0 << 8) | (bw << 16) | (bh << 24);
+    area = bw * bh;
+  }
+  for (uint32_t i = tid; i < n * 8; i += kThreads) {  // 8 x 16 B per 128-byte record
+    const uint32_t rec = i >> 3, q = i & 7;
+    reinterpret_cast<double2 *>(sgeom + rec)[q] = reinterpret_cast<const double2 *>(geom + src[rec])[q];
   }
   uint32_t incl = area;
 #pragma unroll
@@ -604,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster(tfb_scene sc, const doub
       double e[3];
       if (edges_at(sgeom[j], smeta[j].flags, (double)(tx0 + pxl) + 0.5, (double)(ty0 + pyl) + 0.5, e)) {
         const int pix = pyl * kTile + pxl;
-        atomicMin(pfirst + pix, (uint32_t)j);
+        atomicMin(pmin + pix, ((unsigned long long)skey[j] << 32) | (unsigned)j);
         atomicAdd(pcnt + pix, 1u);
         pe[pix][0] = e[0];  // meaningful only when this is the pixel's sole candidate
         pe[pix][1] = e[1];
@@ -626,7 +634,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster(tfb_scene sc, const doub
   }
   __syncthreads();
 
-  // one thread per pixel: fold its covering records in ascending order
+  // one thread per pixel: fold its covering records in ascending key order
   const int pxl = tid & (kTile - 1), pyl = tid / kTile;
   const int px_i = tx0 + pxl, py_i = ty0 + pyl;
   if (px_i >= W || py_i >= H) return;
@@ -635,21 +643,35 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster(tfb_scene sc, const doub
   Fold fd;
   fd.init();
   if (cnt == 1u) {
-    const int j = (int)pfirst[tid];
+    const int j = (int)(pmin[tid] & 0xffffffffu);
     const double e[3] = {pe[tid][0], pe[tid][1], pe[tid][2]};
     fd.step_e(sgeom[j], e, j);
   } else if (cnt > 1u) {
-    for (int j = (int)pfirst[tid]; j < (int)n; ++j) {
-      const uint32_t b = sbox[j];
-      const int bx = b & 0xff, by = (b >> 8) & 0xff;
-      if (pxl < bx || pxl >= bx + (int)((b >> 16) & 0xff) || pyl < by || pyl >= by + (int)(b >> 24)) continue;
-      double e[3];
-      if (edges_at(sgeom[j], smeta[j].flags, px, py, e)) fd.step(sgeom[j], smeta[j].flags, px, py, j);
+    unsigned long long cur = pmin[tid];
+    for (uint32_t k = 0; k < cnt; ++k) {
+      const int j = (int)(cur & 0xffffffffu);
+      fd.step(sgeom[j], smeta[j].flags, px, py, j);
+      if (k + 1 == cnt) break;
+      const uint32_t last = (uint32_t)(cur >> 32);
+      unsigned long long best = ~0ull;
+      for (uint32_t i = 0; i < n; ++i) {
+        const uint32_t key = skey[i];
+        if (key <= last) continue;
+        const uint32_t bb = sbox[i];
+        const int bx = bb & 0xff, by = (bb >> 8) & 0xff;
+        if (pxl < bx || pxl >= bx + (int)((bb >> 16) & 0xff) || pyl < by || pyl >= by + (int)(bb >> 24)) continue;
+        const unsigned long long cand = ((unsigned long long)key << 32) | i;
+        if (cand >= best) continue;
+        double e[3];
+        if (edges_at(sgeom[i], smeta[i].flags, px, py, e)) best = cand;
+      }
+      cur = best;
     }
   }
   const uint32_t flags = fd.win >= 0 ? smeta[fd.win].flags : 0u;
   const int32_t t = fd.win >= 0 ? smeta[fd.win].t : -1;
-  write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t);
+  const int64_t off = fd.win >= 0 ? soff[fd.win] : 0;
+  write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, off);
 }
 
 // Tiles with more than kThreads records, or whose list overflowed the pair
@@ -764,7 +786,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster_big(tfb_scene sc, const 
     if (in_img) {
       const uint32_t flags = fd.win >= 0 ? meta[fd.win].flags : 0u;
       const int32_t t = fd.win >= 0 ? meta[fd.win].t : -1;
-      write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t);
+      write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, t >= 0 ? __ldg(sc.offsets + t) : 0);
     }
   }
 }
@@ -824,7 +846,12 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
     k_fill<<<dim3(fill_blocks, nframes), 256, 0, st>>>(w, m, ntiles, TX);
   }
   Outs o{rows_out, texel_hits, tri_out, texel_out, depth_out, u_out, v_out};
-  k_raster<<<dim3(TX, TY, nframes), kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
+  static bool smem_set = false;
+  if (!smem_set) {
+    cudaFuncSetAttribute(k_raster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem));
+    smem_set = true;
+  }
+  k_raster<<<dim3(TX, TY, nframes), kThreads, sizeof(TileSmem), st>>>(sc, cams, width, height, TX, ntiles, w, o);
   k_raster_big<<<148, kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
   return check_launch("tfb_rasterize");
 }

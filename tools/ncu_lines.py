@@ -37,7 +37,3 @@ for r in rows:
 tot = sum(o[0] for o in out) or 1
 for s, ln, src, best, ins in sorted(out, key=lambda o: -o[0])[:top]:
     print("%5.1f%% L%-4s inst=%-9s %-90s %s" % (100.0 * s / tot, ln, ins, src.strip(), best))
-
-tot_inst = 0
-for r in rows:
-    pass
