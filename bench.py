@@ -62,7 +62,7 @@ def _config(args, n):
     return {"workload": "cfg2: room 299,568 tris, %d frames/GPU 640x480, c=40, %s, %s, steps=1 layout"
                         % (args.frames, AGG, WMODE),
             "frames_per_gpu": args.frames, "triangles": 299568, "texels": 299568, "classes": C,
-            "aggregator": AGG, "weights": WMODE, "accum": "float32", "batch": args.batch,
+            "aggregator": AGG, "weights": WMODE, "accum": "float32", "batch": args.batch, "overlap": bool(args.overlap),
             "parallelism": "frame-sharded dp%d" % n,
             "l2": "inputs larger than L2: 8-map pool per GPU (393 MB), accumulator 47.9 MB L2-resident"}
 
@@ -202,7 +202,7 @@ def run_ours(args):
     pool = softmax_maps(POOL, H, W, C, seed=rank, device=dev)
     probs_list = [pool[i % POOL] for i in range(args.frames)]
     ann = MeshAnnotation(mesh, layout, num_classes=C, aggregator=AGG, weight_mode=WMODE, accum_dtype="float32",
-                         max_batch=args.batch, device=dev)
+                         max_batch=args.batch, device=dev, overlap=args.overlap)
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -238,9 +238,9 @@ def run_ours(args):
     ms_max = float(ms_t.item())
     value = world * args.frames * args.steps / (ms_max / 1000.0)
 
-    raster_ms = sum(e0.elapsed_time(e1) for _, e0, e1, _ in prof)
-    fuse_ms = sum(e1.elapsed_time(e2) for _, _, e1, e2 in prof)
-    fuse_frames = sum(b for b, _, _, _ in prof)
+    raster_ms = sum(r0.elapsed_time(r1) for _, r0, r1, _, _ in prof)
+    fuse_ms = sum(f0.elapsed_time(f1) for _, _, _, f0, f1 in prof)
+    fuse_frames = sum(p_[0] for p_ in prof)
     n_launch_fuse = len(prof)
     # our kernels per timed step: 4 (raster) + 1 (fuse) + 1 (clear) per batch, + 1 finalize
     gpu_launches = args.steps * (6 * ((args.frames + args.batch - 1) // args.batch) + 1)
@@ -321,7 +321,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--frames", type=int, default=FRAMES)
-    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--overlap", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

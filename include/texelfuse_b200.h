@@ -63,6 +63,12 @@ typedef struct tfb_scene {
 const char *tfb_last_error(void);
 int tfb_version(void);
 
+/* Tuning knobs (process-wide).  TFB_OPT_FUSE_CTAS_PER_SM caps the resident
+ * tfb_fuse CTAs per SM (0 = as many as fit), leaving room for a rasterizer
+ * running concurrently on another stream. */
+#define TFB_OPT_FUSE_CTAS_PER_SM 1
+int tfb_set_option(int option, int value);
+
 /* Bytes of scratch tfb_rasterize needs for up to `max_frames` frames of
  * width x height; `pair_capacity` = triangle/tile pairs budgeted per frame
  * (0 = default).  Tiles whose lists overflow it stay exact (slow path). */

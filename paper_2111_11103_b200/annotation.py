@@ -45,7 +45,8 @@ class MeshAnnotation:
     """Fuse per-frame class probabilities onto a mesh's texels on the GPU."""
 
     def __init__(self, mesh, layout=None, num_classes=None, aggregator="mul", weight_mode="images_iid",
-                 accum_dtype="float32", max_batch=8, device=None, memory_budget=None):
+                 accum_dtype="float32", max_batch=8, device=None, memory_budget=None, overlap=False,
+                 fuse_ctas_per_sm=None):
         if num_classes is None:
             raise ValueError("num_classes is required")
         self.mesh = mesh
@@ -59,12 +60,23 @@ class MeshAnnotation:
         self.max_batch = int(max_batch)
         self._staging = None
         self.frames_added = 0
-        # optional list receiving (frames, ev_start, ev_after_raster, ev_after_fuse) per batch
+        # Overlap mode: batch k+1 is rasterized on a side stream while batch k
+        # is scatter-added on the caller's stream (double-buffered row / hit
+        # images); the scatter kernel is capped at fuse_ctas_per_sm resident
+        # CTAs so rasterizer CTAs can share the SMs.
+        self.overlap = bool(overlap)
+        self._side = torch.cuda.Stream(self.device) if self.overlap else None
+        self._free = [None, None]
+        if fuse_ctas_per_sm is None:
+            fuse_ctas_per_sm = 2 if self.overlap else 0
+        N.call("tfb_set_option", 1, int(fuse_ctas_per_sm))
+        # optional list receiving (frames, ev_raster_start, ev_raster_end, ev_fuse_start, ev_fuse_end)
         self.profile = None
 
-    def _event(self):
+    @staticmethod
+    def _event(stream):
         e = torch.cuda.Event(enable_timing=True)
-        e.record(torch.cuda.current_stream(self.device))
+        e.record(stream)
         return e
 
     def reset(self):
@@ -119,38 +131,60 @@ class MeshAnnotation:
         if tex.finalized:
             raise RuntimeError("texture is already finalized")
         W, H = _sizes(cameras, width, height)
-        cams_all = _cams_array(cameras).to(self.device, non_blocking=True)
+        cur = stream if stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(cur):
+            cams_all = _cams_array(cameras).to(self.device, non_blocking=True)
         B = int(cams_all.shape[0])
         hw = H * W
         tex._push_host()
         needs_hits = self.weight_mode != "pixels_iid"
-        for b0 in range(0, B, self.max_batch):
-            b = min(self.max_batch, B - b0)
+        nslots = 2 if self.overlap else 1
+        mb = self.max_batch
+        rows_all = self.scene.buffer("rows", (nslots, mb, hw), torch.int32)
+        hits_all = (self.scene.buffer("hits2", (nslots, mb, max(tex.total_texels, 1)), torch.int32, zero=True)
+                    if needs_hits else None)
+        side = self._side if self.overlap else cur
+        if self.overlap:
+            side.wait_stream(cur)  # cameras and anything queued before this call
+            cams_all.record_stream(side)
+        for i, b0 in enumerate(range(0, B, mb)):
+            b = min(mb, B - b0)
+            slot = i % nslots
             chunk = probs[b0:b0 + b]
-            ptrs, keep = self._probs_batch(chunk, b, H, W)
-            rows = self.scene.buffer("rows", (self.max_batch, hw), torch.int32)[:b]
-            hits = self.scene.hits(self.max_batch)[:b] if needs_hits else None
+            with torch.cuda.stream(cur):
+                ptrs, keep = self._probs_batch(chunk, b, H, W)
+            rows = rows_all[slot, :b]
+            hits = hits_all[slot, :b] if needs_hits else None
+            if self.overlap and self._free[slot] is not None:
+                side.wait_event(self._free[slot])  # the scatter that last read this slot is done
             prof = self.profile
-            if prof is not None:
-                e0 = self._event()
-            self.scene.rasterize(cams_all[b0:b0 + b], W, H, rows, hits=hits, stream=stream)
-            if prof is not None:
-                e1 = self._event()
+            r0 = self._event(side) if prof is not None else None
+            self.scene.rasterize(cams_all[b0:b0 + b], W, H, rows, hits=hits, stream=side)
+            r1 = self._event(side) if prof is not None else None
+            if self.overlap:
+                ready = torch.cuda.Event()
+                ready.record(side)
+                cur.wait_event(ready)
+            f0 = self._event(cur) if prof is not None else None
             parr, _k = N.ptr_array(ptrs)
             fb = fallback_out[b0:b0 + b] if fallback_out is not None else None
             N.call("tfb_fuse", N.ptr(rows), hw, b, parr, self.num_classes, N.ptr(hits), None, tex.total_texels,
                    N.AGG_IDS[tex.aggregator], N.WMODE_IDS[self.weight_mode], float(self.alpha or 0.0),
                    N.ptr(tex._accum), int(tex.is_f64), tex.stride, N.ptr(tex._counts), N.ptr(fb),
-                   N.stream_handle(stream))
+                   N.stream_handle(cur))
             if prof is not None:
-                e2 = self._event()
-                prof.append((b, e0, e1, e2))
+                prof.append((b, r0, r1, f0, self._event(cur)))
             if needs_hits:
                 if tex.total_texels <= 4 * hw:  # a dense memset is cheaper than the scattered reset
-                    hits.zero_()
+                    with torch.cuda.stream(cur):
+                        hits.zero_()
                 else:
                     N.call("tfb_clear_hits", N.ptr(rows), hw, b, tex.total_texels, N.ptr(hits),
-                           N.stream_handle(stream))
+                           N.stream_handle(cur))
+            if self.overlap:
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                self._free[slot] = ev
             del keep
         tex._h_accum = tex._h_counts = None
         self.frames_added += B
@@ -196,7 +230,7 @@ class MeshAnnotation:
         labels = self.texture.labels_device
         for b0 in range(0, B, self.max_batch):
             b = min(self.max_batch, B - b0)
-            rows = self.scene.buffer("rows", (self.max_batch, hw), torch.int32)[:b]
+            rows = self.scene.buffer("render_rows", (self.max_batch, hw), torch.int32)[:b]
             self.scene.rasterize(cams[b0:b0 + b], W, H, rows, stream=stream)
             fb = None
             if fallback is not None:

@@ -455,6 +455,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
   }
 }
 
+int g_fuse_ctas_per_sm = 0;  // 0 = as many as fit (tfb_set_option(TFB_OPT_FUSE_CTAS_PER_SM))
+
 template <typename AccT, int AGG, bool EQW>
 int launch_fuse(const FuseParams &p, cudaStream_t st) {
   const WarpSmem L = warp_layout(p.c, p.NS, (int)sizeof(AccT));
@@ -473,7 +475,9 @@ int launch_fuse(const FuseParams &p, cudaStream_t st) {
     if (blocks_per_sm < 1) blocks_per_sm = 1;
     configured_bytes = bytes;
   }
-  int64_t grid = (int64_t)num_sms * blocks_per_sm;
+  int per_sm = blocks_per_sm;
+  if (g_fuse_ctas_per_sm > 0 && g_fuse_ctas_per_sm < per_sm) per_sm = g_fuse_ctas_per_sm;
+  int64_t grid = (int64_t)num_sms * per_sm;
   const int64_t need = (p.nitems + kWarps - 1) / kWarps;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
@@ -620,6 +624,16 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
     if (rc != TFB_OK) return rc;
   }
   return TFB_OK;
+}
+
+extern "C" int tfb_set_option(int option, int value) {
+  if (option == TFB_OPT_FUSE_CTAS_PER_SM) {
+    TFB_REQUIRE(value >= 0, TFB_ERR_VALUE, "tfb_set_option: negative CTA cap");
+    g_fuse_ctas_per_sm = value;
+    return TFB_OK;
+  }
+  set_error("tfb_set_option: unknown option %d", option);
+  return TFB_ERR_VALUE;
 }
 
 extern "C" int tfb_rows_from_ids(const int32_t *tri, const int32_t *texel, int64_t npix, const tfb_scene *scene,

@@ -505,8 +505,9 @@ __device__ __forceinline__ void write_pixel(const tfb_scene &sc, const Cam &cam,
 
 struct TileSmem {
   RecGeom geom[kThreads];
-  RecMeta meta[kThreads];
-  int64_t off[kThreads];              // offsets[t] of the record's triangle
+  uint32_t flags[kThreads];           // RecMeta::flags
+  int32_t tri[kThreads];              // RecMeta::t
+  int32_t off[kThreads];              // offsets[t] of the record's triangle (n_x < 2^31)
   unsigned long long pmin[kTile * kTile];  // per pixel: min (key << 32 | slot) of covering records
   double pe[kTile * kTile][3];        // edge values of a pixel's (single) covering pair
   Cam cam;
@@ -546,8 +547,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const doub
   extern __shared__ __align__(16) unsigned char raster_smem[];
   TileSmem &S = *reinterpret_cast<TileSmem *>(raster_smem);
   RecGeom *sgeom = S.geom;
-  RecMeta *smeta = S.meta;
-  int64_t *soff = S.off;
+  uint32_t *sflags = S.flags;
+  int32_t *stri = S.tri, *soff = S.off;
   uint32_t *skey = S.key, *sbox = S.box, *spre = S.pre, *pcnt = S.pcnt, *wtot = S.wtot;
   unsigned long long *pmin = S.pmin;
   double(*pe)[3] = S.pe;
@@ -562,8 +563,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const doub
     const uint32_t key = src[tid];
     const RecMeta mt = w.meta[(int64_t)f * w.rs + key];
     skey[tid] = key;
-    smeta[tid] = mt;
-    soff[tid] = __ldg(sc.offsets + mt.t);
+    sflags[tid] = mt.flags;
+    stri[tid] = mt.t;
+    soff[tid] = (int32_t)__ldg(sc.offsets + mt.t);
     const int bx0 = max((int)mt.x0, tx0) - tx0, bx1 = min((int)mt.x1, tx0 + kTile - 1) - tx0;
     const int by0 = max((int)mt.y0, ty0) - ty0, by1 = min((int)mt.y1, ty0 + kTile - 1) - ty0;
     const uint32_t bw = (uint32_t)(bx1 - bx0 + 1), bh = (uint32_t)(by1 - by0 + 1);
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const doub
     for (uint32_t p = p0; p < p1; ++p) {
       const int pxl = (int)(b & 0xffu) + lx, pyl = (int)((b >> 8) & 0xffu) + ly;
       double e[3];
-      if (edges_at(sgeom[j], smeta[j].flags, (double)(tx0 + pxl) + 0.5, (double)(ty0 + pyl) + 0.5, e)) {
+      if (edges_at(sgeom[j], sflags[j], (double)(tx0 + pxl) + 0.5, (double)(ty0 + pyl) + 0.5, e)) {
         const int pix = pyl * kTile + pxl;
         atomicMin(pmin + pix, ((unsigned long long)skey[j] << 32) | (unsigned)j);
         atomicAdd(pcnt + pix, 1u);
@@ -650,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const doub
     unsigned long long cur = pmin[tid];
     for (uint32_t k = 0; k < cnt; ++k) {
       const int j = (int)(cur & 0xffffffffu);
-      fd.step(sgeom[j], smeta[j].flags, px, py, j);
+      fd.step(sgeom[j], sflags[j], px, py, j);
       if (k + 1 == cnt) break;
       const uint32_t last = (uint32_t)(cur >> 32);
       unsigned long long best = ~0ull;
@@ -663,13 +665,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const doub
         const unsigned long long cand = ((unsigned long long)key << 32) | i;
         if (cand >= best) continue;
         double e[3];
-        if (edges_at(sgeom[i], smeta[i].flags, px, py, e)) best = cand;
+        if (edges_at(sgeom[i], sflags[i], px, py, e)) best = cand;
       }
       cur = best;
     }
   }
-  const uint32_t flags = fd.win >= 0 ? smeta[fd.win].flags : 0u;
-  const int32_t t = fd.win >= 0 ? smeta[fd.win].t : -1;
+  const uint32_t flags = fd.win >= 0 ? sflags[fd.win] : 0u;
+  const int32_t t = fd.win >= 0 ? stri[fd.win] : -1;
   const int64_t off = fd.win >= 0 ? soff[fd.win] : 0;
   write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, off);
 }
