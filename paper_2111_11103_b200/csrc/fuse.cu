@@ -190,18 +190,45 @@ __device__ __forceinline__ AccT weight_from(const FuseParams &p, double src, int
 }
 
 // log of a (product of) clipped probabilities, x in [1e-28, 1]: MUFU lg2 (2 ulp
-// below 1/2, 2^-22.6 absolute above) and, where that absolute error would be
-// large relative to |log x| (x > 0.9), the log1p series in t = x - 1 (exact),
-// truncation t^7/7, i.e. < 1.5e-7 relative.
-__device__ __forceinline__ float log_prob(float x) {
+// below 1/2, 2^-22.6 absolute above).  Where that absolute error would be
+// large relative to |log x| (x > 0.9) the log1p series in t = x - 1 (exact)
+// is used instead, truncation t^7/7 < 1.5e-7 relative.  In log4 the series
+// runs behind a warp vote, so warps with no such value skip it.
+__device__ __forceinline__ float lg2_ln(float x) {
   float l;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(x));
-  float y = l * 0.693147180559945f;
-  if (x > 0.9f) {
-    const float t = x - 1.0f;
-    y = t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, fmaf(t, -1.0f / 6.0f, 1.0f / 5.0f), -0.25f), 1.0f / 3.0f), -0.5f), 1.0f);
+  return l * 0.693147180559945f;
+}
+
+__device__ __forceinline__ float log1p_series(float x) {
+  const float t = x - 1.0f;
+  return t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, fmaf(t, -1.0f / 6.0f, 1.0f / 5.0f), -0.25f), 1.0f / 3.0f), -0.5f), 1.0f);
+}
+
+__device__ __forceinline__ void log4(float &a0, float &a1, float &a2, float &a3) {
+  const float x0 = a0, x1 = a1, x2 = a2, x3 = a3;
+  a0 = lg2_ln(x0);
+  a1 = lg2_ln(x1);
+  a2 = lg2_ln(x2);
+  a3 = lg2_ln(x3);
+  const bool near1 = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3)) > 0.9f;
+  if (__any_sync(__activemask(), near1)) {
+    if (x0 > 0.9f) a0 = log1p_series(x0);
+    if (x1 > 0.9f) a1 = log1p_series(x1);
+    if (x2 > 0.9f) a2 = log1p_series(x2);
+    if (x3 > 0.9f) a3 = log1p_series(x3);
   }
-  return y;
+}
+
+__device__ __forceinline__ float log_prob(float x) { return x > 0.9f ? log1p_series(x) : lg2_ln(x); }
+
+// packed float32x2 multiply (sm_100 FMUL2)
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  unsigned long long ra = *reinterpret_cast<unsigned long long *>(&a);
+  unsigned long long rb = *reinterpret_cast<unsigned long long *>(&b);
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(ra), "l"(rb));
+  return *reinterpret_cast<float2 *>(&r);
 }
 
 template <typename AccT, int AGG, bool EQW>
@@ -297,7 +324,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
       const int idx = __popc(smask & upto) - 1;
       const unsigned above = smask & ~upto;
       const int len = (above ? __ffs(above) - 1 : kChunk) - lane;
-      prow[idx] = r_cur;
+      prow[idx] = r_cur >= 0 ? (int32_t)((int64_t)r_cur * p.stride) : -1;  // accumulator row offset
       pw[idx] = w;
       if (r_cur >= 0) atomicAdd(p.counts + r_cur, (uint32_t)len);  // fusion.py:182
     }
@@ -337,62 +364,75 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
       if (g < geo.G && q < geo.nq) {
         const int k0 = q * 4;
         const float *pp = st + (size_t)i0 * c + k0;
-        AccT a0 = 0, a1 = 0, a2 = 0, a3 = 0;
         const float pad = AGG == TFB_AGG_MUL ? 1.0f : 0.0f;
-        int idx = __popc(smask & ((1u << i0) - 1u)) - 1;
-        for (int i = i0; i < i1; ++i, pp += c) {
-          const bool ps = (smask >> i) & 1u;
-          idx += ps ? 1 : 0;
-          float v0, v1, v2, v3;
-          if (vec_ok) {
-            const float4 v = *reinterpret_cast<const float4 *>(pp);
-            v0 = v.x; v1 = v.y; v2 = v.z; v3 = v.w;
-          } else {
-            v0 = pp[0];
-            v1 = k0 + 1 < c ? pp[1] : pad;
-            v2 = k0 + 2 < c ? pp[2] : pad;
-            v3 = k0 + 3 < c ? pp[3] : pad;
-          }
-          if (kProd) {
-            a0 = (ps ? 1.0f : (float)a0) * clip_mul(v0);
-            a1 = (ps ? 1.0f : (float)a1) * clip_mul(v1);
-            a2 = (ps ? 1.0f : (float)a2) * clip_mul(v2);
-            a3 = (ps ? 1.0f : (float)a3) * clip_mul(v3);
-          } else if (sizeof(AccT) == 4) {
-            const float wi = EQW ? 1.0f : (float)sw[i];
-            float t0 = v0, t1 = v1, t2 = v2, t3 = v3;
-            if (AGG == TFB_AGG_MAXSUM) {
-              const float mx = smax[i];
-              t0 = v0 == mx ? v0 : 0.f; t1 = v1 == mx ? v1 : 0.f; t2 = v2 == mx ? v2 : 0.f; t3 = v3 == mx ? v3 : 0.f;
-            } else if (AGG == TFB_AGG_MUL) {
-              t0 = log_prob(clip_mul(v0)); t1 = log_prob(clip_mul(v1));
-              t2 = log_prob(clip_mul(v2)); t3 = log_prob(clip_mul(v3));
+        const int row4 = geo.QW * 4;
+        AccT *t = tab + ((size_t)(__popc(smask & ((1u << i0) - 1u)) - 1) * geo.QW + qi0) * 4;
+        if (kProd) {
+          float2 m01 = make_float2(1.f, 1.f), m23 = make_float2(1.f, 1.f);
+          for (int i = i0; i < i1; ++i, pp += c) {
+            float v0, v1, v2, v3;
+            if (vec_ok) {
+              const float4 v = *reinterpret_cast<const float4 *>(pp);
+              v0 = v.x; v1 = v.y; v2 = v.z; v3 = v.w;
+            } else {
+              v0 = pp[0];
+              v1 = k0 + 1 < c ? pp[1] : pad;
+              v2 = k0 + 2 < c ? pp[2] : pad;
+              v3 = k0 + 3 < c ? pp[3] : pad;
             }
-            a0 = fmaf(wi, t0, ps ? 0.f : (float)a0);
-            a1 = fmaf(wi, t1, ps ? 0.f : (float)a1);
-            a2 = fmaf(wi, t2, ps ? 0.f : (float)a2);
-            a3 = fmaf(wi, t3, ps ? 0.f : (float)a3);
-          } else {
-            // float64 parity mode: the reference's per-pixel w * f(p) (fusion.py:171-177)
-            const double wi = (double)sw[i];
-            const float vv[4] = {v0, v1, v2, v3};
-            double t[4];
+            if ((smask >> i) & 1u) {  // a new piece starts at pixel i
+              m01 = make_float2(1.f, 1.f);
+              m23 = make_float2(1.f, 1.f);
+              t += row4;
+            }
+            m01 = mul2(m01, make_float2(clip_mul(v0), clip_mul(v1)));
+            m23 = mul2(m23, make_float2(clip_mul(v2), clip_mul(v3)));
+            *reinterpret_cast<float4 *>(t) = make_float4(m01.x, m01.y, m23.x, m23.y);
+          }
+        } else {
+          AccT a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+          for (int i = i0; i < i1; ++i, pp += c) {
+            float v0, v1, v2, v3;
+            if (vec_ok) {
+              const float4 v = *reinterpret_cast<const float4 *>(pp);
+              v0 = v.x; v1 = v.y; v2 = v.z; v3 = v.w;
+            } else {
+              v0 = pp[0];
+              v1 = k0 + 1 < c ? pp[1] : pad;
+              v2 = k0 + 2 < c ? pp[2] : pad;
+              v3 = k0 + 3 < c ? pp[3] : pad;
+            }
+            if ((smask >> i) & 1u) {
+              a0 = a1 = a2 = a3 = (AccT)0;
+              t += row4;
+            }
+            if (sizeof(AccT) == 4) {
+              const float wi = EQW ? 1.0f : (float)sw[i];
+              float t0 = v0, t1 = v1, t2 = v2, t3 = v3;
+              if (AGG == TFB_AGG_MAXSUM) {
+                const float mx = smax[i];
+                t0 = v0 == mx ? v0 : 0.f; t1 = v1 == mx ? v1 : 0.f; t2 = v2 == mx ? v2 : 0.f; t3 = v3 == mx ? v3 : 0.f;
+              } else if (AGG == TFB_AGG_MUL) {
+                t0 = log_prob(clip_mul(v0)); t1 = log_prob(clip_mul(v1));
+                t2 = log_prob(clip_mul(v2)); t3 = log_prob(clip_mul(v3));
+              }
+              a0 = fmaf(wi, t0, (float)a0); a1 = fmaf(wi, t1, (float)a1);
+              a2 = fmaf(wi, t2, (float)a2); a3 = fmaf(wi, t3, (float)a3);
+              *reinterpret_cast<float4 *>(t) = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
+            } else {
+              // float64 parity mode: the reference's per-pixel w * f(p) (fusion.py:171-177)
+              const double wi = (double)sw[i];
+              const float vv[4] = {v0, v1, v2, v3};
+              double tt[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              if (AGG == TFB_AGG_SUM) t[k] = (double)vv[k];
-              else if (AGG == TFB_AGG_MAXSUM) t[k] = vv[k] == smax[i] ? (double)vv[k] : 0.0;
-              else t[k] = log(np_clip((double)vv[k], kMulClamp, 1.0));
+              for (int k = 0; k < 4; ++k) {
+                if (AGG == TFB_AGG_SUM) tt[k] = (double)vv[k];
+                else if (AGG == TFB_AGG_MAXSUM) tt[k] = vv[k] == smax[i] ? (double)vv[k] : 0.0;
+                else tt[k] = log(np_clip((double)vv[k], kMulClamp, 1.0));
+              }
+              a0 += wi * tt[0]; a1 += wi * tt[1]; a2 += wi * tt[2]; a3 += wi * tt[3];
+              t[0] = a0; t[1] = a1; t[2] = a2; t[3] = a3;
             }
-            a0 = (ps ? 0.0 : (double)a0) + wi * t[0];
-            a1 = (ps ? 0.0 : (double)a1) + wi * t[1];
-            a2 = (ps ? 0.0 : (double)a2) + wi * t[2];
-            a3 = (ps ? 0.0 : (double)a3) + wi * t[3];
-          }
-          AccT *t = tab + ((size_t)idx * geo.QW + qi0) * 4;
-          if (sizeof(AccT) == 4) {
-            *reinterpret_cast<float4 *>(t) = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
-          } else {
-            t[0] = a0; t[1] = a1; t[2] = a2; t[3] = a3;
           }
         }
       }
@@ -401,18 +441,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
       // ---- phase B (converged): log / weight / one vector reduction per (piece, quad)
       for (int e = lane; e < npieces * geo.QW; e += 32) {
         const int pc = (int)(((float)e + 0.5f) * inv_qw);
-        const int qi = e - pc * geo.QW;
-        const int q2 = qb + qi;
-        const int32_t r = prow[pc];
-        if (r < 0 || q2 >= geo.nq) continue;
-        const int k0 = q2 * 4;
+        const int32_t doff = prow[pc];
+        const int k0 = (qb + e - pc * geo.QW) * 4;
+        if (doff < 0 || k0 >= c) continue;
         const AccT *t = tab + (size_t)e * 4;
         if (sizeof(AccT) == 4) {
           const float4 v = *reinterpret_cast<const float4 *>(t);
           float a0 = v.x, a1 = v.y, a2 = v.z, a3 = v.w;
-          if (kProd) {
-            a0 = log_prob(a0); a1 = log_prob(a1); a2 = log_prob(a2); a3 = log_prob(a3);
-          }
+          if (kProd) log4(a0, a1, a2, a3);
           if (EQW) {
             const float wv = (float)pw[pc];
             a0 *= wv; a1 *= wv; a2 *= wv; a3 *= wv;
@@ -422,12 +458,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
             if (k0 + 2 >= c) a2 = 0.f;
             if (k0 + 3 >= c) a3 = 0.f;
           }
-          float *dst = reinterpret_cast<float *>(p.accum) + (int64_t)r * p.stride + k0;
+          float *dst = reinterpret_cast<float *>(p.accum) + doff + k0;
           asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a0), "f"(a1), "f"(a2),
                        "f"(a3)
                        : "memory");
         } else {
-          double *dst = reinterpret_cast<double *>(p.accum) + (int64_t)r * p.stride + k0;
+          double *dst = reinterpret_cast<double *>(p.accum) + doff + k0;
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             if (k0 + k < c) atomicAdd(dst + k, (double)t[k]);
@@ -578,6 +614,9 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
   if (nframes <= 0 || hw <= 0) return TFB_OK;
   TFB_REQUIRE(hw * kMaxFrames < (1LL << 31), TFB_ERR_CAPACITY, "tfb_fuse: %lld pixels per frame is too many",
               (long long)hw);
+  TFB_REQUIRE(total_texels * accum_stride < (1LL << 31), TFB_ERR_CAPACITY,
+              "tfb_fuse: accumulator of %lld x %lld elements exceeds 32-bit row offsets", (long long)total_texels,
+              (long long)accum_stride);
   const size_t stage = (size_t)kChunk * num_classes * 4;
   const int NS = stage <= 2048 ? 4 : 2;
   TFB_REQUIRE(warp_layout(num_classes, NS, accum_is_f64 ? 8 : 4).total * kWarps <= 227 * 1024, TFB_ERR_CAPACITY,
