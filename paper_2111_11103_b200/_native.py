@@ -11,7 +11,7 @@ import os
 from .errors import CapacityError, DataError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "libtexelfuse_b200.so")
+LIB_PATH = os.environ.get("TFB_LIB") or os.path.join(_PKG, "_lib", "libtexelfuse_b200.so")
 
 TFB_OK, TFB_ERR_DATA, TFB_ERR_CAPACITY, TFB_ERR_STATE, TFB_ERR_CUDA, TFB_ERR_VALUE = range(6)
 AGG_IDS = {"sum": 0, "maxsum": 1, "mul": 2}

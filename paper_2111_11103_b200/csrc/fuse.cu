@@ -70,27 +70,19 @@ __host__ __device__ inline Geo geo_of(int c) {
   return g;
 }
 
-// at most one piece per pixel
-constexpr int kMaxPieces = kChunk;
-
 struct WarpSmem {
   size_t stage_floats;  // per stage, multiple of 4
-  size_t o_tab, o_pw, o_prow, o_w, o_max, o_bar, total;
+  size_t o_w, o_doff, o_max, o_bar, total;
 };
 
 __host__ __device__ inline size_t al(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 __host__ __device__ inline WarpSmem warp_layout(int c, int NS, int accbytes) {
-  const Geo g = geo_of(c);
   WarpSmem s;
   s.stage_floats = al((size_t)kChunk * c, 4);
   size_t o = (size_t)NS * s.stage_floats * 4;
-  s.o_tab = o = al(o, 32);
-  o += (size_t)kMaxPieces * g.QW * 4 * accbytes;
-  s.o_pw = o = al(o, 16);
-  o += (size_t)kMaxPieces * accbytes;
-  s.o_prow = o;
-  o += (size_t)kMaxPieces * 4;
+  s.o_doff = o;
+  o += (size_t)kChunk * 4;
   s.o_w = o = al(o, 16);
   o += (size_t)kChunk * accbytes;
   s.o_max = o;
@@ -211,8 +203,12 @@ __device__ __forceinline__ void log4(float &a0, float &a1, float &a2, float &a3)
   a1 = lg2_ln(x1);
   a2 = lg2_ln(x2);
   a3 = lg2_ln(x3);
+#ifdef TFB_LOG_SELECT
+  if (true) {
+#else
   const bool near1 = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3)) > 0.9f;
   if (__any_sync(__activemask(), near1)) {
+#endif
     if (x0 > 0.9f) a0 = log1p_series(x0);
     if (x1 > 0.9f) a1 = log1p_series(x1);
     if (x2 > 0.9f) a2 = log1p_series(x2);
@@ -242,9 +238,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
   const WarpSmem L = warp_layout(c, NS, (int)sizeof(AccT));
   unsigned char *ws = smem + (size_t)warp * L.total;
   float *stages = reinterpret_cast<float *>(ws);
-  AccT *tab = reinterpret_cast<AccT *>(ws + L.o_tab);
-  AccT *pw = reinterpret_cast<AccT *>(ws + L.o_pw);
-  int32_t *prow = reinterpret_cast<int32_t *>(ws + L.o_prow);
+  int32_t *sdoff = reinterpret_cast<int32_t *>(ws + L.o_doff);
   AccT *sw = reinterpret_cast<AccT *>(ws + L.o_w);
   float *smax = reinterpret_cast<float *>(ws + L.o_max);
   uint64_t *bar = reinterpret_cast<uint64_t *>(ws + L.o_bar);
@@ -291,7 +285,6 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
   const int i0 = g * geo.span;
   const int i1 = min(i0 + geo.span, kChunk);
   const bool grp_start = (lane % geo.span) == 0;  // lane as a pixel: first pixel of its group
-  const float inv_qw = 1.0f / (float)geo.QW;
 
   int32_t r_cur = row_at(p, cur, lane);
   double ws_cur = wsrc_at(p, cur, lane, r_cur);
@@ -308,7 +301,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
     const float *src = p.probs[cur.f] + start * c;
     float *st = stages + (size_t)s * L.stage_floats;
 
-    // pieces: runs of equal rows, split at group starts (and every 4 pixels for the product rule)
+    // pieces: runs of equal rows, split at group starts (and every 4 pixels for
+    // the product rule, so a piece's product of clipped probabilities stays normal)
     const AccT w = weight_from<AccT>(p, ws_cur, r_cur);
     const int32_t prev = __shfl_up_sync(0xffffffffu, r_cur, 1);
     const bool chg = lane == 0 || prev != r_cur || grp_start;
@@ -319,15 +313,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
       pstart = ((lane - rs) & 3) == 0;
     }
     const unsigned smask = __ballot_sync(0xffffffffu, pstart);
-    const int npieces = __popc(smask);
-    if (pstart) {
-      const int idx = __popc(smask & upto) - 1;
+    if (pstart && r_cur >= 0) {
       const unsigned above = smask & ~upto;
-      const int len = (above ? __ffs(above) - 1 : kChunk) - lane;
-      prow[idx] = r_cur >= 0 ? (int32_t)((int64_t)r_cur * p.stride) : -1;  // accumulator row offset
-      pw[idx] = w;
-      if (r_cur >= 0) atomicAdd(p.counts + r_cur, (uint32_t)len);  // fusion.py:182
+      atomicAdd(p.counts + r_cur, (uint32_t)((above ? __ffs(above) - 1 : kChunk) - lane));  // fusion.py:182
     }
+    sdoff[lane] = r_cur >= 0 ? (int32_t)((int64_t)r_cur * p.stride) : -1;  // accumulator row offset
     sw[lane] = w;
 
     if (tma_ok(src, npix, c)) {
@@ -357,121 +347,108 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
       __syncwarp();
     }
 
+#ifdef TFB_EXP_NOCOMPUTE
+    if (false)
+#endif
     for (int qb = 0; qb < geo.nq; qb += geo.QW) {
-      // ---- phase A (branch-free): lanes = (group g, quad qi) scan their pixels in order;
-      //      each pixel folds into its piece's running value, stored to the piece's table slot
+      // lanes = (pixel group g, class quad q): each group scans its pixels in
+      // order, folding them into the running value of their piece; when a piece
+      // ends the lane lands its quad with one vector reduction (fusion.py:180-181)
       const int q = qb + qi0;
       if (g < geo.G && q < geo.nq) {
         const int k0 = q * 4;
         const float *pp = st + (size_t)i0 * c + k0;
         const float pad = AGG == TFB_AGG_MUL ? 1.0f : 0.0f;
-        const int row4 = geo.QW * 4;
-        AccT *t = tab + ((size_t)(__popc(smask & ((1u << i0) - 1u)) - 1) * geo.QW + qi0) * 4;
-        if (kProd) {
-          float2 m01 = make_float2(1.f, 1.f), m23 = make_float2(1.f, 1.f);
-          for (int i = i0; i < i1; ++i, pp += c) {
-            float v0, v1, v2, v3;
-            if (vec_ok) {
-              const float4 v = *reinterpret_cast<const float4 *>(pp);
-              v0 = v.x; v1 = v.y; v2 = v.z; v3 = v.w;
+        AccT a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        float2 m01 = make_float2(1.f, 1.f), m23 = make_float2(1.f, 1.f);
+        int32_t doff = -1;
+        AccT wrun = 0;
+        auto flush = [&]() {
+          if (doff < 0) return;
+          if (sizeof(AccT) == 4) {
+            float b0, b1, b2, b3;
+            if (kProd) {
+              b0 = m01.x; b1 = m01.y; b2 = m23.x; b3 = m23.y;
+              log4(b0, b1, b2, b3);
             } else {
-              v0 = pp[0];
-              v1 = k0 + 1 < c ? pp[1] : pad;
-              v2 = k0 + 2 < c ? pp[2] : pad;
-              v3 = k0 + 3 < c ? pp[3] : pad;
+              b0 = (float)a0; b1 = (float)a1; b2 = (float)a2; b3 = (float)a3;
             }
-            if ((smask >> i) & 1u) {  // a new piece starts at pixel i
-              m01 = make_float2(1.f, 1.f);
-              m23 = make_float2(1.f, 1.f);
-              t += row4;
+            if (EQW) {
+              const float wv = (float)wrun;
+              b0 *= wv; b1 *= wv; b2 *= wv; b3 *= wv;
             }
+            if (!vec_ok) {  // padding columns receive exact zeros
+              if (k0 + 1 >= c) b1 = 0.f;
+              if (k0 + 2 >= c) b2 = 0.f;
+              if (k0 + 3 >= c) b3 = 0.f;
+            }
+            float *dst = reinterpret_cast<float *>(p.accum) + doff + k0;
+#ifdef TFB_EXP_NORED
+            if (b0 == 12345.0f)
+#endif
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(b0), "f"(b1), "f"(b2),
+                         "f"(b3));
+          } else {
+            double *dst = reinterpret_cast<double *>(p.accum) + doff + k0;
+            const double v[4] = {(double)a0, (double)a1, (double)a2, (double)a3};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (k0 + k < c) atomicAdd(dst + k, v[k]);
+          }
+        };
+#pragma unroll 2
+        for (int i = i0; i < i1; ++i, pp += c) {
+          float v0, v1, v2, v3;
+          if (vec_ok) {
+            const float4 v = *reinterpret_cast<const float4 *>(pp);
+            v0 = v.x; v1 = v.y; v2 = v.z; v3 = v.w;
+          } else {
+            v0 = pp[0];
+            v1 = k0 + 1 < c ? pp[1] : pad;
+            v2 = k0 + 2 < c ? pp[2] : pad;
+            v3 = k0 + 3 < c ? pp[3] : pad;
+          }
+          if ((smask >> i) & 1u) {  // a new piece starts at pixel i
+            flush();
+            doff = sdoff[i];
+            wrun = sw[i];
+            a0 = a1 = a2 = a3 = (AccT)0;
+            m01 = make_float2(1.f, 1.f);
+            m23 = make_float2(1.f, 1.f);
+          }
+          if (kProd) {
             m01 = mul2(m01, make_float2(clip_mul(v0), clip_mul(v1)));
             m23 = mul2(m23, make_float2(clip_mul(v2), clip_mul(v3)));
-            *reinterpret_cast<float4 *>(t) = make_float4(m01.x, m01.y, m23.x, m23.y);
-          }
-        } else {
-          AccT a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-          for (int i = i0; i < i1; ++i, pp += c) {
-            float v0, v1, v2, v3;
-            if (vec_ok) {
-              const float4 v = *reinterpret_cast<const float4 *>(pp);
-              v0 = v.x; v1 = v.y; v2 = v.z; v3 = v.w;
-            } else {
-              v0 = pp[0];
-              v1 = k0 + 1 < c ? pp[1] : pad;
-              v2 = k0 + 2 < c ? pp[2] : pad;
-              v3 = k0 + 3 < c ? pp[3] : pad;
+          } else if (sizeof(AccT) == 4) {
+            const float wi = EQW ? 1.0f : (float)sw[i];
+            float t0 = v0, t1 = v1, t2 = v2, t3 = v3;
+            if (AGG == TFB_AGG_MAXSUM) {
+              const float mx = smax[i];
+              t0 = v0 == mx ? v0 : 0.f; t1 = v1 == mx ? v1 : 0.f; t2 = v2 == mx ? v2 : 0.f; t3 = v3 == mx ? v3 : 0.f;
+            } else if (AGG == TFB_AGG_MUL) {
+              t0 = log_prob(clip_mul(v0)); t1 = log_prob(clip_mul(v1));
+              t2 = log_prob(clip_mul(v2)); t3 = log_prob(clip_mul(v3));
             }
-            if ((smask >> i) & 1u) {
-              a0 = a1 = a2 = a3 = (AccT)0;
-              t += row4;
-            }
-            if (sizeof(AccT) == 4) {
-              const float wi = EQW ? 1.0f : (float)sw[i];
-              float t0 = v0, t1 = v1, t2 = v2, t3 = v3;
-              if (AGG == TFB_AGG_MAXSUM) {
-                const float mx = smax[i];
-                t0 = v0 == mx ? v0 : 0.f; t1 = v1 == mx ? v1 : 0.f; t2 = v2 == mx ? v2 : 0.f; t3 = v3 == mx ? v3 : 0.f;
-              } else if (AGG == TFB_AGG_MUL) {
-                t0 = log_prob(clip_mul(v0)); t1 = log_prob(clip_mul(v1));
-                t2 = log_prob(clip_mul(v2)); t3 = log_prob(clip_mul(v3));
-              }
-              a0 = fmaf(wi, t0, (float)a0); a1 = fmaf(wi, t1, (float)a1);
-              a2 = fmaf(wi, t2, (float)a2); a3 = fmaf(wi, t3, (float)a3);
-              *reinterpret_cast<float4 *>(t) = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
-            } else {
-              // float64 parity mode: the reference's per-pixel w * f(p) (fusion.py:171-177)
-              const double wi = (double)sw[i];
-              const float vv[4] = {v0, v1, v2, v3};
-              double tt[4];
+            a0 = fmaf(wi, t0, (float)a0); a1 = fmaf(wi, t1, (float)a1);
+            a2 = fmaf(wi, t2, (float)a2); a3 = fmaf(wi, t3, (float)a3);
+          } else {
+            // float64 parity mode: the reference's per-pixel w * f(p) (fusion.py:171-177)
+            const double wi = (double)sw[i];
+            const float vv[4] = {v0, v1, v2, v3};
+            double tt[4];
 #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                if (AGG == TFB_AGG_SUM) tt[k] = (double)vv[k];
-                else if (AGG == TFB_AGG_MAXSUM) tt[k] = vv[k] == smax[i] ? (double)vv[k] : 0.0;
-                else tt[k] = log(np_clip((double)vv[k], kMulClamp, 1.0));
-              }
-              a0 += wi * tt[0]; a1 += wi * tt[1]; a2 += wi * tt[2]; a3 += wi * tt[3];
-              t[0] = a0; t[1] = a1; t[2] = a2; t[3] = a3;
+            for (int k = 0; k < 4; ++k) {
+              if (AGG == TFB_AGG_SUM) tt[k] = (double)vv[k];
+              else if (AGG == TFB_AGG_MAXSUM) tt[k] = vv[k] == smax[i] ? (double)vv[k] : 0.0;
+              else tt[k] = log(np_clip((double)vv[k], kMulClamp, 1.0));
             }
+            a0 += wi * tt[0]; a1 += wi * tt[1]; a2 += wi * tt[2]; a3 += wi * tt[3];
           }
         }
+        flush();
       }
-      __syncwarp();
-
-      // ---- phase B (converged): log / weight / one vector reduction per (piece, quad)
-      for (int e = lane; e < npieces * geo.QW; e += 32) {
-        const int pc = (int)(((float)e + 0.5f) * inv_qw);
-        const int32_t doff = prow[pc];
-        const int k0 = (qb + e - pc * geo.QW) * 4;
-        if (doff < 0 || k0 >= c) continue;
-        const AccT *t = tab + (size_t)e * 4;
-        if (sizeof(AccT) == 4) {
-          const float4 v = *reinterpret_cast<const float4 *>(t);
-          float a0 = v.x, a1 = v.y, a2 = v.z, a3 = v.w;
-          if (kProd) log4(a0, a1, a2, a3);
-          if (EQW) {
-            const float wv = (float)pw[pc];
-            a0 *= wv; a1 *= wv; a2 *= wv; a3 *= wv;
-          }
-          if (!vec_ok) {  // padding columns receive exact zeros
-            if (k0 + 1 >= c) a1 = 0.f;
-            if (k0 + 2 >= c) a2 = 0.f;
-            if (k0 + 3 >= c) a3 = 0.f;
-          }
-          float *dst = reinterpret_cast<float *>(p.accum) + doff + k0;
-          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a0), "f"(a1), "f"(a2),
-                       "f"(a3)
-                       : "memory");
-        } else {
-          double *dst = reinterpret_cast<double *>(p.accum) + doff + k0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (k0 + k < c) atomicAdd(dst + k, (double)t[k]);
-        }
-      }
-      __syncwarp();
     }
-
+    __syncwarp();
     // stage s, table and side arrays are free again
     if (lane == 0) {
       Pos ahead = cur;
