@@ -30,7 +30,13 @@
 namespace tfb {
 namespace {
 
-constexpr int kWarps = 4;        // warps per CTA (independent pipelines)
+#ifndef TFB_FUSE_WARPS
+#define TFB_FUSE_WARPS 4
+#endif
+#ifndef TFB_FUSE_NS
+#define TFB_FUSE_NS 2
+#endif
+constexpr int kWarps = TFB_FUSE_WARPS;  // warps per CTA (independent pipelines)
 constexpr int kChunk = 32;       // pixels per work item = one per lane
 constexpr int kMaxFrames = 32;   // frames per launch (pointers travel in the kernel parameters)
 
@@ -595,7 +601,7 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
               "tfb_fuse: accumulator of %lld x %lld elements exceeds 32-bit row offsets", (long long)total_texels,
               (long long)accum_stride);
   const size_t stage = (size_t)kChunk * num_classes * 4;
-  const int NS = stage <= 2048 ? 4 : 2;
+  const int NS = stage <= 2048 ? 4 : TFB_FUSE_NS;
   TFB_REQUIRE(warp_layout(num_classes, NS, accum_is_f64 ? 8 : 4).total * kWarps <= 227 * 1024, TFB_ERR_CAPACITY,
               "tfb_fuse: %d classes exceed the shared-memory staging budget", num_classes);
   FuseParams p;
