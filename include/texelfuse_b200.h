@@ -72,8 +72,8 @@ int tfb_set_option(int option, int value);
 /* Bytes of scratch tfb_rasterize needs for up to `max_frames` frames of
  * width x height; `pair_capacity` = triangle/tile pairs budgeted per frame
  * (0 = default).  Tiles whose lists overflow it stay exact (slow path). */
-size_t tfb_raster_workspace_bytes(int64_t num_triangles, int width, int height, int max_frames,
-                                  int64_t pair_capacity);
+size_t tfb_raster_workspace_bytes(int64_t num_vertices, int64_t num_triangles, int width, int height,
+                                  int max_frames, int64_t pair_capacity);
 
 /* rasterizer.py:93-202 (rasterize) for `nframes` cameras of one size.
  * Bit-exact with the reference: ascending-triangle sequential depth fold

@@ -59,6 +59,10 @@ struct Work {
   RecGeom *geom;
   RecMeta *meta;
   uint8_t *vmask;       // per frame per triangle: bit k = fan sub-triangle k has a record
+  uint32_t *cand;       // per frame: triangles surviving the outcode cull (count in fcnt[4f+2])
+  double *vcam;         // per frame per vertex: camera-space xyz (k_verts)
+  uint8_t *vcode;       // per frame per vertex: clip outcode (k_verts)
+  int64_t nv;
   uint32_t *fcnt;       // fcnt[1]: big-tile count
   uint32_t *tile_count; // per frame per tile
   uint32_t *tile_cursor;
@@ -71,7 +75,7 @@ struct Work {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-bool carve(void *ws, size_t ws_bytes, int64_t m, int nframes, int ntiles, int64_t cap, Work &w,
+bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int ntiles, int64_t cap, Work &w,
            size_t *need_out) {
   const int64_t rs = 2 * (m > 0 ? m : 1);
   size_t off = 0;
@@ -83,6 +87,9 @@ bool carve(void *ws, size_t ws_bytes, int64_t m, int nframes, int ntiles, int64_
   size_t o_geom = take(sizeof(RecGeom) * rs * nframes);
   size_t o_meta = take(sizeof(RecMeta) * rs * nframes);
   size_t o_vis = take((size_t)(rs / 2) * nframes);
+  size_t o_cand = take(sizeof(uint32_t) * (size_t)(rs / 2) * nframes);
+  size_t o_vcam = take(sizeof(double) * 3 * (size_t)(nv > 0 ? nv : 1) * nframes);
+  size_t o_vcode = take((size_t)(nv > 0 ? nv : 1) * nframes);
   size_t o_fcnt = take(sizeof(uint32_t) * 4 * nframes);
   size_t o_tc = take(sizeof(uint32_t) * ntiles * nframes);
   size_t o_cur = take(sizeof(uint32_t) * ntiles * nframes);
@@ -95,6 +102,10 @@ bool carve(void *ws, size_t ws_bytes, int64_t m, int nframes, int ntiles, int64_
   w.geom = reinterpret_cast<RecGeom *>(b + o_geom);
   w.meta = reinterpret_cast<RecMeta *>(b + o_meta);
   w.vmask = reinterpret_cast<uint8_t *>(b + o_vis);
+  w.cand = reinterpret_cast<uint32_t *>(b + o_cand);
+  w.vcam = reinterpret_cast<double *>(b + o_vcam);
+  w.vcode = reinterpret_cast<uint8_t *>(b + o_vcode);
+  w.nv = nv > 0 ? nv : 1;
   w.fcnt = reinterpret_cast<uint32_t *>(b + o_fcnt);
   w.tile_count = reinterpret_cast<uint32_t *>(b + o_tc);
   w.tile_cursor = reinterpret_cast<uint32_t *>(b + o_cur);
@@ -229,65 +240,128 @@ __device__ __forceinline__ void store_record(const Work &w, int f, int64_t slot,
     for (int tx = mt.x0 / kTile; tx <= mt.x1 / kTile; ++tx) atomicAdd(tc + ty * TX + tx, 1u);
 }
 
+// Per (frame, vertex): the camera-space position (FMA order of geometry.py:161)
+// and a clip outcode.  bit 0: z < NEAR_PLANE; bits 1-4: the vertex projects
+// more than 1/4 pixel beyond the left / right / top / bottom image edge (set
+// only when z >= NEAR_PLANE, tested without divisions).  A triangle whose
+// three outcodes share bit 0 is skipped exactly as rasterizer.py:111 skips it;
+// one sharing an edge bit has an empty bbox in the reference
+// (rasterizer.py:141-146) — the 1/4 px margin dwarfs the rounding of these
+// products, so no visible triangle is dropped.
+__global__ void __launch_bounds__(kThreads) k_verts(tfb_scene sc, const double *__restrict__ cams, int W, int H,
+                                                    Work w) {
+  const int f = blockIdx.y;
+  __shared__ Cam cam;
+  load_cam(cam, cams, f);
+  __syncthreads();
+  const int64_t v = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (v >= sc.num_vertices) return;
+  double P[3];
+  xform(cam, sc.vertices + 3 * v, P);
+  double *dst = w.vcam + ((int64_t)f * w.nv + v) * 3;
+  dst[0] = P[0];
+  dst[1] = P[1];
+  dst[2] = P[2];
+  uint32_t code;
+  if (P[2] < kNearPlane) {
+    code = 1u;
+  } else {
+    const double z = P[2];
+    code = ((P[0] * cam.fx + (cam.cx - 0.25) * z < 0.0) ? 2u : 0u) |
+           ((P[0] * cam.fx + (cam.cx - ((double)W - 0.25)) * z > 0.0) ? 4u : 0u) |
+           ((P[1] * cam.fy + (cam.cy - 0.25) * z < 0.0) ? 8u : 0u) |
+           ((P[1] * cam.fy + (cam.cy - ((double)H - 0.25)) * z > 0.0) ? 16u : 0u);
+  }
+  w.vcode[(int64_t)f * w.nv + v] = (uint8_t)code;
+}
+
+// Per (frame, triangle), light and fully occupied: the AND of the three
+// vertex outcodes decides whether the triangle can produce a record at all;
+// survivors are appended (one global atomic per block) to the frame's
+// candidate list; every triangle's visibility mask is reset.
+__global__ void __launch_bounds__(kThreads) k_cull(tfb_scene sc, Work w) {
+  const int f = blockIdx.y;
+  __shared__ uint32_t wtot[kThreads / 32];
+  __shared__ uint32_t base;
+  const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  bool cand = false;
+  if (t < sc.num_triangles) {
+    const int64_t i0 = __ldg(sc.triangles + 3 * t), i1 = __ldg(sc.triangles + 3 * t + 1),
+                  i2 = __ldg(sc.triangles + 3 * t + 2);
+    const uint8_t *vc = w.vcode + (int64_t)f * w.nv;
+    cand = (vc[i0] & vc[i1] & vc[i2]) == 0u;  // not all behind the near plane nor beyond one edge
+    w.vmask[(int64_t)f * (w.rs / 2) + t] = 0;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned bal = __ballot_sync(0xffffffffu, cand);
+  if (lane == 0) wtot[warp] = __popc(bal);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t s = 0;
+    for (int i = 0; i < kThreads / 32; ++i) {
+      const uint32_t v = wtot[i];
+      wtot[i] = s;
+      s += v;
+    }
+    base = s ? atomicAdd(w.fcnt + 4 * f + 2, s) : 0u;
+  }
+  __syncthreads();
+  if (cand) w.cand[(int64_t)f * (w.rs / 2) + base + wtot[warp] + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)t;
+}
+
+// Per surviving (frame, triangle): near clip + fan, projection, bbox, signed
+// area, CCW reorder and edge setup (rasterizer.py:113-164) into 128-byte
+// records at slot 2t+sub; tile coverage counted.
 __global__ void __launch_bounds__(kThreads, 4) k_setup(tfb_scene sc, const double *__restrict__ cams, int W,
                                                     int H, int TX, int ntiles, Work w) {
   const int f = blockIdx.y;
   __shared__ Cam cam;
   load_cam(cam, cams, f);
   __syncthreads();
-  const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  uint32_t mask = 0;
-  if (t < sc.num_triangles) {
+  const uint32_t ncand = w.fcnt[4 * f + 2];
+  const uint32_t *cl = w.cand + (int64_t)f * (w.rs / 2);
+  for (uint32_t ci = blockIdx.x * kThreads + threadIdx.x; ci < ncand; ci += gridDim.x * kThreads) {
+    const int64_t t = cl[ci];
+    const int64_t i0 = __ldg(sc.triangles + 3 * t), i1 = __ldg(sc.triangles + 3 * t + 1),
+                  i2 = __ldg(sc.triangles + 3 * t + 2);
+    const uint8_t *vc = w.vcode + (int64_t)f * w.nv;
+    const bool unclipped = ((vc[i0] | vc[i1] | vc[i2]) & 1u) == 0u;  // zmin >= NEAR_PLANE
+    const double *vp = w.vcam + (int64_t)f * w.nv * 3;
     double P[3][3];
-    tri_cam(sc, cam, t, P);
-    const double zmax = fmax(fmax(P[0][2], P[1][2]), P[2][2]);
-    const double zmin = fmin(fmin(P[0][2], P[1][2]), P[2][2]);
-    bool live = !(zmax < kNearPlane);  // rasterizer.py:111
-    if (live && zmin >= kNearPlane) {
-      // Conservative frustum cull without divisions: a triangle whose vertices
-      // all project more than 1/4 pixel beyond one image edge has an empty
-      // bbox in the reference (rasterizer.py:141-146); the 1/4 px margin dwarfs
-      // the rounding of these products, so no visible triangle is dropped.
-      bool l = true, r = true, u = true, d = true;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const double z = P[k][2];
-        l = l && (P[k][0] * cam.fx + (cam.cx - 0.25) * z < 0.0);
-        r = r && (P[k][0] * cam.fx + (cam.cx - ((double)W - 0.25)) * z > 0.0);
-        u = u && (P[k][1] * cam.fy + (cam.cy - 0.25) * z < 0.0);
-        d = d && (P[k][1] * cam.fy + (cam.cy - ((double)H - 0.25)) * z > 0.0);
-      }
-      live = !(l || r || u || d);
+    for (int q = 0; q < 3; ++q) {
+      P[0][q] = vp[3 * i0 + q];
+      P[1][q] = vp[3 * i1 + q];
+      P[2][q] = vp[3 * i2 + q];
     }
-    if (live) {
-      RecGeom g;
-      RecMeta mt;
-      const uint32_t tflags = ((uint32_t)__ldg(sc.origins + t) << 5) | ((uint32_t)__ldg(sc.steps + t) << 16);
-      if (zmin >= kNearPlane) {
-        if (build_record(cam, W, H, P, (int)t, false, 0, tflags, g, mt)) {
-          store_record(w, f, 2 * t, g, mt, ntiles, TX);
-          mask = 1;
-        }
-      } else {
-        double op[4][3], ob[4][3];
-        const int n = clip_near(P, op, ob);
-        for (int k = 1; k + 1 < n; ++k) {  // fan (0, k, k+1), rasterizer.py:119-122
-          double S[3][3];
+    uint32_t mask = 0;
+    RecGeom g;
+    RecMeta mt;
+    const uint32_t tflags = ((uint32_t)__ldg(sc.origins + t) << 5) | ((uint32_t)__ldg(sc.steps + t) << 16);
+    if (unclipped) {
+      if (build_record(cam, W, H, P, (int)t, false, 0, tflags, g, mt)) {
+        store_record(w, f, 2 * t, g, mt, ntiles, TX);
+        mask = 1;
+      }
+    } else {
+      double op[4][3], ob[4][3];
+      const int n = clip_near(P, op, ob);
+      for (int k = 1; k + 1 < n; ++k) {  // fan (0, k, k+1), rasterizer.py:119-122
+        double S[3][3];
 #pragma unroll
-          for (int q = 0; q < 3; ++q) {
-            S[0][q] = op[0][q];
-            S[1][q] = op[k][q];
-            S[2][q] = op[k + 1][q];
-          }
-          if (build_record(cam, W, H, S, (int)t, true, k - 1, tflags, g, mt)) {
-            store_record(w, f, 2 * t + (k - 1), g, mt, ntiles, TX);
-            mask |= 1u << (k - 1);
-          }
+        for (int q = 0; q < 3; ++q) {
+          S[0][q] = op[0][q];
+          S[1][q] = op[k][q];
+          S[2][q] = op[k + 1][q];
+        }
+        if (build_record(cam, W, H, S, (int)t, true, k - 1, tflags, g, mt)) {
+          store_record(w, f, 2 * t + (k - 1), g, mt, ntiles, TX);
+          mask |= 1u << (k - 1);
         }
       }
     }
+    if (mask) w.vmask[(int64_t)f * (w.rs / 2) + t] = (uint8_t)mask;
   }
-  if (t < sc.num_triangles) w.vmask[(int64_t)f * (w.rs / 2) + t] = (uint8_t)mask;
 }
 
 __global__ void __launch_bounds__(1024) k_scan(Work w, int ntiles) {
@@ -332,15 +406,18 @@ __global__ void __launch_bounds__(1024) k_scan(Work w, int ntiles) {
 __global__ void __launch_bounds__(256) k_fill(Work w, int64_t m, int ntiles, int TX) {
   const int f = blockIdx.y;
   const uint8_t *vm = w.vmask + (int64_t)f * m;
+  const uint32_t *cl = w.cand + (int64_t)f * m;
+  const uint32_t ncand = w.fcnt[4 * f + 2];
   const RecMeta *meta = w.meta + (int64_t)f * w.rs;
   const uint64_t *toff = w.tile_off + (int64_t)f * ntiles;
   uint32_t *cur = w.tile_cursor + (int64_t)f * ntiles;
   uint32_t *list = w.list + (int64_t)f * w.cap;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+  for (uint32_t ci = blockIdx.x * blockDim.x + threadIdx.x; ci < ncand; ci += gridDim.x * blockDim.x) {
+    const uint32_t t = cl[ci];
     const uint32_t mask = vm[t];
     for (int sub = 0; sub < 2; ++sub) {
       if (!((mask >> sub) & 1u)) continue;
-      const uint32_t r = (uint32_t)(2 * t + sub);
+      const uint32_t r = 2 * t + sub;
       const RecMeta mt = meta[r];
       for (int ty = mt.y0 / kTile; ty <= mt.y1 / kTile; ++ty)
         for (int tx = mt.x0 / kTile; tx <= mt.x1 / kTile; ++tx) {
@@ -572,10 +649,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const doub
     sbox[tid] = (uint32_t)bx0 | ((uint32_t)by0 << 8) | (bw << 16) | (bh << 24);
     area = bw * bh;
   }
-  for (uint32_t i = tid; i < n * 8; i += kThreads) {  // 8 x 16 B per 128-byte record
+  // 8 x 16 B per 128-byte record, all in flight at once (cp.async), completed before the barrier
+  for (uint32_t i = tid; i < n * 8; i += kThreads) {
     const uint32_t rec = i >> 3, q = i & 7;
-    reinterpret_cast<double2 *>(sgeom + rec)[q] = reinterpret_cast<const double2 *>(geom + src[rec])[q];
+    const void *gsrc = reinterpret_cast<const double2 *>(geom + src[rec]) + q;
+    const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(reinterpret_cast<double2 *>(sgeom + rec) + q);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(gsrc) : "memory");
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   uint32_t incl = area;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -583,6 +664,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const doub
     if (lane >= d) incl += v;
   }
   if (lane == 31) wtot[warp] = incl;
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   uint32_t wbase = 0, total = 0;
 #pragma unroll
@@ -800,14 +882,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster_big(tfb_scene sc, const 
 
 using namespace tfb;
 
-extern "C" size_t tfb_raster_workspace_bytes(int64_t num_triangles, int width, int height, int max_frames,
-                                             int64_t pair_capacity) {
+extern "C" size_t tfb_raster_workspace_bytes(int64_t num_vertices, int64_t num_triangles, int width, int height,
+                                             int max_frames, int64_t pair_capacity) {
   const int TX = (width + kTile - 1) / kTile, TY = (height + kTile - 1) / kTile;
   const int ntiles = TX * TY;
   const int64_t cap = pair_capacity > 0 ? pair_capacity : default_cap(num_triangles, ntiles);
   Work w;
   size_t need = 0;
-  carve(nullptr, 0, num_triangles, max_frames, ntiles, cap, w, &need);
+  carve(nullptr, 0, num_vertices, num_triangles, max_frames, ntiles, cap, w, &need);
   return need;
 }
 
@@ -831,7 +913,7 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
   const int64_t cap = pair_capacity > 0 ? pair_capacity : default_cap(m, ntiles);
   Work w;
   size_t need = 0;
-  if (!carve(workspace, workspace_bytes, m, nframes, ntiles, cap, w, &need)) {
+  if (!carve(workspace, workspace_bytes, scene->num_vertices, m, nframes, ntiles, cap, w, &need)) {
     set_error("tfb_rasterize: workspace of %zu bytes is smaller than the %zu required", workspace_bytes, need);
     return TFB_ERR_CAPACITY;
   }
@@ -840,8 +922,15 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
   cudaMemsetAsync(w.tile_cursor, 0, sizeof(uint32_t) * ntiles * nframes, st);
   tfb_scene sc = *scene;
   if (m > 0) {
+    if (sc.num_vertices > 0) {
+      dim3 g0((unsigned)((sc.num_vertices + kThreads - 1) / kThreads), nframes);
+      k_verts<<<g0, kThreads, 0, st>>>(sc, cams, width, height, w);
+    }
     dim3 g1((unsigned)((m + kThreads - 1) / kThreads), nframes);
-    k_setup<<<g1, kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w);
+    k_cull<<<g1, kThreads, 0, st>>>(sc, w);
+    int64_t sb = (m / 3 + kThreads - 1) / kThreads;  // ~1/3 of the triangles survive a typical cull
+    dim3 g2((unsigned)(sb < 1 ? 1 : sb), nframes);
+    k_setup<<<g2, kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w);
     k_scan<<<nframes, 1024, 0, st>>>(w, ntiles);
     int64_t fb = (m + 255) / 256;
     const int fill_blocks = (int)(fb < 1184 ? fb : 1184);

@@ -69,7 +69,8 @@ class DeviceScene:
         key = (width, height)
         ws = self._ws.get(key)
         if ws is None or ws[0] < nframes:
-            nbytes = N.load().tfb_raster_workspace_bytes(self.num_triangles, width, height, nframes, 0)
+            nbytes = N.load().tfb_raster_workspace_bytes(int(self.struct.num_vertices), self.num_triangles, width,
+                                                         height, nframes, 0)
             ws = (nframes, torch.empty(nbytes, dtype=torch.uint8, device=self.device))
             self._ws[key] = ws
         return ws[1]

@@ -108,7 +108,7 @@ def test_raster_overflow_fallback_exact():
     ann = MeshAnnotation(mesh, layout, num_classes=4, max_batch=2)
     sc = ann.scene
     cams = sc.cams_tensor(frames)
-    nbytes = N.load().tfb_raster_workspace_bytes(mesh.num_triangles, 128, 96, 2, 16)
+    nbytes = N.load().tfb_raster_workspace_bytes(mesh.num_vertices, mesh.num_triangles, 128, 96, 2, 16)
     ws = torch.empty(nbytes, dtype=torch.uint8, device=ann.device)
     rows = torch.empty((2, 128 * 96), dtype=torch.int32, device=ann.device)
     N.call("tfb_rasterize", sc.sref, N.ptr(cams), 2, 128, 96, N.ptr(ws), nbytes, 16, N.ptr(rows), None, None, None,

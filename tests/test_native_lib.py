@@ -41,8 +41,8 @@ def test_library_is_sm100a():
 
 def test_workspace_query_is_host_only():
     lib = N.load()
-    a = lib.tfb_raster_workspace_bytes(299568, 640, 480, 1, 0)
-    b = lib.tfb_raster_workspace_bytes(299568, 640, 480, 8, 0)
+    a = lib.tfb_raster_workspace_bytes(151686, 299568, 640, 480, 1, 0)
+    b = lib.tfb_raster_workspace_bytes(151686, 299568, 640, 480, 8, 0)
     assert a > 299568 * 2 * 128 and b > 7 * a
 
 
