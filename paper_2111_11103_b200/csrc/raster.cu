@@ -45,7 +45,7 @@ static_assert(sizeof(RecGeom) == 128, "record geometry is one 128-byte line");
 
 struct __align__(16) RecMeta {
   int16_t x0, x1, y0, y1;  // clamped pixel bbox (rasterizer.py:141-146)
-  int32_t t;               // triangle index
+  int32_t off;             // offsets[t]: first global texel row of the triangle (n_x < 2^31)
   uint32_t flags;          // bits 0-2 edge accept, 3 reordered, 4 clipped, 5-6 uv origin,
                            // 7 fan sub-triangle, 16-31 subdivision steps
 };
@@ -185,7 +185,7 @@ __device__ __forceinline__ bool boundary_accept(double ax, double ay, double bx,
 
 // rasterizer.py:136-164 up to the per-pixel loop.  Returns false when the
 // reference would return early (empty bbox, zero or non-finite area).
-__device__ bool build_record(const Cam &cam, int W, int H, const double P[3][3], int t, bool clipped, int sub,
+__device__ bool build_record(const Cam &cam, int W, int H, const double P[3][3], int32_t off, bool clipped, int sub,
                              uint32_t tflags, RecGeom &g, RecMeta &mt) {
   double xs0[3], ys0[3], zs0[3];
 #pragma unroll
@@ -222,7 +222,7 @@ __device__ bool build_record(const Cam &cam, int W, int H, const double P[3][3],
   mt.x1 = (int16_t)x1d;
   mt.y0 = (int16_t)y0d;
   mt.y1 = (int16_t)y1d;
-  mt.t = t;
+  mt.off = off;
   mt.flags = flags;
   return true;
 }
@@ -338,8 +338,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_setup(tfb_scene sc, const doubl
     RecGeom g;
     RecMeta mt;
     const uint32_t tflags = ((uint32_t)__ldg(sc.origins + t) << 5) | ((uint32_t)__ldg(sc.steps + t) << 16);
+    const int32_t toff = (int32_t)__ldg(sc.offsets + t);
     if (unclipped) {
-      if (build_record(cam, W, H, P, (int)t, false, 0, tflags, g, mt)) {
+      if (build_record(cam, W, H, P, toff, false, 0, tflags, g, mt)) {
         store_record(w, f, 2 * t, g, mt, ntiles, TX);
         mask = 1;
       }
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_setup(tfb_scene sc, const doubl
           S[1][q] = op[k][q];
           S[2][q] = op[k + 1][q];
         }
-        if (build_record(cam, W, H, S, (int)t, true, k - 1, tflags, g, mt)) {
+        if (build_record(cam, W, H, S, toff, true, k - 1, tflags, g, mt)) {
           store_record(w, f, 2 * t + (k - 1), g, mt, ntiles, TX);
           mask |= 1u << (k - 1);
         }
@@ -637,24 +638,24 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const doub
   const RecGeom *geom = w.geom + (int64_t)f * w.rs;
   uint32_t area = 0;
   if (tid < n) {
+    // one thread per record: 8 x 16 B async copies of its geometry, in flight
+    // while the meta is read; completed before the barrier
     const uint32_t key = src[tid];
+    const double2 *gsrc = reinterpret_cast<const double2 *>(geom + key);
+    const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(sgeom + tid);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst + 16 * q), "l"(gsrc + q) : "memory");
     const RecMeta mt = w.meta[(int64_t)f * w.rs + key];
     skey[tid] = key;
     sflags[tid] = mt.flags;
-    stri[tid] = mt.t;
-    soff[tid] = (int32_t)__ldg(sc.offsets + mt.t);
+    stri[tid] = (int32_t)(key >> 1);
+    soff[tid] = mt.off;
     const int bx0 = max((int)mt.x0, tx0) - tx0, bx1 = min((int)mt.x1, tx0 + kTile - 1) - tx0;
     const int by0 = max((int)mt.y0, ty0) - ty0, by1 = min((int)mt.y1, ty0 + kTile - 1) - ty0;
     const uint32_t bw = (uint32_t)(bx1 - bx0 + 1), bh = (uint32_t)(by1 - by0 + 1);
     sbox[tid] = (uint32_t)bx0 | ((uint32_t)by0 << 8) | (bw << 16) | (bh << 24);
     area = bw * bh;
-  }
-  // 8 x 16 B per 128-byte record, all in flight at once (cp.async), completed before the barrier
-  for (uint32_t i = tid; i < n * 8; i += kThreads) {
-    const uint32_t rec = i >> 3, q = i & 7;
-    const void *gsrc = reinterpret_cast<const double2 *>(geom + src[rec]) + q;
-    const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(reinterpret_cast<double2 *>(sgeom + rec) + q);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(gsrc) : "memory");
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
   uint32_t incl = area;
@@ -819,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster_big(tfb_scene sc, const 
             empty.x1 = 0;
             empty.y0 = 1;
             empty.y1 = 0;
-            empty.t = -1;
+            empty.off = 0;
             empty.flags = 0;
             smeta[threadIdx.x] = empty;
           }
@@ -869,8 +870,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster_big(tfb_scene sc, const 
     }
     if (in_img) {
       const uint32_t flags = fd.win >= 0 ? meta[fd.win].flags : 0u;
-      const int32_t t = fd.win >= 0 ? meta[fd.win].t : -1;
-      write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, t >= 0 ? __ldg(sc.offsets + t) : 0);
+      const int32_t t = fd.win >= 0 ? (int32_t)((uint32_t)fd.win >> 1) : -1;
+      write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, fd.win >= 0 ? meta[fd.win].off : 0);
     }
   }
 }
