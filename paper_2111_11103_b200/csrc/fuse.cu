@@ -10,11 +10,14 @@
 // warp's lanes
 //   1. hold the chunk's texel rows and weights in registers, prefetched one
 //      and two items ahead (rows, then the dependent hit-count gather);
-//   2. find runs of consecutive pixels on the same texel with two ballots
-//      (segments; ~2.5 pixels per run at the BASELINE scene);
-//   3. take (segment, 4-class quad) items: the run's transformed probabilities
-//      are reduced from shared memory and land with ONE vector reduction
-//      red.global.add.v4.f32 per quad, plus one u32 count add per run.
+//   2. find runs of consecutive pixels on the same texel with ballots and cut
+//      them into pieces at pixel-group starts (and every 4 pixels for the
+//      product rule); ~2.5 pixels per run at the BASELINE scene;
+//   3. work as lanes = (pixel group g, class quad q): each lane folds its
+//      group's pixels of quad q straight out of the staged shared-memory rows
+//      (sum, or product of <= 4 clipped probabilities with f32x2 multiplies)
+//      and lands every finished piece with ONE red.global.add.v4.f32, plus one
+//      u32 count add by the piece's head lane.
 // Weights derived from the hit counts (pixels_iid / images_iid / blend) are
 // equal inside a run, so w is applied once per item, and for the product
 // rule sum_i w*log(p_i) is evaluated as w*log(prod_i p_i) over up to four
