@@ -65,8 +65,11 @@ int tfb_version(void);
 
 /* Tuning knobs (process-wide).  TFB_OPT_FUSE_CTAS_PER_SM caps the resident
  * tfb_fuse CTAs per SM (0 = as many as fit), leaving room for a rasterizer
- * running concurrently on another stream. */
+ * running concurrently on another stream.  TFB_OPT_FUSE_FAST (default 1)
+ * enables the specialised float32 / count-weight / c % 4 == 0 scatter-add
+ * kernel; 0 routes every tfb_fuse call through the general kernel. */
 #define TFB_OPT_FUSE_CTAS_PER_SM 1
+#define TFB_OPT_FUSE_FAST 2
 int tfb_set_option(int option, int value);
 
 /* Bytes of scratch tfb_rasterize needs for up to `max_frames` frames of

@@ -54,6 +54,7 @@ struct FuseParams {
   int64_t n_x;
   int wmode;
   double alpha;
+  float wa, wb;  // k_fuse_fast: w = wa + wb / hits (pixels_iid 1,0; images_iid 0,1; blend 1-alpha,alpha)
   void *accum;
   int64_t stride;
   uint32_t *counts;
@@ -477,34 +478,345 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
   }
 }
 
-int g_fuse_ctas_per_sm = 0;  // 0 = as many as fit (tfb_set_option(TFB_OPT_FUSE_CTAS_PER_SM))
+// ---------------------------------------------------------------------------
+// k_fuse_fast: the float32-accumulator, count-derived-weight (pixels_iid /
+// images_iid / blend), 16-byte-aligned, c % 4 == 0 case -- the BASELINE
+// workload.  Same pipeline as k_fuse, but the piece epilogue is taken out of
+// the divergent pixel scan:
+//   scan      lanes = (pixel group g, class quad q) fold their group's pixels
+//             into per-piece values (product / sum) and write each finished
+//             piece's quad IN PLACE over the piece's first pixel in the staged
+//             rows (that lane has already consumed those 16 bytes);
+//   epilogue  converged: lanes = (piece, quad) pairs read the folded quads back
+//             and land w*log2(prod)*ln2 (or w*sum) with one red.v4 each; the
+//             near-1 log correction runs behind a full-warp vote.
+// The product rule clips lazily: the scan tracks min/max of the raw values
+// (2 FMNMX3 per pixel for each) and recomputes a piece with np.clip semantics
+// only when a value falls outside [1e-7, 1] (NaN propagates through the
+// product unchanged, as through np.clip + np.log).
+// ---------------------------------------------------------------------------
+struct FastSmem {
+  size_t stage_floats, o_head, o_max, o_bar, total;
+};
 
-template <typename AccT, int AGG, bool EQW>
-int launch_fuse(const FuseParams &p, cudaStream_t st) {
-  const WarpSmem L = warp_layout(p.c, p.NS, (int)sizeof(AccT));
-  const size_t bytes = L.total * kWarps;
-  auto kern = k_fuse<AccT, AGG, EQW>;
-  static size_t configured_bytes = 0;
-  static int blocks_per_sm = 0;
-  static int num_sms = 0;
-  if (configured_bytes != bytes) {
+__host__ __device__ inline FastSmem fast_layout(int c, int NS) {
+  FastSmem s;
+  s.stage_floats = (size_t)kChunk * c;  // c % 4 == 0
+  size_t o = (size_t)NS * s.stage_floats * 4;
+  s.o_head = o;  // int4 per valid piece: {accumulator offset, weight bits, first-pixel float offset, 0}
+  o += (size_t)kChunk * 16;
+  s.o_max = o;
+  o += (size_t)kChunk * 4;
+  s.o_bar = o = al(o, 16);
+  o += (size_t)NS * 8;
+  s.total = al(o, 128);
+  return s;
+}
+
+__device__ __forceinline__ float lg2_approx(float x) {
+  float l;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(x));
+  return l;
+}
+
+// log2(x) for x in (0.9, 1] from the log1p series in t = x - 1 (exact), scaled by 1/ln2
+__device__ __forceinline__ float log2_series(float x) {
+  const float t = x - 1.0f;
+  constexpr float k = 1.4426950408889634f;
+  return t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, fmaf(t, -k / 6.0f, k / 5.0f), -k / 4.0f), k / 3.0f), -k / 2.0f), k);
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long ra = *reinterpret_cast<unsigned long long *>(&a);
+  unsigned long long rb = *reinterpret_cast<unsigned long long *>(&b);
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(ra), "l"(rb));
+  return *reinterpret_cast<float2 *>(&r);
+}
+
+template <int AGG>
+__global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant__ FuseParams p) {
+  constexpr bool kProd = AGG == TFB_AGG_MUL;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = p.c, NS = p.NS;
+  const Geo geo = geo_of(c);
+  const FastSmem L = fast_layout(c, NS);
+  unsigned char *ws = smem + (size_t)warp * L.total;
+  float *stages = reinterpret_cast<float *>(ws);
+  int4 *shead = reinterpret_cast<int4 *>(ws + L.o_head);
+  float *smax = reinterpret_cast<float *>(ws + L.o_max);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(ws + L.o_bar);
+  const int GW = gridDim.x * kWarps;
+  const int gw = blockIdx.x * kWarps + warp;
+  const int cpf = (int)p.cpf, hw = (int)p.hw;
+  const int dF = GW / cpf, dC = GW - dF * cpf;
+  const float wa = p.wa, wb = p.wb;
+
+  uint64_t policy = 0;
+  if (lane == 0) {
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    for (int s = 0; s < NS; ++s) mbar_init(bar + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
+  auto issue = [&](Pos q, int s) {
+    const int start = q.ch * kChunk;
+    const int npix = min(kChunk, hw - start);
+    const uint32_t bytes = (uint32_t)(npix * c * 4);
+    mbar_expect_tx(bar + s, bytes);
+    bulk_g2s(stages + (size_t)s * L.stage_floats, p.probs[q.f] + (size_t)start * c, bytes, bar + s, policy);
+  };
+  Pos cur{gw / cpf, gw % cpf};
+  Pos ahead = cur;  // next item to stage
+  for (int s = 0; s < NS && ahead.f < p.nframes; ++s) {
+    if (lane == 0) issue(ahead, s);
+    advance(ahead, dF, dC, cpf);
+  }
+  Pos nxt = cur, nn = cur;
+  advance(nxt, dF, dC, cpf);
+  advance(nn, dF, dC, cpf);
+  advance(nn, dF, dC, cpf);
+
+  const unsigned upto = (2u << lane) - 1u;  // lanes <= this one
+  const int g = lane / geo.QW, qi0 = lane - g * geo.QW;
+  const int i0 = g * geo.span;
+  const int i1 = min(i0 + geo.span, kChunk);
+  const bool grp_start = (lane % geo.span) == 0;
+  const bool scan_lane = g < geo.G;
+
+  auto hits_at = [&](Pos q, int32_t r) -> uint32_t {
+    if (r < 0 || q.f >= p.nframes || wb == 0.0f) return 1u;
+    return __ldg(p.hits + ((int64_t)q.f * p.n_x + r));
+  };
+  int32_t r_cur = row_at(p, cur, lane);
+  uint32_t n_cur = hits_at(cur, r_cur);
+  int32_t r_nxt = row_at(p, nxt, lane);
+  uint32_t phase = 0;
+  int s = 0;
+  while (cur.f < p.nframes) {
+    const uint32_t n_nxt = hits_at(nxt, r_nxt);
+    const int32_t r_nn = row_at(p, nn, lane);
+    const int npix = min(kChunk, hw - cur.ch * kChunk);
+    float *st = stages + (size_t)s * L.stage_floats;
+
+    // pieces (as in k_fuse) and their head records: one per piece on a covered texel
+    const float w = fmaf(wb, rcp_approx((float)n_cur), wa);  // fusion.py:132-141
+    const int32_t prev = __shfl_up_sync(0xffffffffu, r_cur, 1);
+    const bool chg = lane == 0 || prev != r_cur || grp_start;
+    const unsigned cmask = __ballot_sync(0xffffffffu, chg);
+    bool pstart = chg;
+    if (kProd) {
+      const int rs = 31 - __clz(cmask & upto);
+      pstart = ((lane - rs) & 3) == 0;
+    }
+    const unsigned smask = __ballot_sync(0xffffffffu, pstart);
+    const bool valid = pstart && r_cur >= 0;
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      const unsigned above = smask & ~upto;
+      atomicAdd(p.counts + r_cur, (uint32_t)((above ? __ffs(above) - 1 : kChunk) - lane));  // fusion.py:182
+      const float wv = kProd ? w * 0.693147180559945f : w;
+      shead[__popc(vmask & (upto >> 1))] = make_int4(r_cur * (int)p.stride, __float_as_int(wv), lane * c, 0);
+    }
+    const int npv = __popc(vmask);
+
+    mbar_wait(bar + s, (phase >> s) & 1u);
+    phase ^= 1u << s;
+    __syncwarp();
+
+    if (AGG == TFB_AGG_MAXSUM || p.fallback) {  // fusion.py:174, cli.py:293
+      if (lane < npix) {
+        const float *pp = st + (size_t)lane * c;
+        float best = pp[0];
+        int bi = 0;
+        for (int k = 1; k < c; ++k) {
+          const float v = pp[k];
+          if (!isnan(best) && (isnan(v) || v > best)) {
+            best = v;
+            bi = k;
+          }
+        }
+        smax[lane] = best;
+        if (p.fallback) p.fallback[(int64_t)cur.f * p.hw + cur.ch * kChunk + lane] = bi;
+      }
+      __syncwarp();
+    }
+
+    for (int qb = 0; qb < geo.nq; qb += geo.QW) {
+      const int q = qb + qi0;
+      // ---- scan: fold each piece of this lane's group into its first pixel's slot.
+      // Branch-free over the group's pixels: at a piece start the running value
+      // is stored (one predicated STS.128) and reset by selects.
+      if (scan_lane && q < geo.nq && vmask != 0u) {
+        const unsigned sm = smask >> i0;  // bit j: a piece starts at pixel i0 + j (bit 0 always set)
+        const int n = i1 - i0;
+        float *pp = st + (size_t)i0 * c + 4 * q;
+        float *ps = pp;
+        const float one = kProd ? 1.0f : 0.0f;  // fold identity
+        float4 v = *reinterpret_cast<const float4 *>(pp);
+        if (AGG == TFB_AGG_MAXSUM) {
+          const float mx = smax[i0];
+          v.x = v.x == mx ? v.x : 0.f; v.y = v.y == mx ? v.y : 0.f;
+          v.z = v.z == mx ? v.z : 0.f; v.w = v.w == mx ? v.w : 0.f;
+        }
+        float2 a01 = make_float2(v.x, v.y), a23 = make_float2(v.z, v.w);
+        float mn01 = fminf(v.x, v.y), mn23 = fminf(v.z, v.w);
+        float mx01 = fmaxf(v.x, v.y), mx23 = fmaxf(v.z, v.w);
+#pragma unroll 2
+        for (int j = 1; j < n; ++j) {
+          pp += c;
+          v = *reinterpret_cast<const float4 *>(pp);
+          const bool start = (sm >> j) & 1u;
+          if (start) *reinterpret_cast<float4 *>(ps) = make_float4(a01.x, a01.y, a23.x, a23.y);
+          ps = start ? pp : ps;
+          a01.x = start ? one : a01.x; a01.y = start ? one : a01.y;
+          a23.x = start ? one : a23.x; a23.y = start ? one : a23.y;
+          if (kProd) {
+            a01 = mul2(a01, make_float2(v.x, v.y));
+            a23 = mul2(a23, make_float2(v.z, v.w));
+            mn01 = fminf(fminf(mn01, v.x), v.y);
+            mn23 = fminf(fminf(mn23, v.z), v.w);
+            mx01 = fmaxf(fmaxf(mx01, v.x), v.y);
+            mx23 = fmaxf(fmaxf(mx23, v.z), v.w);
+          } else {
+            if (AGG == TFB_AGG_MAXSUM) {
+              const float mx = smax[i0 + j];
+              v.x = v.x == mx ? v.x : 0.f; v.y = v.y == mx ? v.y : 0.f;
+              v.z = v.z == mx ? v.z : 0.f; v.w = v.w == mx ? v.w : 0.f;
+            }
+            a01 = add2(a01, make_float2(v.x, v.y));
+            a23 = add2(a23, make_float2(v.z, v.w));
+          }
+        }
+        *reinterpret_cast<float4 *>(ps) = make_float4(a01.x, a01.y, a23.x, a23.y);
+        if (kProd && (fminf(mn01, mn23) < kMulClampF || fmaxf(mx01, mx23) > 1.0f)) {
+          // rare: a value outside [1e-7, 1] in this group -> redo its pieces with
+          // np.clip(p, 1e-7, 1) (fusion.py:177) from the global copy (the staged
+          // first-pixel slots are already overwritten)
+          const float *g4 = p.probs[cur.f] + ((size_t)cur.ch * kChunk + i0) * c + 4 * q;
+          pp = st + (size_t)i0 * c + 4 * q;
+          ps = pp;
+          a01 = make_float2(1.f, 1.f);
+          a23 = a01;
+          for (int j = 0; j < n; ++j, pp += c, g4 += c) {
+            const bool start = (sm >> j) & 1u;
+            if (start && j > 0) {
+              *reinterpret_cast<float4 *>(ps) = make_float4(a01.x, a01.y, a23.x, a23.y);
+              ps = pp;
+              a01 = make_float2(1.f, 1.f);
+              a23 = a01;
+            }
+            const float4 u = __ldg(reinterpret_cast<const float4 *>(g4));
+            a01 = mul2(a01, make_float2(clip_mul(u.x), clip_mul(u.y)));
+            a23 = mul2(a23, make_float2(clip_mul(u.z), clip_mul(u.w)));
+          }
+          *reinterpret_cast<float4 *>(ps) = make_float4(a01.x, a01.y, a23.x, a23.y);
+        }
+      }
+      __syncwarp();
+      // ---- epilogue (converged): lanes = (piece, quad), one red.v4 per pair (fusion.py:180-181)
+      float *accq = reinterpret_cast<float *>(p.accum) + 4 * q;
+      const float *stq = st + 4 * q;
+      const bool lane_ok = scan_lane && q < geo.nq;
+      for (int P = g; P - g < npv; P += geo.G) {
+        const bool ok = lane_ok && P < npv;
+        int4 h = make_int4(0, 0, 0, 0);
+        float4 m = make_float4(0.5f, 0.5f, 0.5f, 0.5f);  // idle lanes must not trip the near-1 vote
+        if (ok) {
+          h = shead[P];
+          m = *reinterpret_cast<const float4 *>(stq + h.z);
+        }
+        float b0 = m.x, b1 = m.y, b2 = m.z, b3 = m.w;
+        if (kProd) {
+          b0 = lg2_approx(m.x);
+          b1 = lg2_approx(m.y);
+          b2 = lg2_approx(m.z);
+          b3 = lg2_approx(m.w);
+          const bool near1 = fmaxf(fmaxf(m.x, m.y), fmaxf(m.z, m.w)) > 0.9f;
+          if (__any_sync(0xffffffffu, near1)) {
+            if (m.x > 0.9f) b0 = log2_series(m.x);
+            if (m.y > 0.9f) b1 = log2_series(m.y);
+            if (m.z > 0.9f) b2 = log2_series(m.z);
+            if (m.w > 0.9f) b3 = log2_series(m.w);
+          }
+        }
+        const float wv = __int_as_float(h.y);
+        const float2 o01 = mul2(make_float2(b0, b1), make_float2(wv, wv));
+        const float2 o23 = mul2(make_float2(b2, b3), make_float2(wv, wv));
+        if (ok)
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(accq + h.x), "f"(o01.x), "f"(o01.y),
+                       "f"(o23.x), "f"(o23.y));
+      }
+      __syncwarp();
+    }
+    // stage s is free again
+    if (ahead.f < p.nframes) {
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(ahead, s);
+      }
+      advance(ahead, dF, dC, cpf);
+    }
+    cur = nxt;
+    nxt = nn;
+    advance(nn, dF, dC, cpf);
+    r_cur = r_nxt;
+    n_cur = n_nxt;
+    r_nxt = r_nn;
+    s = (s + 1 == NS) ? 0 : s + 1;
+  }
+}
+
+int g_fuse_ctas_per_sm = 0;  // 0 = as many as fit (tfb_set_option(TFB_OPT_FUSE_CTAS_PER_SM))
+int g_fuse_fast = 1;         // tfb_set_option(TFB_OPT_FUSE_FAST): 0 routes everything through k_fuse
+
+struct LaunchCache {
+  size_t bytes = 0;
+  int blocks_per_sm = 0;
+  int num_sms = 0;
+};
+
+template <typename Kern>
+int launch_persistent(Kern kern, LaunchCache &lc, size_t bytes, const FuseParams &p, cudaStream_t st) {
+  if (lc.bytes != bytes) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
       return check_launch("tfb_fuse: shared memory configuration");
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kWarps * 32, bytes);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-    configured_bytes = bytes;
+    cudaDeviceGetAttribute(&lc.num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lc.blocks_per_sm, kern, kWarps * 32, bytes);
+    if (lc.blocks_per_sm < 1) lc.blocks_per_sm = 1;
+    lc.bytes = bytes;
   }
-  int per_sm = blocks_per_sm;
+  int per_sm = lc.blocks_per_sm;
   if (g_fuse_ctas_per_sm > 0 && g_fuse_ctas_per_sm < per_sm) per_sm = g_fuse_ctas_per_sm;
-  int64_t grid = (int64_t)num_sms * per_sm;
+  int64_t grid = (int64_t)lc.num_sms * per_sm;
   const int64_t need = (p.nitems + kWarps - 1) / kWarps;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
   kern<<<(unsigned)grid, kWarps * 32, bytes, st>>>(p);
   return check_launch("tfb_fuse");
+}
+
+template <typename AccT, int AGG, bool EQW>
+int launch_fuse(const FuseParams &p, cudaStream_t st) {
+  static LaunchCache lc;
+  return launch_persistent(k_fuse<AccT, AGG, EQW>, lc, warp_layout(p.c, p.NS, (int)sizeof(AccT)).total * kWarps, p,
+                           st);
+}
+
+template <int AGG>
+int launch_fuse_fast(const FuseParams &p, cudaStream_t st) {
+  static LaunchCache lc;
+  return launch_persistent(k_fuse_fast<AGG>, lc, fast_layout(p.c, p.NS).total * kWarps, p, st);
 }
 
 template <typename AccT, int AGG>
@@ -615,6 +927,8 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
   p.n_x = total_texels;
   p.wmode = weight_mode;
   p.alpha = alpha;
+  p.wa = weight_mode == TFB_W_IMAGES_IID ? 0.0f : weight_mode == TFB_W_BLEND ? (float)(1.0 - alpha) : 1.0f;
+  p.wb = weight_mode == TFB_W_IMAGES_IID ? 1.0f : weight_mode == TFB_W_BLEND ? (float)alpha : 0.0f;
   p.accum = accum;
   p.stride = accum_stride;
   p.counts = counts;
@@ -632,8 +946,16 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
     p.fallback = fallback_out ? fallback_out + (int64_t)f0 * hw : nullptr;
     p.nframes = nf;
     p.nitems = p.cpf * nf;
+    bool fast = !accum_is_f64 && weight_mode != TFB_W_EXPLICIT && num_classes % 4 == 0 && g_fuse_fast;
+    for (int i = 0; i < nf && fast; ++i) fast = ((uintptr_t)p.probs[i] & 15) == 0;
     int rc;
-    if (accum_is_f64) {
+    if (fast) {
+      switch (aggregator) {
+        case TFB_AGG_SUM: rc = launch_fuse_fast<TFB_AGG_SUM>(p, st); break;
+        case TFB_AGG_MAXSUM: rc = launch_fuse_fast<TFB_AGG_MAXSUM>(p, st); break;
+        default: rc = launch_fuse_fast<TFB_AGG_MUL>(p, st); break;
+      }
+    } else if (accum_is_f64) {
       switch (aggregator) {
         case TFB_AGG_SUM: rc = launch_fuse_w<double, TFB_AGG_SUM>(p, st); break;
         case TFB_AGG_MAXSUM: rc = launch_fuse_w<double, TFB_AGG_MAXSUM>(p, st); break;
@@ -655,6 +977,10 @@ extern "C" int tfb_set_option(int option, int value) {
   if (option == TFB_OPT_FUSE_CTAS_PER_SM) {
     TFB_REQUIRE(value >= 0, TFB_ERR_VALUE, "tfb_set_option: negative CTA cap");
     g_fuse_ctas_per_sm = value;
+    return TFB_OK;
+  }
+  if (option == TFB_OPT_FUSE_FAST) {
+    g_fuse_fast = value != 0;
     return TFB_OK;
   }
   set_error("tfb_set_option: unknown option %d", option);

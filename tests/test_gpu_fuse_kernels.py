@@ -1,0 +1,148 @@
+"""tfb_fuse kernel coverage beyond the scene tests: both scatter-add kernels
+(the specialised float32 / count-weight / c % 4 == 0 kernel and the general
+one, selected with TFB_OPT_FUSE_FAST) against the float64 oracle
+(oracle.accumulate_frame, fusion.py:145-183) on synthetic row images with
+texel runs, partial last chunks, several quad passes (c = 132), and the
+probability values the clip / log paths care about: 0, tiny, exactly 1,
+above 1, negative, NaN and values just below 1 (log1p series path)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O  # noqa: E402
+from paper_2111_11103_b200 import _native as N  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+P = ctypes.c_void_p
+TFB_OPT_FUSE_FAST = 2
+
+
+def _rows(rng, nframes, hw, n_x):
+    """Row images made of runs (1..9 pixels) on random texels, ~15% uncovered."""
+    out = np.empty((nframes, hw), np.int32)
+    for f in range(nframes):
+        i = 0
+        while i < hw:
+            n = int(rng.integers(1, 10))
+            r = -1 if rng.random() < 0.15 else int(rng.integers(0, n_x))
+            out[f, i:i + n] = r
+            i += n
+    return out
+
+
+def _probs(rng, nframes, hw, c, special):
+    logits = rng.normal(size=(nframes, hw, c)) * 2.0
+    p = np.exp(logits - logits.max(axis=2, keepdims=True))
+    p = (p / p.sum(axis=2, keepdims=True)).astype(np.float32)
+    if special:
+        flat = p.reshape(-1)
+        m = flat.size
+        pick = lambda k: rng.choice(m, size=k, replace=False)  # noqa: E731
+        flat[pick(m // 50)] = 0.0
+        flat[pick(m // 200)] = 1e-9
+        flat[pick(m // 200)] = 1.0
+        flat[pick(m // 500)] = 1.5
+        flat[pick(m // 500)] = -0.25
+        flat[pick(m // 50)] = rng.uniform(0.9, 0.99999, size=m // 50).astype(np.float32)
+        flat[pick(3)] = np.nan
+    return p
+
+
+def _run(rows, probs, n_x, agg, wm, alpha, fast):
+    lib = N.load()
+    nframes, hw = rows.shape
+    c = probs.shape[2]
+    stride = (c + 3) // 4 * 4
+    dev = torch.device("cuda")
+    rows_d = torch.as_tensor(rows, device=dev)
+    pd = [torch.as_tensor(probs[f], device=dev).contiguous() for f in range(nframes)]
+    ptrs = (P * nframes)(*[t.data_ptr() for t in pd])
+    hits = torch.zeros((nframes, n_x), dtype=torch.int32, device=dev)
+    acc = torch.zeros((n_x, stride), dtype=torch.float32, device=dev)
+    cnt = torch.zeros(n_x, dtype=torch.int32, device=dev)
+    fb = torch.full((nframes, hw), -7, dtype=torch.int32, device=dev)
+    stream = P(torch.cuda.current_stream().cuda_stream)
+    N.check(lib.tfb_set_option(TFB_OPT_FUSE_FAST, 1 if fast else 0))
+    try:
+        N.check(lib.tfb_count_hits(P(rows_d.data_ptr()), hw, nframes, n_x, P(hits.data_ptr()), stream))
+        N.check(lib.tfb_fuse(P(rows_d.data_ptr()), hw, nframes, ctypes.cast(ptrs, P), c, P(hits.data_ptr()), None,
+                             n_x, N.AGG_IDS[agg], N.WMODE_IDS[wm], alpha, P(acc.data_ptr()), 0, stride,
+                             P(cnt.data_ptr()), P(fb.data_ptr()), stream))
+        torch.cuda.synchronize()
+    finally:
+        lib.tfb_set_option(TFB_OPT_FUSE_FAST, 1)
+    return acc.cpu().numpy()[:, :c], cnt.cpu().numpy(), fb.cpu().numpy()
+
+
+def _oracle(rows, probs, n_x, agg, wm, alpha):
+    acc = np.zeros((n_x, probs.shape[2]))
+    cnt = np.zeros(n_x, np.int64)
+    offsets = np.arange(n_x, dtype=np.int64)
+    for f in range(rows.shape[0]):
+        tri = rows[f]
+        texel = np.zeros_like(tri)
+        w = O.compute_pixel_weights(tri, texel, wm, alpha if wm == "blend" else None)
+        O.accumulate_frame(acc, cnt, offsets, tri, texel, probs[f], w, agg)
+    return acc, cnt
+
+
+def _check(got, ref, scale, tol=1e-5):
+    """float32 accumulation bound: relative to the sum of |terms| (scale), floored at 1e-3."""
+    assert np.array_equal(np.isnan(got), np.isnan(ref))
+    ok = ~np.isnan(ref)
+    err = np.abs(got[ok] - ref[ok]) / np.maximum(np.maximum(np.abs(scale[ok]), np.abs(ref[ok])), 1e-3)
+    assert err.max(initial=0.0) < tol, err.max()
+
+
+def _scale(rows, probs, n_x, agg, wm, alpha):
+    if agg == "mul":  # all terms are <= 0: no cancellation
+        return np.abs(_oracle(rows, probs, n_x, agg, wm, alpha)[0])
+    return _oracle(rows, np.abs(probs), n_x, agg, wm, alpha)[0]
+
+
+@pytest.mark.parametrize("fast", [True, False])
+@pytest.mark.parametrize("c", [4, 40, 132])
+@pytest.mark.parametrize("agg", ["sum", "maxsum", "mul"])
+def test_fuse_kernels_vs_oracle(fast, c, agg):
+    rng = np.random.default_rng(1000 + c)
+    nframes, hw, n_x = 3, 61 * 37, 300
+    rows = _rows(rng, nframes, hw, n_x)
+    probs = _probs(rng, nframes, hw, c, special=True)
+    for wm, alpha in (("images_iid", 0.0), ("pixels_iid", 0.0), ("blend", 0.3)):
+        got, cnt, fb = _run(rows, probs, n_x, agg, wm, alpha, fast)
+        ref, cref = _oracle(rows, probs, n_x, agg, wm, alpha)
+        np.testing.assert_array_equal(cnt, cref)
+        _check(got, ref, _scale(rows, probs, n_x, agg, wm, alpha))
+    np.testing.assert_array_equal(fb, probs.argmax(axis=2))
+
+
+def test_fuse_fast_many_frames_and_launch_split():
+    """More frames than one launch carries (32): the frame loop and pointer table."""
+    rng = np.random.default_rng(5)
+    nframes, hw, n_x, c = 37, 32 * 20 + 5, 64, 8
+    rows = _rows(rng, nframes, hw, n_x)
+    probs = _probs(rng, nframes, hw, c, special=False)
+    got, cnt, _ = _run(rows, probs, n_x, "mul", "images_iid", 0.0, True)
+    ref, cref = _oracle(rows, probs, n_x, "mul", "images_iid", 0.0)
+    np.testing.assert_array_equal(cnt, cref)
+    _check(got, ref, ref)
+
+
+def test_fuse_fast_and_general_agree_on_long_runs():
+    """Whole chunks on one texel (pieces cut every 4 pixels for the product)."""
+    rng = np.random.default_rng(9)
+    hw, c = 32 * 64, 40
+    rows = np.repeat(np.arange(hw // 256, dtype=np.int32), 256)[None, :]
+    probs = _probs(rng, 1, hw, c, special=False)
+    a, ca, _ = _run(rows, probs, hw // 256, "mul", "blend", 0.5, True)
+    b, cb, _ = _run(rows, probs, hw // 256, "mul", "blend", 0.5, False)
+    ref, cref = _oracle(rows, probs, hw // 256, "mul", "blend", 0.5)
+    np.testing.assert_array_equal(ca, cref)
+    np.testing.assert_array_equal(cb, cref)
+    _check(a, ref, ref)
+    _check(b, ref, ref)
