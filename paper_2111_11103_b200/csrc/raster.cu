@@ -29,12 +29,21 @@
 #include <math.h>
 
 #include "common.cuh"
+#include "exact_div.cuh"
 
 namespace tfb {
 namespace {
 
-constexpr int kTile = 16;
-constexpr int kThreads = 256;
+#ifndef TFB_TW
+#define TFB_TW 16
+#endif
+#ifndef TFB_TH
+#define TFB_TH 8
+#endif
+constexpr int kTW = TFB_TW, kTH = TFB_TH;  // raster tile (pixels); one k_raster thread per pixel
+constexpr int kTP = kTW * kTH;             // k_raster threads = tile pixels = staged records per tile
+constexpr int kThreads = 256;              // setup-side kernels
+static_assert(kTW % 8 == 0 && kTH % 4 == 0 && kTP >= 64 && kTP <= 256, "tile shape: 8x4-pixel warp blocks");
 constexpr int kCand = 8;
 constexpr uint32_t kNoKey = 0xffffffffu;
 
@@ -236,8 +245,8 @@ __device__ __forceinline__ void store_record(const Work &w, int f, int64_t slot,
   for (int q = 0; q < 8; ++q) dst[q] = src[q];
   w.meta[idx] = mt;
   uint32_t *tc = w.tile_count + (int64_t)f * ntiles;
-  for (int ty = mt.y0 / kTile; ty <= mt.y1 / kTile; ++ty)
-    for (int tx = mt.x0 / kTile; tx <= mt.x1 / kTile; ++tx) atomicAdd(tc + ty * TX + tx, 1u);
+  for (int ty = mt.y0 / kTH; ty <= mt.y1 / kTH; ++ty)
+    for (int tx = mt.x0 / kTW; tx <= mt.x1 / kTW; ++tx) atomicAdd(tc + ty * TX + tx, 1u);
 }
 
 // Per (frame, vertex): the camera-space position (FMA order of geometry.py:161)
@@ -420,8 +429,8 @@ __global__ void __launch_bounds__(256) k_fill(Work w, int64_t m, int ntiles, int
       if (!((mask >> sub) & 1u)) continue;
       const uint32_t r = 2 * t + sub;
       const RecMeta mt = meta[r];
-      for (int ty = mt.y0 / kTile; ty <= mt.y1 / kTile; ++ty)
-        for (int tx = mt.x0 / kTile; tx <= mt.x1 / kTile; ++tx) {
+      for (int ty = mt.y0 / kTH; ty <= mt.y1 / kTH; ++ty)
+        for (int tx = mt.x0 / kTW; tx <= mt.x1 / kTW; ++tx) {
           const int tile = ty * TX + tx;
           const uint64_t pos = toff[tile] + atomicAdd(cur + tile, 1u);
           if (pos < (uint64_t)w.cap) list[pos] = r;
@@ -429,6 +438,15 @@ __global__ void __launch_bounds__(256) k_fill(Work w, int64_t m, int ntiles, int
     }
   }
 }
+
+#ifdef TFB_RASTER_STATS
+// experiment-only histograms (tools/raster_stats.py): [0,16) records per tile /32,
+// [16,32) covering records per pixel, [32,48) pairs per tile /256, [48] big tiles
+__device__ unsigned long long g_rstats[64];
+#define RSTAT(i) atomicAdd(&g_rstats[(i)], 1ull)
+#else
+#define RSTAT(i) ((void)0)
+#endif
 
 struct Outs {
   int32_t *rows;
@@ -440,13 +458,30 @@ struct Outs {
   double *v;
 };
 
+// Record geometry views.  RecGeom is 16 doubles: xs[3] ys[3] zs[3] dX[3] dY[3] area2.
+enum { kFXs = 0, kFYs = 3, kFZs = 6, kFDX = 9, kFDY = 12, kFA2 = 15, kFields = 16 };
+constexpr int kFS = kTP + 1;  // field stride of the staged (SoA) tile records, +1 double: fields on distinct banks
+
+struct AosRec {  // one RecGeom (global memory or AoS shared memory)
+  const RecGeom *g;
+  __device__ __forceinline__ double f(int k) const { return reinterpret_cast<const double *>(g)[k]; }
+};
+
+struct SoaRec {  // record j of a tile staged field-major: lanes reading different records hit different banks
+  const double *base;
+  int j;
+  __device__ __forceinline__ double f(int k) const { return base[k * kFS + j]; }
+};
+
 // edge functions at one pixel centre, rasterizer.py:161-162
-__device__ __forceinline__ bool edges_at(const RecGeom &g, uint32_t flags, double px, double py, double e[3]) {
+template <typename R>
+__device__ __forceinline__ bool edges_at(const R &g, uint32_t flags, double px, double py, double e[3]) {
   bool inside = true;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     const int a = (k + 1) % 3;
-    e[k] = __dsub_rn(__dmul_rn(g.dX[k], __dsub_rn(py, g.ys[a])), __dmul_rn(g.dY[k], __dsub_rn(px, g.xs[a])));
+    e[k] = __dsub_rn(__dmul_rn(g.f(kFDX + k), __dsub_rn(py, g.f(kFYs + a))),
+                     __dmul_rn(g.f(kFDY + k), __dsub_rn(px, g.f(kFXs + a))));
     inside = inside && (e[k] > 0.0 || (e[k] == 0.0 && ((flags >> k) & 1u)));
   }
   return inside;
@@ -465,14 +500,25 @@ struct Fold {
     w0 = w1 = w2 = 0.0;
     win = -1;
   }
-  __device__ __forceinline__ void step(const RecGeom &g, uint32_t flags, double px, double py, int32_t id) {
+  template <typename R>
+  __device__ __forceinline__ void step(const R &g, uint32_t flags, double px, double py, int32_t id) {
     double e[3];
     edges_at(g, flags, px, py, e);
     step_e(g, e, id);
   }
-  __device__ __forceinline__ void step_e(const RecGeom &g, const double e[3], int32_t id) {
-    const double a = __ddiv_rn(e[0], g.zs[0]), b = __ddiv_rn(e[1], g.zs[1]), c = __ddiv_rn(e[2], g.zs[2]);
-    const double z = __ddiv_rn(g.area2, __dadd_rn(__dadd_rn(a, b), c));
+  template <typename R>
+  __device__ __forceinline__ void step_e(const R &g, const double e[3], int32_t id) {
+    // rasterizer.py:166-169; divisions via the branch-free fast path (exact_div.cuh)
+    const double z0 = g.f(kFZs), z1 = g.f(kFZs + 1), z2 = g.f(kFZs + 2), a2 = g.f(kFA2);
+    bool ok = true;
+    double a = ddiv_try(e[0], z0, ok), b = ddiv_try(e[1], z1, ok), c = ddiv_try(e[2], z2, ok);
+    double z = ddiv_try(a2, __dadd_rn(__dadd_rn(a, b), c), ok);
+    if (!ok) {
+      a = __ddiv_rn(e[0], z0);
+      b = __ddiv_rn(e[1], z1);
+      c = __ddiv_rn(e[2], z2);
+      z = __ddiv_rn(a2, __dadd_rn(__dadd_rn(a, b), c));
+    }
     if (z > 0.0 && z < __dsub_rn(depth, kDepthTie)) {
       depth = z;
       win = id;
@@ -518,20 +564,25 @@ __device__ __forceinline__ void write_pixel(const tfb_scene &sc, const Cam &cam,
           B[2][q] = tmp;
         }
       }
-      double bb[3];
+      double nb[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k)
-        bb[k] = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(fd.w0, B[0][k]), __dmul_rn(fd.w1, B[1][k])),
-                                    __dmul_rn(fd.w2, B[2][k])),
-                          wsum);
-      b0 = bb[0];
-      b1 = bb[1];
-      b2 = bb[2];
+        nb[k] = __dadd_rn(__dadd_rn(__dmul_rn(fd.w0, B[0][k]), __dmul_rn(fd.w1, B[1][k])), __dmul_rn(fd.w2, B[2][k]));
+      b0 = __ddiv_rn(nb[0], wsum);
+      b1 = __ddiv_rn(nb[1], wsum);
+      b2 = __ddiv_rn(nb[2], wsum);
     } else {
       // rows = identity reordered by (0, 1, 2) or (0, 2, 1): b_k = w_perm(k) / wsum
-      b0 = __ddiv_rn(fd.w0, wsum);
-      b1 = __ddiv_rn((flags & 8u) ? fd.w2 : fd.w1, wsum);
-      b2 = __ddiv_rn((flags & 8u) ? fd.w1 : fd.w2, wsum);
+      const double n1 = (flags & 8u) ? fd.w2 : fd.w1, n2 = (flags & 8u) ? fd.w1 : fd.w2;
+      bool ok = true;
+      b0 = ddiv_try(fd.w0, wsum, ok);
+      b1 = ddiv_try(n1, wsum, ok);
+      b2 = ddiv_try(n2, wsum, ok);
+      if (!ok) {
+        b0 = __ddiv_rn(fd.w0, wsum);
+        b1 = __ddiv_rn(n1, wsum);
+        b2 = __ddiv_rn(n2, wsum);
+      }
     }
     if (b0 < 0.0) b0 = 0.0;  // np.clip(b, 0, None)
     if (b1 < 0.0) b1 = 0.0;
@@ -541,8 +592,13 @@ __device__ __forceinline__ void write_pixel(const tfb_scene &sc, const Cam &cam,
     const int s = (int)(flags >> 16);
     const double bo = origin == 0 ? b0 : (origin == 1 ? b1 : b2);
     const double bv = origin == 0 ? b2 : (origin == 1 ? b0 : b1);
-    double u = __dsub_rn(1.0, __ddiv_rn(bo, bs));
-    double v = __ddiv_rn(bv, bs);
+    bool ok = true;
+    double qo = ddiv_try(bo, bs, ok), v = ddiv_try(bv, bs, ok);
+    if (!ok) {
+      qo = __ddiv_rn(bo, bs);
+      v = __ddiv_rn(bv, bs);
+    }
+    double u = __dsub_rn(1.0, qo);
     u = np_min(np_max(u, 0.0), 1.0);
     v = np_min(np_max(v, 0.0), u);
     int i = (int)__dmul_rn((double)s, u);
@@ -582,21 +638,21 @@ __device__ __forceinline__ void write_pixel(const tfb_scene &sc, const Cam &cam,
 }
 
 struct TileSmem {
-  RecGeom geom[kThreads];
-  uint32_t flags[kThreads];           // RecMeta::flags
-  int32_t tri[kThreads];              // RecMeta::t
-  int32_t off[kThreads];              // offsets[t] of the record's triangle (n_x < 2^31)
-  unsigned long long pmin[kTile * kTile];  // per pixel: min (key << 32 | slot) of covering records
-  double pe[kTile * kTile][3];        // edge values of a pixel's (single) covering pair
+  double g[kFields * kFS];          // staged records, field-major (SoA): g[k * kFS + j]
+  double pe[3][kTP];                // edge values of a pixel's (single) covering pair
+  unsigned long long pmin[kTP];     // per pixel: min (key << 32 | slot) of covering records
+  uint32_t flags[kTP];              // RecMeta::flags
+  int32_t tri[kTP];                 // triangle of the record
+  int32_t off[kTP];                 // offsets[t] of the record's triangle (n_x < 2^31)
   Cam cam;
-  uint32_t key[kThreads];
-  uint32_t box[kThreads];             // tile-relative bbox: x0 | y0 << 8 | w << 16 | h << 24
-  uint32_t pre[kThreads];             // exclusive prefix of bbox areas
-  uint32_t pcnt[kTile * kTile];
-  uint32_t wtot[kThreads / 32];
+  uint32_t key[kTP];
+  uint32_t box[kTP];                // tile-relative bbox: x0 | y0 << 8 | w << 16 | h << 24
+  uint32_t pre[kTP];                // exclusive prefix of bbox areas
+  uint32_t pcnt[kTP];
+  uint32_t wtot[kTP / 32];
 };
 
-// One CTA per 16x16 tile with at most kThreads records (the common case).
+// One CTA of kTP threads per kTW x kTH tile with at most kTP records (the common case).
 //  1. The tile's records are staged in shared memory in list order (all
 //     threads cooperate on the 128-byte copies); bbox-in-tile and area per
 //     record, exclusive scan of areas.
@@ -610,26 +666,28 @@ struct TileSmem {
 //     the last folded one — the reference's ascending sequential fold
 //     (rasterizer.py:108, 170-171) without sorting the list.
 //  Larger or overflowed tiles are handed to k_raster_big.
-__global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const double *__restrict__ cams, int W, int H,
+__global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const double *__restrict__ cams, int W, int H,
                                                         int TX, int ntiles, Work w, Outs o) {
   const int f = blockIdx.z;
   const int tile = blockIdx.y * TX + blockIdx.x;
-  const int tx0 = blockIdx.x * kTile, ty0 = blockIdx.y * kTile;
+  const int tx0 = blockIdx.x * kTW, ty0 = blockIdx.y * kTH;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t n = w.tile_count[(int64_t)f * ntiles + tile];
   const uint64_t toff = w.tile_off[(int64_t)f * ntiles + tile];
-  if (toff + n > (uint64_t)w.cap || n > (uint32_t)kThreads) {
+  if (toff + n > (uint64_t)w.cap || n > (uint32_t)kTP) {
     if (tid == 0) w.big[atomicAdd(w.fcnt + 1, 1u)] = (uint32_t)(f * ntiles + tile);
+    if (tid == 0) RSTAT(48);
     return;
   }
+  if (tid == 0) RSTAT(min(n / 32u, 15u));
   extern __shared__ __align__(16) unsigned char raster_smem[];
   TileSmem &S = *reinterpret_cast<TileSmem *>(raster_smem);
-  RecGeom *sgeom = S.geom;
+  double *sg = S.g;
   uint32_t *sflags = S.flags;
   int32_t *stri = S.tri, *soff = S.off;
   uint32_t *skey = S.key, *sbox = S.box, *spre = S.pre, *pcnt = S.pcnt, *wtot = S.wtot;
   unsigned long long *pmin = S.pmin;
-  double(*pe)[3] = S.pe;
+  double(*pe)[kTP] = S.pe;
   Cam &cam = S.cam;
   load_cam(cam, cams, f);
   pmin[tid] = ~0ull;
@@ -641,18 +699,18 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const doub
     // one thread per record: 8 x 16 B async copies of its geometry, in flight
     // while the meta is read; completed before the barrier
     const uint32_t key = src[tid];
-    const double2 *gsrc = reinterpret_cast<const double2 *>(geom + key);
-    const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(sgeom + tid);
+    const double *gsrc = reinterpret_cast<const double *>(geom + key);
+    const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(sg + tid);
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst + 16 * q), "l"(gsrc + q) : "memory");
+    for (int q = 0; q < kFields; ++q)  // field q of record tid -> sg[q * kFS + tid]: consecutive lanes, no conflicts
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sdst + 8 * kFS * q), "l"(gsrc + q) : "memory");
     const RecMeta mt = w.meta[(int64_t)f * w.rs + key];
     skey[tid] = key;
     sflags[tid] = mt.flags;
     stri[tid] = (int32_t)(key >> 1);
     soff[tid] = mt.off;
-    const int bx0 = max((int)mt.x0, tx0) - tx0, bx1 = min((int)mt.x1, tx0 + kTile - 1) - tx0;
-    const int by0 = max((int)mt.y0, ty0) - ty0, by1 = min((int)mt.y1, ty0 + kTile - 1) - ty0;
+    const int bx0 = max((int)mt.x0, tx0) - tx0, bx1 = min((int)mt.x1, tx0 + kTW - 1) - tx0;
+    const int by0 = max((int)mt.y0, ty0) - ty0, by1 = min((int)mt.y1, ty0 + kTH - 1) - ty0;
     const uint32_t bw = (uint32_t)(bx1 - bx0 + 1), bh = (uint32_t)(by1 - by0 + 1);
     sbox[tid] = (uint32_t)bx0 | ((uint32_t)by0 << 8) | (bw << 16) | (bh << 24);
     area = bw * bh;
@@ -669,7 +727,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const doub
   __syncthreads();
   uint32_t wbase = 0, total = 0;
 #pragma unroll
-  for (int i = 0; i < kThreads / 32; ++i) {
+  for (int i = 0; i < kTP / 32; ++i) {
     const uint32_t v = wtot[i];
     wbase += i < warp ? v : 0u;
     total += v;
@@ -677,8 +735,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const doub
   spre[tid] = wbase + incl - area;
   __syncthreads();
 
+  if (tid == 0) RSTAT(32 + min(total / 256u, 15u));
   // pair-parallel edge tests: thread handles pairs [p0, p1)
-  const uint32_t ppt = (total + kThreads - 1) / kThreads;
+  const uint32_t ppt = (total + kTP - 1) / kTP;
   const uint32_t p0 = tid * ppt, p1 = min(p0 + ppt, total);
   if (p0 < p1) {
     int lo = 0, hi = (int)n - 1;
@@ -695,13 +754,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const doub
     for (uint32_t p = p0; p < p1; ++p) {
       const int pxl = (int)(b & 0xffu) + lx, pyl = (int)((b >> 8) & 0xffu) + ly;
       double e[3];
-      if (edges_at(sgeom[j], sflags[j], (double)(tx0 + pxl) + 0.5, (double)(ty0 + pyl) + 0.5, e)) {
-        const int pix = pyl * kTile + pxl;
+      if (edges_at(SoaRec{sg, j}, sflags[j], (double)(tx0 + pxl) + 0.5, (double)(ty0 + pyl) + 0.5, e)) {
+        const int pix = pyl * kTW + pxl;
         atomicMin(pmin + pix, ((unsigned long long)skey[j] << 32) | (unsigned)j);
         atomicAdd(pcnt + pix, 1u);
-        pe[pix][0] = e[0];  // meaningful only when this is the pixel's sole candidate
-        pe[pix][1] = e[1];
-        pe[pix][2] = e[2];
+        pe[0][pix] = e[0];  // meaningful only when this is the pixel's sole candidate
+        pe[1][pix] = e[1];
+        pe[2][pix] = e[2];
       }
       if (++lx == bw) {
         lx = 0;
@@ -720,22 +779,23 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const doub
   __syncthreads();
 
   // one thread per pixel: fold its covering records in ascending key order
-  const int pxl = tid & (kTile - 1), pyl = tid / kTile;
+  const int pxl = tid & (kTW - 1), pyl = tid / kTW;
   const int px_i = tx0 + pxl, py_i = ty0 + pyl;
   if (px_i >= W || py_i >= H) return;
   const double px = (double)px_i + 0.5, py = (double)py_i + 0.5;
   const uint32_t cnt = pcnt[tid];
+  RSTAT(16 + min(cnt, 15u));
   Fold fd;
   fd.init();
   if (cnt == 1u) {
     const int j = (int)(pmin[tid] & 0xffffffffu);
-    const double e[3] = {pe[tid][0], pe[tid][1], pe[tid][2]};
-    fd.step_e(sgeom[j], e, j);
+    const double e[3] = {pe[0][tid], pe[1][tid], pe[2][tid]};
+    fd.step_e(SoaRec{sg, j}, e, j);
   } else if (cnt > 1u) {
     unsigned long long cur = pmin[tid];
     for (uint32_t k = 0; k < cnt; ++k) {
       const int j = (int)(cur & 0xffffffffu);
-      fd.step(sgeom[j], sflags[j], px, py, j);
+      fd.step(SoaRec{sg, j}, sflags[j], px, py, j);
       if (k + 1 == cnt) break;
       const uint32_t last = (uint32_t)(cur >> 32);
       unsigned long long best = ~0ull;
@@ -748,7 +808,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const doub
         const unsigned long long cand = ((unsigned long long)key << 32) | i;
         if (cand >= best) continue;
         double e[3];
-        if (edges_at(sgeom[i], sflags[i], px, py, e)) best = cand;
+        if (edges_at(SoaRec{sg, (int)i}, sflags[i], px, py, e)) best = cand;
       }
       cur = best;
     }
@@ -759,17 +819,17 @@ __global__ void __launch_bounds__(kThreads, 4) k_raster(tfb_scene sc, const doub
   write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, off);
 }
 
-// Tiles with more than kThreads records, or whose list overflowed the pair
+// Tiles with more than kTP records, or whose list overflowed the pair
 // budget (then every record slot of the frame is scanned, invalid slots
 // masked out by vmask).  Records stream through shared memory in chunks in
 // arbitrary order; each pixel keeps the kCand smallest covering keys above
 // `lo`, folds them in ascending order and repeats with `lo` past the last
 // folded key until no covering record is left — the same sequential fold.
-__global__ void __launch_bounds__(kThreads, 2) k_raster_big(tfb_scene sc, const double *__restrict__ cams, int W,
+__global__ void __launch_bounds__(kTP) k_raster_big(tfb_scene sc, const double *__restrict__ cams, int W,
                                                             int H, int TX, int ntiles, Work w, Outs o) {
-  __shared__ RecGeom sgeom[kThreads];
-  __shared__ RecMeta smeta[kThreads];
-  __shared__ uint32_t skey[kThreads];
+  __shared__ RecGeom sgeom[kTP];
+  __shared__ RecMeta smeta[kTP];
+  __shared__ uint32_t skey[kTP];
   __shared__ Cam cam;
   const uint32_t nbig = w.fcnt[1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -777,7 +837,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster_big(tfb_scene sc, const 
     const uint32_t code = w.big[bi];
     const int f = (int)(code / ntiles), tile = (int)(code % ntiles);
     const int tx = tile % TX, ty = tile / TX;
-    const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
+    const int wx0 = tx * kTW + (warp % (kTW / 8)) * 8, wy0 = ty * kTH + (warp / (kTW / 8)) * 4;
     const int px_i = wx0 + (lane & 7), py_i = wy0 + (lane >> 3);
     const bool in_img = px_i < W && py_i < H;
     const double px = (double)px_i + 0.5, py = (double)py_i + 0.5;
@@ -801,8 +861,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster_big(tfb_scene sc, const 
 #pragma unroll
       for (int i = 0; i < kCand; ++i) ck[i] = kNoKey;
       uint32_t ncand = 0;
-      for (uint32_t b0 = 0; b0 < nsrc; b0 += kThreads) {
-        const uint32_t n = min((uint32_t)kThreads, nsrc - b0);
+      for (uint32_t b0 = 0; b0 < nsrc; b0 += kTP) {
+        const uint32_t n = min((uint32_t)kTP, nsrc - b0);
         __syncthreads();
         if (threadIdx.x < n) {
           const uint32_t i = b0 + threadIdx.x;
@@ -842,7 +902,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster_big(tfb_scene sc, const 
             if (need && px_i >= mt.x0 && px_i <= mt.x1 && py_i >= mt.y0 && py_i <= mt.y1) {
               const uint32_t key = skey[jj];
               double e[3];
-              if (key >= lo && edges_at(sgeom[jj], mt.flags, px, py, e)) {
+              if (key >= lo && edges_at(AosRec{sgeom + jj}, mt.flags, px, py, e)) {
                 ++ncand;
                 uint32_t k = key;
 #pragma unroll
@@ -861,7 +921,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_raster_big(tfb_scene sc, const 
       const uint32_t nf = min(ncand, (uint32_t)kCand);
       for (uint32_t i = 0; i < nf; ++i) {
         const uint32_t key = ck[i];
-        fd.step(geom[key], meta[key].flags, px, py, (int32_t)key);
+        fd.step(AosRec{geom + key}, meta[key].flags, px, py, (int32_t)key);
       }
       const bool more = need && ncand > (uint32_t)kCand;
       if (more) lo = ck[kCand - 1] + 1;
@@ -885,7 +945,7 @@ using namespace tfb;
 
 extern "C" size_t tfb_raster_workspace_bytes(int64_t num_vertices, int64_t num_triangles, int width, int height,
                                              int max_frames, int64_t pair_capacity) {
-  const int TX = (width + kTile - 1) / kTile, TY = (height + kTile - 1) / kTile;
+  const int TX = (width + kTW - 1) / kTW, TY = (height + kTH - 1) / kTH;
   const int ntiles = TX * TY;
   const int64_t cap = pair_capacity > 0 ? pair_capacity : default_cap(num_triangles, ntiles);
   Work w;
@@ -908,7 +968,7 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
               "tfb_rasterize: %lld texels exceed int32 row ids", (long long)scene->total_texels);
   if (nframes == 0) return TFB_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int TX = (width + kTile - 1) / kTile, TY = (height + kTile - 1) / kTile;
+  const int TX = (width + kTW - 1) / kTW, TY = (height + kTH - 1) / kTH;
   const int ntiles = TX * TY;
   const int64_t m = scene->num_triangles;
   const int64_t cap = pair_capacity > 0 ? pair_capacity : default_cap(m, ntiles);
@@ -943,7 +1003,18 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
     cudaFuncSetAttribute(k_raster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem));
     smem_set = true;
   }
-  k_raster<<<dim3(TX, TY, nframes), kThreads, sizeof(TileSmem), st>>>(sc, cams, width, height, TX, ntiles, w, o);
-  k_raster_big<<<148, kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
+  k_raster<<<dim3(TX, TY, nframes), kTP, sizeof(TileSmem), st>>>(sc, cams, width, height, TX, ntiles, w, o);
+  k_raster_big<<<148 * (256 / kTP), kTP, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
   return check_launch("tfb_rasterize");
 }
+
+#ifdef TFB_RASTER_STATS
+extern "C" int tfb_debug_raster_stats(unsigned long long *out, int reset) {
+  cudaMemcpyFromSymbol(out, g_rstats, sizeof(g_rstats));
+  if (reset) {
+    static unsigned long long zero[64] = {0};
+    cudaMemcpyToSymbol(g_rstats, zero, sizeof(zero));
+  }
+  return 0;
+}
+#endif
