@@ -640,7 +640,7 @@ __device__ __forceinline__ void write_pixel(const tfb_scene &sc, const Cam &cam,
 struct TileSmem {
   double g[kFields * kFS];          // staged records, field-major (SoA): g[k * kFS + j]
   double pe[3][kTP];                // edge values of a pixel's (single) covering pair
-  unsigned long long pmin[kTP];     // per pixel: min (key << 32 | slot) of covering records
+  int32_t pc[2][kTP];               // per pixel: slots of its first two covering pairs (arrival order)
   uint32_t flags[kTP];              // RecMeta::flags
   int32_t tri[kTP];                 // triangle of the record
   int32_t off[kTP];                 // offsets[t] of the record's triangle (n_x < 2^31)
@@ -659,12 +659,12 @@ struct TileSmem {
 //  2. Pair-parallel edge tests: every (record, pixel of its bbox in the tile)
 //     pair gets its own thread (one binary search per thread-run), so float64
 //     lanes are not wasted on pixels outside a small triangle's bbox.  A
-//     covering pair bumps the pixel's candidate count and atomicMin's its
-//     (record key, slot).
-//  3. One thread per pixel: a single candidate is folded directly; with
-//     several, the pixel repeatedly selects the smallest covering key above
-//     the last folded one — the reference's ascending sequential fold
-//     (rasterizer.py:108, 170-171) without sorting the list.
+//     covering pair bumps the pixel's candidate count (32-bit smem atomic)
+//     and the first two covering slots are kept.
+//  3. One thread per pixel: one or two candidates are folded directly in
+//     ascending key order; with more, the pixel repeatedly selects the
+//     smallest covering key above the last folded one — the reference's
+//     ascending sequential fold (rasterizer.py:108, 170-171) without sorting.
 //  Larger or overflowed tiles are handed to k_raster_big.
 __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const double *__restrict__ cams, int W, int H,
                                                         int TX, int ntiles, Work w, Outs o) {
@@ -686,11 +686,10 @@ __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const 
   uint32_t *sflags = S.flags;
   int32_t *stri = S.tri, *soff = S.off;
   uint32_t *skey = S.key, *sbox = S.box, *spre = S.pre, *pcnt = S.pcnt, *wtot = S.wtot;
-  unsigned long long *pmin = S.pmin;
+  int32_t(*pc)[kTP] = S.pc;
   double(*pe)[kTP] = S.pe;
   Cam &cam = S.cam;
   load_cam(cam, cams, f);
-  pmin[tid] = ~0ull;
   pcnt[tid] = 0u;
   const uint32_t *src = w.list + (int64_t)f * w.cap + toff;
   const RecGeom *geom = w.geom + (int64_t)f * w.rs;
@@ -756,11 +755,13 @@ __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const 
       double e[3];
       if (edges_at(SoaRec{sg, j}, sflags[j], (double)(tx0 + pxl) + 0.5, (double)(ty0 + pyl) + 0.5, e)) {
         const int pix = pyl * kTW + pxl;
-        atomicMin(pmin + pix, ((unsigned long long)skey[j] << 32) | (unsigned)j);
-        atomicAdd(pcnt + pix, 1u);
-        pe[0][pix] = e[0];  // meaningful only when this is the pixel's sole candidate
-        pe[1][pix] = e[1];
-        pe[2][pix] = e[2];
+        const uint32_t idx = atomicAdd(pcnt + pix, 1u);
+        if (idx < 2u) pc[idx][pix] = j;
+        if (idx == 0u) {  // used only when this is the pixel's sole candidate
+          pe[0][pix] = e[0];
+          pe[1][pix] = e[1];
+          pe[2][pix] = e[2];
+        }
       }
       if (++lx == bw) {
         lx = 0;
@@ -788,20 +789,25 @@ __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const 
   Fold fd;
   fd.init();
   if (cnt == 1u) {
-    const int j = (int)(pmin[tid] & 0xffffffffu);
+    const int j = pc[0][tid];
     const double e[3] = {pe[0][tid], pe[1][tid], pe[2][tid]};
     fd.step_e(SoaRec{sg, j}, e, j);
-  } else if (cnt > 1u) {
-    unsigned long long cur = pmin[tid];
+  } else if (cnt == 2u) {  // both slots known: fold in ascending key order
+    int j0 = pc[0][tid], j1 = pc[1][tid];
+    if (skey[j1] < skey[j0]) {
+      const int tmp = j0;
+      j0 = j1;
+      j1 = tmp;
+    }
+    fd.step(SoaRec{sg, j0}, sflags[j0], px, py, j0);
+    fd.step(SoaRec{sg, j1}, sflags[j1], px, py, j1);
+  } else if (cnt > 2u) {
+    int64_t last = -1;  // key of the last folded record
     for (uint32_t k = 0; k < cnt; ++k) {
-      const int j = (int)(cur & 0xffffffffu);
-      fd.step(SoaRec{sg, j}, sflags[j], px, py, j);
-      if (k + 1 == cnt) break;
-      const uint32_t last = (uint32_t)(cur >> 32);
       unsigned long long best = ~0ull;
       for (uint32_t i = 0; i < n; ++i) {
         const uint32_t key = skey[i];
-        if (key <= last) continue;
+        if ((int64_t)key <= last) continue;
         const uint32_t bb = sbox[i];
         const int bx = bb & 0xff, by = (bb >> 8) & 0xff;
         if (pxl < bx || pxl >= bx + (int)((bb >> 16) & 0xff) || pyl < by || pyl >= by + (int)(bb >> 24)) continue;
@@ -810,7 +816,9 @@ __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const 
         double e[3];
         if (edges_at(SoaRec{sg, (int)i}, sflags[i], px, py, e)) best = cand;
       }
-      cur = best;
+      const int j = (int)(best & 0xffffffffu);
+      fd.step(SoaRec{sg, j}, sflags[j], px, py, j);
+      last = (int64_t)(best >> 32);
     }
   }
   const uint32_t flags = fd.win >= 0 ? sflags[fd.win] : 0u;
