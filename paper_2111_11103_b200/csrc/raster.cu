@@ -43,6 +43,9 @@ namespace {
 constexpr int kTW = TFB_TW, kTH = TFB_TH;  // raster tile (pixels); one k_raster thread per pixel
 constexpr int kTP = kTW * kTH;             // k_raster threads = tile pixels = staged records per tile
 constexpr int kThreads = 256;              // setup-side kernels
+#ifndef TFB_RASTER_PIPE
+#define TFB_RASTER_PIPE 0  // 1: persistent, software-pipelined tile kernel (k_raster_pipe)
+#endif
 static_assert(kTW % 8 == 0 && kTH % 4 == 0 && kTP >= 64 && kTP <= 256, "tile shape: 8x4-pixel warp blocks");
 constexpr int kCand = 8;
 constexpr uint32_t kNoKey = 0xffffffffu;
@@ -750,17 +753,41 @@ __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const 
     int bw = (b >> 16) & 0xff, bh = b >> 24;
     const int local = (int)(p0 - spre[j]);
     int ly = local / bw, lx = local - ly * bw;
+    // the record's edge coefficients stay in registers while its pairs are walked, and
+    // the row terms dX[k] * (py - ys[a]) of edges_at are formed once per bbox row
+    double dX0, dX1, dX2, dY0, dY1, dY2, xa0, xa1, xa2, A0, A1, A2;
+    uint32_t fl;
+    auto load_rec = [&]() {
+      const SoaRec R{sg, j};
+      dX0 = R.f(kFDX); dX1 = R.f(kFDX + 1); dX2 = R.f(kFDX + 2);
+      dY0 = R.f(kFDY); dY1 = R.f(kFDY + 1); dY2 = R.f(kFDY + 2);
+      xa0 = R.f(kFXs + 1); xa1 = R.f(kFXs + 2); xa2 = R.f(kFXs);
+      fl = sflags[j];
+    };
+    auto load_row = [&]() {
+      const SoaRec R{sg, j};
+      const double py = (double)(ty0 + (int)((b >> 8) & 0xffu) + ly) + 0.5;
+      A0 = __dmul_rn(dX0, __dsub_rn(py, R.f(kFYs + 1)));
+      A1 = __dmul_rn(dX1, __dsub_rn(py, R.f(kFYs + 2)));
+      A2 = __dmul_rn(dX2, __dsub_rn(py, R.f(kFYs)));
+    };
+    load_rec();
+    load_row();
     for (uint32_t p = p0; p < p1; ++p) {
       const int pxl = (int)(b & 0xffu) + lx, pyl = (int)((b >> 8) & 0xffu) + ly;
-      double e[3];
-      if (edges_at(SoaRec{sg, j}, sflags[j], (double)(tx0 + pxl) + 0.5, (double)(ty0 + pyl) + 0.5, e)) {
+      const double px = (double)(tx0 + pxl) + 0.5;
+      const double e0 = __dsub_rn(A0, __dmul_rn(dY0, __dsub_rn(px, xa0)));  // rasterizer.py:161-162
+      const double e1 = __dsub_rn(A1, __dmul_rn(dY1, __dsub_rn(px, xa1)));
+      const double e2 = __dsub_rn(A2, __dmul_rn(dY2, __dsub_rn(px, xa2)));
+      if ((e0 > 0.0 || (e0 == 0.0 && (fl & 1u))) && (e1 > 0.0 || (e1 == 0.0 && (fl & 2u))) &&
+          (e2 > 0.0 || (e2 == 0.0 && (fl & 4u)))) {
         const int pix = pyl * kTW + pxl;
         const uint32_t idx = atomicAdd(pcnt + pix, 1u);
         if (idx < 2u) pc[idx][pix] = j;
         if (idx == 0u) {  // used only when this is the pixel's sole candidate
-          pe[0][pix] = e[0];
-          pe[1][pix] = e[1];
-          pe[2][pix] = e[2];
+          pe[0][pix] = e0;
+          pe[1][pix] = e1;
+          pe[2][pix] = e2;
         }
       }
       if (++lx == bw) {
@@ -768,12 +795,14 @@ __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const 
         if (++ly == bh) {
           ly = 0;
           ++j;
-          if (j < (int)n) {
+          if (j < (int)n && p + 1 < p1) {
             b = sbox[j];
             bw = (b >> 16) & 0xff;
             bh = b >> 24;
+            load_rec();
           }
         }
+        if (p + 1 < p1) load_row();
       }
     }
   }
@@ -825,6 +854,246 @@ __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const 
   const int32_t t = fd.win >= 0 ? stri[fd.win] : -1;
   const int64_t off = fd.win >= 0 ? soff[fd.win] : 0;
   write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, off);
+}
+
+// ---------------------------------------------------------------------------
+// k_raster_pipe: the same per-tile algorithm as k_raster, in persistent CTAs
+// that walk the (frame, tile) tasks with a two-deep software pipeline: while
+// tile k is scanned, edge-tested and folded, the list entries, 128-byte
+// geometry records, meta and camera of tile k+1 are already in flight into
+// the other shared-memory buffer (cp.async), and the count/offset of tile k+2
+// are being read.  The three dependent global round trips of a tile's prologue
+// (count -> list -> records) overlap the previous tile's work instead of
+// stalling the CTA.
+// ---------------------------------------------------------------------------
+struct PipeBuf {
+  double g[kFields * kFS];  // staged geometry, field-major (SoA)
+  RecMeta meta[kTP];
+  uint32_t key[kTP];
+  Cam cam;
+};
+
+struct PipeSmem {
+  PipeBuf buf[2];
+  double pe[3][kTP];
+  int32_t pc[2][kTP];
+  uint32_t pcnt[kTP];
+  uint32_t flags[kTP];
+  uint32_t box[kTP];
+  uint32_t pre[kTP];
+  uint32_t wtot[kTP / 32];
+};
+
+#ifndef TFB_PIPE_CTAS
+#define TFB_PIPE_CTAS 5
+#endif
+
+__device__ __forceinline__ void task_head(const Work &w, int total, int t, uint32_t &n, uint64_t &off) {
+  n = 0;
+  off = 0;
+  if (t < total) {
+    n = w.tile_count[t];
+    off = w.tile_off[t];
+  }
+}
+
+__device__ __forceinline__ bool task_staged(const Work &w, int total, int t, uint32_t n, uint64_t off) {
+  return t < total && n <= (uint32_t)kTP && off + n <= (uint64_t)w.cap;
+}
+
+// issue the cp.async copies of task t's records (thread r < n: record list[r]) and camera into B
+__device__ __forceinline__ void stage_task(const Work &w, const double *cams, int ntiles, int t, uint32_t n,
+                                           uint32_t key, PipeBuf &B, int tid) {
+  const int f = t / ntiles;
+  if ((uint32_t)tid < n) {
+    const double *gsrc = reinterpret_cast<const double *>(w.geom + (int64_t)f * w.rs + key);
+    const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(B.g + tid);
+#pragma unroll
+    for (int q = 0; q < kFields; ++q)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sdst + 8 * kFS * q), "l"(gsrc + q) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(B.meta + tid)),
+                 "l"(w.meta + (int64_t)f * w.rs + key)
+                 : "memory");
+    B.key[tid] = key;
+  }
+  if (tid < 16)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(reinterpret_cast<double *>(&B.cam) + tid)),
+                 "l"(cams + (int64_t)f * 16 + tid)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(kTP, TFB_PIPE_CTAS) k_raster_pipe(tfb_scene sc, const double *__restrict__ cams,
+                                                                    int W, int H, int TX, int ntiles, int total,
+                                                                    Work w, Outs o) {
+  extern __shared__ __align__(16) unsigned char raster_smem[];
+  PipeSmem &S = *reinterpret_cast<PipeSmem *>(raster_smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x;
+  uint32_t *sflags = S.flags, *sbox = S.box, *spre = S.pre, *pcnt = S.pcnt, *wtot = S.wtot;
+  int32_t(*pc)[kTP] = S.pc;
+  double(*pe)[kTP] = S.pe;
+
+  int t = blockIdx.x;
+  uint32_t n_cur, n_nxt;
+  uint64_t off_cur, off_nxt;
+  task_head(w, total, t, n_cur, off_cur);
+  bool st_cur = task_staged(w, total, t, n_cur, off_cur);
+  if (st_cur) {
+    const uint32_t key = (uint32_t)tid < n_cur ? w.list[(int64_t)(t / ntiles) * w.cap + off_cur + tid] : 0u;
+    stage_task(w, cams, ntiles, t, n_cur, key, S.buf[0], tid);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  int tn = t + G;
+  task_head(w, total, tn, n_nxt, off_nxt);
+  for (int b = 0; t < total; t = tn, tn += G, b ^= 1) {
+    PipeBuf &B = S.buf[b];
+    // (1) next task's list entries and the head of the one after: in flight during this tile
+    const bool st_nxt = task_staged(w, total, tn, n_nxt, off_nxt);
+    uint32_t key_nxt = 0u;
+    if (st_nxt && (uint32_t)tid < n_nxt) key_nxt = w.list[(int64_t)(tn / ntiles) * w.cap + off_nxt + tid];
+    uint32_t n_nn;
+    uint64_t off_nn;
+    task_head(w, total, tn + G, n_nn, off_nn);
+
+    // (2) this tile's records have landed (own copies visible after the wait)
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    const int f = t / ntiles, tile = t - f * ntiles;
+    const int tx0 = (tile % TX) * kTW, ty0 = (tile / TX) * kTH;
+    const uint32_t n = st_cur ? n_cur : 0u;
+    uint32_t area = 0;
+    if ((uint32_t)tid < n) {
+      const RecMeta mt = B.meta[tid];
+      sflags[tid] = mt.flags;
+      const int bx0 = max((int)mt.x0, tx0) - tx0, bx1 = min((int)mt.x1, tx0 + kTW - 1) - tx0;
+      const int by0 = max((int)mt.y0, ty0) - ty0, by1 = min((int)mt.y1, ty0 + kTH - 1) - ty0;
+      const uint32_t bw = (uint32_t)(bx1 - bx0 + 1), bh = (uint32_t)(by1 - by0 + 1);
+      sbox[tid] = (uint32_t)bx0 | ((uint32_t)by0 << 8) | (bw << 16) | (bh << 24);
+      area = bw * bh;
+    }
+    pcnt[tid] = 0u;
+    uint32_t incl = area;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    if (lane == 31) wtot[warp] = incl;
+    if (!st_cur && tid == 0) w.big[atomicAdd(w.fcnt + 1, 1u)] = (uint32_t)t;
+    __syncthreads();
+    uint32_t wbase = 0, ptotal = 0;
+#pragma unroll
+    for (int i = 0; i < kTP / 32; ++i) {
+      const uint32_t v = wtot[i];
+      wbase += i < warp ? v : 0u;
+      ptotal += v;
+    }
+    spre[tid] = wbase + incl - area;
+    __syncthreads();
+
+    // (3) stage the next tile into the other buffer (its readers finished before the barrier above)
+    if (st_nxt) stage_task(w, cams, ntiles, tn, n_nxt, key_nxt, S.buf[b ^ 1], tid);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+
+    // (4) pair-parallel edge tests, as k_raster
+    const double *sg = B.g;
+    const uint32_t ppt = (ptotal + kTP - 1) / kTP;
+    const uint32_t p0 = tid * ppt, p1 = min(p0 + ppt, ptotal);
+    if (p0 < p1) {
+      int lo = 0, hi = (int)n - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (spre[mid] <= p0) lo = mid;
+        else hi = mid - 1;
+      }
+      int j = lo;
+      uint32_t bb = sbox[j];
+      int bw = (bb >> 16) & 0xff, bh = bb >> 24;
+      const int local = (int)(p0 - spre[j]);
+      int ly = local / bw, lx = local - ly * bw;
+      for (uint32_t q = p0; q < p1; ++q) {
+        const int pxl = (int)(bb & 0xffu) + lx, pyl = (int)((bb >> 8) & 0xffu) + ly;
+        double e[3];
+        if (edges_at(SoaRec{sg, j}, sflags[j], (double)(tx0 + pxl) + 0.5, (double)(ty0 + pyl) + 0.5, e)) {
+          const int pix = pyl * kTW + pxl;
+          const uint32_t idx = atomicAdd(pcnt + pix, 1u);
+          if (idx < 2u) pc[idx][pix] = j;
+          if (idx == 0u) {
+            pe[0][pix] = e[0];
+            pe[1][pix] = e[1];
+            pe[2][pix] = e[2];
+          }
+        }
+        if (++lx == bw) {
+          lx = 0;
+          if (++ly == bh) {
+            ly = 0;
+            ++j;
+            if (j < (int)n) {
+              bb = sbox[j];
+              bw = (bb >> 16) & 0xff;
+              bh = bb >> 24;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    // (5) one thread per pixel: fold in ascending key order, write the winner
+    const int pxl = tid & (kTW - 1), pyl = tid / kTW;
+    const int px_i = tx0 + pxl, py_i = ty0 + pyl;
+    if (st_cur && px_i < W && py_i < H) {
+      const double px = (double)px_i + 0.5, py = (double)py_i + 0.5;
+      const uint32_t cnt = pcnt[tid];
+      const uint32_t *skey = B.key;
+      Fold fd;
+      fd.init();
+      if (cnt == 1u) {
+        const int j = pc[0][tid];
+        const double e[3] = {pe[0][tid], pe[1][tid], pe[2][tid]};
+        fd.step_e(SoaRec{sg, j}, e, j);
+      } else if (cnt == 2u) {
+        int j0 = pc[0][tid], j1 = pc[1][tid];
+        if (skey[j1] < skey[j0]) {
+          const int tmp = j0;
+          j0 = j1;
+          j1 = tmp;
+        }
+        fd.step(SoaRec{sg, j0}, sflags[j0], px, py, j0);
+        fd.step(SoaRec{sg, j1}, sflags[j1], px, py, j1);
+      } else if (cnt > 2u) {
+        int64_t last = -1;
+        for (uint32_t k = 0; k < cnt; ++k) {
+          unsigned long long best = ~0ull;
+          for (uint32_t i = 0; i < n; ++i) {
+            const uint32_t key = skey[i];
+            if ((int64_t)key <= last) continue;
+            const uint32_t b2 = sbox[i];
+            const int bx = b2 & 0xff, by = (b2 >> 8) & 0xff;
+            if (pxl < bx || pxl >= bx + (int)((b2 >> 16) & 0xff) || pyl < by || pyl >= by + (int)(b2 >> 24)) continue;
+            const unsigned long long cand = ((unsigned long long)key << 32) | i;
+            if (cand >= best) continue;
+            double e[3];
+            if (edges_at(SoaRec{sg, (int)i}, sflags[i], px, py, e)) best = cand;
+          }
+          const int j = (int)(best & 0xffffffffu);
+          fd.step(SoaRec{sg, j}, sflags[j], px, py, j);
+          last = (int64_t)(best >> 32);
+        }
+      }
+      const uint32_t flags = fd.win >= 0 ? sflags[fd.win] : 0u;
+      const int32_t tri = fd.win >= 0 ? (int32_t)(skey[fd.win] >> 1) : -1;
+      const int64_t off = fd.win >= 0 ? B.meta[fd.win].off : 0;
+      write_pixel(sc, B.cam, o, f, W, H, px_i, py_i, fd, flags, tri, off);
+    }
+    st_cur = st_nxt;
+    n_cur = n_nxt;
+    off_cur = off_nxt;
+    n_nxt = n_nn;
+    off_nxt = off_nn;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // Tiles with more than kTP records, or whose list overflowed the pair
@@ -1006,12 +1275,27 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
     k_fill<<<dim3(fill_blocks, nframes), 256, 0, st>>>(w, m, ntiles, TX);
   }
   Outs o{rows_out, texel_hits, tri_out, texel_out, depth_out, u_out, v_out};
+#if TFB_RASTER_PIPE
+  static int pipe_grid = 0;
+  if (!pipe_grid) {
+    cudaFuncSetAttribute(k_raster_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem));
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster_pipe, kTP, sizeof(PipeSmem));
+    pipe_grid = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const int total = ntiles * nframes;
+  k_raster_pipe<<<total < pipe_grid ? total : pipe_grid, kTP, sizeof(PipeSmem), st>>>(sc, cams, width, height, TX,
+                                                                                      ntiles, total, w, o);
+#else
   static bool smem_set = false;
   if (!smem_set) {
     cudaFuncSetAttribute(k_raster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem));
     smem_set = true;
   }
   k_raster<<<dim3(TX, TY, nframes), kTP, sizeof(TileSmem), st>>>(sc, cams, width, height, TX, ntiles, w, o);
+#endif
   k_raster_big<<<148 * (256 / kTP), kTP, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
   return check_launch("tfb_rasterize");
 }
