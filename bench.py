@@ -202,7 +202,8 @@ def run_ours(args):
     pool = softmax_maps(POOL, H, W, C, seed=rank, device=dev)
     probs_list = [pool[i % POOL] for i in range(args.frames)]
     ann = MeshAnnotation(mesh, layout, num_classes=C, aggregator=AGG, weight_mode=WMODE, accum_dtype="float32",
-                         max_batch=args.batch, device=dev, overlap=args.overlap)
+                         max_batch=args.batch, device=dev, overlap=args.overlap,
+                         fuse_ctas_per_sm=args.fuse_ctas if args.fuse_ctas >= 0 else None)
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -321,8 +322,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--frames", type=int, default=FRAMES)
-    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--overlap", type=int, default=0)
+    ap.add_argument("--fuse-ctas", type=int, default=-1, help="cap on resident scatter-add CTAs per SM (-1: auto)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
