@@ -72,7 +72,6 @@ struct Work {
   RecMeta *meta;
   uint8_t *vmask;       // per frame per triangle: bit k = fan sub-triangle k has a record
   uint32_t *cand;       // per frame: triangles surviving the outcode cull (count in fcnt[4f+2])
-  double *vcam;         // per frame per vertex: camera-space xyz (k_verts)
   uint8_t *vcode;       // per frame per vertex: clip outcode (k_verts)
   int64_t nv;
   uint32_t *fcnt;       // fcnt[1]: big-tile count
@@ -100,7 +99,6 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
   size_t o_meta = take(sizeof(RecMeta) * rs * nframes);
   size_t o_vis = take((size_t)(rs / 2) * nframes);
   size_t o_cand = take(sizeof(uint32_t) * (size_t)(rs / 2) * nframes);
-  size_t o_vcam = take(sizeof(double) * 3 * (size_t)(nv > 0 ? nv : 1) * nframes);
   size_t o_vcode = take((size_t)(nv > 0 ? nv : 1) * nframes);
   size_t o_fcnt = take(sizeof(uint32_t) * 4 * nframes);
   size_t o_tc = take(sizeof(uint32_t) * ntiles * nframes);
@@ -115,7 +113,6 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
   w.meta = reinterpret_cast<RecMeta *>(b + o_meta);
   w.vmask = reinterpret_cast<uint8_t *>(b + o_vis);
   w.cand = reinterpret_cast<uint32_t *>(b + o_cand);
-  w.vcam = reinterpret_cast<double *>(b + o_vcam);
   w.vcode = reinterpret_cast<uint8_t *>(b + o_vcode);
   w.nv = nv > 0 ? nv : 1;
   w.fcnt = reinterpret_cast<uint32_t *>(b + o_fcnt);
@@ -252,8 +249,8 @@ __device__ __forceinline__ void store_record(const Work &w, int f, int64_t slot,
     for (int tx = mt.x0 / kTW; tx <= mt.x1 / kTW; ++tx) atomicAdd(tc + ty * TX + tx, 1u);
 }
 
-// Per (frame, vertex): the camera-space position (FMA order of geometry.py:161)
-// and a clip outcode.  bit 0: z < NEAR_PLANE; bits 1-4: the vertex projects
+// Per (frame, vertex): a clip outcode of the camera-space position (FMA order
+// of geometry.py:161).  bit 0: z < NEAR_PLANE; bits 1-4: the vertex projects
 // more than 1/4 pixel beyond the left / right / top / bottom image edge (set
 // only when z >= NEAR_PLANE, tested without divisions).  A triangle whose
 // three outcodes share bit 0 is skipped exactly as rasterizer.py:111 skips it;
@@ -270,10 +267,6 @@ __global__ void __launch_bounds__(kThreads) k_verts(tfb_scene sc, const double *
   if (v >= sc.num_vertices) return;
   double P[3];
   xform(cam, sc.vertices + 3 * v, P);
-  double *dst = w.vcam + ((int64_t)f * w.nv + v) * 3;
-  dst[0] = P[0];
-  dst[1] = P[1];
-  dst[2] = P[2];
   uint32_t code;
   if (P[2] < kNearPlane) {
     code = 1u;
@@ -338,14 +331,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_setup(tfb_scene sc, const doubl
                   i2 = __ldg(sc.triangles + 3 * t + 2);
     const uint8_t *vc = w.vcode + (int64_t)f * w.nv;
     const bool unclipped = ((vc[i0] | vc[i1] | vc[i2]) & 1u) == 0u;  // zmin >= NEAR_PLANE
-    const double *vp = w.vcam + (int64_t)f * w.nv * 3;
+    // camera-space vertices recomputed here (bit-identical to k_verts' transform): the
+    // vertex array is L2-resident across frames, a per-frame camera-space copy is not
     double P[3][3];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      P[0][q] = vp[3 * i0 + q];
-      P[1][q] = vp[3 * i1 + q];
-      P[2][q] = vp[3 * i2 + q];
-    }
+    xform(cam, sc.vertices + 3 * i0, P[0]);
+    xform(cam, sc.vertices + 3 * i1, P[1]);
+    xform(cam, sc.vertices + 3 * i2, P[2]);
     uint32_t mask = 0;
     RecGeom g;
     RecMeta mt;
