@@ -5,10 +5,9 @@
 //            transform (geometry.py:161), near-plane clip + fan
 //            (rasterizer.py:62-82, 113-122), projection, bbox, signed area,
 //            CCW reorder and edge setup (rasterizer.py:136-164).  Surviving
-//            (sub)triangles become 128-byte records at slot 2t+sub; their
-//            tile coverage is counted.
-//   k_scan   per-frame exclusive scan of tile counts.
-//   k_fill   record ids into per-tile lists (unordered).
+//            (sub)triangles become 128-byte records at slot 2t+sub and are
+//            appended to the fixed-capacity bins of the tiles their bbox
+//            overlaps (one returning atomic per tile; unordered).
 //   k_raster one CTA per 16x16 tile, one thread per pixel.  Each pixel keeps
 //            the K smallest (triangle, sub) keys of the records that cover it
 //            (edge test in float64, ownership rule rasterizer.py:85-90), then
@@ -43,9 +42,6 @@ namespace {
 constexpr int kTW = TFB_TW, kTH = TFB_TH;  // raster tile (pixels); one k_raster thread per pixel
 constexpr int kTP = kTW * kTH;             // k_raster threads = tile pixels = staged records per tile
 constexpr int kThreads = 256;              // setup-side kernels
-#ifndef TFB_RASTER_PIPE
-#define TFB_RASTER_PIPE 0  // 1: persistent, software-pipelined tile kernel (k_raster_pipe)
-#endif
 static_assert(kTW % 8 == 0 && kTH % 4 == 0 && kTP >= 64 && kTP <= 256, "tile shape: 8x4-pixel warp blocks");
 constexpr int kCand = 8;
 constexpr uint32_t kNoKey = 0xffffffffu;
@@ -76,17 +72,15 @@ struct Work {
   int64_t nv;
   uint32_t *fcnt;       // fcnt[1]: big-tile count
   uint32_t *tile_count; // per frame per tile
-  uint32_t *tile_cursor;
-  uint64_t *tile_off;
   uint32_t *list;
   uint32_t *big;  // (frame, tile) codes handed to k_raster_big; count in fcnt[1]
   int64_t rs;   // record slots per frame (2m)
-  int64_t cap;  // list capacity per frame
+  int64_t bincap;  // records per tile bin (list holds nframes x ntiles bins)
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int ntiles, int64_t cap, Work &w,
+bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int ntiles, int64_t bincap, Work &w,
            size_t *need_out) {
   const int64_t rs = 2 * (m > 0 ? m : 1);
   size_t off = 0;
@@ -102,9 +96,7 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
   size_t o_vcode = take((size_t)(nv > 0 ? nv : 1) * nframes);
   size_t o_fcnt = take(sizeof(uint32_t) * 4 * nframes);
   size_t o_tc = take(sizeof(uint32_t) * ntiles * nframes);
-  size_t o_cur = take(sizeof(uint32_t) * ntiles * nframes);
-  size_t o_off = take(sizeof(uint64_t) * ntiles * nframes);
-  size_t o_list = take(sizeof(uint32_t) * cap * nframes);
+  size_t o_list = take(sizeof(uint32_t) * (size_t)bincap * ntiles * nframes);
   size_t o_big = take(sizeof(uint32_t) * ntiles * nframes);
   if (need_out) *need_out = off;
   if (!ws || ws_bytes < off) return false;
@@ -117,20 +109,27 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
   w.nv = nv > 0 ? nv : 1;
   w.fcnt = reinterpret_cast<uint32_t *>(b + o_fcnt);
   w.tile_count = reinterpret_cast<uint32_t *>(b + o_tc);
-  w.tile_cursor = reinterpret_cast<uint32_t *>(b + o_cur);
-  w.tile_off = reinterpret_cast<uint64_t *>(b + o_off);
   w.list = reinterpret_cast<uint32_t *>(b + o_list);
   w.big = reinterpret_cast<uint32_t *>(b + o_big);
   w.rs = rs;
-  w.cap = cap;
+  w.bincap = bincap;
   return true;
 }
 
-int64_t default_cap(int64_t m, int ntiles) {
-  int64_t c = 4 * m;
-  if (c < (int64_t)16 * ntiles) c = (int64_t)16 * ntiles;
-  if (c < 65536) c = 65536;
-  if (c > 0xffffffffLL) c = 0xffffffffLL;
+// Tile bin capacity: `pair_capacity` (record/tile pairs budgeted per frame)
+// spread over the tiles, default 4 pairs per triangle, at least 512 per tile
+// (a 16x8 tile of the BASELINE scene holds ~20-60).  A tile whose bin
+// overflows is still rasterized exactly by k_raster_big's full scan.
+int64_t bin_capacity(int64_t pair_capacity, int64_t m, int ntiles) {
+  int64_t c;
+  if (pair_capacity > 0) {
+    c = (pair_capacity + ntiles - 1) / ntiles;
+  } else {
+    c = (4 * m + ntiles - 1) / ntiles;
+    if (c < 512) c = 512;
+  }
+  if (c < 1) c = 1;
+  if (c > 0x7fffffffLL / (ntiles > 0 ? ntiles : 1)) c = 0x7fffffffLL / (ntiles > 0 ? ntiles : 1);
   return c;
 }
 
@@ -246,7 +245,11 @@ __device__ __forceinline__ void store_record(const Work &w, int f, int64_t slot,
   w.meta[idx] = mt;
   uint32_t *tc = w.tile_count + (int64_t)f * ntiles;
   for (int ty = mt.y0 / kTH; ty <= mt.y1 / kTH; ++ty)
-    for (int tx = mt.x0 / kTW; tx <= mt.x1 / kTW; ++tx) atomicAdd(tc + ty * TX + tx, 1u);
+    for (int tx = mt.x0 / kTW; tx <= mt.x1 / kTW; ++tx) {
+      const int tile = ty * TX + tx;
+      const uint32_t pos = atomicAdd(tc + tile, 1u);
+      if (pos < (uint64_t)w.bincap) w.list[((int64_t)f * ntiles + tile) * w.bincap + pos] = (uint32_t)slot;
+    }
 }
 
 // Per (frame, vertex): a clip outcode of the camera-space position (FMA order
@@ -365,71 +368,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_setup(tfb_scene sc, const doubl
       }
     }
     if (mask) w.vmask[(int64_t)f * (w.rs / 2) + t] = (uint8_t)mask;
-  }
-}
-
-__global__ void __launch_bounds__(1024) k_scan(Work w, int ntiles) {
-  const int f = blockIdx.x;
-  const uint32_t *cnt = w.tile_count + (int64_t)f * ntiles;
-  uint64_t *off = w.tile_off + (int64_t)f * ntiles;
-  __shared__ uint64_t warp_tot[32];
-  __shared__ uint64_t running;
-  if (threadIdx.x == 0) running = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int b0 = 0; b0 < ntiles; b0 += 1024) {
-    const int i = b0 + threadIdx.x;
-    const uint64_t v = i < ntiles ? cnt[i] : 0;
-    uint64_t incl = v;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint64_t u = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += u;
-    }
-    if (lane == 31) warp_tot[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      uint64_t s = warp_tot[lane];
-      uint64_t x = s;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint64_t u = __shfl_up_sync(0xffffffffu, x, d);
-        if (lane >= d) x += u;
-      }
-      warp_tot[lane] = x - s;  // exclusive warp prefix
-    }
-    __syncthreads();
-    const uint64_t r0 = running;
-    if (i < ntiles) off[i] = r0 + warp_tot[warp] + incl - v;
-    __syncthreads();
-    if (threadIdx.x == 1023) running = r0 + warp_tot[warp] + incl;
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(256) k_fill(Work w, int64_t m, int ntiles, int TX) {
-  const int f = blockIdx.y;
-  const uint8_t *vm = w.vmask + (int64_t)f * m;
-  const uint32_t *cl = w.cand + (int64_t)f * m;
-  const uint32_t ncand = w.fcnt[4 * f + 2];
-  const RecMeta *meta = w.meta + (int64_t)f * w.rs;
-  const uint64_t *toff = w.tile_off + (int64_t)f * ntiles;
-  uint32_t *cur = w.tile_cursor + (int64_t)f * ntiles;
-  uint32_t *list = w.list + (int64_t)f * w.cap;
-  for (uint32_t ci = blockIdx.x * blockDim.x + threadIdx.x; ci < ncand; ci += gridDim.x * blockDim.x) {
-    const uint32_t t = cl[ci];
-    const uint32_t mask = vm[t];
-    for (int sub = 0; sub < 2; ++sub) {
-      if (!((mask >> sub) & 1u)) continue;
-      const uint32_t r = 2 * t + sub;
-      const RecMeta mt = meta[r];
-      for (int ty = mt.y0 / kTH; ty <= mt.y1 / kTH; ++ty)
-        for (int tx = mt.x0 / kTW; tx <= mt.x1 / kTW; ++tx) {
-          const int tile = ty * TX + tx;
-          const uint64_t pos = toff[tile] + atomicAdd(cur + tile, 1u);
-          if (pos < (uint64_t)w.cap) list[pos] = r;
-        }
-    }
   }
 }
 
@@ -667,8 +605,7 @@ __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const 
   const int tx0 = blockIdx.x * kTW, ty0 = blockIdx.y * kTH;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t n = w.tile_count[(int64_t)f * ntiles + tile];
-  const uint64_t toff = w.tile_off[(int64_t)f * ntiles + tile];
-  if (toff + n > (uint64_t)w.cap || n > (uint32_t)kTP) {
+  if (n > (uint64_t)w.bincap || n > (uint32_t)kTP) {
     if (tid == 0) w.big[atomicAdd(w.fcnt + 1, 1u)] = (uint32_t)(f * ntiles + tile);
     if (tid == 0) RSTAT(48);
     return;
@@ -685,7 +622,7 @@ __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const 
   Cam &cam = S.cam;
   load_cam(cam, cams, f);
   pcnt[tid] = 0u;
-  const uint32_t *src = w.list + (int64_t)f * w.cap + toff;
+  const uint32_t *src = w.list + ((int64_t)f * ntiles + tile) * w.bincap;
   const RecGeom *geom = w.geom + (int64_t)f * w.rs;
   uint32_t area = 0;
   if (tid < n) {
@@ -847,246 +784,6 @@ __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const 
   write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, off);
 }
 
-// ---------------------------------------------------------------------------
-// k_raster_pipe: the same per-tile algorithm as k_raster, in persistent CTAs
-// that walk the (frame, tile) tasks with a two-deep software pipeline: while
-// tile k is scanned, edge-tested and folded, the list entries, 128-byte
-// geometry records, meta and camera of tile k+1 are already in flight into
-// the other shared-memory buffer (cp.async), and the count/offset of tile k+2
-// are being read.  The three dependent global round trips of a tile's prologue
-// (count -> list -> records) overlap the previous tile's work instead of
-// stalling the CTA.
-// ---------------------------------------------------------------------------
-struct PipeBuf {
-  double g[kFields * kFS];  // staged geometry, field-major (SoA)
-  RecMeta meta[kTP];
-  uint32_t key[kTP];
-  Cam cam;
-};
-
-struct PipeSmem {
-  PipeBuf buf[2];
-  double pe[3][kTP];
-  int32_t pc[2][kTP];
-  uint32_t pcnt[kTP];
-  uint32_t flags[kTP];
-  uint32_t box[kTP];
-  uint32_t pre[kTP];
-  uint32_t wtot[kTP / 32];
-};
-
-#ifndef TFB_PIPE_CTAS
-#define TFB_PIPE_CTAS 5
-#endif
-
-__device__ __forceinline__ void task_head(const Work &w, int total, int t, uint32_t &n, uint64_t &off) {
-  n = 0;
-  off = 0;
-  if (t < total) {
-    n = w.tile_count[t];
-    off = w.tile_off[t];
-  }
-}
-
-__device__ __forceinline__ bool task_staged(const Work &w, int total, int t, uint32_t n, uint64_t off) {
-  return t < total && n <= (uint32_t)kTP && off + n <= (uint64_t)w.cap;
-}
-
-// issue the cp.async copies of task t's records (thread r < n: record list[r]) and camera into B
-__device__ __forceinline__ void stage_task(const Work &w, const double *cams, int ntiles, int t, uint32_t n,
-                                           uint32_t key, PipeBuf &B, int tid) {
-  const int f = t / ntiles;
-  if ((uint32_t)tid < n) {
-    const double *gsrc = reinterpret_cast<const double *>(w.geom + (int64_t)f * w.rs + key);
-    const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(B.g + tid);
-#pragma unroll
-    for (int q = 0; q < kFields; ++q)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sdst + 8 * kFS * q), "l"(gsrc + q) : "memory");
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(B.meta + tid)),
-                 "l"(w.meta + (int64_t)f * w.rs + key)
-                 : "memory");
-    B.key[tid] = key;
-  }
-  if (tid < 16)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                     (uint32_t)__cvta_generic_to_shared(reinterpret_cast<double *>(&B.cam) + tid)),
-                 "l"(cams + (int64_t)f * 16 + tid)
-                 : "memory");
-}
-
-__global__ void __launch_bounds__(kTP, TFB_PIPE_CTAS) k_raster_pipe(tfb_scene sc, const double *__restrict__ cams,
-                                                                    int W, int H, int TX, int ntiles, int total,
-                                                                    Work w, Outs o) {
-  extern __shared__ __align__(16) unsigned char raster_smem[];
-  PipeSmem &S = *reinterpret_cast<PipeSmem *>(raster_smem);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = gridDim.x;
-  uint32_t *sflags = S.flags, *sbox = S.box, *spre = S.pre, *pcnt = S.pcnt, *wtot = S.wtot;
-  int32_t(*pc)[kTP] = S.pc;
-  double(*pe)[kTP] = S.pe;
-
-  int t = blockIdx.x;
-  uint32_t n_cur, n_nxt;
-  uint64_t off_cur, off_nxt;
-  task_head(w, total, t, n_cur, off_cur);
-  bool st_cur = task_staged(w, total, t, n_cur, off_cur);
-  if (st_cur) {
-    const uint32_t key = (uint32_t)tid < n_cur ? w.list[(int64_t)(t / ntiles) * w.cap + off_cur + tid] : 0u;
-    stage_task(w, cams, ntiles, t, n_cur, key, S.buf[0], tid);
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  int tn = t + G;
-  task_head(w, total, tn, n_nxt, off_nxt);
-  for (int b = 0; t < total; t = tn, tn += G, b ^= 1) {
-    PipeBuf &B = S.buf[b];
-    // (1) next task's list entries and the head of the one after: in flight during this tile
-    const bool st_nxt = task_staged(w, total, tn, n_nxt, off_nxt);
-    uint32_t key_nxt = 0u;
-    if (st_nxt && (uint32_t)tid < n_nxt) key_nxt = w.list[(int64_t)(tn / ntiles) * w.cap + off_nxt + tid];
-    uint32_t n_nn;
-    uint64_t off_nn;
-    task_head(w, total, tn + G, n_nn, off_nn);
-
-    // (2) this tile's records have landed (own copies visible after the wait)
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    const int f = t / ntiles, tile = t - f * ntiles;
-    const int tx0 = (tile % TX) * kTW, ty0 = (tile / TX) * kTH;
-    const uint32_t n = st_cur ? n_cur : 0u;
-    uint32_t area = 0;
-    if ((uint32_t)tid < n) {
-      const RecMeta mt = B.meta[tid];
-      sflags[tid] = mt.flags;
-      const int bx0 = max((int)mt.x0, tx0) - tx0, bx1 = min((int)mt.x1, tx0 + kTW - 1) - tx0;
-      const int by0 = max((int)mt.y0, ty0) - ty0, by1 = min((int)mt.y1, ty0 + kTH - 1) - ty0;
-      const uint32_t bw = (uint32_t)(bx1 - bx0 + 1), bh = (uint32_t)(by1 - by0 + 1);
-      sbox[tid] = (uint32_t)bx0 | ((uint32_t)by0 << 8) | (bw << 16) | (bh << 24);
-      area = bw * bh;
-    }
-    pcnt[tid] = 0u;
-    uint32_t incl = area;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += v;
-    }
-    if (lane == 31) wtot[warp] = incl;
-    if (!st_cur && tid == 0) w.big[atomicAdd(w.fcnt + 1, 1u)] = (uint32_t)t;
-    __syncthreads();
-    uint32_t wbase = 0, ptotal = 0;
-#pragma unroll
-    for (int i = 0; i < kTP / 32; ++i) {
-      const uint32_t v = wtot[i];
-      wbase += i < warp ? v : 0u;
-      ptotal += v;
-    }
-    spre[tid] = wbase + incl - area;
-    __syncthreads();
-
-    // (3) stage the next tile into the other buffer (its readers finished before the barrier above)
-    if (st_nxt) stage_task(w, cams, ntiles, tn, n_nxt, key_nxt, S.buf[b ^ 1], tid);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-
-    // (4) pair-parallel edge tests, as k_raster
-    const double *sg = B.g;
-    const uint32_t ppt = (ptotal + kTP - 1) / kTP;
-    const uint32_t p0 = tid * ppt, p1 = min(p0 + ppt, ptotal);
-    if (p0 < p1) {
-      int lo = 0, hi = (int)n - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (spre[mid] <= p0) lo = mid;
-        else hi = mid - 1;
-      }
-      int j = lo;
-      uint32_t bb = sbox[j];
-      int bw = (bb >> 16) & 0xff, bh = bb >> 24;
-      const int local = (int)(p0 - spre[j]);
-      int ly = local / bw, lx = local - ly * bw;
-      for (uint32_t q = p0; q < p1; ++q) {
-        const int pxl = (int)(bb & 0xffu) + lx, pyl = (int)((bb >> 8) & 0xffu) + ly;
-        double e[3];
-        if (edges_at(SoaRec{sg, j}, sflags[j], (double)(tx0 + pxl) + 0.5, (double)(ty0 + pyl) + 0.5, e)) {
-          const int pix = pyl * kTW + pxl;
-          const uint32_t idx = atomicAdd(pcnt + pix, 1u);
-          if (idx < 2u) pc[idx][pix] = j;
-          if (idx == 0u) {
-            pe[0][pix] = e[0];
-            pe[1][pix] = e[1];
-            pe[2][pix] = e[2];
-          }
-        }
-        if (++lx == bw) {
-          lx = 0;
-          if (++ly == bh) {
-            ly = 0;
-            ++j;
-            if (j < (int)n) {
-              bb = sbox[j];
-              bw = (bb >> 16) & 0xff;
-              bh = bb >> 24;
-            }
-          }
-        }
-      }
-    }
-    __syncthreads();
-
-    // (5) one thread per pixel: fold in ascending key order, write the winner
-    const int pxl = tid & (kTW - 1), pyl = tid / kTW;
-    const int px_i = tx0 + pxl, py_i = ty0 + pyl;
-    if (st_cur && px_i < W && py_i < H) {
-      const double px = (double)px_i + 0.5, py = (double)py_i + 0.5;
-      const uint32_t cnt = pcnt[tid];
-      const uint32_t *skey = B.key;
-      Fold fd;
-      fd.init();
-      if (cnt == 1u) {
-        const int j = pc[0][tid];
-        const double e[3] = {pe[0][tid], pe[1][tid], pe[2][tid]};
-        fd.step_e(SoaRec{sg, j}, e, j);
-      } else if (cnt == 2u) {
-        int j0 = pc[0][tid], j1 = pc[1][tid];
-        if (skey[j1] < skey[j0]) {
-          const int tmp = j0;
-          j0 = j1;
-          j1 = tmp;
-        }
-        fd.step(SoaRec{sg, j0}, sflags[j0], px, py, j0);
-        fd.step(SoaRec{sg, j1}, sflags[j1], px, py, j1);
-      } else if (cnt > 2u) {
-        int64_t last = -1;
-        for (uint32_t k = 0; k < cnt; ++k) {
-          unsigned long long best = ~0ull;
-          for (uint32_t i = 0; i < n; ++i) {
-            const uint32_t key = skey[i];
-            if ((int64_t)key <= last) continue;
-            const uint32_t b2 = sbox[i];
-            const int bx = b2 & 0xff, by = (b2 >> 8) & 0xff;
-            if (pxl < bx || pxl >= bx + (int)((b2 >> 16) & 0xff) || pyl < by || pyl >= by + (int)(b2 >> 24)) continue;
-            const unsigned long long cand = ((unsigned long long)key << 32) | i;
-            if (cand >= best) continue;
-            double e[3];
-            if (edges_at(SoaRec{sg, (int)i}, sflags[i], px, py, e)) best = cand;
-          }
-          const int j = (int)(best & 0xffffffffu);
-          fd.step(SoaRec{sg, j}, sflags[j], px, py, j);
-          last = (int64_t)(best >> 32);
-        }
-      }
-      const uint32_t flags = fd.win >= 0 ? sflags[fd.win] : 0u;
-      const int32_t tri = fd.win >= 0 ? (int32_t)(skey[fd.win] >> 1) : -1;
-      const int64_t off = fd.win >= 0 ? B.meta[fd.win].off : 0;
-      write_pixel(sc, B.cam, o, f, W, H, px_i, py_i, fd, flags, tri, off);
-    }
-    st_cur = st_nxt;
-    n_cur = n_nxt;
-    off_cur = off_nxt;
-    n_nxt = n_nn;
-    off_nxt = off_nn;
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
 // Tiles with more than kTP records, or whose list overflowed the pair
 // budget (then every record slot of the frame is scanned, invalid slots
 // masked out by vmask).  Records stream through shared memory in chunks in
@@ -1112,9 +809,8 @@ __global__ void __launch_bounds__(kTP) k_raster_big(tfb_scene sc, const double *
     __syncthreads();
     load_cam(cam, cams, f);
     const uint32_t tcount = w.tile_count[(int64_t)f * ntiles + tile];
-    const uint64_t toff = w.tile_off[(int64_t)f * ntiles + tile];
-    const bool ovf = toff + tcount > (uint64_t)w.cap;
-    const uint32_t *list = w.list + (int64_t)f * w.cap + toff;
+    const bool ovf = tcount > (uint64_t)w.bincap;
+    const uint32_t *list = w.list + ((int64_t)f * ntiles + tile) * w.bincap;
     const uint8_t *vm = w.vmask + (int64_t)f * (w.rs / 2);
     const uint32_t nsrc = ovf ? (uint32_t)w.rs : tcount;
     const RecGeom *geom = w.geom + (int64_t)f * w.rs;
@@ -1215,10 +911,10 @@ extern "C" size_t tfb_raster_workspace_bytes(int64_t num_vertices, int64_t num_t
                                              int max_frames, int64_t pair_capacity) {
   const int TX = (width + kTW - 1) / kTW, TY = (height + kTH - 1) / kTH;
   const int ntiles = TX * TY;
-  const int64_t cap = pair_capacity > 0 ? pair_capacity : default_cap(num_triangles, ntiles);
+  const int64_t bincap = bin_capacity(pair_capacity, num_triangles, ntiles);
   Work w;
   size_t need = 0;
-  carve(nullptr, 0, num_vertices, num_triangles, max_frames, ntiles, cap, w, &need);
+  carve(nullptr, 0, num_vertices, num_triangles, max_frames, ntiles, bincap, w, &need);
   return need;
 }
 
@@ -1239,16 +935,15 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
   const int TX = (width + kTW - 1) / kTW, TY = (height + kTH - 1) / kTH;
   const int ntiles = TX * TY;
   const int64_t m = scene->num_triangles;
-  const int64_t cap = pair_capacity > 0 ? pair_capacity : default_cap(m, ntiles);
+  const int64_t bincap = bin_capacity(pair_capacity, m, ntiles);
   Work w;
   size_t need = 0;
-  if (!carve(workspace, workspace_bytes, scene->num_vertices, m, nframes, ntiles, cap, w, &need)) {
+  if (!carve(workspace, workspace_bytes, scene->num_vertices, m, nframes, ntiles, bincap, w, &need)) {
     set_error("tfb_rasterize: workspace of %zu bytes is smaller than the %zu required", workspace_bytes, need);
     return TFB_ERR_CAPACITY;
   }
   cudaMemsetAsync(w.fcnt, 0, sizeof(uint32_t) * 4 * nframes, st);
   cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ntiles * nframes, st);
-  cudaMemsetAsync(w.tile_cursor, 0, sizeof(uint32_t) * ntiles * nframes, st);
   tfb_scene sc = *scene;
   if (m > 0) {
     if (sc.num_vertices > 0) {
@@ -1260,33 +955,14 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
     int64_t sb = (m / 3 + kThreads - 1) / kThreads;  // ~1/3 of the triangles survive a typical cull
     dim3 g2((unsigned)(sb < 1 ? 1 : sb), nframes);
     k_setup<<<g2, kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w);
-    k_scan<<<nframes, 1024, 0, st>>>(w, ntiles);
-    int64_t fb = (m + 255) / 256;
-    const int fill_blocks = (int)(fb < 1184 ? fb : 1184);
-    k_fill<<<dim3(fill_blocks, nframes), 256, 0, st>>>(w, m, ntiles, TX);
   }
   Outs o{rows_out, texel_hits, tri_out, texel_out, depth_out, u_out, v_out};
-#if TFB_RASTER_PIPE
-  static int pipe_grid = 0;
-  if (!pipe_grid) {
-    cudaFuncSetAttribute(k_raster_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem));
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster_pipe, kTP, sizeof(PipeSmem));
-    pipe_grid = sms * (per_sm > 0 ? per_sm : 1);
-  }
-  const int total = ntiles * nframes;
-  k_raster_pipe<<<total < pipe_grid ? total : pipe_grid, kTP, sizeof(PipeSmem), st>>>(sc, cams, width, height, TX,
-                                                                                      ntiles, total, w, o);
-#else
   static bool smem_set = false;
   if (!smem_set) {
     cudaFuncSetAttribute(k_raster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem));
     smem_set = true;
   }
   k_raster<<<dim3(TX, TY, nframes), kTP, sizeof(TileSmem), st>>>(sc, cams, width, height, TX, ntiles, w, o);
-#endif
   k_raster_big<<<148 * (256 / kTP), kTP, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
   return check_launch("tfb_rasterize");
 }
