@@ -287,22 +287,35 @@ __global__ void __launch_bounds__(kThreads) k_verts(tfb_scene sc, const double *
 // vertex outcodes decides whether the triangle can produce a record at all;
 // survivors are appended (one global atomic per block) to the frame's
 // candidate list; every triangle's visibility mask is reset.
+constexpr int kCullPer = 4;  // triangles per k_cull thread (independent loads in flight)
+
 __global__ void __launch_bounds__(kThreads) k_cull(tfb_scene sc, Work w) {
   const int f = blockIdx.y;
   __shared__ uint32_t wtot[kThreads / 32];
   __shared__ uint32_t base;
-  const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  bool cand = false;
-  if (t < sc.num_triangles) {
-    const int64_t i0 = __ldg(sc.triangles + 3 * t), i1 = __ldg(sc.triangles + 3 * t + 1),
-                  i2 = __ldg(sc.triangles + 3 * t + 2);
-    const uint8_t *vc = w.vcode + (int64_t)f * w.nv;
-    cand = (vc[i0] & vc[i1] & vc[i2]) == 0u;  // not all behind the near plane nor beyond one edge
-    w.vmask[(int64_t)f * (w.rs / 2) + t] = 0;
+  const int64_t t0 = (int64_t)blockIdx.x * kThreads * kCullPer + threadIdx.x;
+  const uint8_t *vc = w.vcode + (int64_t)f * w.nv;
+  int32_t vi[kCullPer][3];
+#pragma unroll
+  for (int k = 0; k < kCullPer; ++k) {
+    const int64_t t = t0 + (int64_t)k * kThreads;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) vi[k][q] = t < sc.num_triangles ? __ldg(sc.triangles + 3 * t + q) : -1;
   }
+  unsigned cmask = 0;  // bit k: triangle t0 + k * kThreads is a candidate
+#pragma unroll
+  for (int k = 0; k < kCullPer; ++k)
+    if (vi[k][0] >= 0 && (vc[vi[k][0]] & vc[vi[k][1]] & vc[vi[k][2]]) == 0u)  // not all behind the near plane
+      cmask |= 1u << k;                                                     // nor beyond one image edge
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned bal = __ballot_sync(0xffffffffu, cand);
-  if (lane == 0) wtot[warp] = __popc(bal);
+  const uint32_t mine = __popc(cmask);
+  uint32_t incl = mine;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  if (lane == 31) wtot[warp] = incl;
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t s = 0;
@@ -314,7 +327,10 @@ __global__ void __launch_bounds__(kThreads) k_cull(tfb_scene sc, Work w) {
     base = s ? atomicAdd(w.fcnt + 4 * f + 2, s) : 0u;
   }
   __syncthreads();
-  if (cand) w.cand[(int64_t)f * (w.rs / 2) + base + wtot[warp] + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)t;
+  uint32_t *out = w.cand + (int64_t)f * (w.rs / 2) + base + wtot[warp] + incl - mine;
+#pragma unroll
+  for (int k = 0; k < kCullPer; ++k)
+    if ((cmask >> k) & 1u) *out++ = (uint32_t)(t0 + (int64_t)k * kThreads);
 }
 
 // Per surviving (frame, triangle): near clip + fan, projection, bbox, signed
@@ -367,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_setup(tfb_scene sc, const doubl
         }
       }
     }
-    if (mask) w.vmask[(int64_t)f * (w.rs / 2) + t] = (uint8_t)mask;
+    w.vmask[(int64_t)f * (w.rs / 2) + t] = (uint8_t)mask;  // every candidate, 0 included
   }
 }
 
@@ -784,8 +800,8 @@ __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const 
   write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, off);
 }
 
-// Tiles with more than kTP records, or whose list overflowed the pair
-// budget (then every record slot of the frame is scanned, invalid slots
+// Tiles with more than kTP records, or whose bin overflowed (then both
+// record slots of every cull survivor of the frame are scanned, empty slots
 // masked out by vmask).  Records stream through shared memory in chunks in
 // arbitrary order; each pixel keeps the kCand smallest covering keys above
 // `lo`, folds them in ascending order and repeats with `lo` past the last
@@ -812,7 +828,8 @@ __global__ void __launch_bounds__(kTP) k_raster_big(tfb_scene sc, const double *
     const bool ovf = tcount > (uint64_t)w.bincap;
     const uint32_t *list = w.list + ((int64_t)f * ntiles + tile) * w.bincap;
     const uint8_t *vm = w.vmask + (int64_t)f * (w.rs / 2);
-    const uint32_t nsrc = ovf ? (uint32_t)w.rs : tcount;
+    const uint32_t *cl = w.cand + (int64_t)f * (w.rs / 2);  // overflow: every slot of every candidate
+    const uint32_t nsrc = ovf ? 2u * w.fcnt[4 * f + 2] : tcount;
     const RecGeom *geom = w.geom + (int64_t)f * w.rs;
     const RecMeta *meta = w.meta + (int64_t)f * w.rs;
 
@@ -830,7 +847,7 @@ __global__ void __launch_bounds__(kTP) k_raster_big(tfb_scene sc, const double *
         __syncthreads();
         if (threadIdx.x < n) {
           const uint32_t i = b0 + threadIdx.x;
-          const uint32_t r = ovf ? i : list[i];
+          const uint32_t r = ovf ? 2u * cl[i >> 1] + (i & 1u) : list[i];
           skey[threadIdx.x] = r;
           if (!ovf || ((vm[r >> 1] >> (r & 1u)) & 1u)) {
             smeta[threadIdx.x] = meta[r];
@@ -950,7 +967,7 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
       dim3 g0((unsigned)((sc.num_vertices + kThreads - 1) / kThreads), nframes);
       k_verts<<<g0, kThreads, 0, st>>>(sc, cams, width, height, w);
     }
-    dim3 g1((unsigned)((m + kThreads - 1) / kThreads), nframes);
+    dim3 g1((unsigned)((m + kThreads * kCullPer - 1) / (kThreads * kCullPer)), nframes);
     k_cull<<<g1, kThreads, 0, st>>>(sc, w);
     int64_t sb = (m / 3 + kThreads - 1) / kThreads;  // ~1/3 of the triangles survive a typical cull
     dim3 g2((unsigned)(sb < 1 ? 1 : sb), nframes);
