@@ -235,21 +235,31 @@ __device__ bool build_record(const Cam &cam, int W, int H, const double P[3][3],
   return true;
 }
 
+// A stored record whose tile-bin appends are still to be issued.  k_setup
+// batches the appends of several records so their returning atomics are in
+// flight together instead of one dependent round trip per record.
+struct Pend {
+  uint32_t slot;
+  uint32_t tx, ty;  // first tile (x | last x << 16), (y | last y << 16)
+  bool valid;
+};
+
 __device__ __forceinline__ void store_record(const Work &w, int f, int64_t slot, const RecGeom &g,
-                                             const RecMeta &mt, int ntiles, int TX) {
+                                             const RecMeta &mt, Pend &pd) {
   const int64_t idx = (int64_t)f * w.rs + slot;
   const double2 *src = reinterpret_cast<const double2 *>(&g);
   double2 *dst = reinterpret_cast<double2 *>(w.geom + idx);
 #pragma unroll
   for (int q = 0; q < 8; ++q) dst[q] = src[q];
   w.meta[idx] = mt;
-  uint32_t *tc = w.tile_count + (int64_t)f * ntiles;
-  for (int ty = mt.y0 / kTH; ty <= mt.y1 / kTH; ++ty)
-    for (int tx = mt.x0 / kTW; tx <= mt.x1 / kTW; ++tx) {
-      const int tile = ty * TX + tx;
-      const uint32_t pos = atomicAdd(tc + tile, 1u);
-      if (pos < (uint64_t)w.bincap) w.list[((int64_t)f * ntiles + tile) * w.bincap + pos] = (uint32_t)slot;
-    }
+  pd.slot = (uint32_t)slot;
+  pd.tx = (uint32_t)(mt.x0 / kTW) | ((uint32_t)(mt.x1 / kTW) << 16);
+  pd.ty = (uint32_t)(mt.y0 / kTH) | ((uint32_t)(mt.y1 / kTH) << 16);
+  pd.valid = true;
+}
+
+__device__ __forceinline__ void bin_put(const Work &w, int f, int ntiles, int tile, uint32_t pos, uint32_t slot) {
+  if (pos < (uint64_t)w.bincap) w.list[((int64_t)f * ntiles + tile) * w.bincap + pos] = slot;
 }
 
 // Per (frame, vertex): a clip outcode of the camera-space position (FMA order
@@ -336,6 +346,8 @@ __global__ void __launch_bounds__(kThreads) k_cull(tfb_scene sc, Work w) {
 // Per surviving (frame, triangle): near clip + fan, projection, bbox, signed
 // area, CCW reorder and edge setup (rasterizer.py:113-164) into 128-byte
 // records at slot 2t+sub; tile coverage counted.
+constexpr int kSetupPer = 2;  // candidates per k_setup thread (their bin appends are batched)
+
 __global__ void __launch_bounds__(kThreads, 4) k_setup(tfb_scene sc, const double *__restrict__ cams, int W,
                                                     int H, int TX, int ntiles, Work w) {
   const int f = blockIdx.y;
@@ -344,7 +356,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_setup(tfb_scene sc, const doubl
   __syncthreads();
   const uint32_t ncand = w.fcnt[4 * f + 2];
   const uint32_t *cl = w.cand + (int64_t)f * (w.rs / 2);
-  for (uint32_t ci = blockIdx.x * kThreads + threadIdx.x; ci < ncand; ci += gridDim.x * kThreads) {
+  auto one = [&](uint32_t ci, Pend &p0, Pend &p1) {
+    p0.valid = p1.valid = false;
+    if (ci >= ncand) return;
     const int64_t t = cl[ci];
     const int64_t i0 = __ldg(sc.triangles + 3 * t), i1 = __ldg(sc.triangles + 3 * t + 1),
                   i2 = __ldg(sc.triangles + 3 * t + 2);
@@ -363,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_setup(tfb_scene sc, const doubl
     const int32_t toff = (int32_t)__ldg(sc.offsets + t);
     if (unclipped) {
       if (build_record(cam, W, H, P, toff, false, 0, tflags, g, mt)) {
-        store_record(w, f, 2 * t, g, mt, ntiles, TX);
+        store_record(w, f, 2 * t, g, mt, p0);
         mask = 1;
       }
     } else {
@@ -378,12 +392,36 @@ __global__ void __launch_bounds__(kThreads, 4) k_setup(tfb_scene sc, const doubl
           S[2][q] = op[k + 1][q];
         }
         if (build_record(cam, W, H, S, toff, true, k - 1, tflags, g, mt)) {
-          store_record(w, f, 2 * t + (k - 1), g, mt, ntiles, TX);
+          store_record(w, f, 2 * t + (k - 1), g, mt, k == 1 ? p0 : p1);
           mask |= 1u << (k - 1);
         }
       }
     }
     w.vmask[(int64_t)f * (w.rs / 2) + t] = (uint8_t)mask;  // every candidate, 0 included
+  };
+  uint32_t *tc = w.tile_count + (int64_t)f * ntiles;
+  const uint32_t stride = gridDim.x * kThreads * kSetupPer;
+  for (uint32_t c0 = blockIdx.x * kThreads * kSetupPer + threadIdx.x; c0 < ncand; c0 += stride) {
+    Pend p[2 * kSetupPer];
+    one(c0, p[0], p[1]);
+    one(c0 + kThreads, p[2], p[3]);
+    // first-tile appends of all pending records in flight together, then the rest
+    uint32_t pos[2 * kSetupPer];
+#pragma unroll
+    for (int e = 0; e < 2 * kSetupPer; ++e)
+      if (p[e].valid) pos[e] = atomicAdd(tc + (int)(p[e].ty & 0xffffu) * TX + (int)(p[e].tx & 0xffffu), 1u);
+#pragma unroll
+    for (int e = 0; e < 2 * kSetupPer; ++e) {
+      if (!p[e].valid) continue;
+      const int x0 = (int)(p[e].tx & 0xffffu), x1 = (int)(p[e].tx >> 16);
+      const int y0 = (int)(p[e].ty & 0xffffu), y1 = (int)(p[e].ty >> 16);
+      bin_put(w, f, ntiles, y0 * TX + x0, pos[e], p[e].slot);
+      for (int ty = y0; ty <= y1; ++ty)
+        for (int tx = (ty == y0 ? x0 + 1 : x0); tx <= x1; ++tx) {
+          const int tile = ty * TX + tx;
+          bin_put(w, f, ntiles, tile, atomicAdd(tc + tile, 1u), p[e].slot);
+        }
+    }
   }
 }
 
@@ -969,7 +1007,7 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
     }
     dim3 g1((unsigned)((m + kThreads * kCullPer - 1) / (kThreads * kCullPer)), nframes);
     k_cull<<<g1, kThreads, 0, st>>>(sc, w);
-    int64_t sb = (m / 3 + kThreads - 1) / kThreads;  // ~1/3 of the triangles survive a typical cull
+    int64_t sb = (m / 3 + kThreads * kSetupPer - 1) / (kThreads * kSetupPer);  // ~1/3 survive a typical cull
     dim3 g2((unsigned)(sb < 1 ? 1 : sb), nframes);
     k_setup<<<g2, kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w);
   }
