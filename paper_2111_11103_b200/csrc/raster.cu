@@ -59,13 +59,65 @@ struct __align__(16) RecMeta {
 };
 static_assert(sizeof(RecMeta) == 16, "record meta is 16 bytes");
 
+// What k_setup stores per record: the projected, CCW-ordered vertices and the
+// meta (96 B).  The edge deltas and |area2| are derived exactly again where a
+// record is staged (expand()), which keeps the per-frame record traffic at 3/4
+// of a 128-byte line.
+struct __align__(16) RecStore {
+  RecMeta meta;
+  double xs[3], ys[3], zs[3];
+  uint64_t pad;
+};
+static_assert(sizeof(RecStore) == 96, "stored record is 96 bytes");
+
+// RecMeta from the first two doubles of a RecStore loaded as double2s
+__device__ __forceinline__ RecMeta unpack_meta(double lo, double hi) {
+  const unsigned long long a = (unsigned long long)__double_as_longlong(lo);
+  const unsigned long long b = (unsigned long long)__double_as_longlong(hi);
+  RecMeta m;
+  m.x0 = (int16_t)(a & 0xffffu);
+  m.x1 = (int16_t)((a >> 16) & 0xffffu);
+  m.y0 = (int16_t)((a >> 32) & 0xffffu);
+  m.y1 = (int16_t)(a >> 48);
+  m.off = (int32_t)(b & 0xffffffffu);
+  m.flags = (uint32_t)(b >> 32);
+  return m;
+}
+
+// dX[k] = xs[b] - xs[a], dY[k] = ys[b] - ys[a] (a = k+1, b = k+2 mod 3) exactly as
+// build_record forms them; |area2| from the reordered vertices: the reorder swaps
+// the two products of rasterizer.py:148, and RN(B - A) = -RN(A - B), so the
+// magnitude is bit-identical to the unordered value build_record took fabs of.
+__device__ __forceinline__ void expand_derived(const double xs[3], const double ys[3], double dX[3], double dY[3],
+                                               double &area2) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int a = (k + 1) % 3, b = (k + 2) % 3;
+    dX[k] = __dsub_rn(xs[b], xs[a]);
+    dY[k] = __dsub_rn(ys[b], ys[a]);
+  }
+  area2 = fabs(__dsub_rn(__dmul_rn(__dsub_rn(xs[1], xs[0]), __dsub_rn(ys[2], ys[0])),
+                         __dmul_rn(__dsub_rn(ys[1], ys[0]), __dsub_rn(xs[2], xs[0]))));
+}
+
+__device__ __forceinline__ RecGeom expand(const RecStore &r) {
+  RecGeom g;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    g.xs[k] = r.xs[k];
+    g.ys[k] = r.ys[k];
+    g.zs[k] = r.zs[k];
+  }
+  expand_derived(g.xs, g.ys, g.dX, g.dY, g.area2);
+  return g;
+}
+
 struct Cam {
   double R[9], T[3], fx, fy, cx, cy;
 };
 
 struct Work {
-  RecGeom *geom;
-  RecMeta *meta;
+  RecStore *rec;
   uint8_t *vmask;       // per frame per triangle: bit k = fan sub-triangle k has a record
   uint32_t *cand;       // per frame: triangles surviving the outcode cull (count in fcnt[4f+2])
   uint8_t *vcode;       // per frame per vertex: clip outcode (k_verts)
@@ -89,8 +141,7 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
     off = align256(off + bytes);
     return o;
   };
-  size_t o_geom = take(sizeof(RecGeom) * rs * nframes);
-  size_t o_meta = take(sizeof(RecMeta) * rs * nframes);
+  size_t o_rec = take(sizeof(RecStore) * rs * nframes);
   size_t o_vis = take((size_t)(rs / 2) * nframes);
   size_t o_cand = take(sizeof(uint32_t) * (size_t)(rs / 2) * nframes);
   size_t o_vcode = take((size_t)(nv > 0 ? nv : 1) * nframes);
@@ -101,8 +152,7 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
   if (need_out) *need_out = off;
   if (!ws || ws_bytes < off) return false;
   char *b = static_cast<char *>(ws);
-  w.geom = reinterpret_cast<RecGeom *>(b + o_geom);
-  w.meta = reinterpret_cast<RecMeta *>(b + o_meta);
+  w.rec = reinterpret_cast<RecStore *>(b + o_rec);
   w.vmask = reinterpret_cast<uint8_t *>(b + o_vis);
   w.cand = reinterpret_cast<uint32_t *>(b + o_cand);
   w.vcode = reinterpret_cast<uint8_t *>(b + o_vcode);
@@ -246,12 +296,13 @@ struct Pend {
 
 __device__ __forceinline__ void store_record(const Work &w, int f, int64_t slot, const RecGeom &g,
                                              const RecMeta &mt, Pend &pd) {
-  const int64_t idx = (int64_t)f * w.rs + slot;
-  const double2 *src = reinterpret_cast<const double2 *>(&g);
-  double2 *dst = reinterpret_cast<double2 *>(w.geom + idx);
+  RecStore *dst = w.rec + (int64_t)f * w.rs + slot;
+  dst->meta = mt;
+  double2 *d2 = reinterpret_cast<double2 *>(dst->xs);
+  const double *gd = reinterpret_cast<const double *>(&g);  // xs, ys, zs lead RecGeom
 #pragma unroll
-  for (int q = 0; q < 8; ++q) dst[q] = src[q];
-  w.meta[idx] = mt;
+  for (int q = 0; q < 4; ++q) d2[q] = make_double2(gd[2 * q], gd[2 * q + 1]);
+  dst->zs[2] = g.zs[2];
   pd.slot = (uint32_t)slot;
   pd.tx = (uint32_t)(mt.x0 / kTW) | ((uint32_t)(mt.x1 / kTW) << 16);
   pd.ty = (uint32_t)(mt.y0 / kTH) | ((uint32_t)(mt.y1 / kTH) << 16);
@@ -677,18 +728,31 @@ __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const 
   load_cam(cam, cams, f);
   pcnt[tid] = 0u;
   const uint32_t *src = w.list + ((int64_t)f * ntiles + tile) * w.bincap;
-  const RecGeom *geom = w.geom + (int64_t)f * w.rs;
+  const RecStore *recs = w.rec + (int64_t)f * w.rs;
   uint32_t area = 0;
   if (tid < n) {
-    // one thread per record: 8 x 16 B async copies of its geometry, in flight
-    // while the meta is read; completed before the barrier
+    // one thread per record: its 96 bytes in six 16-byte loads, the derived
+    // fields formed in registers, all 16 fields stored field-major
     const uint32_t key = src[tid];
-    const double *gsrc = reinterpret_cast<const double *>(geom + key);
-    const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(sg + tid);
+    const double2 *r2 = reinterpret_cast<const double2 *>(recs + key);
+    double v[12];
 #pragma unroll
-    for (int q = 0; q < kFields; ++q)  // field q of record tid -> sg[q * kFS + tid]: consecutive lanes, no conflicts
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sdst + 8 * kFS * q), "l"(gsrc + q) : "memory");
-    const RecMeta mt = w.meta[(int64_t)f * w.rs + key];
+    for (int q = 0; q < 6; ++q) {
+      const double2 d = __ldg(r2 + q);
+      v[2 * q] = d.x;
+      v[2 * q + 1] = d.y;
+    }
+    const RecMeta mt = unpack_meta(v[0], v[1]);
+    double dX[3], dY[3], a2;
+    expand_derived(v + 2, v + 5, dX, dY, a2);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) sg[q * kFS + tid] = v[2 + q];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      sg[(kFDX + k) * kFS + tid] = dX[k];
+      sg[(kFDY + k) * kFS + tid] = dY[k];
+    }
+    sg[kFA2 * kFS + tid] = a2;
     skey[tid] = key;
     sflags[tid] = mt.flags;
     stri[tid] = (int32_t)(key >> 1);
@@ -699,7 +763,6 @@ __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const 
     sbox[tid] = (uint32_t)bx0 | ((uint32_t)by0 << 8) | (bw << 16) | (bh << 24);
     area = bw * bh;
   }
-  asm volatile("cp.async.commit_group;" ::: "memory");
   uint32_t incl = area;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -707,7 +770,6 @@ __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const 
     if (lane >= d) incl += v;
   }
   if (lane == 31) wtot[warp] = incl;
-  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   uint32_t wbase = 0, total = 0;
 #pragma unroll
@@ -868,8 +930,7 @@ __global__ void __launch_bounds__(kTP) k_raster_big(tfb_scene sc, const double *
     const uint8_t *vm = w.vmask + (int64_t)f * (w.rs / 2);
     const uint32_t *cl = w.cand + (int64_t)f * (w.rs / 2);  // overflow: every slot of every candidate
     const uint32_t nsrc = ovf ? 2u * w.fcnt[4 * f + 2] : tcount;
-    const RecGeom *geom = w.geom + (int64_t)f * w.rs;
-    const RecMeta *meta = w.meta + (int64_t)f * w.rs;
+    const RecStore *recs = w.rec + (int64_t)f * w.rs;
 
     Fold fd;
     fd.init();
@@ -888,11 +949,8 @@ __global__ void __launch_bounds__(kTP) k_raster_big(tfb_scene sc, const double *
           const uint32_t r = ovf ? 2u * cl[i >> 1] + (i & 1u) : list[i];
           skey[threadIdx.x] = r;
           if (!ovf || ((vm[r >> 1] >> (r & 1u)) & 1u)) {
-            smeta[threadIdx.x] = meta[r];
-            const double2 *gs = reinterpret_cast<const double2 *>(geom + r);
-            double2 *gd = reinterpret_cast<double2 *>(sgeom + threadIdx.x);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) gd[q] = gs[q];
+            smeta[threadIdx.x] = recs[r].meta;
+            sgeom[threadIdx.x] = expand(recs[r]);
           } else {
             RecMeta empty;
             empty.x0 = 1;
@@ -940,7 +998,8 @@ __global__ void __launch_bounds__(kTP) k_raster_big(tfb_scene sc, const double *
       const uint32_t nf = min(ncand, (uint32_t)kCand);
       for (uint32_t i = 0; i < nf; ++i) {
         const uint32_t key = ck[i];
-        fd.step(AosRec{geom + key}, meta[key].flags, px, py, (int32_t)key);
+        const RecGeom gk = expand(recs[key]);
+        fd.step(AosRec{&gk}, recs[key].meta.flags, px, py, (int32_t)key);
       }
       const bool more = need && ncand > (uint32_t)kCand;
       if (more) lo = ck[kCand - 1] + 1;
@@ -948,9 +1007,9 @@ __global__ void __launch_bounds__(kTP) k_raster_big(tfb_scene sc, const double *
       if (!__syncthreads_or(more)) break;
     }
     if (in_img) {
-      const uint32_t flags = fd.win >= 0 ? meta[fd.win].flags : 0u;
+      const uint32_t flags = fd.win >= 0 ? recs[fd.win].meta.flags : 0u;
       const int32_t t = fd.win >= 0 ? (int32_t)((uint32_t)fd.win >> 1) : -1;
-      write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, fd.win >= 0 ? meta[fd.win].off : 0);
+      write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, fd.win >= 0 ? recs[fd.win].meta.off : 0);
     }
   }
 }
