@@ -456,11 +456,22 @@ __global__ void __launch_bounds__(kThreads, 4) k_setup(tfb_scene sc, const doubl
     Pend p[2 * kSetupPer];
     one(c0, p[0], p[1]);
     one(c0 + kThreads, p[2], p[3]);
-    // first-tile appends of all pending records in flight together, then the rest
+    // first-tile appends of all pending records in flight together (one atomic per
+    // distinct tile per warp: neighbouring candidates mostly share a tile), then the rest
+    const unsigned act = __activemask();
+    const int lane = threadIdx.x & 31;
     uint32_t pos[2 * kSetupPer];
+    unsigned peers[2 * kSetupPer];
+#pragma unroll
+    for (int e = 0; e < 2 * kSetupPer; ++e) {
+      const int tile = p[e].valid ? (int)(p[e].ty & 0xffffu) * TX + (int)(p[e].tx & 0xffffu) : -1 - lane;
+      peers[e] = __match_any_sync(act, tile);
+      pos[e] = 0u;
+      if (p[e].valid && lane == __ffs(peers[e]) - 1) pos[e] = atomicAdd(tc + tile, (uint32_t)__popc(peers[e]));
+    }
 #pragma unroll
     for (int e = 0; e < 2 * kSetupPer; ++e)
-      if (p[e].valid) pos[e] = atomicAdd(tc + (int)(p[e].ty & 0xffffu) * TX + (int)(p[e].tx & 0xffffu), 1u);
+      pos[e] = __shfl_sync(act, pos[e], __ffs(peers[e]) - 1) + __popc(peers[e] & ((1u << lane) - 1u));
 #pragma unroll
     for (int e = 0; e < 2 * kSetupPer; ++e) {
       if (!p[e].valid) continue;
