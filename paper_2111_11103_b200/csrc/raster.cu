@@ -575,6 +575,30 @@ struct Fold {
       w2 = c;
     }
   }
+  // A pixel's first (here: only) covering record when no depth plane is wanted.
+  // Against depth = +inf the test `z > 0 && z < inf - 1e-9` only asks for a
+  // finite positive z = area2 / (a + b + c); with a + b + c > area2 * 1e-300 the
+  // quotient is below 1e300, so the division is skipped.  Otherwise the exact step.
+  template <typename R>
+  __device__ __forceinline__ void first_e(const R &g, const double e[3], int32_t id) {
+    const double z0 = g.f(kFZs), z1 = g.f(kFZs + 1), z2 = g.f(kFZs + 2), a2 = g.f(kFA2);
+    bool ok = true;
+    double a = ddiv_try(e[0], z0, ok), b = ddiv_try(e[1], z1, ok), c = ddiv_try(e[2], z2, ok);
+    if (!ok) {
+      a = __ddiv_rn(e[0], z0);
+      b = __ddiv_rn(e[1], z1);
+      c = __ddiv_rn(e[2], z2);
+    }
+    const double sum = __dadd_rn(__dadd_rn(a, b), c);
+    if (sum > a2 * 1e-300) {
+      win = id;
+      w0 = a;
+      w1 = b;
+      w2 = c;
+    } else {
+      step_e(g, e, id);
+    }
+  }
 };
 
 // Winner epilogue, rasterizer.py:177-202: perspective-correct barycentrics of
@@ -875,7 +899,8 @@ __global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const 
   if (cnt == 1u) {
     const int j = pc[0][tid];
     const double e[3] = {pe[0][tid], pe[1][tid], pe[2][tid]};
-    fd.step_e(SoaRec{sg, j}, e, j);
+    if (o.depth) fd.step_e(SoaRec{sg, j}, e, j);
+    else fd.first_e(SoaRec{sg, j}, e, j);
   } else if (cnt == 2u) {  // both slots known: fold in ascending key order
     int j0 = pc[0][tid], j1 = pc[1][tid];
     if (skey[j1] < skey[j0]) {
