@@ -42,6 +42,9 @@ namespace {
 constexpr int kTW = TFB_TW, kTH = TFB_TH;  // raster tile (pixels); one k_raster thread per pixel
 constexpr int kTP = kTW * kTH;             // k_raster threads = tile pixels = staged records per tile
 constexpr int kThreads = 256;              // setup-side kernels
+#ifndef TFB_RASTER_MINB
+#define TFB_RASTER_MINB (1024 / kTP)  // k_raster CTAs per SM the register budget must allow
+#endif
 static_assert(kTW % 8 == 0 && kTH % 4 == 0 && kTP >= 64 && kTP <= 256, "tile shape: 8x4-pixel warp blocks");
 constexpr int kCand = 8;
 constexpr uint32_t kNoKey = 0xffffffffu;
@@ -738,7 +741,7 @@ struct TileSmem {
 //     smallest covering key above the last folded one — the reference's
 //     ascending sequential fold (rasterizer.py:108, 170-171) without sorting.
 //  Larger or overflowed tiles are handed to k_raster_big.
-__global__ void __launch_bounds__(kTP, 1024 / kTP) k_raster(tfb_scene sc, const double *__restrict__ cams, int W, int H,
+__global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, const double *__restrict__ cams, int W, int H,
                                                         int TX, int ntiles, Work w, Outs o) {
   const int f = blockIdx.z;
   const int tile = blockIdx.y * TX + blockIdx.x;
