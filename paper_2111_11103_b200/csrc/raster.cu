@@ -1,24 +1,26 @@
 // Tile-binned z-buffer rasterizer, bit-exact with rasterizer.py:93-202.
 //
 // Per batch of frames (one launch per stage, all frames at once):
-//   k_setup  one thread per (frame, triangle): FMA-ordered world→camera
-//            transform (geometry.py:161), near-plane clip + fan
-//            (rasterizer.py:62-82, 113-122), projection, bbox, signed area,
-//            CCW reorder and edge setup (rasterizer.py:136-164).  Surviving
-//            (sub)triangles become 128-byte records at slot 2t+sub and are
-//            appended to the fixed-capacity bins of the tiles their bbox
-//            overlaps (one returning atomic per tile; unordered).
-//   k_raster one CTA per 16x16 tile, one thread per pixel.  Each pixel keeps
-//            the K smallest (triangle, sub) keys of the records that cover it
-//            (edge test in float64, ownership rule rasterizer.py:85-90), then
-//            folds them in ascending key order with the reference's exact
-//            test `z > 0 && z < depth - 1e-9` (rasterizer.py:171).  Pixels
-//            covered by more than K records run further passes over keys
-//            above the last folded one, so the fold always equals the
-//            reference's sequential ascending-index loop — including the
+//   k_verts  per (frame, vertex): camera transform, clip outcode.
+//   k_cull   per (frame, triangle): outcode cull (rasterizer.py:111 and empty
+//            bboxes), survivors compacted.
+//   k_setup  per survivor: FMA-ordered world->camera transform (geometry.py:161,
+//            SURVEY A1), near-plane clip + fan (rasterizer.py:62-82, 113-122),
+//            projection, bbox, signed area, CCW reorder and edge ownership
+//            (rasterizer.py:136-164).  Each (sub)triangle becomes a 96-byte
+//            record at slot 2t+sub and is appended to the fixed-capacity bin
+//            of every tile its bbox overlaps (unordered).
+//   k_raster one CTA per 16x8 tile, one thread per pixel.  Records staged
+//            field-major; pair-parallel float64 edge tests (ownership rule
+//            rasterizer.py:85-90); each pixel folds its covering records in
+//            ascending (triangle, sub) key order with the reference's exact
+//            test `z > 0 && z < depth - 1e-9` (rasterizer.py:171) — the
+//            reference's sequential ascending-index loop, including the
 //            non-transitive tie chains a packed atomicMin cannot reproduce.
 //            The winner's perspective-correct barycentrics, (u, v) and texel
 //            id (rasterizer.py:177-196) are evaluated once, in the epilogue.
+//   k_raster_big  tiles with more records than a CTA stages, or an
+//            overflowed bin: multipass K-smallest fold, same semantics.
 //
 // Exactness: every float64 operation of the reference expression is issued
 // as an explicit round-to-nearest intrinsic in the reference's order and this
