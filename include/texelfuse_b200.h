@@ -147,6 +147,27 @@ int tfb_worst_case_areas(const tfb_scene *scene, const double *cams, const int32
 /* probs.argmax(axis=2) (cli.py:293): first maximum, NaN-first like NumPy. */
 int tfb_probs_argmax(const float *probs, int64_t npix, int num_classes, int32_t *out, void *stream);
 
+/* SMPB load validation (formats.py:77-93).  out4: 4 doubles of device memory;
+ * on completion out4[0] = minimum over all values (NaN if any value is NaN,
+ * like np.min) and out4[1] = max over pixels of |sum_k p - 1| with each
+ * pixel's sum in float64 in NumPy's pairwise order (NaN if any sum is NaN). */
+int tfb_probs_check(const float *probs, int64_t npix, int num_classes, double *out4, void *stream);
+
+/* pixel_accuracy (renderback.py:152-172) for npix label pixels: reference
+ * pixels outside [0, c) or flagged in `ignore` (c bytes, may be NULL) are
+ * skipped; predictions outside [0, c) count as unknown.  Accumulates (+=)
+ * into confusion (c*c u64, row = reference), unknown (c u64) and
+ * valid_count (1 u64); the caller zeroes them. */
+int tfb_confusion(const int32_t *pred, const int32_t *ref, int64_t npix, int num_classes, const uint8_t *ignore,
+                  unsigned long long *confusion, unsigned long long *unknown, unsigned long long *valid_count,
+                  void *stream);
+
+/* export_colored_mesh vote (renderback.py:275-294): per triangle the class
+ * with the most texels (first maximum wins), -1 when none of its texels has
+ * a label in [0, c). */
+int tfb_face_majority(const int32_t *texel_labels, const int32_t *steps, const int64_t *offsets,
+                      int64_t num_triangles, int num_classes, int32_t *face_class, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

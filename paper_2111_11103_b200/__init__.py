@@ -38,6 +38,13 @@ from .geometry import (
     texel_id,
     uniform_layout,
 )
+from .formats import (
+    read_probability_header,
+    read_probability_image,
+    read_texture,
+    write_probability_image,
+    write_texture,
+)
 from .meshio import load_mesh, load_trajectory, save_ply, save_trajectory
 from .rasterizer import IdImage, pixel_world_points, project_point, rasterize
 from .renderback import render_labels

@@ -48,6 +48,9 @@ _SIGNATURES = {
     "tfb_render": ([_P, _I64, _I, _P, _I64, _P, _P, _P], _I),
     "tfb_probs_argmax": ([_P, _I64, _I, _P, _P], _I),
     "tfb_worst_case_areas": ([_P, _P, _P, _I, _P, _P], _I),
+    "tfb_probs_check": ([_P, _I64, _I, _P, _P], _I),
+    "tfb_confusion": ([_P, _P, _I64, _I, _P, _P, _P, _P, _P], _I),
+    "tfb_face_majority": ([_P, _P, _P, _I64, _I, _P, _P], _I),
 }
 
 EXPORTED = tuple(_SIGNATURES)
