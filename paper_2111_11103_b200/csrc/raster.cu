@@ -749,6 +749,10 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
   const int tile = blockIdx.y * TX + blockIdx.x;
   const int tx0 = blockIdx.x * kTW, ty0 = blockIdx.y * kTH;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // the bin entry this thread would stage is read speculatively, in flight together
+  // with the tile's count (entries past the count are stale and ignored)
+  const uint32_t *src = w.list + ((int64_t)f * ntiles + tile) * w.bincap;
+  const uint32_t key_spec = (int64_t)tid < w.bincap ? src[tid] : 0u;
   const uint32_t n = w.tile_count[(int64_t)f * ntiles + tile];
   if (n > (uint64_t)w.bincap || n > (uint32_t)kTP) {
     if (tid == 0) w.big[atomicAdd(w.fcnt + 1, 1u)] = (uint32_t)(f * ntiles + tile);
@@ -767,13 +771,12 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
   Cam &cam = S.cam;
   load_cam(cam, cams, f);
   pcnt[tid] = 0u;
-  const uint32_t *src = w.list + ((int64_t)f * ntiles + tile) * w.bincap;
   const RecStore *recs = w.rec + (int64_t)f * w.rs;
   uint32_t area = 0;
   if (tid < n) {
     // one thread per record: its 96 bytes in six 16-byte loads, the derived
     // fields formed in registers, all 16 fields stored field-major
-    const uint32_t key = src[tid];
+    const uint32_t key = key_spec;
     const double2 *r2 = reinterpret_cast<const double2 *>(recs + key);
     double v[12];
 #pragma unroll
