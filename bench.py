@@ -242,12 +242,12 @@ def run_ours(args):
     raster_ms = sum(r0.elapsed_time(r1) for _, r0, r1, _, _ in prof)
     fuse_ms = sum(f0.elapsed_time(f1) for _, _, _, f0, f1 in prof)
     fuse_frames = sum(p_[0] for p_ in prof)
-    # k_fuse launches: tfb_fuse carries at most 32 frames per launch
-    n_launch_fuse = sum((p_[0] + 31) // 32 for p_ in prof)
+    # k_fuse launches: tfb_fuse carries at most 256 frames per launch
+    n_launch_fuse = sum((p_[0] + 255) // 256 for p_ in prof)
     # our kernels per timed step: per batch k_verts, k_cull, k_setup, k_scan, k_fill, k_raster,
     # k_raster_big + the k_fuse launches (hit-count reset is a dense torch memset here), + k_finalize
     batches = [min(args.batch, args.frames - b0) for b0 in range(0, args.frames, args.batch)]
-    gpu_launches = args.steps * (sum(7 + (b + 31) // 32 for b in batches) + 1)
+    gpu_launches = args.steps * (sum(7 + (b + 255) // 256 for b in batches) + 1)
     peak, peak_kind = _peaks()
     achieved = B_FRAME * fuse_frames / (fuse_ms / 1000.0) / 1e9
     traffic = None

@@ -41,7 +41,7 @@ namespace {
 #endif
 constexpr int kWarps = TFB_FUSE_WARPS;  // warps per CTA (independent pipelines)
 constexpr int kChunk = 32;       // pixels per work item = one per lane
-constexpr int kMaxFrames = 32;   // frames per launch (pointers travel in the kernel parameters)
+constexpr int kMaxFrames = 256;  // frames per launch (pointers travel in the kernel parameters, 2 KB)
 
 struct FuseParams {
   const float *probs[kMaxFrames];
@@ -910,8 +910,11 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
   TFB_REQUIRE(accum_is_f64 || (accum_stride % 4 == 0 && ((uintptr_t)accum & 15) == 0), TFB_ERR_DATA,
               "tfb_fuse: float32 accumulator rows must be 16-byte aligned (stride multiple of 4)");
   if (nframes <= 0 || hw <= 0) return TFB_OK;
-  TFB_REQUIRE(hw * kMaxFrames < (1LL << 31), TFB_ERR_CAPACITY, "tfb_fuse: %lld pixels per frame is too many",
+  TFB_REQUIRE(hw + kChunk < (1LL << 31), TFB_ERR_CAPACITY, "tfb_fuse: %lld pixels per frame is too many",
               (long long)hw);
+  // frames per launch: the kernel indexes a launch's pixels with 32-bit frame * hw + pixel
+  int fpl = (int)(((1LL << 31) - 1) / (hw + kChunk));
+  if (fpl > kMaxFrames) fpl = kMaxFrames;
   TFB_REQUIRE(total_texels * accum_stride < (1LL << 31), TFB_ERR_CAPACITY,
               "tfb_fuse: accumulator of %lld x %lld elements exceeds 32-bit row offsets", (long long)total_texels,
               (long long)accum_stride);
@@ -935,8 +938,8 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
   p.NS = NS;
   p.cpf = (hw + kChunk - 1) / kChunk;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  for (int f0 = 0; f0 < nframes; f0 += kMaxFrames) {
-    const int nf = nframes - f0 < kMaxFrames ? nframes - f0 : kMaxFrames;
+  for (int f0 = 0; f0 < nframes; f0 += fpl) {
+    const int nf = nframes - f0 < fpl ? nframes - f0 : fpl;
     for (int i = 0; i < kMaxFrames; ++i) p.probs[i] = i < nf ? probs[f0 + i] : nullptr;
     for (int i = 0; i < nf; ++i)
       TFB_REQUIRE(p.probs[i], TFB_ERR_DATA, "tfb_fuse: null probability pointer for frame %d", f0 + i);

@@ -122,9 +122,9 @@ def test_fuse_kernels_vs_oracle(fast, c, agg):
 
 
 def test_fuse_fast_many_frames_and_launch_split():
-    """More frames than one launch carries (32): the frame loop and pointer table."""
+    """More frames than one launch carries (256): the frame loop and pointer table."""
     rng = np.random.default_rng(5)
-    nframes, hw, n_x, c = 37, 32 * 20 + 5, 64, 8
+    nframes, hw, n_x, c = 261, 32 * 20 + 5, 64, 8
     rows = _rows(rng, nframes, hw, n_x)
     probs = _probs(rng, nframes, hw, c, special=False)
     got, cnt, _ = _run(rows, probs, n_x, "mul", "images_iid", 0.0, True)
