@@ -64,7 +64,7 @@ def _config(args, n):
             "frames_per_gpu": args.frames, "triangles": 299568, "texels": 299568, "classes": C,
             "aggregator": AGG, "weights": WMODE, "accum": "float32", "batch": args.batch, "overlap": bool(args.overlap),
             "parallelism": "frame-sharded dp%d" % n,
-            "l2": "inputs larger than L2: 8-map pool per GPU (393 MB), accumulator 47.9 MB L2-resident"}
+            "l2": "inputs larger than L2: 8-map pool per GPU (393 MB) cycled, accumulator 47.9 MB"}
 
 
 class ClockSampler:
