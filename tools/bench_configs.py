@@ -1,0 +1,78 @@
+"""Secondary measurements of the other BASELINE/SURVEY §8(d) configurations
+(not bench lines: bench.py's headline is cfg2).  One fusion job per config,
+timed with CUDA events after a warm-up job; prints one JSON line per config.
+
+    python tools/bench_configs.py [cfg1 cfg2sum cfg4 cfg5]
+"""
+
+import json
+import os
+import sys
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2111_11103_b200 import Mesh, MeshAnnotation, uniform_layout  # noqa: E402
+from paper_2111_11103_b200.geometry import Intrinsics  # noqa: E402
+from paper_2111_11103_b200.synth import make_room, random_room_trajectory, softmax_maps  # noqa: E402
+
+CONFIGS = {
+    # name: (tess, width, height, fx, classes, frames, aggregator, layout steps, batch, pool)
+    "cfg1": (32, 160, 120, 160.0, 13, 20, "sum", 1, 20, 4),
+    "cfg2sum": (158, 640, 480, 577.87, 40, 2000, "sum", 1, 256, 8),
+    "cfg4": (158, 640, 480, 577.87, 40, 2000, "mul", 8, 256, 8),
+    "cfg5": (646, 1920, 1080, 1728.0, 19, 500, "mul", 1, 32, 4),  # one GPU's share of the 8-GPU job
+}
+
+
+def run(name):
+    tess, W, H, fx, c, frames, agg, steps, batch, pool = CONFIGS[name]
+    t0 = time.time()
+    v, t = make_room((6.0, 5.0, 3.0), tess)
+    mesh = Mesh.from_arrays(v, t)
+    layout = uniform_layout(mesh, steps)
+    intr = Intrinsics(fx=fx, fy=fx, cx=(W - 1) / 2.0, cy=(H - 1) / 2.0, width=W, height=H)
+    cams = random_room_trajectory(frames, intr, seed=0)
+    maps = softmax_maps(pool, H, W, c, seed=0, device="cuda")
+    probs = [maps[i % pool] for i in range(frames)]
+    ann = MeshAnnotation(mesh, layout, num_classes=c, aggregator=agg, weight_mode="images_iid",
+                         accum_dtype="float32", max_batch=batch)
+    cams_dev = ann.scene.cams_tensor(cams)
+    setup_s = time.time() - t0
+
+    def job():
+        ann.reset()
+        ann.add_batch(probs, cams_dev, width=W, height=H)
+        ann.labels()
+
+    job()
+    torch.cuda.synchronize()
+    ann.profile = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    job()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    prof, ann.profile = ann.profile, None
+    raster = sum(r0.elapsed_time(r1) for _, r0, r1, _, _ in prof)
+    fuse = sum(f0.elapsed_time(f1) for _, _, _, f0, f1 in prof)
+    b_frame = H * W * (4 * c + 8)
+    print(json.dumps({
+        "config": name, "triangles": mesh.num_triangles, "texels": layout.total_texels, "size": [W, H],
+        "classes": c, "aggregator": agg, "frames": frames, "batch": batch,
+        "frames_per_s": frames / (ms / 1000.0), "ms_per_job": ms,
+        "raster_us_per_frame": 1000.0 * raster / frames, "fuse_us_per_frame": 1000.0 * fuse / frames,
+        "fuse_gbs": b_frame * frames / (fuse / 1000.0) / 1e9, "setup_s": round(setup_s, 1),
+        "fuse_kernel": "k_fuse_fast" if c % 4 == 0 else "k_fuse (general)",
+    }), flush=True)
+    del ann, maps, probs
+    torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    for name in (sys.argv[1:] or list(CONFIGS)):
+        run(name)
