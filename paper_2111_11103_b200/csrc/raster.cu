@@ -71,7 +71,8 @@ static_assert(sizeof(RecMeta) == 16, "record meta is 16 bytes");
 struct __align__(16) RecStore {
   RecMeta meta;
   double xs[3], ys[3], zs[3];
-  uint64_t pad;
+  uint32_t key;  // 2t + sub: the reference's (triangle, fan) order; kNoKey for an unused slot
+  uint32_t pad;
 };
 static_assert(sizeof(RecStore) == 96, "stored record is 96 bytes");
 
@@ -123,7 +124,6 @@ struct Cam {
 
 struct Work {
   RecStore *rec;
-  uint8_t *vmask;       // per frame per triangle: bit k = fan sub-triangle k has a record
   uint32_t *cand;       // per frame: triangles surviving the outcode cull (count in fcnt[4f+2])
   uint8_t *vcode;       // per frame per vertex: clip outcode (k_verts)
   int64_t nv;
@@ -147,7 +147,6 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
     return o;
   };
   size_t o_rec = take(sizeof(RecStore) * rs * nframes);
-  size_t o_vis = take((size_t)(rs / 2) * nframes);
   size_t o_cand = take(sizeof(uint32_t) * (size_t)(rs / 2) * nframes);
   size_t o_vcode = take((size_t)(nv > 0 ? nv : 1) * nframes);
   size_t o_fcnt = take(sizeof(uint32_t) * 4 * nframes);
@@ -158,7 +157,6 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
   if (!ws || ws_bytes < off) return false;
   char *b = static_cast<char *>(ws);
   w.rec = reinterpret_cast<RecStore *>(b + o_rec);
-  w.vmask = reinterpret_cast<uint8_t *>(b + o_vis);
   w.cand = reinterpret_cast<uint32_t *>(b + o_cand);
   w.vcode = reinterpret_cast<uint8_t *>(b + o_vcode);
   w.nv = nv > 0 ? nv : 1;
@@ -294,24 +292,40 @@ __device__ bool build_record(const Cam &cam, int W, int H, const double P[3][3],
 // batches the appends of several records so their returning atomics are in
 // flight together instead of one dependent round trip per record.
 struct Pend {
-  uint32_t slot;
+  uint32_t slot;  // record index (records of a frame are allocated densely)
   uint32_t tx, ty;  // first tile (x | last x << 16), (y | last y << 16)
   bool valid;
 };
 
-__device__ __forceinline__ void store_record(const Work &w, int f, int64_t slot, const RecGeom &g,
+__device__ __forceinline__ void store_record(const Work &w, int f, uint32_t slot, uint32_t key, const RecGeom &g,
                                              const RecMeta &mt, Pend &pd) {
   RecStore *dst = w.rec + (int64_t)f * w.rs + slot;
   dst->meta = mt;
+  dst->key = key;
   double2 *d2 = reinterpret_cast<double2 *>(dst->xs);
   const double *gd = reinterpret_cast<const double *>(&g);  // xs, ys, zs lead RecGeom
 #pragma unroll
   for (int q = 0; q < 4; ++q) d2[q] = make_double2(gd[2 * q], gd[2 * q + 1]);
   dst->zs[2] = g.zs[2];
-  pd.slot = (uint32_t)slot;
+  pd.slot = slot;
   pd.tx = (uint32_t)(mt.x0 / kTW) | ((uint32_t)(mt.x1 / kTW) << 16);
   pd.ty = (uint32_t)(mt.y0 / kTH) | ((uint32_t)(mt.y1 / kTH) << 16);
   pd.valid = true;
+}
+
+// an allocated slot whose (sub)triangle produced no record (empty bbox, zero
+// area, or the second fan slot of a 3-vertex clip): empty bbox, never binned
+__device__ __forceinline__ void store_hole(const Work &w, int f, uint32_t slot) {
+  RecStore *dst = w.rec + (int64_t)f * w.rs + slot;
+  RecMeta e;
+  e.x0 = 1;
+  e.x1 = 0;
+  e.y0 = 1;
+  e.y1 = 0;
+  e.off = 0;
+  e.flags = 0;
+  dst->meta = e;
+  dst->key = kNoKey;
 }
 
 __device__ __forceinline__ void bin_put(const Work &w, int f, int ntiles, int tile, uint32_t pos, uint32_t slot) {
@@ -352,7 +366,7 @@ __global__ void __launch_bounds__(kThreads) k_verts(tfb_scene sc, const double *
 // Per (frame, triangle), light and fully occupied: the AND of the three
 // vertex outcodes decides whether the triangle can produce a record at all;
 // survivors are appended (one global atomic per block) to the frame's
-// candidate list; every triangle's visibility mask is reset.
+// candidate list.
 constexpr int kCullPer = 4;  // triangles per k_cull thread (independent loads in flight)
 
 __global__ void __launch_bounds__(kThreads) k_cull(tfb_scene sc, Work w) {
@@ -412,59 +426,87 @@ __global__ void __launch_bounds__(kThreads, 4) k_setup(tfb_scene sc, const doubl
   __syncthreads();
   const uint32_t ncand = w.fcnt[4 * f + 2];
   const uint32_t *cl = w.cand + (int64_t)f * (w.rs / 2);
-  auto one = [&](uint32_t ci, Pend &p0, Pend &p1) {
-    p0.valid = p1.valid = false;
+  // candidate prologue: triangle, vertex ids, outcodes -> 1 record slot if no vertex is
+  // behind the near plane, else 2 (the fan of rasterizer.py:119-122 has at most two)
+  struct Cand {
+    int64_t t, i0, i1, i2;
+    uint32_t nslot;
+    bool unclipped;
+  };
+  auto head = [&](uint32_t ci, Cand &c) {
+    c.nslot = 0;
     if (ci >= ncand) return;
-    const int64_t t = cl[ci];
-    const int64_t i0 = __ldg(sc.triangles + 3 * t), i1 = __ldg(sc.triangles + 3 * t + 1),
-                  i2 = __ldg(sc.triangles + 3 * t + 2);
+    c.t = cl[ci];
+    c.i0 = __ldg(sc.triangles + 3 * c.t);
+    c.i1 = __ldg(sc.triangles + 3 * c.t + 1);
+    c.i2 = __ldg(sc.triangles + 3 * c.t + 2);
     const uint8_t *vc = w.vcode + (int64_t)f * w.nv;
-    const bool unclipped = ((vc[i0] | vc[i1] | vc[i2]) & 1u) == 0u;  // zmin >= NEAR_PLANE
+    c.unclipped = ((vc[c.i0] | vc[c.i1] | vc[c.i2]) & 1u) == 0u;  // zmin >= NEAR_PLANE
+    c.nslot = c.unclipped ? 1u : 2u;
+  };
+  auto one = [&](const Cand &c, uint32_t slot, Pend &p0, Pend &p1) {
+    p0.valid = p1.valid = false;
+    if (!c.nslot) return;
+    const int64_t t = c.t;
     // camera-space vertices recomputed here (bit-identical to k_verts' transform): the
     // vertex array is L2-resident across frames, a per-frame camera-space copy is not
     double P[3][3];
-    xform(cam, sc.vertices + 3 * i0, P[0]);
-    xform(cam, sc.vertices + 3 * i1, P[1]);
-    xform(cam, sc.vertices + 3 * i2, P[2]);
-    uint32_t mask = 0;
+    xform(cam, sc.vertices + 3 * c.i0, P[0]);
+    xform(cam, sc.vertices + 3 * c.i1, P[1]);
+    xform(cam, sc.vertices + 3 * c.i2, P[2]);
     RecGeom g;
     RecMeta mt;
     const uint32_t tflags = ((uint32_t)__ldg(sc.origins + t) << 5) | ((uint32_t)__ldg(sc.steps + t) << 16);
     const int32_t toff = (int32_t)__ldg(sc.offsets + t);
-    if (unclipped) {
-      if (build_record(cam, W, H, P, toff, false, 0, tflags, g, mt)) {
-        store_record(w, f, 2 * t, g, mt, p0);
-        mask = 1;
-      }
+    if (c.unclipped) {
+      if (build_record(cam, W, H, P, toff, false, 0, tflags, g, mt)) store_record(w, f, slot, (uint32_t)(2 * t), g, mt, p0);
+      else store_hole(w, f, slot);
     } else {
       double op[4][3], ob[4][3];
       const int n = clip_near(P, op, ob);
-      for (int k = 1; k + 1 < n; ++k) {  // fan (0, k, k+1), rasterizer.py:119-122
-        double S[3][3];
+      for (int k = 1; k <= 2; ++k) {  // fan (0, k, k+1), rasterizer.py:119-122
+        bool ok = false;
+        if (k + 1 < n) {
+          double S[3][3];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          S[0][q] = op[0][q];
-          S[1][q] = op[k][q];
-          S[2][q] = op[k + 1][q];
+          for (int q = 0; q < 3; ++q) {
+            S[0][q] = op[0][q];
+            S[1][q] = op[k][q];
+            S[2][q] = op[k + 1][q];
+          }
+          ok = build_record(cam, W, H, S, toff, true, k - 1, tflags, g, mt);
         }
-        if (build_record(cam, W, H, S, toff, true, k - 1, tflags, g, mt)) {
-          store_record(w, f, 2 * t + (k - 1), g, mt, k == 1 ? p0 : p1);
-          mask |= 1u << (k - 1);
-        }
+        if (ok) store_record(w, f, slot + (k - 1), (uint32_t)(2 * t + (k - 1)), g, mt, k == 1 ? p0 : p1);
+        else store_hole(w, f, slot + (k - 1));
       }
     }
-    w.vmask[(int64_t)f * (w.rs / 2) + t] = (uint8_t)mask;  // every candidate, 0 included
   };
   uint32_t *tc = w.tile_count + (int64_t)f * ntiles;
   const uint32_t stride = gridDim.x * kThreads * kSetupPer;
   for (uint32_t c0 = blockIdx.x * kThreads * kSetupPer + threadIdx.x; c0 < ncand; c0 += stride) {
-    Pend p[2 * kSetupPer];
-    one(c0, p[0], p[1]);
-    one(c0 + kThreads, p[2], p[3]);
-    // first-tile appends of all pending records in flight together (one atomic per
-    // distinct tile per warp: neighbouring candidates mostly share a tile), then the rest
     const unsigned act = __activemask();
     const int lane = threadIdx.x & 31;
+    Cand cd[kSetupPer];
+    head(c0, cd[0]);
+    head(c0 + kThreads, cd[1]);
+    // dense record slots: one atomic per warp; its result is needed only by the stores
+    const uint32_t mine = cd[0].nslot + cd[1].nslot;
+    uint32_t incl = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(act, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const int last = 31 - __clz(act);
+    const uint32_t wtotal = __shfl_sync(act, incl, last);
+    uint32_t base = 0u;
+    if (lane == __ffs(act) - 1 && wtotal) base = atomicAdd(w.fcnt + 4 * f + 3, wtotal);
+    base = __shfl_sync(act, base, __ffs(act) - 1) + incl - mine;
+    Pend p[2 * kSetupPer];
+    one(cd[0], base, p[0], p[1]);
+    one(cd[1], base + cd[0].nslot, p[2], p[3]);
+    // first-tile appends of all pending records in flight together (one atomic per
+    // distinct tile per warp: neighbouring candidates mostly share a tile), then the rest
     uint32_t pos[2 * kSetupPer];
     unsigned peers[2 * kSetupPer];
 #pragma unroll
@@ -776,8 +818,7 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
   if (tid < n) {
     // one thread per record: its 96 bytes in six 16-byte loads, the derived
     // fields formed in registers, all 16 fields stored field-major
-    const uint32_t key = key_spec;
-    const double2 *r2 = reinterpret_cast<const double2 *>(recs + key);
+    const double2 *r2 = reinterpret_cast<const double2 *>(recs + key_spec);  // bin entry = record index
     double v[12];
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
@@ -786,6 +827,7 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
       v[2 * q + 1] = d.y;
     }
     const RecMeta mt = unpack_meta(v[0], v[1]);
+    const uint32_t key = (uint32_t)(unsigned long long)__double_as_longlong(v[11]);  // RecStore::key
     double dX[3], dY[3], a2;
     expand_derived(v + 2, v + 5, dX, dY, a2);
 #pragma unroll
@@ -944,17 +986,18 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
   write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, off);
 }
 
-// Tiles with more than kTP records, or whose bin overflowed (then both
-// record slots of every cull survivor of the frame are scanned, empty slots
-// masked out by vmask).  Records stream through shared memory in chunks in
-// arbitrary order; each pixel keeps the kCand smallest covering keys above
-// `lo`, folds them in ascending order and repeats with `lo` past the last
-// folded key until no covering record is left — the same sequential fold.
+// Tiles with more than kTP records, or whose bin overflowed (then every
+// allocated record slot of the frame is scanned; unused slots carry an empty
+// bbox).  Records stream through shared memory in chunks in arbitrary order;
+// each pixel keeps the kCand smallest covering keys above `lo`, folds them in
+// ascending order and repeats with `lo` past the last folded key until no
+// covering record is left — the same sequential fold.
 __global__ void __launch_bounds__(kTP) k_raster_big(tfb_scene sc, const double *__restrict__ cams, int W,
                                                             int H, int TX, int ntiles, Work w, Outs o) {
   __shared__ RecGeom sgeom[kTP];
   __shared__ RecMeta smeta[kTP];
   __shared__ uint32_t skey[kTP];
+  __shared__ uint32_t sidx[kTP];
   __shared__ Cam cam;
   const uint32_t nbig = w.fcnt[1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -971,9 +1014,7 @@ __global__ void __launch_bounds__(kTP) k_raster_big(tfb_scene sc, const double *
     const uint32_t tcount = w.tile_count[(int64_t)f * ntiles + tile];
     const bool ovf = tcount > (uint64_t)w.bincap;
     const uint32_t *list = w.list + ((int64_t)f * ntiles + tile) * w.bincap;
-    const uint8_t *vm = w.vmask + (int64_t)f * (w.rs / 2);
-    const uint32_t *cl = w.cand + (int64_t)f * (w.rs / 2);  // overflow: every slot of every candidate
-    const uint32_t nsrc = ovf ? 2u * w.fcnt[4 * f + 2] : tcount;
+    const uint32_t nsrc = ovf ? w.fcnt[4 * f + 3] : tcount;  // overflow: every allocated record slot
     const RecStore *recs = w.rec + (int64_t)f * w.rs;
 
     Fold fd;
@@ -981,30 +1022,20 @@ __global__ void __launch_bounds__(kTP) k_raster_big(tfb_scene sc, const double *
     uint32_t lo = 0;     // next key to consider
     bool need = in_img;  // this pixel still has unfolded candidates
     for (;;) {
-      uint32_t ck[kCand];
+      unsigned long long ck[kCand];  // (key << 32) | record index, ascending
 #pragma unroll
-      for (int i = 0; i < kCand; ++i) ck[i] = kNoKey;
+      for (int i = 0; i < kCand; ++i) ck[i] = ~0ull;
       uint32_t ncand = 0;
       for (uint32_t b0 = 0; b0 < nsrc; b0 += kTP) {
         const uint32_t n = min((uint32_t)kTP, nsrc - b0);
         __syncthreads();
         if (threadIdx.x < n) {
           const uint32_t i = b0 + threadIdx.x;
-          const uint32_t r = ovf ? 2u * cl[i >> 1] + (i & 1u) : list[i];
-          skey[threadIdx.x] = r;
-          if (!ovf || ((vm[r >> 1] >> (r & 1u)) & 1u)) {
-            smeta[threadIdx.x] = recs[r].meta;
-            sgeom[threadIdx.x] = expand(recs[r]);
-          } else {
-            RecMeta empty;
-            empty.x0 = 1;
-            empty.x1 = 0;
-            empty.y0 = 1;
-            empty.y1 = 0;
-            empty.off = 0;
-            empty.flags = 0;
-            smeta[threadIdx.x] = empty;
-          }
+          const uint32_t r = ovf ? i : list[i];  // unused slots carry an empty bbox
+          sidx[threadIdx.x] = r;
+          skey[threadIdx.x] = recs[r].key;
+          smeta[threadIdx.x] = recs[r].meta;
+          sgeom[threadIdx.x] = expand(recs[r]);
         }
         __syncthreads();
         for (uint32_t j0 = 0; j0 < n; j0 += 32) {
@@ -1025,11 +1056,11 @@ __global__ void __launch_bounds__(kTP) k_raster_big(tfb_scene sc, const double *
               double e[3];
               if (key >= lo && edges_at(AosRec{sgeom + jj}, mt.flags, px, py, e)) {
                 ++ncand;
-                uint32_t k = key;
+                unsigned long long k = ((unsigned long long)key << 32) | sidx[jj];
 #pragma unroll
                 for (int i = 0; i < kCand; ++i) {
                   if (k < ck[i]) {
-                    const uint32_t tk = ck[i];
+                    const unsigned long long tk = ck[i];
                     ck[i] = k;
                     k = tk;
                   }
@@ -1041,18 +1072,18 @@ __global__ void __launch_bounds__(kTP) k_raster_big(tfb_scene sc, const double *
       }
       const uint32_t nf = min(ncand, (uint32_t)kCand);
       for (uint32_t i = 0; i < nf; ++i) {
-        const uint32_t key = ck[i];
-        const RecGeom gk = expand(recs[key]);
-        fd.step(AosRec{&gk}, recs[key].meta.flags, px, py, (int32_t)key);
+        const uint32_t r = (uint32_t)(ck[i] & 0xffffffffu);
+        const RecGeom gk = expand(recs[r]);
+        fd.step(AosRec{&gk}, recs[r].meta.flags, px, py, (int32_t)r);
       }
       const bool more = need && ncand > (uint32_t)kCand;
-      if (more) lo = ck[kCand - 1] + 1;
+      if (more) lo = (uint32_t)(ck[kCand - 1] >> 32) + 1;
       need = more;
       if (!__syncthreads_or(more)) break;
     }
     if (in_img) {
       const uint32_t flags = fd.win >= 0 ? recs[fd.win].meta.flags : 0u;
-      const int32_t t = fd.win >= 0 ? (int32_t)((uint32_t)fd.win >> 1) : -1;
+      const int32_t t = fd.win >= 0 ? (int32_t)(recs[fd.win].key >> 1) : -1;
       write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, fd.win >= 0 ? recs[fd.win].meta.off : 0);
     }
   }
