@@ -480,8 +480,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
 
 // ---------------------------------------------------------------------------
 // k_fuse_fast: the float32-accumulator, count-derived-weight (pixels_iid /
-// images_iid / blend), 16-byte-aligned, c % 4 == 0 case -- the BASELINE
-// workload.  Same pipeline as k_fuse, but the piece epilogue is taken out of
+// images_iid / blend) case with 16-byte-aligned maps -- the BASELINE
+// workload (VEC: c % 4 == 0, quads move as 16-byte vectors; otherwise as
+// masked scalars, the last quad padded with the fold identity).  Same pipeline as k_fuse, but the piece epilogue is taken out of
 // the divergent pixel scan:
 //   scan      lanes = (pixel group g, class quad q) fold their group's pixels
 //             into per-piece values (product / sum) and write each finished
@@ -501,7 +502,7 @@ struct FastSmem {
 
 __host__ __device__ inline FastSmem fast_layout(int c, int NS) {
   FastSmem s;
-  s.stage_floats = (size_t)kChunk * c;  // c % 4 == 0
+  s.stage_floats = (size_t)kChunk * c;  // 128*c bytes: every stage starts 16-byte aligned
   size_t o = (size_t)NS * s.stage_floats * 4;
   s.o_head = o;  // int4 per valid piece: {accumulator offset, weight bits, first-pixel float offset, 0}
   o += (size_t)kChunk * 16;
@@ -540,7 +541,33 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) {
   return *reinterpret_cast<float2 *>(&r);
 }
 
-template <int AGG>
+// quad access: 16-byte vectors when rows are 16-byte aligned (c % 4 == 0), else nv <= 4
+// valid scalars with `pad` (the fold identity) in the missing lanes
+template <bool VEC>
+__device__ __forceinline__ float4 lds4(const float *p, int nv, float pad) {
+  if (VEC) return *reinterpret_cast<const float4 *>(p);
+  return make_float4(p[0], nv > 1 ? p[1] : pad, nv > 2 ? p[2] : pad, nv > 3 ? p[3] : pad);
+}
+
+template <bool VEC>
+__device__ __forceinline__ float4 ldg4(const float *p, int nv, float pad) {
+  if (VEC) return __ldg(reinterpret_cast<const float4 *>(p));
+  return make_float4(__ldg(p), nv > 1 ? __ldg(p + 1) : pad, nv > 2 ? __ldg(p + 2) : pad, nv > 3 ? __ldg(p + 3) : pad);
+}
+
+template <bool VEC>
+__device__ __forceinline__ void sts4(float *p, float4 v, int nv) {
+  if (VEC) {
+    *reinterpret_cast<float4 *>(p) = v;
+    return;
+  }
+  p[0] = v.x;
+  if (nv > 1) p[1] = v.y;
+  if (nv > 2) p[2] = v.z;
+  if (nv > 3) p[3] = v.w;
+}
+
+template <int AGG, bool VEC>
 __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant__ FuseParams p) {
   constexpr bool kProd = AGG == TFB_AGG_MUL;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -570,9 +597,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
   auto issue = [&](Pos q, int s) {
     const int start = q.ch * kChunk;
     const int npix = min(kChunk, hw - start);
-    const uint32_t bytes = (uint32_t)(npix * c * 4);
+    // the bulk copy moves whole 16-byte units; a partial last chunk's tail (< 16 B,
+    // only when c % 4 != 0) is copied by the lanes after the wait
+    const uint32_t bytes = (uint32_t)(npix * c * 4) & ~15u;
     mbar_expect_tx(bar + s, bytes);
-    bulk_g2s(stages + (size_t)s * L.stage_floats, p.probs[q.f] + (size_t)start * c, bytes, bar + s, policy);
+    if (bytes)
+      bulk_g2s(stages + (size_t)s * L.stage_floats, p.probs[q.f] + (size_t)start * c, bytes, bar + s, policy);
   };
   Pos cur{gw / cpf, gw % cpf};
   Pos ahead = cur;  // next item to stage
@@ -630,6 +660,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
 
     mbar_wait(bar + s, (phase >> s) & 1u);
     phase ^= 1u << s;
+    if (!VEC) {
+      const int nfl = npix * c, done = (nfl * 4 & ~15) / 4;
+      const float *src = p.probs[cur.f] + (size_t)cur.ch * kChunk * c;
+      for (int i = done + lane; i < nfl; i += 32) st[i] = src[i];
+    }
     __syncwarp();
 
     if (AGG == TFB_AGG_MAXSUM || p.fallback) {  // fusion.py:174, cli.py:293
@@ -652,6 +687,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
 
     for (int qb = 0; qb < geo.nq; qb += geo.QW) {
       const int q = qb + qi0;
+      const int nv = min(4, c - 4 * q);  // valid classes of this lane's quad
+      const float one = kProd ? 1.0f : 0.0f;  // fold identity
       // ---- scan: fold each piece of this lane's group into its first pixel's slot.
       // Branch-free over the group's pixels: at a piece start the running value
       // is stored (one predicated STS.128) and reset by selects.
@@ -660,8 +697,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
         const int n = i1 - i0;
         float *pp = st + (size_t)i0 * c + 4 * q;
         float *ps = pp;
-        const float one = kProd ? 1.0f : 0.0f;  // fold identity
-        float4 v = *reinterpret_cast<const float4 *>(pp);
+        float4 v = lds4<VEC>(pp, nv, one);
         if (AGG == TFB_AGG_MAXSUM) {
           const float mx = smax[i0];
           v.x = v.x == mx ? v.x : 0.f; v.y = v.y == mx ? v.y : 0.f;
@@ -673,9 +709,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
 #pragma unroll 2
         for (int j = 1; j < n; ++j) {
           pp += c;
-          v = *reinterpret_cast<const float4 *>(pp);
+          v = lds4<VEC>(pp, nv, one);
           const bool start = (sm >> j) & 1u;
-          if (start) *reinterpret_cast<float4 *>(ps) = make_float4(a01.x, a01.y, a23.x, a23.y);
+          if (start) sts4<VEC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
           ps = start ? pp : ps;
           a01.x = start ? one : a01.x; a01.y = start ? one : a01.y;
           a23.x = start ? one : a23.x; a23.y = start ? one : a23.y;
@@ -696,7 +732,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
             a23 = add2(a23, make_float2(v.z, v.w));
           }
         }
-        *reinterpret_cast<float4 *>(ps) = make_float4(a01.x, a01.y, a23.x, a23.y);
+        sts4<VEC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
         if (kProd && (fminf(mn01, mn23) < kMulClampF || fmaxf(mx01, mx23) > 1.0f)) {
           // rare: a value outside [1e-7, 1] in this group -> redo its pieces with
           // np.clip(p, 1e-7, 1) (fusion.py:177) from the global copy (the staged
@@ -709,16 +745,16 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
           for (int j = 0; j < n; ++j, pp += c, g4 += c) {
             const bool start = (sm >> j) & 1u;
             if (start && j > 0) {
-              *reinterpret_cast<float4 *>(ps) = make_float4(a01.x, a01.y, a23.x, a23.y);
+              sts4<VEC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
               ps = pp;
               a01 = make_float2(1.f, 1.f);
               a23 = a01;
             }
-            const float4 u = __ldg(reinterpret_cast<const float4 *>(g4));
+            const float4 u = ldg4<VEC>(g4, nv, 1.0f);
             a01 = mul2(a01, make_float2(clip_mul(u.x), clip_mul(u.y)));
             a23 = mul2(a23, make_float2(clip_mul(u.z), clip_mul(u.w)));
           }
-          *reinterpret_cast<float4 *>(ps) = make_float4(a01.x, a01.y, a23.x, a23.y);
+          sts4<VEC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
         }
       }
       __syncwarp();
@@ -732,7 +768,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
         float4 m = make_float4(0.5f, 0.5f, 0.5f, 0.5f);  // idle lanes must not trip the near-1 vote
         if (ok) {
           h = shead[P];
-          m = *reinterpret_cast<const float4 *>(stq + h.z);
+          m = lds4<VEC>(stq + h.z, nv, one);
         }
         float b0 = m.x, b1 = m.y, b2 = m.z, b3 = m.w;
         if (kProd) {
@@ -813,10 +849,10 @@ int launch_fuse(const FuseParams &p, cudaStream_t st) {
                            st);
 }
 
-template <int AGG>
+template <int AGG, bool VEC>
 int launch_fuse_fast(const FuseParams &p, cudaStream_t st) {
   static LaunchCache lc;
-  return launch_persistent(k_fuse_fast<AGG>, lc, fast_layout(p.c, p.NS).total * kWarps, p, st);
+  return launch_persistent(k_fuse_fast<AGG, VEC>, lc, fast_layout(p.c, p.NS).total * kWarps, p, st);
 }
 
 template <typename AccT, int AGG>
@@ -949,14 +985,21 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
     p.fallback = fallback_out ? fallback_out + (int64_t)f0 * hw : nullptr;
     p.nframes = nf;
     p.nitems = p.cpf * nf;
-    bool fast = !accum_is_f64 && weight_mode != TFB_W_EXPLICIT && num_classes % 4 == 0 && g_fuse_fast;
+    bool fast = !accum_is_f64 && weight_mode != TFB_W_EXPLICIT && g_fuse_fast;
     for (int i = 0; i < nf && fast; ++i) fast = ((uintptr_t)p.probs[i] & 15) == 0;
+    const bool vec = num_classes % 4 == 0;
     int rc;
     if (fast) {
       switch (aggregator) {
-        case TFB_AGG_SUM: rc = launch_fuse_fast<TFB_AGG_SUM>(p, st); break;
-        case TFB_AGG_MAXSUM: rc = launch_fuse_fast<TFB_AGG_MAXSUM>(p, st); break;
-        default: rc = launch_fuse_fast<TFB_AGG_MUL>(p, st); break;
+        case TFB_AGG_SUM:
+          rc = vec ? launch_fuse_fast<TFB_AGG_SUM, true>(p, st) : launch_fuse_fast<TFB_AGG_SUM, false>(p, st);
+          break;
+        case TFB_AGG_MAXSUM:
+          rc = vec ? launch_fuse_fast<TFB_AGG_MAXSUM, true>(p, st) : launch_fuse_fast<TFB_AGG_MAXSUM, false>(p, st);
+          break;
+        default:
+          rc = vec ? launch_fuse_fast<TFB_AGG_MUL, true>(p, st) : launch_fuse_fast<TFB_AGG_MUL, false>(p, st);
+          break;
       }
     } else if (accum_is_f64) {
       switch (aggregator) {

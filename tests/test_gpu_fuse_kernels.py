@@ -2,7 +2,8 @@
 (the specialised float32 / count-weight / c % 4 == 0 kernel and the general
 one, selected with TFB_OPT_FUSE_FAST) against the float64 oracle
 (oracle.accumulate_frame, fusion.py:145-183) on synthetic row images with
-texel runs, partial last chunks, several quad passes (c = 132), and the
+texel runs, partial last chunks, several quad passes (c = 132), class counts
+that are not a multiple of 4 (masked quads, bulk-copy tails), and the
 probability values the clip / log paths care about: 0, tiny, exactly 1,
 above 1, negative, NaN and values just below 1 (log1p series path)."""
 
@@ -106,7 +107,7 @@ def _scale(rows, probs, n_x, agg, wm, alpha):
 
 
 @pytest.mark.parametrize("fast", [True, False])
-@pytest.mark.parametrize("c", [4, 40, 132])
+@pytest.mark.parametrize("c", [3, 4, 13, 19, 40, 132])
 @pytest.mark.parametrize("agg", ["sum", "maxsum", "mul"])
 def test_fuse_kernels_vs_oracle(fast, c, agg):
     rng = np.random.default_rng(1000 + c)

@@ -67,7 +67,7 @@ def run(name):
         "frames_per_s": frames / (ms / 1000.0), "ms_per_job": ms,
         "raster_us_per_frame": 1000.0 * raster / frames, "fuse_us_per_frame": 1000.0 * fuse / frames,
         "fuse_gbs": b_frame * frames / (fuse / 1000.0) / 1e9, "setup_s": round(setup_s, 1),
-        "fuse_kernel": "k_fuse_fast" if c % 4 == 0 else "k_fuse (general)",
+        "fuse_kernel": "k_fuse_fast<VEC>" if c % 4 == 0 else "k_fuse_fast<scalar quads>",
     }), flush=True)
     del ann, maps, probs
     torch.cuda.empty_cache()
