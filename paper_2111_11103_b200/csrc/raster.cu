@@ -44,6 +44,9 @@ namespace {
 constexpr int kTW = TFB_TW, kTH = TFB_TH;  // raster tile (pixels); one k_raster thread per pixel
 constexpr int kTP = kTW * kTH;             // k_raster threads = tile pixels = staged records per tile
 constexpr int kThreads = 256;              // setup-side kernels
+#ifndef TFB_SETUP_MINB
+#define TFB_SETUP_MINB 3  // k_setup CTAs per SM the register budget must allow (80 regs)
+#endif
 #ifndef TFB_RASTER_MINB
 #define TFB_RASTER_MINB (1024 / kTP)  // k_raster CTAs per SM the register budget must allow
 #endif
@@ -418,7 +421,7 @@ __global__ void __launch_bounds__(kThreads) k_cull(tfb_scene sc, Work w) {
 // records at slot 2t+sub; tile coverage counted.
 constexpr int kSetupPer = 2;  // candidates per k_setup thread (their bin appends are batched)
 
-__global__ void __launch_bounds__(kThreads, 4) k_setup(tfb_scene sc, const double *__restrict__ cams, int W,
+__global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc, const double *__restrict__ cams, int W,
                                                     int H, int TX, int ntiles, Work w) {
   const int f = blockIdx.y;
   __shared__ Cam cam;
