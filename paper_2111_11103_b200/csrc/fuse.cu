@@ -28,6 +28,9 @@
 // (render fallback, cli.py:293) is emitted from the same staged bytes.
 #include <math.h>
 
+#include <atomic>
+#include <mutex>
+
 #include "common.cuh"
 
 namespace tfb {
@@ -811,30 +814,40 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
   }
 }
 
-int g_fuse_ctas_per_sm = 0;  // 0 = as many as fit (tfb_set_option(TFB_OPT_FUSE_CTAS_PER_SM))
-int g_fuse_fast = 1;         // tfb_set_option(TFB_OPT_FUSE_FAST): 0 routes everything through k_fuse
+std::atomic<int> g_fuse_ctas_per_sm{0};  // 0 = as many as fit (tfb_set_option(TFB_OPT_FUSE_CTAS_PER_SM))
+std::atomic<int> g_fuse_fast{1};         // tfb_set_option(TFB_OPT_FUSE_FAST): 0 routes everything through k_fuse
 
+// Per-device launch configuration of one kernel (dynamic shared memory attribute,
+// occupancy), computed once per device and size; entry points stay re-entrant.
+constexpr int kMaxDevices = 64;
 struct LaunchCache {
-  size_t bytes = 0;
-  int blocks_per_sm = 0;
-  int num_sms = 0;
+  std::mutex mu;
+  size_t bytes[kMaxDevices] = {};
+  int blocks_per_sm[kMaxDevices] = {};
+  int num_sms[kMaxDevices] = {};
 };
 
 template <typename Kern>
 int launch_persistent(Kern kern, LaunchCache &lc, size_t bytes, const FuseParams &p, cudaStream_t st) {
-  if (lc.bytes != bytes) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
-      return check_launch("tfb_fuse: shared memory configuration");
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&lc.num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lc.blocks_per_sm, kern, kWarps * 32, bytes);
-    if (lc.blocks_per_sm < 1) lc.blocks_per_sm = 1;
-    lc.bytes = bytes;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  TFB_REQUIRE(dev >= 0 && dev < kMaxDevices, TFB_ERR_CUDA, "tfb_fuse: device ordinal %d out of range", dev);
+  int per_sm, sms;
+  {
+    std::lock_guard<std::mutex> guard(lc.mu);
+    if (lc.bytes[dev] != bytes) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+        return check_launch("tfb_fuse: shared memory configuration");
+      cudaDeviceGetAttribute(&lc.num_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lc.blocks_per_sm[dev], kern, kWarps * 32, bytes);
+      if (lc.blocks_per_sm[dev] < 1) lc.blocks_per_sm[dev] = 1;
+      lc.bytes[dev] = bytes;
+    }
+    per_sm = lc.blocks_per_sm[dev];
+    sms = lc.num_sms[dev];
   }
-  int per_sm = lc.blocks_per_sm;
   if (g_fuse_ctas_per_sm > 0 && g_fuse_ctas_per_sm < per_sm) per_sm = g_fuse_ctas_per_sm;
-  int64_t grid = (int64_t)lc.num_sms * per_sm;
+  int64_t grid = (int64_t)sms * per_sm;
   const int64_t need = (p.nitems + kWarps - 1) / kWarps;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;

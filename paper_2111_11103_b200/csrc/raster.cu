@@ -29,6 +29,8 @@
 // evaluates `points @ R.T + t`.
 #include <math.h>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "exact_div.cuh"
 
@@ -1149,13 +1151,26 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
     k_setup<<<g2, kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w);
   }
   Outs o{rows_out, texel_hits, tri_out, texel_out, depth_out, u_out, v_out};
-  static bool smem_set = false;
-  if (!smem_set) {
-    cudaFuncSetAttribute(k_raster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem));
-    smem_set = true;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  {  // per-device one-time setup; entry points stay re-entrant
+    static std::mutex mu;
+    static bool smem_set[64] = {};
+    static int num_sms[64] = {};
+    std::lock_guard<std::mutex> guard(mu);
+    if (dev >= 0 && dev < 64) {
+      if (!smem_set[dev]) {
+        cudaFuncSetAttribute(k_raster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem));
+        cudaDeviceGetAttribute(&num_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+        smem_set[dev] = true;
+      }
+      sms = num_sms[dev];
+    } else {
+      cudaFuncSetAttribute(k_raster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem));
+    }
   }
   k_raster<<<dim3(TX, TY, nframes), kTP, sizeof(TileSmem), st>>>(sc, cams, width, height, TX, ntiles, w, o);
-  k_raster_big<<<148 * (256 / kTP), kTP, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
+  k_raster_big<<<sms * (256 / kTP), kTP, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
   return check_launch("tfb_rasterize");
 }
 
