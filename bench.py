@@ -9,8 +9,9 @@ c = 40 classes, softmax(N(0, 2^2)) float32 probability maps, aggregator mul
 (the paper default), weights images_iid, float32 accumulator.
 
 One step = one whole fusion job: zero the texture, rasterize + weight +
-scatter-add all 2000 frames (batches of --batch frames), NCCL all-reduce of
-accumulator + counts when N > 1, finalize + argmax.  `value` = frames of all
+scatter-add all 2000 frames (batches of --batch frames), finalize + argmax;
+with N > 1 the accumulator rows are sum-reduce-scattered (NCCL), each rank
+finalizes its slice and the int32 labels are all-gathered.  `value` = frames of all
 ranks / max-over-ranks device time (weak scaling: 2000 frames per GPU).
 Inputs are larger than L2: the frames cycle a pool of 8 distinct maps per
 GPU (8 x 49.2 MB = 393 MB > 126 MB L2), so every frame's probabilities are
@@ -210,7 +211,7 @@ def run_ours(args):
         ann.reset()
         ann.add_batch(probs_list, cams_dev, width=W, height=H)
         if world > 1:
-            ann.allreduce()
+            ann.finalize_distributed()  # reduce-scatter rows, finalize a slice per rank, all-gather labels
         ann.labels()
 
     def barrier():
@@ -269,7 +270,7 @@ def run_ours(args):
             ann.reset()
             ann.add_batch(host_list, cams_host)
             if world > 1:
-                ann.allreduce()
+                ann.finalize_distributed()
             return ann.labels(host=True)
 
         e2e_step()

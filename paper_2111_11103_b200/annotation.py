@@ -203,6 +203,33 @@ class MeshAnnotation:
         allreduce_sum_([tex._accum, tex._counts], group)
         tex._h_accum = tex._h_counts = None
 
+    def finalize_distributed(self, group=None):
+        """Multi-rank end of a job: sum reduce-scatter of the accumulator rows,
+        each rank finalizes its slice on its GPU, int32 labels all-gathered
+        (dist.reduce_scatter_finalize).  Afterwards labels() / render() work on
+        every rank; the per-texel distributions (get()) are not gathered."""
+        from .dist import reduce_scatter_finalize
+
+        tex = self.texture
+        if tex.finalized:
+            raise RuntimeError("texture is already finalized")
+        tex._push_host()
+        c = tex.num_classes
+
+        def finalize_slice(acc, cnt):
+            n = int(acc.shape[0])
+            labels = torch.empty(n, dtype=torch.int32, device=acc.device)
+            unobs = torch.empty(n, dtype=torch.uint8, device=acc.device)
+            N.call("tfb_finalize", N.ptr(acc), int(tex.is_f64), tex.stride, N.ptr(cnt), n, c,
+                   N.AGG_IDS[tex.aggregator], None, N.ptr(unobs), N.ptr(labels), N.stream_handle())
+            return labels
+
+        tex._labels = reduce_scatter_finalize(tex._accum, tex._counts, finalize_slice, group)
+        tex._rows = None
+        tex._unobs = None
+        tex.finalized = True
+        return tex._labels
+
     # -- results -------------------------------------------------------------------------
     def _finalize(self):
         from .fusion import finalize

@@ -91,3 +91,43 @@ def test_shard_bounds_partition():
             assert all(got[i][1] == got[i + 1][0] for i in range(p - 1))
     with pytest.raises(ValueError):
         shard_bounds(10, 2, 2)
+
+
+def _rs_worker(rank, world, port, agg, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import oracle as O
+    from paper_2111_11103_b200 import dist as D
+
+    D.init_from_env("gloo")
+    z, probs = _scene()
+    mine = D.shard_frames(list(range(len(z["cams"]))))
+    acc, cnt = _fold(z, probs, mine, agg)
+
+    def finalize_slice(a, c):  # stands in for tfb_finalize on the rank's GPU
+        rows, unobs = O.finalize(a.numpy(), c.numpy(), agg)
+        return torch.from_numpy(O.texel_argmax(rows, unobs).astype(np.int32))
+
+    labels = D.reduce_scatter_finalize(torch.from_numpy(acc), torch.from_numpy(cnt), finalize_slice)
+    np.save(out + "_labels%d.npy" % rank, labels.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_reduce_scatter_finalize_equals_single_rank_labels(tmp_path, world):
+    """Slice-wise finalize after the exchange + label all-gather == one-rank labels (uneven slices for 3)."""
+    out = str(tmp_path / "rs")
+    mp.spawn(_rs_worker, args=(world, _free_port(), "mul", out), nprocs=world, join=True)
+    import oracle as O
+
+    z, probs = _scene()
+    acc1, cnt1 = _fold(z, probs, range(len(z["cams"])), "mul")
+    rows, unobs = O.finalize(acc1, cnt1, "mul")
+    ref = O.texel_argmax(rows, unobs)
+    for r in range(world):
+        got = np.load(out + "_labels%d.npy" % r)
+        decided = np.ones(len(ref), bool)
+        top2 = np.sort(rows, axis=1)[:, -2:]
+        decided &= (top2[:, 1] - top2[:, 0]) > 1e-9
+        np.testing.assert_array_equal(got[decided | unobs], ref[decided | unobs])
