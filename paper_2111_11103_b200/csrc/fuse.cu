@@ -709,11 +709,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
         float2 a01 = make_float2(v.x, v.y), a23 = make_float2(v.z, v.w);
         float mn01 = fminf(v.x, v.y), mn23 = fminf(v.z, v.w);
         float mx01 = fmaxf(v.x, v.y), mx23 = fmaxf(v.z, v.w);
+        unsigned smr = sm >> 1;  // bit 0: does a piece start at the next pixel
 #pragma unroll 2
         for (int j = 1; j < n; ++j) {
           pp += c;
           v = lds4<VEC>(pp, nv, one);
-          const bool start = (sm >> j) & 1u;
+          const bool start = smr & 1u;
+          smr >>= 1;
           if (start) sts4<VEC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
           ps = start ? pp : ps;
           a01.x = start ? one : a01.x; a01.y = start ? one : a01.y;
