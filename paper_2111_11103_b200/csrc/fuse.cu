@@ -255,8 +255,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
   AccT *sw = reinterpret_cast<AccT *>(ws + L.o_w);
   float *smax = reinterpret_cast<float *>(ws + L.o_max);
   uint64_t *bar = reinterpret_cast<uint64_t *>(ws + L.o_bar);
-  const int GW = gridDim.x * kWarps;
-  const int gw = blockIdx.x * kWarps + warp;
+  const int nw = blockDim.x >> 5;  // warps per CTA (fewer when c needs large stages)
+  const int GW = gridDim.x * nw;
+  const int gw = blockIdx.x * nw + warp;
   const int cpf = (int)p.cpf;
   const int dF = GW / cpf, dC = GW - dF * cpf;
 
@@ -583,8 +584,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
   int4 *shead = reinterpret_cast<int4 *>(ws + L.o_head);
   float *smax = reinterpret_cast<float *>(ws + L.o_max);
   uint64_t *bar = reinterpret_cast<uint64_t *>(ws + L.o_bar);
-  const int GW = gridDim.x * kWarps;
-  const int gw = blockIdx.x * kWarps + warp;
+  const int nw = blockDim.x >> 5;  // warps per CTA (fewer when c needs large stages)
+  const int GW = gridDim.x * nw;
+  const int gw = blockIdx.x * nw + warp;
   const int cpf = (int)p.cpf, hw = (int)p.hw;
   const int dF = GW / cpf, dC = GW - dF * cpf;
   const float wa = p.wa, wb = p.wb;
@@ -829,8 +831,19 @@ struct LaunchCache {
   int num_sms[kMaxDevices] = {};
 };
 
+constexpr size_t kSmemBudget = 227 * 1024;
+
+// warps per CTA: kWarps, fewer when that many staging rings do not fit in shared memory
+inline int warps_for(size_t per_warp) {
+  int nw = kWarps;
+  while (nw > 1 && per_warp * nw > kSmemBudget) nw >>= 1;
+  return nw;
+}
+
 template <typename Kern>
-int launch_persistent(Kern kern, LaunchCache &lc, size_t bytes, const FuseParams &p, cudaStream_t st) {
+int launch_persistent(Kern kern, LaunchCache &lc, size_t per_warp, const FuseParams &p, cudaStream_t st) {
+  const int nw = warps_for(per_warp);
+  const size_t bytes = per_warp * nw;
   int dev = 0;
   cudaGetDevice(&dev);
   TFB_REQUIRE(dev >= 0 && dev < kMaxDevices, TFB_ERR_CUDA, "tfb_fuse: device ordinal %d out of range", dev);
@@ -841,7 +854,7 @@ int launch_persistent(Kern kern, LaunchCache &lc, size_t bytes, const FuseParams
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
         return check_launch("tfb_fuse: shared memory configuration");
       cudaDeviceGetAttribute(&lc.num_sms[dev], cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lc.blocks_per_sm[dev], kern, kWarps * 32, bytes);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lc.blocks_per_sm[dev], kern, nw * 32, bytes);
       if (lc.blocks_per_sm[dev] < 1) lc.blocks_per_sm[dev] = 1;
       lc.bytes[dev] = bytes;
     }
@@ -850,24 +863,23 @@ int launch_persistent(Kern kern, LaunchCache &lc, size_t bytes, const FuseParams
   }
   if (g_fuse_ctas_per_sm > 0 && g_fuse_ctas_per_sm < per_sm) per_sm = g_fuse_ctas_per_sm;
   int64_t grid = (int64_t)sms * per_sm;
-  const int64_t need = (p.nitems + kWarps - 1) / kWarps;
+  const int64_t need = (p.nitems + nw - 1) / nw;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, kWarps * 32, bytes, st>>>(p);
+  kern<<<(unsigned)grid, nw * 32, bytes, st>>>(p);
   return check_launch("tfb_fuse");
 }
 
 template <typename AccT, int AGG, bool EQW>
 int launch_fuse(const FuseParams &p, cudaStream_t st) {
   static LaunchCache lc;
-  return launch_persistent(k_fuse<AccT, AGG, EQW>, lc, warp_layout(p.c, p.NS, (int)sizeof(AccT)).total * kWarps, p,
-                           st);
+  return launch_persistent(k_fuse<AccT, AGG, EQW>, lc, warp_layout(p.c, p.NS, (int)sizeof(AccT)).total, p, st);
 }
 
 template <int AGG, bool VEC>
 int launch_fuse_fast(const FuseParams &p, cudaStream_t st) {
   static LaunchCache lc;
-  return launch_persistent(k_fuse_fast<AGG, VEC>, lc, fast_layout(p.c, p.NS).total * kWarps, p, st);
+  return launch_persistent(k_fuse_fast<AGG, VEC>, lc, fast_layout(p.c, p.NS).total, p, st);
 }
 
 template <typename AccT, int AGG>
@@ -971,8 +983,10 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
               (long long)accum_stride);
   const size_t stage = (size_t)kChunk * num_classes * 4;
   const int NS = stage <= 2048 ? 4 : TFB_FUSE_NS;
-  TFB_REQUIRE(warp_layout(num_classes, NS, accum_is_f64 ? 8 : 4).total * kWarps <= 227 * 1024, TFB_ERR_CAPACITY,
-              "tfb_fuse: %d classes exceed the shared-memory staging budget", num_classes);
+  TFB_REQUIRE(warp_layout(num_classes, NS, accum_is_f64 ? 8 : 4).total <= kSmemBudget &&
+                  fast_layout(num_classes, NS).total <= kSmemBudget,
+              TFB_ERR_CAPACITY, "tfb_fuse: %d classes exceed the shared-memory staging budget of one warp",
+              num_classes);
   FuseParams p;
   p.hw = hw;
   p.c = num_classes;
