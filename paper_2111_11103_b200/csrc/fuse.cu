@@ -216,12 +216,8 @@ __device__ __forceinline__ void log4(float &a0, float &a1, float &a2, float &a3)
   a1 = lg2_ln(x1);
   a2 = lg2_ln(x2);
   a3 = lg2_ln(x3);
-#ifdef TFB_LOG_SELECT
-  if (true) {
-#else
   const bool near1 = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3)) > 0.9f;
   if (__any_sync(__activemask(), near1)) {
-#endif
     if (x0 > 0.9f) a0 = log1p_series(x0);
     if (x1 > 0.9f) a1 = log1p_series(x1);
     if (x2 > 0.9f) a2 = log1p_series(x2);
@@ -361,9 +357,6 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
       __syncwarp();
     }
 
-#ifdef TFB_EXP_NOCOMPUTE
-    if (false)
-#endif
     for (int qb = 0; qb < geo.nq; qb += geo.QW) {
       // lanes = (pixel group g, class quad q): each group scans its pixels in
       // order, folding them into the running value of their piece; when a piece
@@ -397,9 +390,6 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
               if (k0 + 3 >= c) b3 = 0.f;
             }
             float *dst = reinterpret_cast<float *>(p.accum) + doff + k0;
-#ifdef TFB_EXP_NORED
-            if (b0 == 12345.0f)
-#endif
             asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(b0), "f"(b1), "f"(b2),
                          "f"(b3));
           } else {
