@@ -1,14 +1,17 @@
 """MeshAnnotation-style fusion: ``add(probs, camera)`` / ``get()`` / ``render(camera)``.
 
 The batched, device-resident front end of the hot path (BASELINE north star):
-for each batch of up to ``max_batch`` frames of one size it issues exactly
-four stream-ordered launches — rasterize (tfb_rasterize: setup, scan, fill,
-tile raster with the per-frame texel hit counts fused into its epilogue),
-scatter-add (tfb_fuse), and the hit-counter reset (tfb_clear_hits) — and
-never synchronizes with the host.  ``get()`` finalizes once (tfb_finalize)
-and returns the per-texel rows; ``render`` rasterizes the requested cameras
-and gathers labels (tfb_render).  Multi-GPU: each rank adds its own frames,
-then ``allreduce()`` sums accumulators and counts over NCCL before ``get()``.
+for each batch of up to ``max_batch`` frames of one size it issues the
+stream-ordered launches of tfb_rasterize (vertex outcodes, cull, setup +
+tile binning, tile raster with the per-frame texel hit counts fused into its
+epilogue), one tfb_fuse scatter-add and the hit-counter reset, and never
+synchronizes with the host.  Host inputs are copied on a separate stream
+into double-buffered device staging, overlapping the previous batch's
+kernels.  ``get()`` finalizes once (tfb_finalize) and returns the per-texel
+rows; ``render`` rasterizes the requested cameras and gathers labels
+(tfb_render).  Multi-GPU: each rank adds its own frames, then
+``finalize_distributed()`` (reduce-scatter, slice finalize, label
+all-gather) or ``allreduce()`` (then ``get()``).
 
 It is a thin layer over the same ProbabilityTexture the reference-compatible
 functions use (fusion.py / session.py), so textures and results interchange.
@@ -58,7 +61,10 @@ class MeshAnnotation:
         self.scene = scene_for(mesh, self.layout, self.texture.device)
         self.device = self.scene.device
         self.max_batch = int(max_batch)
-        self._staging = None
+        self._staging = [None, None]  # device staging for host inputs (double-buffered)
+        self._stage_free = [None, None]
+        self._stage_slot = 0
+        self._copy_stream = None
         self.frames_added = 0
         # Overlap mode: batch k+1 is rasterized on a side stream while batch k
         # is scatter-added on the caller's stream (double-buffered row / hit
@@ -91,36 +97,48 @@ class MeshAnnotation:
 
     # -- accumulation ------------------------------------------------------------------
     def _probs_batch(self, probs, b, H, W):
-        """Per-frame device pointers for b frames (device tensors used in place)."""
+        """Per-frame device pointers for b frames.  Contiguous float32 device
+        tensors are used in place; anything else (host arrays, pinned host
+        tensors) is copied into one of two device staging buffers on a copy
+        stream, so the copy of batch k+1 overlaps the kernels of batch k.
+        Returns (pointers, keep-alive list, copy-done event or None, staging slot)."""
         c = self.num_classes
         if isinstance(probs, (list, tuple)):
             items = list(probs)
         else:
             items = [probs[i] for i in range(b)] if probs.ndim == 4 else [probs]
-        out, keep = [], []
-        need_stage = [i for i, p in enumerate(items) if not (isinstance(p, torch.Tensor) and p.is_cuda
-                                                             and p.dtype == torch.float32 and p.is_contiguous()
-                                                             and p.data_ptr() % 16 == 0)]
-        if need_stage:
-            shape = (self.max_batch, H, W, c)
-            if self._staging is None or tuple(self._staging.shape) != shape:
-                self._staging = torch.empty(shape, dtype=torch.float32, device=self.device)
-        for i, p in enumerate(items):
+        for p in items:
             if tuple(p.shape) != (H, W, c):
                 from .errors import DataError
 
                 raise DataError("probability array shape %s does not match expected %s"
                                 % (tuple(p.shape), (H, W, c)))
-            if i in need_stage:
-                dst = self._staging[i]
-                if isinstance(p, torch.Tensor):
-                    dst.copy_(p, non_blocking=True)
-                else:
-                    dst.copy_(torch.from_numpy(np.ascontiguousarray(p, dtype=np.float32)), non_blocking=True)
-                p = dst
-            out.append(p.data_ptr())
-            keep.append(p)
-        return out, keep
+        need_stage = [i for i, p in enumerate(items) if not (isinstance(p, torch.Tensor) and p.is_cuda
+                                                             and p.dtype == torch.float32 and p.is_contiguous()
+                                                             and p.data_ptr() % 16 == 0)]
+        ready, slot = None, None
+        if need_stage:
+            shape = (self.max_batch, H, W, c)
+            slot = self._stage_slot
+            self._stage_slot ^= 1
+            if self._staging[slot] is None or tuple(self._staging[slot].shape) != shape:
+                self._staging[slot] = torch.empty(shape, dtype=torch.float32, device=self.device)
+            if self._copy_stream is None:
+                self._copy_stream = torch.cuda.Stream(self.device)
+            cs = self._copy_stream
+            if self._stage_free[slot] is not None:
+                cs.wait_event(self._stage_free[slot])  # the scatter that last read this buffer is done
+            with torch.cuda.stream(cs):
+                for i in need_stage:
+                    p, dst = items[i], self._staging[slot][i]
+                    if isinstance(p, torch.Tensor):
+                        dst.copy_(p, non_blocking=True)
+                    else:
+                        dst.copy_(torch.from_numpy(np.ascontiguousarray(p, dtype=np.float32)), non_blocking=True)
+                    items[i] = dst
+            ready = torch.cuda.Event()
+            ready.record(cs)
+        return [p.data_ptr() for p in items], items, ready, slot
 
     def add_batch(self, probs, cameras, width=None, height=None, fallback_out=None, stream=None):
         """Fold B frames: probs (B, H, W, c) tensor/array or a list of (H, W, c);
@@ -151,8 +169,7 @@ class MeshAnnotation:
             b = min(mb, B - b0)
             slot = i % nslots
             chunk = probs[b0:b0 + b]
-            with torch.cuda.stream(cur):
-                ptrs, keep = self._probs_batch(chunk, b, H, W)
+            ptrs, keep, copied, sslot = self._probs_batch(chunk, b, H, W)
             rows = rows_all[slot, :b]
             hits = hits_all[slot, :b] if needs_hits else None
             if self.overlap and self._free[slot] is not None:
@@ -165,6 +182,8 @@ class MeshAnnotation:
                 ready = torch.cuda.Event()
                 ready.record(side)
                 cur.wait_event(ready)
+            if copied is not None:
+                cur.wait_event(copied)
             f0 = self._event(cur) if prof is not None else None
             parr, _k = N.ptr_array(ptrs)
             fb = fallback_out[b0:b0 + b] if fallback_out is not None else None
@@ -174,6 +193,10 @@ class MeshAnnotation:
                    N.stream_handle(cur))
             if prof is not None:
                 prof.append((b, r0, r1, f0, self._event(cur)))
+            if sslot is not None:
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                self._stage_free[sslot] = ev
             if needs_hits:
                 if tex.total_texels <= 4 * hw:  # a dense memset is cheaper than the scattered reset
                     with torch.cuda.stream(cur):
