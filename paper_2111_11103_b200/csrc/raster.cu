@@ -50,7 +50,7 @@ constexpr int kThreads = 256;              // setup-side kernels
 #define TFB_SETUP_MINB 3  // k_setup CTAs per SM the register budget must allow (80 regs)
 #endif
 #ifndef TFB_RASTER_MINB
-#define TFB_RASTER_MINB (1024 / kTP)  // k_raster CTAs per SM the register budget must allow
+#define TFB_RASTER_MINB 9  // k_raster CTAs per SM the register budget must allow (56 regs, 36 warps)
 #endif
 static_assert(kTW % 8 == 0 && kTH % 4 == 0 && kTP >= 64 && kTP <= 256, "tile shape: 8x4-pixel warp blocks");
 constexpr int kCand = 8;
