@@ -236,3 +236,32 @@ def test_host_ids_rows_and_weights():
     tex = init_texture(layout, 2, "sum")
     accumulate_frame(tex, ids, np.full((1, 4, 2), 0.5, np.float32), w)
     assert tex.counts.tolist() == [0, 2, 0, 0, 0, 1]
+
+
+def test_raster_dense_tiles_big_path_exact():
+    """Tiles holding more records than a k_raster CTA stages (> 128 per 16x8
+    tile): k_raster_big's list mode, with heavy overlap (many candidates per
+    pixel, near-coplanar stacks) — ids, depth, u, v bit-exact vs the oracle."""
+    rng = np.random.default_rng(21)
+    m = 1500
+    # small triangles packed into a 40x24-pixel window 2 m in front of the camera,
+    # at depths 1.9..2.1 (many overlaps, several exactly coplanar groups)
+    centers = np.column_stack([rng.uniform(-0.2, 0.2, m), rng.uniform(-0.12, 0.12, m),
+                               np.round(rng.uniform(1.9, 2.1, m), 2)])
+    offs = rng.uniform(-0.03, 0.03, size=(m, 3, 3))
+    offs[:, :, 2] *= 0.1
+    verts = (centers[:, None, :] + offs).reshape(-1, 3)
+    tris = np.arange(3 * m, dtype=np.int32).reshape(m, 3)
+    mesh = Mesh.from_arrays(verts, tris)
+    layout = uniform_layout(mesh, 3)
+    W, H = 96, 64
+    fr = CameraFrame(0, Intrinsics(200.0, 200.0, 47.5, 31.5, W, H), np.eye(3), np.zeros(3))
+    ids = rasterize(mesh, layout, fr)
+    ref = O.rasterize(mesh.vertices, mesh.triangles, layout.steps, layout.origins, pack_camera(fr), W, H)
+    np.testing.assert_array_equal(ids.triangle, ref["triangle"])
+    np.testing.assert_array_equal(ids.texel, ref["texel"])
+    np.testing.assert_array_equal(ids.depth, ref["depth"])
+    cov = ids.triangle >= 0
+    np.testing.assert_array_equal(ids.u[cov], ref["u"][cov])
+    np.testing.assert_array_equal(ids.v[cov], ref["v"][cov])
+    assert cov.mean() > 0.1  # the 40x24-pixel window is covered
