@@ -190,10 +190,10 @@ def run_ours(args):
     from paper_2111_11103_b200.synth import make_room, random_room_trajectory, scannet_intrinsics, softmax_maps
 
     world, rank, local = _dist_env()
-    if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local)  # before the process group, so NCCL binds this rank's GPU
     dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=dev)
 
     v, t = make_room((6.0, 5.0, 3.0), TESS)
     mesh = Mesh.from_arrays(v, t)
