@@ -1,0 +1,56 @@
+"""Throughput of the reference-style per-frame APIs on cfg2 (not a bench line):
+the session (open_session / add_frame / finalize_and_render) and the library
+loop (rasterize -> compute_pixel_weights -> accumulate_frame), device maps.
+
+    python tools/bench_session.py [frames]
+"""
+import os
+import sys
+import tempfile
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2111_11103_b200 import (Mesh, accumulate_frame, compute_pixel_weights, finalize,  # noqa: E402
+                                   init_texture, rasterize, save_ply, save_trajectory, uniform_layout)
+from paper_2111_11103_b200.session import add_frame, finalize_and_render, open_session  # noqa: E402
+from paper_2111_11103_b200.synth import make_room, random_room_trajectory, scannet_intrinsics, softmax_maps  # noqa: E402
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    v, t = make_room((6.0, 5.0, 3.0), 158)
+    mesh = Mesh.from_arrays(v, t)
+    frames = random_room_trajectory(n, scannet_intrinsics(), seed=0)
+    maps = softmax_maps(8, 480, 640, 40, seed=0)
+    with tempfile.TemporaryDirectory() as d:
+        mp, tp = os.path.join(d, "m.ply"), os.path.join(d, "t.txt")
+        save_ply(mp, mesh)
+        save_trajectory(tp, frames)
+        s = open_session(mp, tp, 0.0, "mul", "images_iid", 40, accum_dtype="float32")
+        add_frame(s, frames[0].frame_id, maps[0])
+        torch.cuda.synchronize()
+        t0 = time.time()
+        for i, fr in enumerate(frames):
+            add_frame(s, fr.frame_id, maps[i % 8])
+        torch.cuda.synchronize()
+        dt = time.time() - t0
+        finalize_and_render(s, [frames[0].frame_id])
+    print("session add_frame: %.0f frames/s (%d frames, wall clock)" % (n / dt, n))
+    layout = uniform_layout(mesh, 1)
+    tex = init_texture(layout, 40, "mul", accum_dtype="float32")
+    torch.cuda.synchronize()
+    t0 = time.time()
+    for i, fr in enumerate(frames):
+        ids = rasterize(mesh, layout, fr)
+        accumulate_frame(tex, ids, maps[i % 8], compute_pixel_weights(ids, "images_iid"))
+    finalize(tex)
+    torch.cuda.synchronize()
+    print("library loop: %.0f frames/s (%d frames, wall clock)" % (n / (time.time() - t0), n))
+
+
+if __name__ == "__main__":
+    main()
