@@ -129,7 +129,7 @@ struct Cam {
 
 struct Work {
   RecStore *rec;
-  uint32_t *cand;       // per frame: triangles surviving the outcode cull (count in fcnt[4f+2])
+  uint4 *cand;          // per frame: cull survivors {t | near-clip << 31, v0, v1, v2} (count in fcnt[4f+2])
   uint8_t *vcode;       // per frame per vertex: clip outcode (k_verts)
   int64_t nv;
   uint32_t *fcnt;       // fcnt[1]: big-tile count
@@ -152,7 +152,7 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
     return o;
   };
   size_t o_rec = take(sizeof(RecStore) * rs * nframes);
-  size_t o_cand = take(sizeof(uint32_t) * (size_t)(rs / 2) * nframes);
+  size_t o_cand = take(sizeof(uint4) * (size_t)(rs / 2) * nframes);
   size_t o_vcode = take((size_t)(nv > 0 ? nv : 1) * nframes);
   size_t o_fcnt = take(sizeof(uint32_t) * 4 * nframes);
   size_t o_tc = take(sizeof(uint32_t) * ntiles * nframes);
@@ -162,7 +162,7 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
   if (!ws || ws_bytes < off) return false;
   char *b = static_cast<char *>(ws);
   w.rec = reinterpret_cast<RecStore *>(b + o_rec);
-  w.cand = reinterpret_cast<uint32_t *>(b + o_cand);
+  w.cand = reinterpret_cast<uint4 *>(b + o_cand);
   w.vcode = reinterpret_cast<uint8_t *>(b + o_vcode);
   w.nv = nv > 0 ? nv : 1;
   w.fcnt = reinterpret_cast<uint32_t *>(b + o_fcnt);
@@ -387,11 +387,16 @@ __global__ void __launch_bounds__(kThreads) k_cull(tfb_scene sc, Work w) {
 #pragma unroll
     for (int q = 0; q < 3; ++q) vi[k][q] = t < sc.num_triangles ? __ldg(sc.triangles + 3 * t + q) : -1;
   }
-  unsigned cmask = 0;  // bit k: triangle t0 + k * kThreads is a candidate
+  unsigned cmask = 0, nmask = 0;  // bit k: triangle t0 + k * kThreads is a candidate / has a vertex behind
 #pragma unroll
-  for (int k = 0; k < kCullPer; ++k)
-    if (vi[k][0] >= 0 && (vc[vi[k][0]] & vc[vi[k][1]] & vc[vi[k][2]]) == 0u)  // not all behind the near plane
-      cmask |= 1u << k;                                                     // nor beyond one image edge
+  for (int k = 0; k < kCullPer; ++k) {
+    if (vi[k][0] < 0) continue;
+    const uint32_t c0 = vc[vi[k][0]], c1 = vc[vi[k][1]], c2 = vc[vi[k][2]];
+    if ((c0 & c1 & c2) == 0u) {  // not all behind the near plane nor beyond one image edge
+      cmask |= 1u << k;
+      nmask |= ((c0 | c1 | c2) & 1u) << k;
+    }
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t mine = __popc(cmask);
   uint32_t incl = mine;
@@ -412,10 +417,14 @@ __global__ void __launch_bounds__(kThreads) k_cull(tfb_scene sc, Work w) {
     base = s ? atomicAdd(w.fcnt + 4 * f + 2, s) : 0u;
   }
   __syncthreads();
-  uint32_t *out = w.cand + (int64_t)f * (w.rs / 2) + base + wtot[warp] + incl - mine;
+  // entries carry the vertex ids and the near-clip flag, so k_setup needs no
+  // further dependent loads before its transform
+  uint4 *out = w.cand + (int64_t)f * (w.rs / 2) + base + wtot[warp] + incl - mine;
 #pragma unroll
   for (int k = 0; k < kCullPer; ++k)
-    if ((cmask >> k) & 1u) *out++ = (uint32_t)(t0 + (int64_t)k * kThreads);
+    if ((cmask >> k) & 1u)
+      *out++ = make_uint4((uint32_t)(t0 + (int64_t)k * kThreads) | (((nmask >> k) & 1u) << 31), (uint32_t)vi[k][0],
+                          (uint32_t)vi[k][1], (uint32_t)vi[k][2]);
 }
 
 // Per surviving (frame, triangle): near clip + fan, projection, bbox, signed
@@ -430,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc
   load_cam(cam, cams, f);
   __syncthreads();
   const uint32_t ncand = w.fcnt[4 * f + 2];
-  const uint32_t *cl = w.cand + (int64_t)f * (w.rs / 2);
+  const uint4 *cl = w.cand + (int64_t)f * (w.rs / 2);
   // candidate prologue: triangle, vertex ids, outcodes -> 1 record slot if no vertex is
   // behind the near plane, else 2 (the fan of rasterizer.py:119-122 has at most two)
   struct Cand {
@@ -441,12 +450,12 @@ __global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc
   auto head = [&](uint32_t ci, Cand &c) {
     c.nslot = 0;
     if (ci >= ncand) return;
-    c.t = cl[ci];
-    c.i0 = __ldg(sc.triangles + 3 * c.t);
-    c.i1 = __ldg(sc.triangles + 3 * c.t + 1);
-    c.i2 = __ldg(sc.triangles + 3 * c.t + 2);
-    const uint8_t *vc = w.vcode + (int64_t)f * w.nv;
-    c.unclipped = ((vc[c.i0] | vc[c.i1] | vc[c.i2]) & 1u) == 0u;  // zmin >= NEAR_PLANE
+    const uint4 e = cl[ci];
+    c.t = e.x & 0x7fffffffu;
+    c.i0 = e.y;
+    c.i1 = e.z;
+    c.i2 = e.w;
+    c.unclipped = (e.x >> 31) == 0u;  // zmin >= NEAR_PLANE (k_cull's outcode bit 0)
     c.nslot = c.unclipped ? 1u : 2u;
   };
   auto one = [&](const Cand &c, uint32_t slot, Pend &p0, Pend &p1) {
