@@ -73,8 +73,11 @@ int tfb_version(void);
 int tfb_set_option(int option, int value);
 
 /* Bytes of scratch tfb_rasterize needs for up to `max_frames` frames of
- * width x height; `pair_capacity` = triangle/tile pairs budgeted per frame
- * (0 = default).  Tiles whose lists overflow it stay exact (slow path). */
+ * width x height (per frame: 2 x num_triangles 96-byte record slots, cull
+ * survivors, per-tile counts and fixed-capacity bins of 16x8 tiles).
+ * `pair_capacity` = triangle/tile pairs budgeted per frame, spread evenly
+ * over the tiles (0 = default: 4 per triangle, at least 512 per tile).
+ * Tiles whose bins overflow stay exact through the slow path. */
 size_t tfb_raster_workspace_bytes(int64_t num_vertices, int64_t num_triangles, int width, int height,
                                   int max_frames, int64_t pair_capacity);
 
@@ -109,11 +112,13 @@ int tfb_clear_hits(const int32_t *rows, int64_t hw, int nframes, int64_t total_t
 int tfb_pixel_weights(const int32_t *rows, int64_t hw, int nframes, const uint32_t *hits,
                       int64_t total_texels, int weight_mode, double alpha, double *out, void *stream);
 
-/* accumulate_frame (fusion.py:145-183) for `nframes` frames in one launch.
+/* accumulate_frame (fusion.py:145-183) for `nframes` frames.
  * probs: HOST array of nframes device pointers, each an (H*W, c) float32
- * image (16-byte aligned); they travel in the kernel parameters (up to 32
- * frames per launch), so no pointer table is copied and the call is CUDA-graph
- * capturable.  weight_mode TFB_W_EXPLICIT reads `weights`
+ * image; they travel in the kernel parameters (up to 256 frames per launch,
+ * more frames split into several launches), so no pointer table is copied and
+ * the call is CUDA-graph capturable.  16-byte-aligned maps with float32
+ * accumulators and count-derived weights take the specialised kernel; any
+ * class count up to ~880 is accepted.  weight_mode TFB_W_EXPLICIT reads `weights`
  * (nframes*H*W float64), the other modes derive w from `texel_hits`.
  * accum: (total_texels, accum_stride) float32 (accum_is_f64 = 0; stride a
  * multiple of 4) or float64 (accum_is_f64 = 1); log-space for TFB_AGG_MUL.
