@@ -49,6 +49,9 @@ constexpr int kThreads = 256;              // setup-side kernels
 #ifndef TFB_SETUP_MINB
 #define TFB_SETUP_MINB 3  // k_setup CTAs per SM the register budget must allow (80 regs)
 #endif
+#ifndef TFB_FIRST_FAST
+#define TFB_FIRST_FAST 1
+#endif
 #ifndef TFB_RASTER_MINB
 #define TFB_RASTER_MINB 9  // k_raster CTAs per SM the register budget must allow (56 regs, 36 warps)
 #endif
@@ -651,7 +654,9 @@ struct Fold {
       c = __ddiv_rn(e[2], z2);
     }
     const double sum = __dadd_rn(__dadd_rn(a, b), c);
-    if (sum > a2 * 1e-300) {
+    // a2 * 1e300 may overflow to +inf: then sum < inf still bounds z = a2 / sum
+    // below by a2 / DBL_MAX > 0; a sum of +inf gives z = 0 (no winner)
+    if (sum > __dmul_rn(a2, 1e-300) && sum < __dmul_rn(a2, 1e300)) {
       win = id;
       w0 = a;
       w1 = b;
@@ -661,6 +666,26 @@ struct Fold {
     }
   }
 };
+
+// Division-free form of first_e's acceptance for a covering record (all e_k >= 0):
+// with a2, z_k in [1e-100, 1e100] and max e_k <= 1e100, every quotient e_k / z_k is
+// at most 1e200, so sum = (a + b) + c < 1e201 is finite and z = a2 / sum > 1e-301;
+// with max e_k >= a2 * max z_k * 1e-50 the largest quotient, and so the sum, is at
+// least a2 * 1e-50 * (1 - 2^-53), so z < 1e51.  Then z is finite and positive and
+// wins against depth = +inf exactly as the divisions would decide.  The products
+// stay in the normal range under these bounds.
+template <typename R>
+__device__ __forceinline__ bool first_wins_without_divisions(const R &g, const double e[3]) {
+  const double z0 = g.f(kFZs), z1 = g.f(kFZs + 1), z2 = g.f(kFZs + 2), a2 = g.f(kFA2);
+  // every comparison is false for a NaN operand
+  const bool zok = z0 >= 1e-100 && z0 <= 1e100 && z1 >= 1e-100 && z1 <= 1e100 && z2 >= 1e-100 && z2 <= 1e100;
+  const double zmax = fmax(fmax(z0, z1), z2);
+  const double emax = fmax(fmax(e[0], e[1]), e[2]);
+  return zok && a2 >= 1e-100 && a2 <= 1e100 && emax <= 1e100 && emax >= __dmul_rn(__dmul_rn(a2, zmax), 1e-50);
+}
+
+__device__ __forceinline__ void emit_pixel(const tfb_scene &sc, const Outs &o, int f, int64_t pix, int32_t t,
+                                           int32_t texel, int32_t row);
 
 // Winner epilogue, rasterizer.py:177-202: perspective-correct barycentrics of
 // the original triangle → (u, v) → texel id → global row; optional planes.
@@ -673,7 +698,7 @@ __device__ __forceinline__ void write_pixel(const tfb_scene &sc, const Cam &cam,
                                             int px_i, int py_i, const Fold &fd, uint32_t flags, int32_t t,
                                             int64_t offset) {
   const int64_t pix = (int64_t)f * W * H + (int64_t)(py_i * W + px_i);
-  int32_t row = -1;
+  int32_t row = -1, texel = 0;
   if (fd.win >= 0) {
     const double wsum = __dadd_rn(__dadd_rn(fd.w0, fd.w1), fd.w2);
     double b0, b1, b2;
@@ -738,27 +763,28 @@ __device__ __forceinline__ void write_pixel(const tfb_scene &sc, const Cam &cam,
     if (i > s - 1) i = s - 1;
     int j = (int)__dmul_rn((double)s, v);
     if (j > i) j = i;
-    const int32_t texel = (i * i + i) / 2 + j;
+    texel = (i * i + i) / 2 + j;
     row = (int32_t)(offset + texel);
-    if (o.tri) {
-      o.tri[pix] = t;
-      o.texel[pix] = texel;
-    }
     if (o.depth) {
       o.depth[pix] = fd.depth;
       o.u[pix] = u;
       o.v[pix] = v;
     }
-  } else {
-    if (o.tri) {
-      o.tri[pix] = -1;
-      o.texel[pix] = 0;
-    }
-    if (o.depth) {
-      o.depth[pix] = fd.depth;
-      o.u[pix] = 0.0;
-      o.v[pix] = 0.0;
-    }
+  } else if (o.depth) {
+    o.depth[pix] = fd.depth;
+    o.u[pix] = 0.0;
+    o.v[pix] = 0.0;
+  }
+  emit_pixel(sc, o, f, pix, fd.win >= 0 ? t : -1, texel, row);
+}
+
+// Id planes, the fusion row and the per-frame texel hit count of one pixel
+// (t = -1: no triangle, texel 0, row -1).
+__device__ __forceinline__ void emit_pixel(const tfb_scene &sc, const Outs &o, int f, int64_t pix, int32_t t,
+                                           int32_t texel, int32_t row) {
+  if (o.tri) {
+    o.tri[pix] = t;
+    o.texel[pix] = texel;
   }
   o.rows[pix] = row;
   if (o.hits && row >= 0) {
@@ -963,8 +989,19 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
   if (cnt == 1u) {
     const int j = pc[0][tid];
     const double e[3] = {pe[0][tid], pe[1][tid], pe[2][tid]};
-    if (o.depth) fd.step_e(SoaRec{sg, j}, e, j);
-    else fd.first_e(SoaRec{sg, j}, e, j);
+    if (o.depth) {
+      fd.step_e(SoaRec{sg, j}, e, j);
+    } else if (TFB_FIRST_FAST && (sflags[j] >> 16) == 1u && first_wins_without_divisions(SoaRec{sg, j}, e)) {
+      // One texel per triangle (steps = 1) and no float planes: the sole covering
+      // record wins, and u in [0, 1], v in [0, u] give i = min(int(u), 0) = 0,
+      // j = min(int(v), 0) = 0 (rasterizer.py:196-198), so the texel is 0 whatever
+      // the barycentrics are.  They are finite for a winner: w_k >= 0 with
+      // 0 < wsum < inf, and the b rows sum to about wsum / wsum, so b.sum() > 0.
+      emit_pixel(sc, o, f, (int64_t)f * W * H + (int64_t)(py_i * W + px_i), stri[j], 0, soff[j]);
+      return;
+    } else {
+      fd.first_e(SoaRec{sg, j}, e, j);
+    }
   } else if (cnt == 2u) {  // both slots known: fold in ascending key order
     int j0 = pc[0][tid], j1 = pc[1][tid];
     if (skey[j1] < skey[j0]) {
