@@ -3,13 +3,15 @@
 // Per batch of frames (one launch per stage, all frames at once):
 //   k_verts  per (frame, vertex): camera transform, clip outcode.
 //   k_cull   per (frame, triangle): outcode cull (rasterizer.py:111 and empty
-//            bboxes), survivors compacted.
+//            bboxes), survivors compacted (unclipped ones from the front of
+//            the frame's list, near-clipped ones from the back).
 //   k_setup  per survivor: FMA-ordered world->camera transform (geometry.py:161,
 //            SURVEY A1), near-plane clip + fan (rasterizer.py:62-82, 113-122),
 //            projection, bbox, signed area, CCW reorder and edge ownership
 //            (rasterizer.py:136-164).  Each (sub)triangle becomes a 96-byte
-//            record at slot 2t+sub and is appended to the fixed-capacity bin
-//            of every tile its bbox overlaps (unordered).
+//            record (key 2t+sub) at a slot fixed by its survivor-list position
+//            and is appended to the fixed-capacity bin of every tile its bbox
+//            overlaps (unordered).
 //   k_raster one CTA per 16x8 tile, one thread per pixel.  Records staged
 //            field-major; pair-parallel float64 edge tests (ownership rule
 //            rasterizer.py:85-90); each pixel folds its covering records in
@@ -131,8 +133,10 @@ struct Cam {
 };
 
 struct Work {
-  RecStore *rec;
-  uint4 *cand;          // per frame: cull survivors {t | near-clip << 31, v0, v1, v2} (count in fcnt[4f+2])
+  RecStore *rec;        // per frame (2m slots): survivor at cand index c -> slot c if unclipped, 2c + fan half if
+                        // near-clipped; so records fill [0, nA) and [2(m - nB), 2m) densely
+  uint4 *cand;          // per frame (m entries): cull survivors {t | near-clip << 31, v0, v1, v2}; unclipped ones
+                        // from the front (count fcnt[4f+2]), near-clipped ones from the back (count fcnt[4f+3])
   uint8_t *vcode;       // per frame per vertex: clip outcode (k_verts)
   int64_t nv;
   uint32_t *fcnt;       // fcnt[1]: big-tile count
@@ -380,7 +384,7 @@ constexpr int kCullPer = 4;  // triangles per k_cull thread (independent loads i
 __global__ void __launch_bounds__(kThreads) k_cull(tfb_scene sc, Work w) {
   const int f = blockIdx.y;
   __shared__ uint32_t wtot[kThreads / 32];
-  __shared__ uint32_t base;
+  __shared__ uint32_t base_a, base_b;
   const int64_t t0 = (int64_t)blockIdx.x * kThreads * kCullPer + threadIdx.x;
   const uint8_t *vc = w.vcode + (int64_t)f * w.nv;
   int32_t vi[kCullPer][3];
@@ -401,7 +405,8 @@ __global__ void __launch_bounds__(kThreads) k_cull(tfb_scene sc, Work w) {
     }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t mine = __popc(cmask);
+  // unclipped survivors counted in the low half, near-clipped ones in the high half
+  const uint32_t mine = (uint32_t)__popc(cmask & ~nmask) | ((uint32_t)__popc(cmask & nmask) << 16);
   uint32_t incl = mine;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -417,22 +422,30 @@ __global__ void __launch_bounds__(kThreads) k_cull(tfb_scene sc, Work w) {
       wtot[i] = s;
       s += v;
     }
-    base = s ? atomicAdd(w.fcnt + 4 * f + 2, s) : 0u;
+    base_a = (s & 0xffffu) ? atomicAdd(w.fcnt + 4 * f + 2, s & 0xffffu) : 0u;
+    base_b = (s >> 16) ? atomicAdd(w.fcnt + 4 * f + 3, s >> 16) : 0u;
   }
   __syncthreads();
   // entries carry the vertex ids and the near-clip flag, so k_setup needs no
   // further dependent loads before its transform
-  uint4 *out = w.cand + (int64_t)f * (w.rs / 2) + base + wtot[warp] + incl - mine;
+  const uint32_t ex = wtot[warp] + incl - mine;
+  uint4 *const list = w.cand + (int64_t)f * (w.rs / 2);
+  uint32_t ia = base_a + (ex & 0xffffu);                       // front, ascending
+  int64_t ib = w.rs / 2 - 1 - (int64_t)(base_b + (ex >> 16));  // back, descending
 #pragma unroll
   for (int k = 0; k < kCullPer; ++k)
-    if ((cmask >> k) & 1u)
-      *out++ = make_uint4((uint32_t)(t0 + (int64_t)k * kThreads) | (((nmask >> k) & 1u) << 31), (uint32_t)vi[k][0],
-                          (uint32_t)vi[k][1], (uint32_t)vi[k][2]);
+    if ((cmask >> k) & 1u) {
+      const bool nc = (nmask >> k) & 1u;
+      const uint4 e = make_uint4((uint32_t)(t0 + (int64_t)k * kThreads) | ((uint32_t)nc << 31), (uint32_t)vi[k][0],
+                                 (uint32_t)vi[k][1], (uint32_t)vi[k][2]);
+      if (nc) list[ib--] = e;
+      else list[ia++] = e;
+    }
 }
 
 // Per surviving (frame, triangle): near clip + fan, projection, bbox, signed
-// area, CCW reorder and edge setup (rasterizer.py:113-164) into 128-byte
-// records at slot 2t+sub; tile coverage counted.
+// area, CCW reorder and edge setup (rasterizer.py:113-164) into 96-byte
+// records (see Work::rec for the slots); tile bins filled.
 constexpr int kSetupPer = 2;  // candidates per k_setup thread (their bin appends are batched)
 
 __global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc, const double *__restrict__ cams, int W,
@@ -441,18 +454,23 @@ __global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc
   __shared__ Cam cam;
   load_cam(cam, cams, f);
   __syncthreads();
-  const uint32_t ncand = w.fcnt[4 * f + 2];
-  const uint4 *cl = w.cand + (int64_t)f * (w.rs / 2);
+  const uint32_t na = w.fcnt[4 * f + 2], ncand = na + w.fcnt[4 * f + 3];
+  const int64_t mc = w.rs / 2;  // survivor list length (m)
+  const uint4 *cl = w.cand + (int64_t)f * mc;
   // candidate prologue: triangle, vertex ids, outcodes -> 1 record slot if no vertex is
   // behind the near plane, else 2 (the fan of rasterizer.py:119-122 has at most two)
   struct Cand {
     int64_t t, i0, i1, i2;
-    uint32_t nslot;
+    uint32_t nslot, slot;
     bool unclipped;
   };
-  auto head = [&](uint32_t ci, Cand &c) {
+  // survivor i: the i-th unclipped one (cand index i, record slot i) or, past them, a
+  // near-clipped one from the back (cand index c, record slots 2c and 2c + 1)
+  auto head = [&](uint32_t i, Cand &c) {
     c.nslot = 0;
-    if (ci >= ncand) return;
+    if (i >= ncand) return;
+    const int64_t ci = i < na ? (int64_t)i : mc - 1 - (int64_t)(i - na);
+    c.slot = i < na ? (uint32_t)ci : (uint32_t)(2 * ci);
     const uint4 e = cl[ci];
     c.t = e.x & 0x7fffffffu;
     c.i0 = e.y;
@@ -461,9 +479,10 @@ __global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc
     c.unclipped = (e.x >> 31) == 0u;  // zmin >= NEAR_PLANE (k_cull's outcode bit 0)
     c.nslot = c.unclipped ? 1u : 2u;
   };
-  auto one = [&](const Cand &c, uint32_t slot, Pend &p0, Pend &p1) {
+  auto one = [&](const Cand &c, Pend &p0, Pend &p1) {
     p0.valid = p1.valid = false;
     if (!c.nslot) return;
+    const uint32_t slot = c.slot;
     const int64_t t = c.t;
     // camera-space vertices recomputed here (bit-identical to k_verts' transform): the
     // vertex array is L2-resident across frames, a per-frame camera-space copy is not
@@ -506,22 +525,10 @@ __global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc
     Cand cd[kSetupPer];
     head(c0, cd[0]);
     head(c0 + kThreads, cd[1]);
-    // dense record slots: one atomic per warp; its result is needed only by the stores
-    const uint32_t mine = cd[0].nslot + cd[1].nslot;
-    uint32_t incl = mine;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(act, incl, d);
-      if (lane >= d) incl += v;
-    }
-    const int last = 31 - __clz(act);
-    const uint32_t wtotal = __shfl_sync(act, incl, last);
-    uint32_t base = 0u;
-    if (lane == __ffs(act) - 1 && wtotal) base = atomicAdd(w.fcnt + 4 * f + 3, wtotal);
-    base = __shfl_sync(act, base, __ffs(act) - 1) + incl - mine;
+    // record slots follow from the survivor lists' layout: no allocation round trip
     Pend p[2 * kSetupPer];
-    one(cd[0], base, p[0], p[1]);
-    one(cd[1], base + cd[0].nslot, p[2], p[3]);
+    one(cd[0], p[0], p[1]);
+    one(cd[1], p[2], p[3]);
     // first-tile appends of all pending records in flight together (one atomic per
     // distinct tile per warp: neighbouring candidates mostly share a tile), then the rest
     uint32_t pos[2 * kSetupPer];
@@ -1065,7 +1072,10 @@ __global__ void __launch_bounds__(kTP) k_raster_big(tfb_scene sc, const double *
     const uint32_t tcount = w.tile_count[(int64_t)f * ntiles + tile];
     const bool ovf = tcount > (uint64_t)w.bincap;
     const uint32_t *list = w.list + ((int64_t)f * ntiles + tile) * w.bincap;
-    const uint32_t nsrc = ovf ? w.fcnt[4 * f + 3] : tcount;  // overflow: every allocated record slot
+    // overflow: every written record slot, [0, nA) and [2(m - nB), 2m)
+    const uint32_t na = w.fcnt[4 * f + 2], nb2 = 2u * w.fcnt[4 * f + 3];
+    const uint32_t nsrc = ovf ? na + nb2 : tcount;
+    const uint32_t clip0 = (uint32_t)(w.rs - nb2);
     const RecStore *recs = w.rec + (int64_t)f * w.rs;
 
     Fold fd;
@@ -1082,7 +1092,7 @@ __global__ void __launch_bounds__(kTP) k_raster_big(tfb_scene sc, const double *
         __syncthreads();
         if (threadIdx.x < n) {
           const uint32_t i = b0 + threadIdx.x;
-          const uint32_t r = ovf ? i : list[i];  // unused slots carry an empty bbox
+          const uint32_t r = ovf ? (i < na ? i : clip0 + (i - na)) : list[i];  // holes carry an empty bbox
           sidx[threadIdx.x] = r;
           skey[threadIdx.x] = recs[r].key;
           smeta[threadIdx.x] = recs[r].meta;
