@@ -49,7 +49,7 @@ constexpr int kTW = TFB_TW, kTH = TFB_TH;  // raster tile (pixels); one k_raster
 constexpr int kTP = kTW * kTH;             // k_raster threads = tile pixels = staged records per tile
 constexpr int kThreads = 256;              // setup-side kernels
 #ifndef TFB_SETUP_MINB
-#define TFB_SETUP_MINB 3  // k_setup CTAs per SM the register budget must allow (80 regs)
+#define TFB_SETUP_MINB 4  // k_setup CTAs per SM the register budget must allow (64 regs)
 #endif
 #ifndef TFB_FIRST_FAST
 #define TFB_FIRST_FAST 1
@@ -446,7 +446,10 @@ __global__ void __launch_bounds__(kThreads) k_cull(tfb_scene sc, Work w) {
 // Per surviving (frame, triangle): near clip + fan, projection, bbox, signed
 // area, CCW reorder and edge setup (rasterizer.py:113-164) into 96-byte
 // records (see Work::rec for the slots); tile bins filled.
-constexpr int kSetupPer = 2;  // candidates per k_setup thread (their bin appends are batched)
+#ifndef TFB_SETUP_PER
+#define TFB_SETUP_PER 2
+#endif
+constexpr int kSetupPer = TFB_SETUP_PER;  // candidates per k_setup thread (their bin appends are batched)
 
 __global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc, const double *__restrict__ cams, int W,
                                                     int H, int TX, int ntiles, Work w) {
@@ -523,12 +526,12 @@ __global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc
     const unsigned act = __activemask();
     const int lane = threadIdx.x & 31;
     Cand cd[kSetupPer];
-    head(c0, cd[0]);
-    head(c0 + kThreads, cd[1]);
+#pragma unroll
+    for (int k = 0; k < kSetupPer; ++k) head(c0 + k * kThreads, cd[k]);
     // record slots follow from the survivor lists' layout: no allocation round trip
     Pend p[2 * kSetupPer];
-    one(cd[0], p[0], p[1]);
-    one(cd[1], p[2], p[3]);
+#pragma unroll
+    for (int k = 0; k < kSetupPer; ++k) one(cd[k], p[2 * k], p[2 * k + 1]);
     // first-tile appends of all pending records in flight together (one atomic per
     // distinct tile per warp: neighbouring candidates mostly share a tile), then the rest
     uint32_t pos[2 * kSetupPer];
@@ -586,10 +589,21 @@ struct AosRec {  // one RecGeom (global memory or AoS shared memory)
   __device__ __forceinline__ double f(int k) const { return reinterpret_cast<const double *>(g)[k]; }
 };
 
-struct SoaRec {  // record j of a tile staged field-major: lanes reading different records hit different banks
+// Record j of a tile staged field-major (lanes reading different records hit
+// different banks).  Only xs, ys, zs and |area2| are staged (kStaged fields);
+// the edge deltas are re-derived on read exactly as expand_derived forms them.
+constexpr int kStaged = 10;
+constexpr int kSA2 = 9;  // staged slot of |area2|
+struct SoaRec {
   const double *base;
   int j;
-  __device__ __forceinline__ double f(int k) const { return base[k * kFS + j]; }
+  __device__ __forceinline__ double at(int q) const { return base[q * kFS + j]; }
+  __device__ __forceinline__ double f(int k) const {
+    if (k < kFDX) return at(k);
+    if (k == kFA2) return at(kSA2);
+    const int kk = (k - kFDX) % 3, o = k < kFDY ? kFXs : kFYs;  // dX (xs) or dY (ys)
+    return __dsub_rn(at(o + (kk + 2) % 3), at(o + (kk + 1) % 3));
+  }
 };
 
 // edge functions at one pixel centre, rasterizer.py:161-162
@@ -804,11 +818,10 @@ __device__ __forceinline__ void emit_pixel(const tfb_scene &sc, const Outs &o, i
 }
 
 struct TileSmem {
-  double g[kFields * kFS];          // staged records, field-major (SoA): g[k * kFS + j]
+  double g[kStaged * kFS];          // staged records, field-major (SoA): g[q * kFS + j]
   double pe[3][kTP];                // edge values of a pixel's (single) covering pair
   int32_t pc[2][kTP];               // per pixel: slots of its first two covering pairs (arrival order)
   uint32_t flags[kTP];              // RecMeta::flags
-  int32_t tri[kTP];                 // triangle of the record
   int32_t off[kTP];                 // offsets[t] of the record's triangle (n_x < 2^31)
   Cam cam;
   uint32_t key[kTP];
@@ -853,7 +866,7 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
   TileSmem &S = *reinterpret_cast<TileSmem *>(raster_smem);
   double *sg = S.g;
   uint32_t *sflags = S.flags;
-  int32_t *stri = S.tri, *soff = S.off;
+  int32_t *soff = S.off;
   uint32_t *skey = S.key, *sbox = S.box, *spre = S.pre, *pcnt = S.pcnt, *wtot = S.wtot;
   int32_t(*pc)[kTP] = S.pc;
   double(*pe)[kTP] = S.pe;
@@ -879,15 +892,9 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
     expand_derived(v + 2, v + 5, dX, dY, a2);
 #pragma unroll
     for (int q = 0; q < 9; ++q) sg[q * kFS + tid] = v[2 + q];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      sg[(kFDX + k) * kFS + tid] = dX[k];
-      sg[(kFDY + k) * kFS + tid] = dY[k];
-    }
-    sg[kFA2 * kFS + tid] = a2;
+    sg[kSA2 * kFS + tid] = a2;
     skey[tid] = key;
     sflags[tid] = mt.flags;
-    stri[tid] = (int32_t)(key >> 1);
     soff[tid] = mt.off;
     const int bx0 = max((int)mt.x0, tx0) - tx0, bx1 = min((int)mt.x1, tx0 + kTW - 1) - tx0;
     const int by0 = max((int)mt.y0, ty0) - ty0, by1 = min((int)mt.y1, ty0 + kTH - 1) - ty0;
@@ -1004,7 +1011,7 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
       // j = min(int(v), 0) = 0 (rasterizer.py:196-198), so the texel is 0 whatever
       // the barycentrics are.  They are finite for a winner: w_k >= 0 with
       // 0 < wsum < inf, and the b rows sum to about wsum / wsum, so b.sum() > 0.
-      emit_pixel(sc, o, f, (int64_t)f * W * H + (int64_t)(py_i * W + px_i), stri[j], 0, soff[j]);
+      emit_pixel(sc, o, f, (int64_t)f * W * H + (int64_t)(py_i * W + px_i), (int32_t)(skey[j] >> 1), 0, soff[j]);
       return;
     } else {
       fd.first_e(SoaRec{sg, j}, e, j);
@@ -1039,7 +1046,7 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
     }
   }
   const uint32_t flags = fd.win >= 0 ? sflags[fd.win] : 0u;
-  const int32_t t = fd.win >= 0 ? stri[fd.win] : -1;
+  const int32_t t = fd.win >= 0 ? (int32_t)(skey[fd.win] >> 1) : -1;
   const int64_t off = fd.win >= 0 ? soff[fd.win] : 0;
   write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, off);
 }
