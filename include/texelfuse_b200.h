@@ -58,6 +58,16 @@ typedef struct tfb_scene {
   int64_t num_vertices;
   int64_t num_triangles;
   int64_t total_texels;
+  /* Optional spatial clusters for the rasterizer's cluster cull (NULL / 0 =
+   * none: every triangle is tested every frame).  Cluster c owns the 64 slots
+   * cluster_tris[64c .. 64c+63] (triangle ids, -1 = empty slot); every
+   * triangle must appear in exactly one slot.  cluster_boxes[6c .. 6c+5] is a
+   * world-space box (min x, y, z, max x, y, z) containing the vertices of the
+   * cluster's triangles.  At most 2 * ceil(num_triangles / 64) + 1 clusters.
+   * Results are identical with or without clusters. */
+  const int32_t *cluster_tris;
+  const double *cluster_boxes;
+  int64_t num_clusters;
 } tfb_scene;
 
 const char *tfb_last_error(void);

@@ -143,11 +143,16 @@ struct Work {
   uint32_t *tile_count; // per frame per tile
   uint32_t *list;
   uint32_t *big;  // (frame, tile) codes handed to k_raster_big; count in fcnt[1]
+  uint32_t *csurv;  // per frame: surviving cluster ids (count fcnt[4f]); ncl entries per frame
+  int64_t ncl;
   int64_t rs;   // record slots per frame (2m)
   int64_t bincap;  // records per tile bin (list holds nframes x ntiles bins)
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// scene clusters accepted for m triangles (64 slots each; see tfb_scene)
+int64_t max_clusters(int64_t m) { return 2 * ((m + 63) / 64) + 1; }
 
 bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int ntiles, int64_t bincap, Work &w,
            size_t *need_out) {
@@ -165,6 +170,8 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
   size_t o_tc = take(sizeof(uint32_t) * ntiles * nframes);
   size_t o_list = take(sizeof(uint32_t) * (size_t)bincap * ntiles * nframes);
   size_t o_big = take(sizeof(uint32_t) * ntiles * nframes);
+  const int64_t ncl = max_clusters(m);
+  size_t o_csurv = take(sizeof(uint32_t) * (size_t)ncl * nframes);
   if (need_out) *need_out = off;
   if (!ws || ws_bytes < off) return false;
   char *b = static_cast<char *>(ws);
@@ -176,6 +183,8 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
   w.tile_count = reinterpret_cast<uint32_t *>(b + o_tc);
   w.list = reinterpret_cast<uint32_t *>(b + o_list);
   w.big = reinterpret_cast<uint32_t *>(b + o_big);
+  w.csurv = reinterpret_cast<uint32_t *>(b + o_csurv);
+  w.ncl = ncl;
   w.rs = rs;
   w.bincap = bincap;
   return true;
@@ -352,6 +361,15 @@ __device__ __forceinline__ void bin_put(const Work &w, int f, int ntiles, int ti
 // one sharing an edge bit has an empty bbox in the reference
 // (rasterizer.py:141-146) — the 1/4 px margin dwarfs the rounding of these
 // products, so no visible triangle is dropped.
+__device__ __forceinline__ uint32_t vertex_code(const Cam &cam, const double P[3], int W, int H) {
+  if (P[2] < kNearPlane) return 1u;
+  const double z = P[2];
+  return ((P[0] * cam.fx + (cam.cx - 0.25) * z < 0.0) ? 2u : 0u) |
+         ((P[0] * cam.fx + (cam.cx - ((double)W - 0.25)) * z > 0.0) ? 4u : 0u) |
+         ((P[1] * cam.fy + (cam.cy - 0.25) * z < 0.0) ? 8u : 0u) |
+         ((P[1] * cam.fy + (cam.cy - ((double)H - 0.25)) * z > 0.0) ? 16u : 0u);
+}
+
 __global__ void __launch_bounds__(kThreads) k_verts(tfb_scene sc, const double *__restrict__ cams, int W, int H,
                                                     Work w) {
   const int f = blockIdx.y;
@@ -362,17 +380,7 @@ __global__ void __launch_bounds__(kThreads) k_verts(tfb_scene sc, const double *
   if (v >= sc.num_vertices) return;
   double P[3];
   xform(cam, sc.vertices + 3 * v, P);
-  uint32_t code;
-  if (P[2] < kNearPlane) {
-    code = 1u;
-  } else {
-    const double z = P[2];
-    code = ((P[0] * cam.fx + (cam.cx - 0.25) * z < 0.0) ? 2u : 0u) |
-           ((P[0] * cam.fx + (cam.cx - ((double)W - 0.25)) * z > 0.0) ? 4u : 0u) |
-           ((P[1] * cam.fy + (cam.cy - 0.25) * z < 0.0) ? 8u : 0u) |
-           ((P[1] * cam.fy + (cam.cy - ((double)H - 0.25)) * z > 0.0) ? 16u : 0u);
-  }
-  w.vcode[(int64_t)f * w.nv + v] = (uint8_t)code;
+  w.vcode[(int64_t)f * w.nv + v] = (uint8_t)vertex_code(cam, P, W, H);
 }
 
 // Per (frame, triangle), light and fully occupied: the AND of the three
@@ -441,6 +449,139 @@ __global__ void __launch_bounds__(kThreads) k_cull(tfb_scene sc, Work w) {
       if (nc) list[ib--] = e;
       else list[ia++] = e;
     }
+}
+
+// ---- Cluster cull (scenes with tfb_scene clusters; replaces k_verts + k_cull) ----
+//
+// k_ccull, per (frame, cluster): the camera transform of the 8 corners of the
+// cluster's world AABB.  Each outcode condition of k_verts is a half-space in
+// camera space (z < NEAR_PLANE, or beyond an image edge by 1/4 px as the plane
+// through the camera centre), and camera coordinates are affine in world
+// coordinates, so when all 8 corners lie in one such half-space every vertex of
+// every triangle of the cluster does.  Then every triangle is either skipped by
+// rasterizer.py:111 or, clipped or not, has all of its (clipped) polygon
+// projecting beyond the edge, i.e. an empty bbox (rasterizer.py:141-146) -- it
+// produces nothing, as in the reference.  The corner tests carry a slack of
+// 1e-12 of the magnitudes involved, far above the rounding of the corner and
+// vertex transforms, so only clusters that are strictly outside are culled.
+constexpr int kCluster = 64;  // triangle slots per cluster
+
+__device__ __forceinline__ void xform_point(const Cam &c, const double p[3], double out[3]) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    out[r] = __dadd_rn(__fma_rn(p[2], c.R[3 * r + 2], __fma_rn(p[1], c.R[3 * r + 1], __dmul_rn(p[0], c.R[3 * r]))),
+                       c.T[r]);
+}
+
+__global__ void __launch_bounds__(kThreads) k_ccull(tfb_scene sc, const double *__restrict__ cams, int W, int H,
+                                                    Work w) {
+  const int f = blockIdx.y;
+  __shared__ Cam cam;
+  load_cam(cam, cams, f);
+  __syncthreads();
+  const int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  bool keep = false;
+  if (c < sc.num_clusters) {
+    const double *bx = sc.cluster_boxes + 6 * c;
+    const double lo[3] = {__ldg(bx), __ldg(bx + 1), __ldg(bx + 2)};
+    const double hi[3] = {__ldg(bx + 3), __ldg(bx + 4), __ldg(bx + 5)};
+    double rmax = 0.0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) rmax = fmax(rmax, fabs(cam.R[i]));
+    const double tmag = fabs(cam.T[0]) + fabs(cam.T[1]) + fabs(cam.T[2]);
+    const double kx = fabs(cam.fx) + fabs(cam.cx) + (double)W + 1.0, ky = fabs(cam.fy) + fabs(cam.cy) + (double)H + 1.0;
+    uint32_t all = 31u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double p[3] = {(i & 1) ? hi[0] : lo[0], (i & 2) ? hi[1] : lo[1], (i & 4) ? hi[2] : lo[2]};
+      double P[3];
+      xform_point(cam, p, P);
+      const double z = P[2];
+      const double tol = 1e-12 * ((fabs(p[0]) + fabs(p[1]) + fabs(p[2])) * rmax + tmag) + 1e-300;
+      const double sx = kx * tol + 1e-12 * (fabs(P[0] * cam.fx) + (fabs(cam.cx) + (double)W) * fabs(z));
+      const double sy = ky * tol + 1e-12 * (fabs(P[1] * cam.fy) + (fabs(cam.cy) + (double)H) * fabs(z));
+      uint32_t m = (z < kNearPlane - tol) ? 1u : 0u;
+      m |= (P[0] * cam.fx + (cam.cx - 0.25) * z < -sx) ? 2u : 0u;
+      m |= (P[0] * cam.fx + (cam.cx - ((double)W - 0.25)) * z > sx) ? 4u : 0u;
+      m |= (P[1] * cam.fy + (cam.cy - 0.25) * z < -sy) ? 8u : 0u;
+      m |= (P[1] * cam.fy + (cam.cy - ((double)H - 0.25)) * z > sy) ? 16u : 0u;
+      all &= m;
+    }
+    keep = all == 0u;  // (a NaN corner sets no bit: kept)
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, keep);
+  if (!bal) return;
+  const int lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  if (lane == __ffs(bal) - 1) base = atomicAdd(w.fcnt + 4 * f, (uint32_t)__popc(bal));
+  base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
+  if (keep) w.csurv[(int64_t)f * w.ncl + base + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)c;
+}
+
+// k_ccands, per (frame, surviving cluster) x 64 triangle slots: vertex outcodes
+// computed in place (the same transform and conditions as k_verts), the
+// triangle-level test of k_cull, survivors appended the same way.  Blocks take
+// four clusters at a time and stride over the frame's survivors.
+__global__ void __launch_bounds__(kThreads) k_ccands(tfb_scene sc, const double *__restrict__ cams, int W, int H,
+                                                     Work w) {
+  const int f = blockIdx.y;
+  __shared__ Cam cam;
+  __shared__ uint32_t wtot[kThreads / 32];
+  __shared__ uint32_t base_a, base_b;
+  load_cam(cam, cams, f);
+  __syncthreads();
+  const uint32_t nsurv = w.fcnt[4 * f];
+  const uint32_t *cs = w.csurv + (int64_t)f * w.ncl;
+  uint4 *const list = w.cand + (int64_t)f * (w.rs / 2);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kPer = kThreads / kCluster;
+  for (uint32_t g0 = blockIdx.x * kPer; g0 < nsurv; g0 += gridDim.x * kPer) {
+    const uint32_t gi = g0 + threadIdx.x / kCluster;
+    int64_t t = -1;
+    if (gi < nsurv) t = __ldg(sc.cluster_tris + (int64_t)__ldg(cs + gi) * kCluster + (threadIdx.x % kCluster));
+    bool cand = false, nc = false;
+    int32_t vi[3] = {0, 0, 0};
+    if (t >= 0) {
+      uint32_t code[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        vi[q] = __ldg(sc.triangles + 3 * t + q);
+        double P[3];
+        xform(cam, sc.vertices + 3 * (int64_t)vi[q], P);
+        code[q] = vertex_code(cam, P, W, H);
+      }
+      cand = (code[0] & code[1] & code[2]) == 0u;
+      nc = ((code[0] | code[1] | code[2]) & 1u) != 0u;
+    }
+    const uint32_t mine = (cand && !nc ? 1u : 0u) | (cand && nc ? 0x10000u : 0u);
+    uint32_t incl = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    if (lane == 31) wtot[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t sum = 0;
+      for (int i = 0; i < kThreads / 32; ++i) {
+        const uint32_t v = wtot[i];
+        wtot[i] = sum;
+        sum += v;
+      }
+      base_a = (sum & 0xffffu) ? atomicAdd(w.fcnt + 4 * f + 2, sum & 0xffffu) : 0u;
+      base_b = (sum >> 16) ? atomicAdd(w.fcnt + 4 * f + 3, sum >> 16) : 0u;
+    }
+    __syncthreads();
+    if (cand) {
+      const uint32_t ex = wtot[warp] + incl - mine;
+      const uint4 e = make_uint4((uint32_t)t | ((nc ? 1u : 0u) << 31), (uint32_t)vi[0], (uint32_t)vi[1],
+                                 (uint32_t)vi[2]);
+      if (nc) list[w.rs / 2 - 1 - (int64_t)(base_b + (ex >> 16))] = e;
+      else list[base_a + (ex & 0xffffu)] = e;
+    }
+    __syncthreads();  // wtot / bases reused by the next group
+  }
 }
 
 // Per surviving (frame, triangle): near clip + fan, projection, bbox, signed
@@ -1202,13 +1343,27 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
   cudaMemsetAsync(w.fcnt, 0, sizeof(uint32_t) * 4 * nframes, st);
   cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ntiles * nframes, st);
   tfb_scene sc = *scene;
-  if (m > 0) {
+  const bool clustered = sc.num_clusters > 0 && sc.cluster_tris && sc.cluster_boxes;
+  TFB_REQUIRE(!clustered || sc.num_clusters <= w.ncl, TFB_ERR_DATA,
+              "tfb_rasterize: %lld clusters for %lld triangles (at most %lld accepted)", (long long)sc.num_clusters,
+              (long long)m, (long long)w.ncl);
+  if (m > 0 && clustered) {
+    dim3 g0((unsigned)((sc.num_clusters + kThreads - 1) / kThreads), nframes);
+    k_ccull<<<g0, kThreads, 0, st>>>(sc, cams, width, height, w);
+    // one pass of blocks covers 1/8 of the clusters (a typical view keeps ~1/10);
+    // more survivors are strided over
+    const int64_t gb = (sc.num_clusters + 8 * (kThreads / kCluster) - 1) / (8 * (kThreads / kCluster));
+    dim3 g1((unsigned)(gb < 1 ? 1 : gb), nframes);
+    k_ccands<<<g1, kThreads, 0, st>>>(sc, cams, width, height, w);
+  } else if (m > 0) {
     if (sc.num_vertices > 0) {
       dim3 g0((unsigned)((sc.num_vertices + kThreads - 1) / kThreads), nframes);
       k_verts<<<g0, kThreads, 0, st>>>(sc, cams, width, height, w);
     }
     dim3 g1((unsigned)((m + kThreads * kCullPer - 1) / (kThreads * kCullPer)), nframes);
     k_cull<<<g1, kThreads, 0, st>>>(sc, w);
+  }
+  if (m > 0) {
     int64_t sb = (m / 3 + kThreads * kSetupPer - 1) / (kThreads * kSetupPer);  // ~1/3 survive a typical cull
     dim3 g2((unsigned)(sb < 1 ? 1 : sb), nframes);
     k_setup<<<g2, kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w);

@@ -7,6 +7,7 @@ torch tensors (PyTorch is the allocator); the library never allocates.
 """
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -15,6 +16,43 @@ from . import _native as N
 from .geometry import pack_camera
 
 _CACHE_ATTR = "_tfb_device_scene"
+
+
+CLUSTER = 64  # triangle slots per cluster (tfb_scene.cluster_tris)
+
+
+def _spread10(x):
+    """Interleave the low 10 bits of x with two zero bits (3-D Morton code)."""
+    x = x & np.uint64(0x3FF)
+    x = (x | (x << np.uint64(16))) & np.uint64(0x030000FF)
+    x = (x | (x << np.uint64(8))) & np.uint64(0x0300F00F)
+    x = (x | (x << np.uint64(4))) & np.uint64(0x030C30C3)
+    x = (x | (x << np.uint64(2))) & np.uint64(0x09249249)
+    return x
+
+
+def build_clusters(vertices, triangles):
+    """Spatial clusters of a mesh for tfb_scene: triangles in Morton order of
+    their centroids, 64 consecutive ones per cluster (the last one padded with
+    -1), and each cluster's world AABB over its triangles' vertices.  Returns
+    (cluster_tris int32 (nc * 64,), cluster_boxes float64 (nc, 6))."""
+    v = np.asarray(vertices, dtype=np.float64)
+    t = np.asarray(triangles, dtype=np.int64)
+    m = len(t)
+    cent = v[t].mean(axis=1)
+    lo, hi = cent.min(axis=0), cent.max(axis=0)
+    span = np.where(hi > lo, hi - lo, 1.0)
+    q = np.clip(((cent - lo) / span * 1023.0), 0, 1023).astype(np.uint64)
+    code = _spread10(q[:, 0]) | (_spread10(q[:, 1]) << np.uint64(1)) | (_spread10(q[:, 2]) << np.uint64(2))
+    order = np.argsort(code, kind="stable")
+    nc = (m + CLUSTER - 1) // CLUSTER
+    slots = np.full(nc * CLUSTER, -1, dtype=np.int64)
+    slots[:m] = order
+    pv = v[t[np.maximum(slots, 0)]]  # (nc * 64, 3, 3)
+    empty = (slots < 0)[:, None, None]
+    bmin = np.where(empty, np.inf, pv).reshape(nc, CLUSTER * 3, 3).min(axis=1)
+    bmax = np.where(empty, -np.inf, pv).reshape(nc, CLUSTER * 3, 3).max(axis=1)
+    return slots.astype(np.int32), np.ascontiguousarray(np.concatenate([bmin, bmax], axis=1))
 
 
 def _dev(device):
@@ -47,9 +85,20 @@ class DeviceScene:
         self.offsets = torch.as_tensor(np.ascontiguousarray(layout.offsets, np.int64), device=d)
         self.num_triangles = int(layout.num_triangles)
         self.total_texels = int(layout.total_texels)
+        # spatial clusters for the rasterizer's cluster cull (results are identical
+        # without them; TFB_NO_CLUSTERS=1 disables them)
+        self.cluster_tris = self.cluster_boxes = None
+        nclusters = 0
+        if mesh is not None and len(tris) > 0 and os.environ.get("TFB_NO_CLUSTERS", "0") != "1":
+            ct, cb = build_clusters(verts, tris)
+            self.cluster_tris = torch.as_tensor(ct, device=d)
+            self.cluster_boxes = torch.as_tensor(cb, device=d)
+            nclusters = len(cb)
         self.struct = N.TfbScene(
             self.vertices.data_ptr(), self.triangles.data_ptr(), self.steps.data_ptr(), self.origins.data_ptr(),
-            self.offsets.data_ptr(), len(verts), self.num_triangles, self.total_texels)
+            self.offsets.data_ptr(), len(verts), self.num_triangles, self.total_texels,
+            self.cluster_tris.data_ptr() if nclusters else None,
+            self.cluster_boxes.data_ptr() if nclusters else None, nclusters)
         self._sig = _signature(mesh, layout)
         self._ws = {}
         self._bufs = {}

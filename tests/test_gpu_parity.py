@@ -265,3 +265,68 @@ def test_raster_dense_tiles_big_path_exact():
     np.testing.assert_array_equal(ids.u[cov], ref["u"][cov])
     np.testing.assert_array_equal(ids.v[cov], ref["v"][cov])
     assert cov.mean() > 0.1  # the 40x24-pixel window is covered
+
+
+def _raster_rows_hits(mesh, layout, frames, W, H, clusters, monkeypatch):
+    from paper_2111_11103_b200.device import DeviceScene
+
+    monkeypatch.setenv("TFB_NO_CLUSTERS", "0" if clusters else "1")
+    sc = DeviceScene(mesh, layout)
+    assert (sc.cluster_tris is not None) == clusters
+    cams = sc.cams_tensor(frames)
+    B = len(frames)
+    rows = torch.empty((B, W * H), dtype=torch.int32, device=sc.device)
+    hits = torch.zeros((B, layout.total_texels), dtype=torch.int32, device=sc.device)
+    tri = torch.empty((B, W * H), dtype=torch.int32, device=sc.device)
+    tex = torch.empty((B, W * H), dtype=torch.int32, device=sc.device)
+    sc.rasterize(cams, W, H, rows, hits, tri, tex)
+    return rows.cpu().numpy(), hits.cpu().numpy(), tri.cpu().numpy(), tex.cpu().numpy()
+
+
+def test_raster_cluster_cull_identical(monkeypatch):
+    """The cluster cull (tfb_scene clusters) drops only clusters that produce no
+    pixel: ids and hit counts equal the per-triangle cull's, including cameras
+    grazing walls, in corners and looking along a wall (clusters straddling the
+    near plane and the image edges)."""
+    from paper_2111_11103_b200.synth import look_at
+
+    v, t = make_room((6.0, 5.0, 3.0), 40)
+    mesh = Mesh.from_arrays(v, t)
+    layout = uniform_layout(mesh, 2)
+    intr = Intrinsics(300.0, 300.0, 159.5, 119.5, 320, 240)
+    frames = list(random_room_trajectory(24, intr, seed=3))
+    special = [((2.999, 0.0, 0.0), (3.0, 1.0, 0.0)), ((2.9999, 2.4999, 1.4999), (0.0, 0.0, 0.0)),
+               ((0.0, 0.0, 1.49995), (1.0, 0.0, 1.49995)), ((-2.99, -2.49, -1.49), (-2.99, 2.0, -1.49)),
+               ((0.0, 2.49999, 0.0), (0.0, 0.0, 0.0)), ((1.0, 1.0, 0.0), (1.0, 1.0, -1.0))]
+    for k, (eye, target) in enumerate(special):
+        R, tr = look_at(np.array(eye), np.array(target))
+        frames.append(CameraFrame(100 + k, intr, R, tr))
+    a = _raster_rows_hits(mesh, layout, frames, 320, 240, True, monkeypatch)
+    b = _raster_rows_hits(mesh, layout, frames, 320, 240, False, monkeypatch)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+    for k in (0, len(frames) - 3, len(frames) - 1):  # and both equal the oracle
+        ref = O.rasterize(mesh.vertices, mesh.triangles, layout.steps, layout.origins, pack_camera(frames[k]), 320,
+                          240, want_uv=False)
+        np.testing.assert_array_equal(a[2][k], ref["triangle"].ravel())
+
+
+def test_raster_cluster_cull_sphere_outside(monkeypatch):
+    """A convex object seen from outside (back faces and a silhouette), clusters vs none."""
+    from paper_2111_11103_b200.synth import look_at, make_icosphere
+
+    mesh = make_icosphere(1.0, 4)
+    layout = uniform_layout(mesh, 1)
+    intr = Intrinsics(200.0, 200.0, 79.5, 59.5, 160, 120)
+    rng = np.random.default_rng(7)
+    frames = []
+    for k in range(16):
+        d = rng.normal(size=3)
+        eye = d / np.linalg.norm(d) * rng.uniform(1.05, 4.0)
+        R, tr = look_at(eye, rng.normal(size=3) * 0.5)
+        frames.append(CameraFrame(k, intr, R, tr))
+    a = _raster_rows_hits(mesh, layout, frames, 160, 120, True, monkeypatch)
+    b = _raster_rows_hits(mesh, layout, frames, 160, 120, False, monkeypatch)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+
