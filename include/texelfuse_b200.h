@@ -59,16 +59,23 @@ typedef struct tfb_scene {
   int64_t num_triangles;
   int64_t total_texels;
   /* Optional spatial clusters for the rasterizer's cluster cull (NULL / 0 =
-   * none: every triangle is tested every frame).  Cluster c owns the 64 slots
-   * cluster_tris[64c .. 64c+63] (triangle ids, -1 = empty slot); every
-   * triangle must appear in exactly one slot.  cluster_boxes[6c .. 6c+5] is a
-   * world-space box (min x, y, z, max x, y, z) containing the vertices of the
-   * cluster's triangles.  At most 2 * ceil(num_triangles / 64) + 1 clusters.
-   * Results are identical with or without clusters. */
-  const int32_t *cluster_tris;
-  const double *cluster_boxes;
+   * none: every vertex and triangle is tested every frame).  Every triangle
+   * must sit in exactly one slot of one cluster.  Results are identical with
+   * or without clusters.  At most 2 * ceil(num_triangles / 64) + 1. */
+  const struct tfb_cluster *clusters;
   int64_t num_clusters;
 } tfb_scene;
+
+/* One cluster: up to 64 triangles and the (at most 128) distinct vertices
+ * they use, plus a world-space box containing those vertices. */
+typedef struct tfb_cluster {
+  int32_t tri[64][4];  /* {triangle id, v0, v1, v2} (vertex ids); id -1 = empty slot */
+  uint32_t local[64];  /* corner k of slot i is verts[(local[i] >> 8k) & 0xff]         */
+  int32_t nverts;      /* distinct vertices used (<= 128)                             */
+  int32_t pad[3];
+  int32_t verts[128];  /* their vertex ids                                            */
+  double box[6];       /* min x, y, z, max x, y, z                                    */
+} tfb_cluster;
 
 const char *tfb_last_error(void);
 int tfb_version(void);

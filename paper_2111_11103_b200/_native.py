@@ -30,7 +30,7 @@ class TfbScene(ctypes.Structure):
     _fields_ = [
         ("vertices", _P), ("triangles", _P), ("steps", _P), ("origins", _P), ("offsets", _P),
         ("num_vertices", _I64), ("num_triangles", _I64), ("total_texels", _I64),
-        ("cluster_tris", _P), ("cluster_boxes", _P), ("num_clusters", _I64),
+        ("clusters", _P), ("num_clusters", _I64),
     ]
 
 

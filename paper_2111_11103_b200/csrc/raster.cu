@@ -482,7 +482,8 @@ __global__ void __launch_bounds__(kThreads) k_ccull(tfb_scene sc, const double *
   const int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   bool keep = false;
   if (c < sc.num_clusters) {
-    const double *bx = sc.cluster_boxes + 6 * c;
+    static_assert(sizeof(tfb_cluster) == 1856, "tfb_cluster layout");
+    const double *bx = sc.clusters[c].box;
     const double lo[3] = {__ldg(bx), __ldg(bx + 1), __ldg(bx + 2)};
     const double hi[3] = {__ldg(bx + 3), __ldg(bx + 4), __ldg(bx + 5)};
     double rmax = 0.0;
@@ -518,69 +519,68 @@ __global__ void __launch_bounds__(kThreads) k_ccull(tfb_scene sc, const double *
   if (keep) w.csurv[(int64_t)f * w.ncl + base + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)c;
 }
 
-// k_ccands, per (frame, surviving cluster) x 64 triangle slots: vertex outcodes
-// computed in place (the same transform and conditions as k_verts), the
-// triangle-level test of k_cull, survivors appended the same way.  Blocks take
-// four clusters at a time and stride over the frame's survivors.
+// k_ccands, per (frame, surviving cluster): the outcodes of the cluster's
+// distinct vertices (the same transform and conditions as k_verts) into shared
+// memory, then per triangle slot the test of k_cull, survivors appended the
+// same way (one pair of atomics per warp).  Blocks take four clusters at a
+// time and stride over the frame's survivors.
+constexpr int kCV = 128;  // vertex slots per cluster (tfb_cluster::verts)
+
 __global__ void __launch_bounds__(kThreads) k_ccands(tfb_scene sc, const double *__restrict__ cams, int W, int H,
                                                      Work w) {
   const int f = blockIdx.y;
+  constexpr int kPer = kThreads / kCluster;
   __shared__ Cam cam;
-  __shared__ uint32_t wtot[kThreads / 32];
-  __shared__ uint32_t base_a, base_b;
+  __shared__ uint8_t scode[kPer][kCV];
   load_cam(cam, cams, f);
   __syncthreads();
   const uint32_t nsurv = w.fcnt[4 * f];
   const uint32_t *cs = w.csurv + (int64_t)f * w.ncl;
   uint4 *const list = w.cand + (int64_t)f * (w.rs / 2);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int kPer = kThreads / kCluster;
+  const int lane = threadIdx.x & 31, sub = threadIdx.x / kCluster, slot = threadIdx.x % kCluster;
   for (uint32_t g0 = blockIdx.x * kPer; g0 < nsurv; g0 += gridDim.x * kPer) {
-    const uint32_t gi = g0 + threadIdx.x / kCluster;
-    int64_t t = -1;
-    if (gi < nsurv) t = __ldg(sc.cluster_tris + (int64_t)__ldg(cs + gi) * kCluster + (threadIdx.x % kCluster));
+    const uint32_t gi = g0 + sub;
+    const tfb_cluster *cl = gi < nsurv ? sc.clusters + __ldg(cs + gi) : nullptr;
+    int4 tr = make_int4(-1, 0, 0, 0);
+    uint32_t loc = 0;
+    if (cl) {
+      tr = __ldg(reinterpret_cast<const int4 *>(cl->tri[slot]));
+      loc = __ldg(cl->local + slot);
+      const int nv = __ldg(&cl->nverts);
+#pragma unroll
+      for (int k = 0; k < kCV / kCluster; ++k) {
+        const int j = slot + k * kCluster;
+        if (j < nv) {
+          double P[3];
+          xform(cam, sc.vertices + 3 * (int64_t)__ldg(cl->verts + j), P);
+          scode[sub][j] = (uint8_t)vertex_code(cam, P, W, H);
+        }
+      }
+    }
+    __syncthreads();
     bool cand = false, nc = false;
-    int32_t vi[3] = {0, 0, 0};
-    if (t >= 0) {
-      uint32_t code[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        vi[q] = __ldg(sc.triangles + 3 * t + q);
-        double P[3];
-        xform(cam, sc.vertices + 3 * (int64_t)vi[q], P);
-        code[q] = vertex_code(cam, P, W, H);
-      }
-      cand = (code[0] & code[1] & code[2]) == 0u;
-      nc = ((code[0] | code[1] | code[2]) & 1u) != 0u;
+    if (tr.x >= 0) {
+      const uint32_t c0 = scode[sub][loc & 0xffu], c1 = scode[sub][(loc >> 8) & 0xffu],
+                     c2 = scode[sub][(loc >> 16) & 0xffu];
+      cand = (c0 & c1 & c2) == 0u;
+      nc = ((c0 | c1 | c2) & 1u) != 0u;
     }
-    const uint32_t mine = (cand && !nc ? 1u : 0u) | (cand && nc ? 0x10000u : 0u);
-    uint32_t incl = mine;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += v;
+    const unsigned ba = __ballot_sync(0xffffffffu, cand && !nc), bb = __ballot_sync(0xffffffffu, cand && nc);
+    uint32_t pa = 0, pb = 0;
+    if (lane == 0) {
+      if (ba) pa = atomicAdd(w.fcnt + 4 * f + 2, (uint32_t)__popc(ba));
+      if (bb) pb = atomicAdd(w.fcnt + 4 * f + 3, (uint32_t)__popc(bb));
     }
-    if (lane == 31) wtot[warp] = incl;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t sum = 0;
-      for (int i = 0; i < kThreads / 32; ++i) {
-        const uint32_t v = wtot[i];
-        wtot[i] = sum;
-        sum += v;
-      }
-      base_a = (sum & 0xffffu) ? atomicAdd(w.fcnt + 4 * f + 2, sum & 0xffffu) : 0u;
-      base_b = (sum >> 16) ? atomicAdd(w.fcnt + 4 * f + 3, sum >> 16) : 0u;
-    }
-    __syncthreads();
+    pa = __shfl_sync(0xffffffffu, pa, 0);
+    pb = __shfl_sync(0xffffffffu, pb, 0);
     if (cand) {
-      const uint32_t ex = wtot[warp] + incl - mine;
-      const uint4 e = make_uint4((uint32_t)t | ((nc ? 1u : 0u) << 31), (uint32_t)vi[0], (uint32_t)vi[1],
-                                 (uint32_t)vi[2]);
-      if (nc) list[w.rs / 2 - 1 - (int64_t)(base_b + (ex >> 16))] = e;
-      else list[base_a + (ex & 0xffffu)] = e;
+      const unsigned below = (1u << lane) - 1u;
+      const uint4 e = make_uint4((uint32_t)tr.x | ((nc ? 1u : 0u) << 31), (uint32_t)tr.y, (uint32_t)tr.z,
+                                 (uint32_t)tr.w);
+      if (nc) list[w.rs / 2 - 1 - (int64_t)(pb + __popc(bb & below))] = e;
+      else list[pa + __popc(ba & below)] = e;
     }
-    __syncthreads();  // wtot / bases reused by the next group
+    __syncthreads();  // scode reused by the next group
   }
 }
 
@@ -1343,7 +1343,7 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
   cudaMemsetAsync(w.fcnt, 0, sizeof(uint32_t) * 4 * nframes, st);
   cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ntiles * nframes, st);
   tfb_scene sc = *scene;
-  const bool clustered = sc.num_clusters > 0 && sc.cluster_tris && sc.cluster_boxes;
+  const bool clustered = sc.num_clusters > 0 && sc.clusters;
   TFB_REQUIRE(!clustered || sc.num_clusters <= w.ncl, TFB_ERR_DATA,
               "tfb_rasterize: %lld clusters for %lld triangles (at most %lld accepted)", (long long)sc.num_clusters,
               (long long)m, (long long)w.ncl);

@@ -18,7 +18,13 @@ from .geometry import pack_camera
 _CACHE_ATTR = "_tfb_device_scene"
 
 
-CLUSTER = 64  # triangle slots per cluster (tfb_scene.cluster_tris)
+CLUSTER = 64     # triangle slots per cluster (tfb_cluster.tri)
+CLUSTER_V = 128  # vertex slots per cluster (tfb_cluster.verts)
+
+# numpy mirror of tfb_cluster (include/texelfuse_b200.h), 1856 bytes
+CLUSTER_DTYPE = np.dtype([("tri", "<i4", (CLUSTER, 4)), ("local", "<u4", (CLUSTER,)), ("nverts", "<i4"),
+                          ("pad", "<i4", (3,)), ("verts", "<i4", (CLUSTER_V,)), ("box", "<f8", (6,))])
+assert CLUSTER_DTYPE.itemsize == 1856
 
 
 def _spread10(x):
@@ -32,27 +38,71 @@ def _spread10(x):
 
 
 def build_clusters(vertices, triangles):
-    """Spatial clusters of a mesh for tfb_scene: triangles in Morton order of
-    their centroids, 64 consecutive ones per cluster (the last one padded with
-    -1), and each cluster's world AABB over its triangles' vertices.  Returns
-    (cluster_tris int32 (nc * 64,), cluster_boxes float64 (nc, 6))."""
+    """Spatial clusters of a mesh for tfb_scene.clusters: triangles in Morton
+    order of their centroids, 64 consecutive ones per cluster (32 where 64 would
+    use more than 128 distinct vertices), each cluster's distinct vertices with
+    the corners' local indices, and the world AABB of those vertices.  Returns a
+    structured array of CLUSTER_DTYPE."""
     v = np.asarray(vertices, dtype=np.float64)
     t = np.asarray(triangles, dtype=np.int64)
-    m = len(t)
+    m, nv = len(t), len(v)
+    if m == 0:
+        return np.zeros(0, dtype=CLUSTER_DTYPE)
     cent = v[t].mean(axis=1)
     lo, hi = cent.min(axis=0), cent.max(axis=0)
     span = np.where(hi > lo, hi - lo, 1.0)
     q = np.clip(((cent - lo) / span * 1023.0), 0, 1023).astype(np.uint64)
     code = _spread10(q[:, 0]) | (_spread10(q[:, 1]) << np.uint64(1)) | (_spread10(q[:, 2]) << np.uint64(2))
     order = np.argsort(code, kind="stable")
-    nc = (m + CLUSTER - 1) // CLUSTER
-    slots = np.full(nc * CLUSTER, -1, dtype=np.int64)
-    slots[:m] = order
-    pv = v[t[np.maximum(slots, 0)]]  # (nc * 64, 3, 3)
-    empty = (slots < 0)[:, None, None]
-    bmin = np.where(empty, np.inf, pv).reshape(nc, CLUSTER * 3, 3).min(axis=1)
-    bmax = np.where(empty, -np.inf, pv).reshape(nc, CLUSTER * 3, 3).max(axis=1)
-    return slots.astype(np.int32), np.ascontiguousarray(np.concatenate([bmin, bmax], axis=1))
+
+    def distinct_per_segment(starts, lens):
+        seg = np.repeat(np.arange(len(starts)), lens)
+        pos = np.arange(m)  # the segments tile the Morton order contiguously
+        corners = t[order[pos]]                                   # (n, 3)
+        keys = seg[:, None].astype(np.int64) * nv + corners       # distinct per segment
+        uk, inv = np.unique(keys.ravel(), return_inverse=True)
+        useg = uk // nv
+        first = np.searchsorted(useg, np.arange(len(starts)))
+        counts = np.bincount(useg, minlength=len(starts))
+        return seg, pos, corners, uk % nv, useg, first, counts, inv.reshape(-1, 3)
+
+    starts = np.arange(0, m, CLUSTER)
+    lens = np.minimum(CLUSTER, m - starts)
+    res = distinct_per_segment(starts, lens)
+    big = res[6] > CLUSTER_V
+    if big.any():  # halves of 32 triangles use at most 96 distinct vertices
+        s2, l2 = [], []
+        for s0, n, b in zip(starts, lens, big):
+            if b:
+                s2 += [s0, s0 + n // 2]
+                l2 += [n // 2, n - n // 2]
+            else:
+                s2.append(s0)
+                l2.append(n)
+        starts, lens = np.array(s2), np.array(l2)
+        res = distinct_per_segment(starts, lens)
+    seg, pos, corners, uvid, useg, first, counts, inv = res
+    nc = len(starts)
+    out = np.zeros(nc, dtype=CLUSTER_DTYPE)
+    slot = pos - np.repeat(starts, lens)
+    tri = np.full((nc, CLUSTER, 4), 0, dtype=np.int32)
+    tri[:, :, 0] = -1
+    tri[seg, slot, 0] = order[pos]
+    tri[seg, slot, 1:] = corners
+    out["tri"] = tri
+    local = inv - first[seg][:, None]
+    loc = np.zeros((nc, CLUSTER), dtype=np.uint32)
+    loc[seg, slot] = (local[:, 0] | (local[:, 1] << 8) | (local[:, 2] << 16)).astype(np.uint32)
+    out["local"] = loc
+    out["nverts"] = counts
+    vslot = np.arange(len(uvid)) - first[useg]
+    verts = np.zeros((nc, CLUSTER_V), dtype=np.int32)
+    verts[useg, vslot] = uvid
+    out["verts"] = verts
+    pv = v[uvid]  # grouped by cluster (uvid is sorted by cluster first)
+    out["box"] = np.concatenate([np.minimum.reduceat(pv, first, axis=0), np.maximum.reduceat(pv, first, axis=0)],
+                                axis=1)
+    return out
 
 
 def _dev(device):
@@ -87,18 +137,16 @@ class DeviceScene:
         self.total_texels = int(layout.total_texels)
         # spatial clusters for the rasterizer's cluster cull (results are identical
         # without them; TFB_NO_CLUSTERS=1 disables them)
-        self.cluster_tris = self.cluster_boxes = None
+        self.clusters = None
         nclusters = 0
         if mesh is not None and len(tris) > 0 and os.environ.get("TFB_NO_CLUSTERS", "0") != "1":
-            ct, cb = build_clusters(verts, tris)
-            self.cluster_tris = torch.as_tensor(ct, device=d)
-            self.cluster_boxes = torch.as_tensor(cb, device=d)
-            nclusters = len(cb)
+            cl = build_clusters(verts, tris)
+            self.clusters = torch.as_tensor(cl.view(np.uint8), device=d)
+            nclusters = len(cl)
         self.struct = N.TfbScene(
             self.vertices.data_ptr(), self.triangles.data_ptr(), self.steps.data_ptr(), self.origins.data_ptr(),
             self.offsets.data_ptr(), len(verts), self.num_triangles, self.total_texels,
-            self.cluster_tris.data_ptr() if nclusters else None,
-            self.cluster_boxes.data_ptr() if nclusters else None, nclusters)
+            self.clusters.data_ptr() if nclusters else None, nclusters)
         self._sig = _signature(mesh, layout)
         self._ws = {}
         self._bufs = {}

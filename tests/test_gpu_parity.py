@@ -272,7 +272,7 @@ def _raster_rows_hits(mesh, layout, frames, W, H, clusters, monkeypatch):
 
     monkeypatch.setenv("TFB_NO_CLUSTERS", "0" if clusters else "1")
     sc = DeviceScene(mesh, layout)
-    assert (sc.cluster_tris is not None) == clusters
+    assert (sc.clusters is not None) == clusters
     cams = sc.cams_tensor(frames)
     B = len(frames)
     rows = torch.empty((B, W * H), dtype=torch.int32, device=sc.device)
