@@ -591,6 +591,10 @@ __global__ void __launch_bounds__(kThreads) k_ccands(tfb_scene sc, const double 
 #define TFB_SETUP_PER 2
 #endif
 constexpr int kSetupPer = TFB_SETUP_PER;  // candidates per k_setup thread (their bin appends are batched)
+#ifndef TFB_SETUP_WIDE
+#define TFB_SETUP_WIDE 8
+#endif
+constexpr int kSetupWide = TFB_SETUP_WIDE;  // records over more tiles are binned by the whole warp
 
 __global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc, const double *__restrict__ cams, int W,
                                                     int H, int TX, int ntiles, Work w) {
@@ -687,17 +691,49 @@ __global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc
 #pragma unroll
     for (int e = 0; e < 2 * kSetupPer; ++e)
       pos[e] = __shfl_sync(act, pos[e], __ffs(peers[e]) - 1) + __popc(peers[e] & ((1u << lane) - 1u));
+    // the other tiles: a thread appends its own small records (a few round trips);
+    // a record over more than kSetupWide tiles is appended by the whole warp, one
+    // atomic per lane in flight at a time (a large triangle spans tens of tiles)
+    unsigned wide = 0u;  // bit e: record e goes to the warp
 #pragma unroll
     for (int e = 0; e < 2 * kSetupPer; ++e) {
       if (!p[e].valid) continue;
       const int x0 = (int)(p[e].tx & 0xffffu), x1 = (int)(p[e].tx >> 16);
       const int y0 = (int)(p[e].ty & 0xffffu), y1 = (int)(p[e].ty >> 16);
       bin_put(w, f, ntiles, y0 * TX + x0, pos[e], p[e].slot);
+      if ((x1 - x0 + 1) * (y1 - y0 + 1) > kSetupWide) {
+        wide |= 1u << e;
+        continue;
+      }
       for (int ty = y0; ty <= y1; ++ty)
         for (int tx = (ty == y0 ? x0 + 1 : x0); tx <= x1; ++tx) {
           const int tile = ty * TX + tx;
           bin_put(w, f, ntiles, tile, atomicAdd(tc + tile, 1u), p[e].slot);
         }
+    }
+    for (unsigned todo = __ballot_sync(act, wide != 0u); todo; todo = __ballot_sync(act, wide != 0u)) {
+      const int src = __ffs(todo) - 1;
+      const int e = __shfl_sync(act, wide ? __ffs(wide) - 1 : 0, src);
+      uint32_t mtx = 0, mty = 0, mslot = 0;
+#pragma unroll
+      for (int k = 0; k < 2 * kSetupPer; ++k)
+        if (k == e) {
+          mtx = p[k].tx;
+          mty = p[k].ty;
+          mslot = p[k].slot;
+        }
+      const uint32_t btx = __shfl_sync(act, mtx, src), bty = __shfl_sync(act, mty, src);
+      const uint32_t bslot = __shfl_sync(act, mslot, src);
+      if (lane == src) wide &= wide - 1u;
+      const int x0 = (int)(btx & 0xffffu), nx = (int)(btx >> 16) - x0 + 1;
+      const int y0 = (int)(bty & 0xffffu), ny = (int)(bty >> 16) - y0 + 1;
+      // the active lanes (all 32 but in a frame's last, partial warp) split the tiles;
+      // tile 0 is the first tile, appended above
+      const int rank = __popc(act & ((1u << lane) - 1u)), nact = __popc(act);
+      for (int i = 1 + rank; i < nx * ny; i += nact) {
+        const int tile = (y0 + i / nx) * TX + x0 + i % nx;
+        bin_put(w, f, ntiles, tile, atomicAdd(tc + tile, 1u), bslot);
+      }
     }
   }
 }

@@ -49,6 +49,34 @@ def make_room(size=(6.0, 5.0, 3.0), tess=4):
     return np.array(verts, dtype=np.float64), np.array(tris, dtype=np.int32)
 
 
+def make_furnished_room(size=(6.0, 5.0, 3.0), tess=4, num_boxes=10, box_tess=6, seed=0):
+    """make_room plus `num_boxes` closed, tessellated boxes ("furniture") standing
+    on the floor, each 12 * box_tess^2 triangles (SURVEY §7 hard part 9: the bare
+    room seen from inside has no overdraw; the boxes give occlusion, so pixels
+    with several covering triangles and the depth test).  Boxes may overlap each
+    other; they stay inside the central 80 % of the floor.  Returns (vertices,
+    triangles); the room's triangles come first."""
+    v, t = make_room(size, tess)
+    rng = np.random.default_rng(seed)
+    hx, hy, hz = (float(s) / 2.0 for s in size)
+    verts, tris = [v], [t]
+    nv = len(v)
+    for _ in range(num_boxes):
+        w, d, h = rng.uniform(0.3, 1.2), rng.uniform(0.3, 1.2), rng.uniform(0.3, 1.1)
+        x0 = rng.uniform(-0.8 * hx, 0.8 * hx - w)
+        y0 = rng.uniform(-0.8 * hy, 0.8 * hy - d)
+        z0 = -hz + 1e-3  # just above the floor (no coplanar faces with it)
+        ex, ey, ez = (w, 0, 0), (0, d, 0), (0, 0, h)
+        faces = [((x0, y0, z0), ey, ex), ((x0, y0, z0 + h), ex, ey), ((x0 + w, y0, z0), ey, ez),
+                 ((x0, y0, z0), ez, ey), ((x0, y0 + d, z0), ez, ex), ((x0, y0, z0), ex, ez)]
+        for origin, eu, ev in faces:
+            fv, ft = _grid_face(origin, eu, ev, box_tess, nv)
+            verts.append(np.array(fv, dtype=np.float64))
+            tris.append(np.array(ft, dtype=np.int32))
+            nv += len(fv)
+    return np.concatenate(verts), np.concatenate(tris).astype(np.int32)
+
+
 def room_face_labels(tess, num_classes):
     per = 2 * tess * tess
     return (np.repeat(np.arange(6), per) % num_classes).astype(np.int32)

@@ -330,3 +330,53 @@ def test_raster_cluster_cull_sphere_outside(monkeypatch):
     for x, y in zip(a, b):
         np.testing.assert_array_equal(x, y)
 
+
+
+def test_raster_furnished_room_vs_oracle():
+    """cfg2 with furniture (SURVEY §7 hard part 9): occlusion, so pixels with
+    several covering records and the depth test; rows bit-exact at 640x480 for
+    a batch, and one frame's tri / texel / depth / u / v through rasterize()."""
+    from paper_2111_11103_b200.synth import make_furnished_room
+
+    v, t = make_furnished_room((6.0, 5.0, 3.0), 158)
+    mesh = Mesh.from_arrays(v, t)
+    layout = uniform_layout(mesh, 2)
+    frames = random_room_trajectory(4, scannet_intrinsics(), seed=21)
+    ann = MeshAnnotation(mesh, layout, num_classes=4, max_batch=4)
+    cams = ann.scene.cams_tensor(frames)
+    rows = torch.empty((4, 640 * 480), dtype=torch.int32, device=ann.device)
+    ann.scene.rasterize(cams, 640, 480, rows)
+    rows = rows.cpu().numpy()
+    box_pixels = 0
+    for k, fr in enumerate(frames):
+        ref = O.rasterize(mesh.vertices, mesh.triangles, layout.steps, layout.origins, pack_camera(fr), 640, 480,
+                          want_uv=(k == 0))
+        np.testing.assert_array_equal(rows[k], O.pixel_rows(layout.offsets, ref["triangle"], ref["texel"]).ravel())
+        box_pixels += int((ref["triangle"] >= 299568).sum())
+        if k == 0:
+            ids = rasterize(mesh, layout, fr)
+            np.testing.assert_array_equal(ids.triangle, ref["triangle"])
+            np.testing.assert_array_equal(ids.texel, ref["texel"])
+            np.testing.assert_array_equal(ids.depth, ref["depth"])
+            np.testing.assert_array_equal(ids.u, ref["u"])
+            np.testing.assert_array_equal(ids.v, ref["v"])
+    assert box_pixels > 1000  # the furniture is in view and occludes the walls
+
+
+def test_raster_large_triangles_few_survivors():
+    """Triangles spanning every tile with only 1-3 survivors in a frame (a
+    partial warp in k_setup bins a wide record cooperatively): ids equal the
+    oracle's."""
+    v = np.array([[-10, -10, 5], [10, -10, 5], [0, 10, 5]], dtype=np.float64)
+    for ntri in (1, 2, 3, 40):
+        vs = np.concatenate([v + [0.01 * k, 0.02 * k, k * 0.1] for k in range(ntri)])
+        t = np.arange(3 * ntri, dtype=np.int32).reshape(ntri, 3)
+        mesh = Mesh.from_arrays(vs, t)
+        layout = uniform_layout(mesh, 2)
+        fr = CameraFrame(0, Intrinsics(32.0, 32.0, 31.5, 31.5, 64, 64), np.eye(3), np.zeros(3))
+        ids = rasterize(mesh, layout, fr)
+        ref = O.rasterize(mesh.vertices, mesh.triangles, layout.steps, layout.origins, pack_camera(fr), 64, 64,
+                          want_uv=False)
+        np.testing.assert_array_equal(ids.triangle, ref["triangle"])
+        np.testing.assert_array_equal(ids.texel, ref["texel"])
+        assert (ids.triangle >= 0).mean() > 0.5

@@ -2,7 +2,7 @@
 (not bench lines: bench.py's headline is cfg2).  One fusion job per config,
 timed with CUDA events after a warm-up job; prints one JSON line per config.
 
-    python tools/bench_configs.py [cfg1 cfg2sum cfg4 cfg5]
+    python tools/bench_configs.py [cfg1 cfg2sum cfg4 cfg5 cfg2furn]
 """
 
 import json
@@ -17,7 +17,8 @@ sys.path.insert(0, ROOT)
 
 from paper_2111_11103_b200 import Mesh, MeshAnnotation, uniform_layout  # noqa: E402
 from paper_2111_11103_b200.geometry import Intrinsics  # noqa: E402
-from paper_2111_11103_b200.synth import make_room, random_room_trajectory, softmax_maps  # noqa: E402
+from paper_2111_11103_b200.synth import (make_furnished_room, make_room, random_room_trajectory,  # noqa: E402
+                                         softmax_maps)
 
 CONFIGS = {
     # name: (tess, width, height, fx, classes, frames, aggregator, layout steps, batch, pool)
@@ -25,13 +26,15 @@ CONFIGS = {
     "cfg2sum": (158, 640, 480, 577.87, 40, 2000, "sum", 1, 256, 8),
     "cfg4": (158, 640, 480, 577.87, 40, 2000, "mul", 8, 256, 8),
     "cfg5": (646, 1920, 1080, 1728.0, 19, 500, "mul", 1, 32, 4),  # one GPU's share of the 8-GPU job
+    # cfg2 with furniture (SURVEY §7 hard part 9): 10 boxes, +1.4 % triangles, occlusion / overdraw
+    "cfg2furn": (158, 640, 480, 577.87, 40, 2000, "mul", 1, 256, 8),
 }
 
 
 def run(name):
     tess, W, H, fx, c, frames, agg, steps, batch, pool = CONFIGS[name]
     t0 = time.time()
-    v, t = make_room((6.0, 5.0, 3.0), tess)
+    v, t = make_furnished_room((6.0, 5.0, 3.0), tess) if name.endswith("furn") else make_room((6.0, 5.0, 3.0), tess)
     mesh = Mesh.from_arrays(v, t)
     layout = uniform_layout(mesh, steps)
     intr = Intrinsics(fx=fx, fy=fx, cx=(W - 1) / 2.0, cy=(H - 1) / 2.0, width=W, height=H)
