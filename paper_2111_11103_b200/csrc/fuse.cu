@@ -12,12 +12,13 @@
 //      and two items ahead (rows, then the dependent hit-count gather);
 //   2. find runs of consecutive pixels on the same texel with ballots and cut
 //      them into pieces at pixel-group starts (and every 4 pixels for the
-//      product rule); ~2.5 pixels per run at the BASELINE scene;
+//      product rule, 5 in k_fuse_fast); ~2.5 pixels per run at the BASELINE
+//      scene;
 //   3. work as lanes = (pixel group g, class quad q): each lane folds its
 //      group's pixels of quad q straight out of the staged shared-memory rows
-//      (sum, or product of <= 4 clipped probabilities with f32x2 multiplies)
+//      (sum, or product of <= 4 (5) clipped probabilities, f32x2 multiplies)
 //      and lands every finished piece with ONE red.global.add.v4.f32, plus one
-//      u32 count add by the piece's head lane.
+//      u32 count add per run of equal rows (by its head lane).
 // Weights derived from the hit counts (pixels_iid / images_iid / blend) are
 // equal inside a run, so w is applied once per item, and for the product
 // rule sum_i w*log(p_i) is evaluated as w*log(prod_i p_i) over up to four
@@ -43,6 +44,9 @@ namespace {
 #define TFB_FUSE_NS 2
 #endif
 constexpr int kWarps = TFB_FUSE_WARPS;  // warps per CTA (independent pipelines)
+#ifndef TFB_PIECE
+#define TFB_PIECE 5  // k_fuse_fast product pieces: 5 clipped values >= 1e-7 multiply to >= 1e-35, a normal float
+#endif
 constexpr int kChunk = 32;       // pixels per work item = one per lane
 constexpr int kMaxFrames = 256;  // frames per launch (pointers travel in the kernel parameters, 2 KB)
 
@@ -323,9 +327,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
       pstart = ((lane - rs) & 3) == 0;
     }
     const unsigned smask = __ballot_sync(0xffffffffu, pstart);
-    if (pstart && r_cur >= 0) {
-      const unsigned above = smask & ~upto;
-      atomicAdd(p.counts + r_cur, (uint32_t)((above ? __ffs(above) - 1 : kChunk) - lane));  // fusion.py:182
+    {  // counts (fusion.py:182): one add per run of equal rows in the chunk
+      const bool rstart = lane == 0 || prev != r_cur;
+      const unsigned rmask = __ballot_sync(0xffffffffu, rstart);
+      if (rstart && r_cur >= 0) {
+        const unsigned above = rmask & ~upto;
+        atomicAdd(p.counts + r_cur, (uint32_t)((above ? __ffs(above) - 1 : kChunk) - lane));
+      }
     }
     sdoff[lane] = r_cur >= 0 ? (int32_t)((int64_t)r_cur * p.stride) : -1;  // accumulator row offset
     sw[lane] = w;
@@ -640,14 +648,20 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
     bool pstart = chg;
     if (kProd) {
       const int rs = 31 - __clz(cmask & upto);
-      pstart = ((lane - rs) & 3) == 0;
+      pstart = (lane - rs) % TFB_PIECE == 0;
     }
     const unsigned smask = __ballot_sync(0xffffffffu, pstart);
     const bool valid = pstart && r_cur >= 0;
     const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    // counts (fusion.py:182): one add per run of equal rows in the chunk, not per
+    // piece (a large triangle's pixels would all hit one address piece by piece)
+    const bool rstart = (lane == 0 || prev != r_cur);
+    const unsigned rmask = __ballot_sync(0xffffffffu, rstart);
+    if (rstart && r_cur >= 0) {
+      const unsigned above = rmask & ~upto;
+      atomicAdd(p.counts + r_cur, (uint32_t)((above ? __ffs(above) - 1 : kChunk) - lane));
+    }
     if (valid) {
-      const unsigned above = smask & ~upto;
-      atomicAdd(p.counts + r_cur, (uint32_t)((above ? __ffs(above) - 1 : kChunk) - lane));  // fusion.py:182
       const float wv = kProd ? w * 0.693147180559945f : w;
       shead[__popc(vmask & (upto >> 1))] = make_int4(r_cur * (int)p.stride, __float_as_int(wv), lane * c, 0);
     }
