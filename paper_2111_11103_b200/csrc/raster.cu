@@ -759,6 +759,7 @@ struct Outs {
 
 // Record geometry views.  RecGeom is 16 doubles: xs[3] ys[3] zs[3] dX[3] dY[3] area2.
 enum { kFXs = 0, kFYs = 3, kFZs = 6, kFDX = 9, kFDY = 12, kFA2 = 15, kFields = 16 };
+constexpr int kPC = 4;        // covering slots kept per pixel by the pair phase (more: selection by key)
 constexpr int kFS = kTP + 1;  // field stride of the staged (SoA) tile records, +1 double: fields on distinct banks
 
 struct AosRec {  // one RecGeom (global memory or AoS shared memory)
@@ -997,7 +998,7 @@ __device__ __forceinline__ void emit_pixel(const tfb_scene &sc, const Outs &o, i
 struct TileSmem {
   double g[kStaged * kFS];          // staged records, field-major (SoA): g[q * kFS + j]
   double pe[3][kTP];                // edge values of a pixel's (single) covering pair
-  int32_t pc[2][kTP];               // per pixel: slots of its first two covering pairs (arrival order)
+  int32_t pc[kPC][kTP];             // per pixel: slots of its first kPC covering pairs (arrival order)
   uint32_t flags[kTP];              // RecMeta::flags
   int32_t off[kTP];                 // offsets[t] of the record's triangle (n_x < 2^31)
   Cam cam;
@@ -1016,9 +1017,9 @@ struct TileSmem {
 //     pair gets its own thread (one binary search per thread-run), so float64
 //     lanes are not wasted on pixels outside a small triangle's bbox.  A
 //     covering pair bumps the pixel's candidate count (32-bit smem atomic)
-//     and the first two covering slots are kept.
-//  3. One thread per pixel: one or two candidates are folded directly in
-//     ascending key order; with more, the pixel repeatedly selects the
+//     and the first kPC = 4 covering slots are kept.
+//  3. One thread per pixel: up to four candidates are sorted by key and
+//     folded directly in ascending order; with more, the pixel repeatedly selects the
 //     smallest covering key above the last folded one — the reference's
 //     ascending sequential fold (rasterizer.py:108, 170-171) without sorting.
 //  Larger or overflowed tiles are handed to k_raster_big.
@@ -1143,7 +1144,7 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
           (e2 > 0.0 || (e2 == 0.0 && (fl & 4u)))) {
         const int pix = pyl * kTW + pxl;
         const uint32_t idx = atomicAdd(pcnt + pix, 1u);
-        if (idx < 2u) pc[idx][pix] = j;
+        if (idx < (uint32_t)kPC) pc[idx][pix] = j;
         if (idx == 0u) {  // used only when this is the pixel's sole candidate
           pe[0][pix] = e0;
           pe[1][pix] = e1;
@@ -1202,6 +1203,28 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
     }
     fd.step(SoaRec{sg, j0}, sflags[j0], px, py, j0);
     fd.step(SoaRec{sg, j1}, sflags[j1], px, py, j1);
+  } else if (cnt > 2u && cnt <= (uint32_t)kPC) {  // 3 or 4 slots known: sort by key (a 4-input network) and fold
+    int j0 = pc[0][tid], j1 = pc[1][tid], j2 = pc[2][tid], j3 = cnt > 3u ? pc[3][tid] : 0;
+    uint32_t k0 = skey[j0], k1 = skey[j1], k2 = skey[j2], k3 = cnt > 3u ? skey[j3] : 0xffffffffu;
+    auto cx = [](uint32_t &ka, int &ja, uint32_t &kb, int &jb) {
+      if (kb < ka) {
+        const uint32_t tk = ka;
+        ka = kb;
+        kb = tk;
+        const int tj = ja;
+        ja = jb;
+        jb = tj;
+      }
+    };
+    cx(k0, j0, k1, j1);
+    cx(k2, j2, k3, j3);
+    cx(k0, j0, k2, j2);
+    cx(k1, j1, k3, j3);
+    cx(k1, j1, k2, j2);
+    fd.step(SoaRec{sg, j0}, sflags[j0], px, py, j0);
+    fd.step(SoaRec{sg, j1}, sflags[j1], px, py, j1);
+    fd.step(SoaRec{sg, j2}, sflags[j2], px, py, j2);
+    if (cnt > 3u) fd.step(SoaRec{sg, j3}, sflags[j3], px, py, j3);
   } else if (cnt > 2u) {
     int64_t last = -1;  // key of the last folded record
     for (uint32_t k = 0; k < cnt; ++k) {
