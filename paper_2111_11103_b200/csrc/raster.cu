@@ -898,7 +898,11 @@ __device__ __forceinline__ void write_pixel(const tfb_scene &sc, const Cam &cam,
                                             int64_t offset) {
   const int64_t pix = (int64_t)f * W * H + (int64_t)(py_i * W + px_i);
   int32_t row = -1, texel = 0;
-  if (fd.win >= 0) {
+  if (fd.win >= 0 && (flags >> 16) == 1u && !o.depth) {
+    // steps = 1 and no float planes: the texel is 0 whatever the barycentrics
+    // (see the sole-candidate path in k_raster)
+    row = (int32_t)offset;
+  } else if (fd.win >= 0) {
     const double wsum = __dadd_rn(__dadd_rn(fd.w0, fd.w1), fd.w2);
     double b0, b1, b2;
     if (flags & 16u) {  // clipped: barycentric rows of the fan vertices (rasterizer.py:62-82, 119-122)
