@@ -759,7 +759,8 @@ struct Outs {
 
 // Record geometry views.  RecGeom is 16 doubles: xs[3] ys[3] zs[3] dX[3] dY[3] area2.
 enum { kFXs = 0, kFYs = 3, kFZs = 6, kFDX = 9, kFDY = 12, kFA2 = 15, kFields = 16 };
-constexpr int kPC = 4;        // covering slots kept per pixel by the pair phase (more: selection by key)
+constexpr int kPC = 8;        // covering slots kept per pixel by the pair phase (more: selection by key)
+static_assert(kPC >= 4, "the fold's 4-input network reads four kept slots");
 constexpr int kFS = kTP + 1;  // field stride of the staged (SoA) tile records, +1 double: fields on distinct banks
 
 struct AosRec {  // one RecGeom (global memory or AoS shared memory)
@@ -1021,9 +1022,9 @@ struct TileSmem {
 //     pair gets its own thread (one binary search per thread-run), so float64
 //     lanes are not wasted on pixels outside a small triangle's bbox.  A
 //     covering pair bumps the pixel's candidate count (32-bit smem atomic)
-//     and the first kPC = 4 covering slots are kept.
-//  3. One thread per pixel: up to four candidates are sorted by key and
-//     folded directly in ascending order; with more, the pixel repeatedly selects the
+//     and the first kPC = 8 covering slots are kept.
+//  3. One thread per pixel: up to eight candidates are ordered by key among
+//     the kept slots and folded; with more, the pixel repeatedly selects the
 //     smallest covering key above the last folded one — the reference's
 //     ascending sequential fold (rasterizer.py:108, 170-171) without sorting.
 //  Larger or overflowed tiles are handed to k_raster_big.
@@ -1207,7 +1208,7 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
     }
     fd.step(SoaRec{sg, j0}, sflags[j0], px, py, j0);
     fd.step(SoaRec{sg, j1}, sflags[j1], px, py, j1);
-  } else if (cnt > 2u && cnt <= (uint32_t)kPC) {  // 3 or 4 slots known: sort by key (a 4-input network) and fold
+  } else if (cnt > 2u && cnt <= 4u) {  // 3 or 4 slots known: sort by key (a 4-input network) and fold
     int j0 = pc[0][tid], j1 = pc[1][tid], j2 = pc[2][tid], j3 = cnt > 3u ? pc[3][tid] : 0;
     uint32_t k0 = skey[j0], k1 = skey[j1], k2 = skey[j2], k3 = cnt > 3u ? skey[j3] : 0xffffffffu;
     auto cx = [](uint32_t &ka, int &ja, uint32_t &kb, int &jb) {
@@ -1229,7 +1230,23 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
     fd.step(SoaRec{sg, j1}, sflags[j1], px, py, j1);
     fd.step(SoaRec{sg, j2}, sflags[j2], px, py, j2);
     if (cnt > 3u) fd.step(SoaRec{sg, j3}, sflags[j3], px, py, j3);
-  } else if (cnt > 2u) {
+  } else if (cnt > 4u && cnt <= (uint32_t)kPC) {  // 5..8 slots known: ascending selection among them
+    int64_t last = -1;
+    for (uint32_t k = 0; k < cnt; ++k) {
+      uint32_t bk = 0xffffffffu;
+      int bj = 0;
+      for (uint32_t i = 0; i < cnt; ++i) {
+        const int ji = pc[i][tid];
+        const uint32_t ki = skey[ji];
+        if ((int64_t)ki > last && ki < bk) {
+          bk = ki;
+          bj = ji;
+        }
+      }
+      fd.step(SoaRec{sg, bj}, sflags[bj], px, py, bj);
+      last = bk;
+    }
+  } else if (cnt > (uint32_t)kPC) {  // deeper stacks: repeated smallest-key selection over the tile's records
     int64_t last = -1;  // key of the last folded record
     for (uint32_t k = 0; k < cnt; ++k) {
       unsigned long long best = ~0ull;
