@@ -380,3 +380,29 @@ def test_raster_large_triangles_few_survivors():
         np.testing.assert_array_equal(ids.triangle, ref["triangle"])
         np.testing.assert_array_equal(ids.texel, ref["texel"])
         assert (ids.triangle >= 0).mean() > 0.5
+
+
+@pytest.mark.parametrize("layers", [2, 3, 4, 5, 8, 9, 14])
+def test_raster_stacked_layers_vs_oracle(layers):
+    """`layers` overlapping triangles in front of each other (shuffled order,
+    some nearly coplanar), so pixels hold 2..14 covering records: the 2-slot,
+    4-input-network, kept-slot selection and full-scan fold paths; ids, depth,
+    u, v bit-exact with the oracle."""
+    rng = np.random.default_rng(layers)
+    base = np.array([[-1.0, -1.0, 0.0], [1.2, -0.9, 0.0], [0.1, 1.1, 0.0]])
+    vs, ts = [], []
+    for k in rng.permutation(layers):
+        z = 3.0 + 0.05 * k + (1e-10 if k % 3 == 0 else 0.0)
+        tri = base * (1.0 + 0.03 * k) + [0.02 * k, -0.01 * k, z]
+        vs.append(tri)
+        ts.append(np.arange(3) + 3 * len(ts))
+    mesh = Mesh.from_arrays(np.concatenate(vs), np.array(ts, dtype=np.int32))
+    layout = uniform_layout(mesh, 3)
+    fr = CameraFrame(0, Intrinsics(60.0, 60.0, 39.5, 29.5, 80, 60), np.eye(3), np.zeros(3))
+    ids = rasterize(mesh, layout, fr)
+    ref = O.rasterize(mesh.vertices, mesh.triangles, layout.steps, layout.origins, pack_camera(fr), 80, 60)
+    for key, plane in (("triangle", ids.triangle), ("texel", ids.texel), ("depth", ids.depth)):
+        np.testing.assert_array_equal(plane, ref[key], err_msg=key)
+    cov = ids.triangle >= 0
+    np.testing.assert_array_equal(ids.u[cov], ref["u"][cov])
+    np.testing.assert_array_equal(ids.v[cov], ref["v"][cov])
