@@ -95,6 +95,57 @@ class MeshAnnotation:
         tex._h_accum = tex._h_counts = tex._h_rows = tex._h_unobs = None
         self.frames_added = 0
 
+    # -- checkpoint / resume (the accumulator is a sum monoid) --------------
+    CHECKPOINT_VERSION = 1
+
+    def save_checkpoint(self, path):
+        """Write the un-finalized accumulation state (accumulator rows, counts,
+        frames added and what they must match) to ``path`` (.npz).  A job
+        resumed from it with load_checkpoint() and fed the remaining frames
+        ends with the same fused result (sums, up to float rounding order)."""
+        tex = self.texture
+        if tex.finalized:
+            raise RuntimeError("texture is already finalized; checkpoint before labels()/render()")
+        tex._push_host()
+        torch.cuda.synchronize(self.device)
+        np.savez(path, version=np.int64(self.CHECKPOINT_VERSION),
+                 accum=tex._accum[:, : self.num_classes].cpu().numpy(), counts=tex._counts.cpu().numpy(),
+                 frames_added=np.int64(self.frames_added), num_classes=np.int64(self.num_classes),
+                 aggregator=np.array(tex.aggregator), weight_mode=np.array(self.weight_mode),
+                 alpha=np.float64(self.alpha or 0.0), total_texels=np.int64(tex.total_texels),
+                 accum_dtype=np.array(str(tex.dtype).replace("torch.", "")),
+                 steps=self.layout.steps, offsets=self.layout.offsets)
+
+    def load_checkpoint(self, path):
+        """Resume from save_checkpoint(): the accumulator and counts are
+        replaced by the saved ones.  The checkpoint must come from the same
+        layout, class count, aggregator and weight mode (DataError otherwise);
+        per-rank checkpoints of a sharded job can be loaded on their ranks and
+        reduced as usual."""
+        from .errors import DataError
+
+        tex = self.texture
+        with np.load(path, allow_pickle=False) as z:
+            if int(z["version"]) != self.CHECKPOINT_VERSION:
+                raise DataError("checkpoint version %d is not supported" % int(z["version"]))
+            want = {"num_classes": self.num_classes, "total_texels": tex.total_texels}
+            for key, val in want.items():
+                if int(z[key]) != int(val):
+                    raise DataError("checkpoint %s %d does not match %d" % (key, int(z[key]), int(val)))
+            if str(z["aggregator"]) != tex.aggregator or str(z["weight_mode"]) != self.weight_mode or \
+                    float(z["alpha"]) != float(self.alpha or 0.0):
+                raise DataError("checkpoint aggregator / weight mode (%s, %s) do not match (%s, %s)" % (
+                    str(z["aggregator"]), str(z["weight_mode"]), tex.aggregator, self.weight_mode))
+            if not (np.array_equal(z["steps"], self.layout.steps) and np.array_equal(z["offsets"], self.layout.offsets)):
+                raise DataError("checkpoint texel layout does not match")
+            accum, counts = z["accum"], z["counts"]
+            if accum.shape != (tex.total_texels, self.num_classes) or counts.shape != (tex.total_texels,):
+                raise DataError("checkpoint arrays have the wrong shape")
+            self.reset()
+            tex._accum[:, : self.num_classes].copy_(torch.as_tensor(accum).to(self.device, tex.dtype))
+            tex._counts.copy_(torch.as_tensor(counts).to(self.device, tex._counts.dtype))
+            self.frames_added = int(z["frames_added"])
+
     # -- accumulation ------------------------------------------------------------------
     def _probs_batch(self, probs, b, H, W):
         """Per-frame device pointers for b frames.  Contiguous float32 device
