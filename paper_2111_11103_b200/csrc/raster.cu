@@ -1085,23 +1085,40 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
     sbox[tid] = (uint32_t)bx0 | ((uint32_t)by0 << 8) | (bw << 16) | (bh << 24);
     area = bw * bh;
   }
-  uint32_t incl = area;
+  uint32_t total = 0;
+  if (n <= 32u) {
+    // all records sit in warp 0: it scans their areas alone, one barrier publishes
+    if (warp == 0) {
+      uint32_t incl = area;
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += v;
-  }
-  if (lane == 31) wtot[warp] = incl;
-  __syncthreads();
-  uint32_t wbase = 0, total = 0;
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+      }
+      spre[tid] = incl - area;
+      if (lane == 31) wtot[0] = incl;
+    }
+    __syncthreads();
+    total = wtot[0];
+  } else {
+    uint32_t incl = area;
 #pragma unroll
-  for (int i = 0; i < kTP / 32; ++i) {
-    const uint32_t v = wtot[i];
-    wbase += i < warp ? v : 0u;
-    total += v;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    if (lane == 31) wtot[warp] = incl;
+    __syncthreads();
+    uint32_t wbase = 0;
+#pragma unroll
+    for (int i = 0; i < kTP / 32; ++i) {
+      const uint32_t v = wtot[i];
+      wbase += i < warp ? v : 0u;
+      total += v;
+    }
+    spre[tid] = wbase + incl - area;
+    __syncthreads();
   }
-  spre[tid] = wbase + incl - area;
-  __syncthreads();
 
   if (tid == 0) RSTAT(32 + min(total / 256u, 15u));
   // pair-parallel edge tests: thread handles pairs [p0, p1)
