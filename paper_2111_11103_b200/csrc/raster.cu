@@ -546,13 +546,18 @@ __global__ void __launch_bounds__(kThreads) k_ccands(tfb_scene sc, const double 
     if (cl) {
       tr = __ldg(reinterpret_cast<const int4 *>(cl->tri[slot]));
       loc = __ldg(cl->local + slot);
+      // the vertex ids are read unconditionally (all 128 slots exist), in flight
+      // with the count; only the first nverts are transformed
+      int32_t vid[kCV / kCluster];
+#pragma unroll
+      for (int k = 0; k < kCV / kCluster; ++k) vid[k] = __ldg(cl->verts + slot + k * kCluster);
       const int nv = __ldg(&cl->nverts);
 #pragma unroll
       for (int k = 0; k < kCV / kCluster; ++k) {
         const int j = slot + k * kCluster;
         if (j < nv) {
           double P[3];
-          xform(cam, sc.vertices + 3 * (int64_t)__ldg(cl->verts + j), P);
+          xform(cam, sc.vertices + 3 * (int64_t)vid[k], P);
           scode[sub][j] = (uint8_t)vertex_code(cam, P, W, H);
         }
       }
