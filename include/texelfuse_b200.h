@@ -103,8 +103,8 @@ size_t tfb_raster_workspace_bytes(int64_t num_vertices, int64_t num_triangles, i
  * with the 1e-9 tie rule, top-left-style edge ownership, near-plane clip +
  * fan, perspective-correct (u, v) → texel id.
  * Outputs (device, nframes*H*W each): rows_out (required).  Optional (NULL
- * to skip): tri_out / texel_out (IdImage.triangle / .texel), depth_out / u_out
- * / v_out (IdImage.depth / .u / .v).  texel_hits (nframes*total_texels u32,
+ * to skip), each group all-or-none: tri_out + texel_out (IdImage.triangle /
+ * .texel), depth_out + u_out + v_out (IdImage.depth / .u / .v).  texel_hits (nframes*total_texels u32,
  * zeroed by the caller, may be NULL) receives per-frame per-row pixel counts
  * (the np.unique count of fusion.py:135-136). */
 int tfb_rasterize(const tfb_scene *scene, const double *cams, int nframes, int width, int height,

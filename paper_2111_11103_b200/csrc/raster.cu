@@ -1426,6 +1426,10 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
   TFB_REQUIRE(width > 0 && height > 0 && width < 32768 && height < 32768, TFB_ERR_DATA,
               "tfb_rasterize: image size %dx%d outside 1..32767", width, height);
   TFB_REQUIRE(nframes >= 0, TFB_ERR_DATA, "tfb_rasterize: negative frame count");
+  TFB_REQUIRE((tri_out == nullptr) == (texel_out == nullptr), TFB_ERR_VALUE,
+              "tfb_rasterize: tri_out and texel_out are given together");
+  TFB_REQUIRE((depth_out == nullptr) == (u_out == nullptr) && (u_out == nullptr) == (v_out == nullptr), TFB_ERR_VALUE,
+              "tfb_rasterize: depth_out, u_out and v_out are given together");
   TFB_REQUIRE(scene->num_triangles < (1LL << 30), TFB_ERR_CAPACITY,
               "tfb_rasterize: %lld triangles exceed the 2^30 record-key range", (long long)scene->num_triangles);
   TFB_REQUIRE(scene->total_texels < (1LL << 31), TFB_ERR_CAPACITY,

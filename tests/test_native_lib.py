@@ -61,6 +61,15 @@ def test_argument_errors_map_to_reference_exceptions():
     rc = lib.tfb_fuse(ctypes.c_void_p(16), 4, 1, ctypes.c_void_p(16), 3, None, None, 10, 0, 1, 0.0,
                       ctypes.c_void_p(16), 0, 4, ctypes.c_void_p(16), None, None)
     assert rc == N.TFB_ERR_DATA and "hit counts" in N.last_error()
+    # optional output planes come in groups (checked before any device work)
+    scene = N.TfbScene(None, None, None, None, None, 3, 1, 1, None, 0)
+    dev = ctypes.c_void_p(256)
+    rc = lib.tfb_rasterize(ctypes.byref(scene), dev, 1, 64, 64, dev, 1 << 30, 0, dev, None, dev, None, None, None,
+                           None, None)
+    assert rc == N.TFB_ERR_VALUE and "together" in N.last_error()
+    rc = lib.tfb_rasterize(ctypes.byref(scene), dev, 1, 64, 64, dev, 1 << 30, 0, dev, None, None, None, dev, dev,
+                           None, None)
+    assert rc == N.TFB_ERR_VALUE and "together" in N.last_error()
 
 
 def test_product_path_fails_loudly_without_cuda():
