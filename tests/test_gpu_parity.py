@@ -406,3 +406,22 @@ def test_raster_stacked_layers_vs_oracle(layers):
     cov = ids.triangle >= 0
     np.testing.assert_array_equal(ids.u[cov], ref["u"][cov])
     np.testing.assert_array_equal(ids.v[cov], ref["v"][cov])
+
+
+def test_raster_cfg5_scale_frame_vs_oracle():
+    """BASELINE cfg5 scale: the 5M-triangle room at 1920x1080 (ids of one
+    frame bit-exact with the C oracle; clusters, large bins, every kernel at
+    full size)."""
+    v, t = make_room((6.0, 5.0, 3.0), 646)
+    mesh = Mesh.from_arrays(v, t)
+    layout = uniform_layout(mesh, 1)
+    intr = Intrinsics(1728.0, 1728.0, 959.5, 539.5, 1920, 1080)
+    fr = random_room_trajectory(1, intr, seed=17)[0]
+    ann = MeshAnnotation(mesh, layout, num_classes=4, max_batch=1)
+    cams = ann.scene.cams_tensor([fr])
+    rows = torch.empty((1, 1920 * 1080), dtype=torch.int32, device=ann.device)
+    ann.scene.rasterize(cams, 1920, 1080, rows)
+    ref = O.rasterize(mesh.vertices, mesh.triangles, layout.steps, layout.origins, pack_camera(fr), 1920, 1080,
+                      want_uv=False)
+    np.testing.assert_array_equal(rows[0].cpu().numpy(), O.pixel_rows(layout.offsets, ref["triangle"],
+                                                                       ref["texel"]).ravel())
