@@ -135,7 +135,7 @@ def test_fuse_fast_many_frames_and_launch_split():
 
 
 def test_fuse_fast_and_general_agree_on_long_runs():
-    """Whole chunks on one texel (pieces cut every 4 pixels for the product)."""
+    """Whole chunks on one texel (product pieces of 5 pixels in the fast kernel, 4 in the general one)."""
     rng = np.random.default_rng(9)
     hw, c = 32 * 64, 40
     rows = np.repeat(np.arange(hw // 256, dtype=np.int32), 256)[None, :]
@@ -147,3 +147,21 @@ def test_fuse_fast_and_general_agree_on_long_runs():
     np.testing.assert_array_equal(cb, cref)
     _check(a, ref, ref)
     _check(b, ref, ref)
+
+
+def test_fuse_fast_products_at_the_clip_floor():
+    """Long runs whose values sit at (and just above) the clip floor 1e-7: a
+    5-pixel product piece reaches 1e-35, still a normal float32, so no clip
+    redo and no underflow; plus values just below the floor (clip redo)."""
+    rng = np.random.default_rng(11)
+    hw, c = 32 * 40, 8
+    rows = np.repeat(np.arange(hw // 160, dtype=np.int32), 160)[None, :]
+    probs = np.full((1, hw, c), 1e-7, dtype=np.float32)
+    probs[0, :, 0] = 1.0 - 7e-7
+    probs[0, ::7, 3] = np.float32(1.0000001e-7)
+    probs[0, 5::11, 5] = np.float32(0.99e-7)  # below the floor: np.clip raises it
+    for agg in ("mul", "sum"):
+        got, cnt, _ = _run(rows, probs, hw // 160, agg, "images_iid", 0.0, True)
+        ref, cref = _oracle(rows, probs, hw // 160, agg, "images_iid", 0.0)
+        np.testing.assert_array_equal(cnt, cref)
+        _check(got, ref, _scale(rows, probs, hw // 160, agg, "images_iid", 0.0))
