@@ -435,8 +435,9 @@ def _gt(mesh, frame, labels_fn=None, face_labels=None):
     return out
 
 
-def _orbit_fusion(mesh, c, frames, model, gamma, agg, wmode, gt_fn):
-    layout = build_texel_layout(mesh, compute_worst_case_areas(mesh, frames), gamma)
+def _orbit_fusion(mesh, c, frames, model, gamma, agg, wmode, gt_fn, subset=None):
+    used = list(range(len(frames))) if subset is None else list(subset)
+    layout = build_texel_layout(mesh, compute_worst_case_areas(mesh, [frames[k] for k in used]), gamma)
     ids_all, gts, probs = [], [], []
     for fr in frames:
         ids_all.append(rasterize(mesh, layout, fr))
@@ -444,8 +445,8 @@ def _orbit_fusion(mesh, c, frames, model, gamma, agg, wmode, gt_fn):
         gts.append(g)
         probs.append(corrupt(g, model, c, fr.frame_id))
     tex = init_texture(layout, c, agg)
-    for ids, p in zip(ids_all, probs):
-        accumulate_frame(tex, ids, p, compute_pixel_weights(ids, wmode))
+    for k in used:
+        accumulate_frame(tex, ids_all[k], probs[k], compute_pixel_weights(ids_all[k], wmode))
     finalize(tex)
     labels = texel_argmax(tex)
     bc = bn = fc = fn = 0
@@ -468,6 +469,28 @@ def test_criterion_05_end_to_end_fusion_gain():
     base, fused = _orbit_fusion(cube, 6, frames, model, 0.2, "mul", "images_iid",
                                 lambda fr: _gt(cube, fr, face_labels=face))
     assert abs(base - 0.70) <= 0.01 and fused >= 0.99, (base, fused)
+
+
+def test_criterion_06_frame_fraction_monotonicity():
+    # test_acceptance.py:273-293: mean fused accuracy over 5 noise seeds is
+    # non-decreasing in the fraction of frames fused (0.5 pt slack) and
+    # saturated by half of the frames
+    from paper_2111_11103_b200.renderback import select_frames
+
+    cube = make_cube()
+    face = np.repeat(np.arange(6), 2).astype(np.int32)
+    intr = Intrinsics(fx=64, fy=64, cx=32, cy=24, width=64, height=48)
+    frames = make_orbit_trajectory((0, 0, 0), 3.0, 20, intr)
+    fractions = (0.05, 0.1, 0.2, 0.5, 1.0)
+    curves = []
+    for seed in range(5):
+        model = NoiseModel(kind="flip", epsilon=0.35, q=0.7, seed=100 + seed)
+        curves.append([_orbit_fusion(cube, 6, frames, model, 0.2, "mul", "images_iid",
+                                     lambda fr: _gt(cube, fr, face_labels=face),
+                                     subset=select_frames(len(frames), frac))[1] for frac in fractions])
+    mean = np.mean(curves, axis=0)
+    assert (np.diff(mean) >= -0.005).all(), mean
+    assert abs(mean[-1] - mean[-2]) <= 0.005, mean
 
 
 def test_criterion_07_weighting_separation():
@@ -671,3 +694,30 @@ def test_session_matches_library_pipeline(scene_dir):
         ids = rasterize(mesh, layout, fr)
         want = render_labels(lab, layout, ids, fallback=scene_dir[1][fr.frame_id].argmax(axis=2).astype(np.int32))
         np.testing.assert_array_equal(img, want)
+
+
+def test_criterion_11_session_matches_cli(scene_dir, tmp_path):
+    # bindings/tests/test_session.py:182-212: session-driven fusion equals the
+    # fuse command (texture rows and label images), frames in ascending order
+    from paper_2111_11103_b200.cli import main as cli_main
+    from paper_2111_11103_b200.formats import read_texture, write_probability_image
+    from paper_2111_11103_b200.renderback import read_label_png
+
+    pred = tmp_path / "probs"
+    pred.mkdir()
+    for fid, p in scene_dir[1].items():
+        write_probability_image(pred / ("%d.smpb" % fid), p)
+    out = tmp_path / "cli"
+    code = cli_main(["fuse", "mesh=%s" % (scene_dir[0] / "mesh.ply"), "trajectory=%s" % (scene_dir[0] / "trajectory.txt"),
+                     "predictions=%s" % pred, "classes=6", "gamma=0.2", "aggregator=mul", "weights=images_iid",
+                     "deterministic=true", "output=%s" % out])
+    assert code == 0
+    ids = [f.frame_id for f in tf.load_trajectory(scene_dir[0] / "trajectory.txt")]
+    ses = _fresh(scene_dir)
+    for fid in ids:
+        tf.add_frame(ses, fid, scene_dir[1][fid])
+    labels, rows = tf.finalize_and_render(ses, ids)
+    cli_rows = read_texture(out / "texture.smtx")[1]
+    np.testing.assert_array_equal(rows, cli_rows)
+    for fid, img in zip(ids, labels):
+        np.testing.assert_array_equal(img, read_label_png(out / "labels" / ("%d.png" % fid)))
