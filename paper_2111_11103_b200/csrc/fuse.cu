@@ -44,6 +44,9 @@ namespace {
 #define TFB_FUSE_NS 2
 #endif
 constexpr int kWarps = TFB_FUSE_WARPS;  // warps per CTA (independent pipelines)
+#ifndef TFB_FUSE_CSPEC
+#define TFB_FUSE_CSPEC 1
+#endif
 #ifndef TFB_PIECE
 #define TFB_PIECE 5  // k_fuse_fast product pieces: 5 clipped values >= 1e-7 multiply to >= 1e-35, a normal float
 #endif
@@ -569,12 +572,14 @@ __device__ __forceinline__ void sts4(float *p, float4 v, int nv) {
   if (nv > 3) p[3] = v.w;
 }
 
-template <int AGG, bool VEC>
+template <int AGG, bool VEC, int CC>
 __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant__ FuseParams p) {
   constexpr bool kProd = AGG == TFB_AGG_MUL;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c = p.c, NS = p.NS;
+  // CC != 0: the class count is a compile-time constant (address steps and the
+  // quad geometry fold into immediates); 0: read from the parameters
+  const int c = CC ? CC : p.c, NS = p.NS;
   const Geo geo = geo_of(c);
   const FastSmem L = fast_layout(c, NS);
   unsigned char *ws = smem + (size_t)warp * L.total;
@@ -880,10 +885,26 @@ int launch_fuse(const FuseParams &p, cudaStream_t st) {
   return launch_persistent(k_fuse<AccT, AGG, EQW>, lc, warp_layout(p.c, p.NS, (int)sizeof(AccT)).total, p, st);
 }
 
-template <int AGG, bool VEC>
+template <int AGG, bool VEC, int CC = 0>
 int launch_fuse_fast(const FuseParams &p, cudaStream_t st) {
   static LaunchCache lc;
-  return launch_persistent(k_fuse_fast<AGG, VEC>, lc, fast_layout(p.c, p.NS).total, p, st);
+  return launch_persistent(k_fuse_fast<AGG, VEC, CC>, lc, fast_layout(p.c, p.NS).total, p, st);
+}
+
+// Common class counts get their own instantiation (NYU40, ScanNet 20,
+// Cityscapes 19, NYU13): 3-4 % faster than the runtime-c kernel at c = 40.
+template <int AGG>
+int launch_fuse_fast_c(const FuseParams &p, bool vec, cudaStream_t st) {
+#if TFB_FUSE_CSPEC
+  switch (p.c) {
+    case 40: return launch_fuse_fast<AGG, true, 40>(p, st);
+    case 20: return launch_fuse_fast<AGG, true, 20>(p, st);
+    case 19: return launch_fuse_fast<AGG, false, 19>(p, st);
+    case 13: return launch_fuse_fast<AGG, false, 13>(p, st);
+    default: break;
+  }
+#endif
+  return vec ? launch_fuse_fast<AGG, true>(p, st) : launch_fuse_fast<AGG, false>(p, st);
 }
 
 template <typename AccT, int AGG>
@@ -1025,13 +1046,13 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
     if (fast) {
       switch (aggregator) {
         case TFB_AGG_SUM:
-          rc = vec ? launch_fuse_fast<TFB_AGG_SUM, true>(p, st) : launch_fuse_fast<TFB_AGG_SUM, false>(p, st);
+          rc = launch_fuse_fast_c<TFB_AGG_SUM>(p, vec, st);
           break;
         case TFB_AGG_MAXSUM:
-          rc = vec ? launch_fuse_fast<TFB_AGG_MAXSUM, true>(p, st) : launch_fuse_fast<TFB_AGG_MAXSUM, false>(p, st);
+          rc = launch_fuse_fast_c<TFB_AGG_MAXSUM>(p, vec, st);
           break;
         default:
-          rc = vec ? launch_fuse_fast<TFB_AGG_MUL, true>(p, st) : launch_fuse_fast<TFB_AGG_MUL, false>(p, st);
+          rc = launch_fuse_fast_c<TFB_AGG_MUL>(p, vec, st);
           break;
       }
     } else if (accum_is_f64) {
