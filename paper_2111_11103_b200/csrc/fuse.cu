@@ -247,6 +247,7 @@ template <typename AccT, int AGG, bool EQW>
 __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ FuseParams p) {
   // product rule in float32 with weights constant per run: fold w*log(prod p)
   constexpr bool kProd = (AGG == TFB_AGG_MUL) && EQW && sizeof(AccT) == 4;
+  constexpr bool kProd64 = (AGG == TFB_AGG_MUL) && EQW && sizeof(AccT) == 8;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = p.c, NS = p.NS;
@@ -319,7 +320,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
     float *st = stages + (size_t)s * L.stage_floats;
 
     // pieces: runs of equal rows, split at group starts (and every 4 pixels for
-    // the product rule, so a piece's product of clipped probabilities stays normal)
+    // the float32 product rule, so a piece's product of clipped probabilities
+    // stays normal; a float64 product of up to 32 values >= 1e-7 cannot underflow)
     const AccT w = weight_from<AccT>(p, ws_cur, r_cur);
     const int32_t prev = __shfl_up_sync(0xffffffffu, r_cur, 1);
     const bool chg = lane == 0 || prev != r_cur || grp_start;
@@ -379,6 +381,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
         const float pad = AGG == TFB_AGG_MUL ? 1.0f : 0.0f;
         AccT a0 = 0, a1 = 0, a2 = 0, a3 = 0;
         float2 m01 = make_float2(1.f, 1.f), m23 = make_float2(1.f, 1.f);
+        double2 d01 = make_double2(1.0, 1.0), d23 = make_double2(1.0, 1.0);  // float64 products
         int32_t doff = -1;
         AccT wrun = 0;
         auto flush = [&]() {
@@ -405,7 +408,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
                          "f"(b3));
           } else {
             double *dst = reinterpret_cast<double *>(p.accum) + doff + k0;
-            const double v[4] = {(double)a0, (double)a1, (double)a2, (double)a3};
+            double v[4] = {(double)a0, (double)a1, (double)a2, (double)a3};
+            if (kProd64) {  // w * log(prod of the piece's clipped values) = sum of w * log(p)
+              const double wv = (double)wrun;
+              v[0] = wv * log(d01.x);
+              v[1] = wv * log(d01.y);
+              v[2] = wv * log(d23.x);
+              v[3] = wv * log(d23.y);
+            }
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               if (k0 + k < c) atomicAdd(dst + k, v[k]);
@@ -430,8 +440,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
             a0 = a1 = a2 = a3 = (AccT)0;
             m01 = make_float2(1.f, 1.f);
             m23 = make_float2(1.f, 1.f);
+            d01 = make_double2(1.0, 1.0);
+            d23 = make_double2(1.0, 1.0);
           }
-          if (kProd) {
+          if (kProd64) {
+            // float64 parity mode, product rule with one weight per piece: the
+            // clipped values multiply in double, one log per piece and class
+            d01.x *= np_clip((double)v0, kMulClamp, 1.0);
+            d01.y *= np_clip((double)v1, kMulClamp, 1.0);
+            d23.x *= np_clip((double)v2, kMulClamp, 1.0);
+            d23.y *= np_clip((double)v3, kMulClamp, 1.0);
+          } else if (kProd) {
             m01 = mul2(m01, make_float2(clip_mul(v0), clip_mul(v1)));
             m23 = mul2(m23, make_float2(clip_mul(v2), clip_mul(v3)));
           } else if (sizeof(AccT) == 4) {

@@ -28,6 +28,8 @@ CONFIGS = {
     "cfg5": (646, 1920, 1080, 1728.0, 19, 500, "mul", 1, 32, 4),  # one GPU's share of the 8-GPU job
     # cfg2 with furniture (SURVEY §7 hard part 9): 10 boxes, +1.4 % triangles, occlusion / overdraw
     "cfg2furn": (158, 640, 480, 577.87, 40, 2000, "mul", 1, 256, 8),
+    # cfg2 with the float64 accumulator (the library / session API default, the reference's precision)
+    "cfg2f64": (158, 640, 480, 577.87, 40, 2000, "mul", 1, 256, 8),
 }
 
 
@@ -42,7 +44,7 @@ def run(name):
     maps = softmax_maps(pool, H, W, c, seed=0, device="cuda")
     probs = [maps[i % pool] for i in range(frames)]
     ann = MeshAnnotation(mesh, layout, num_classes=c, aggregator=agg, weight_mode="images_iid",
-                         accum_dtype="float32", max_batch=batch)
+                         accum_dtype="float64" if name.endswith("f64") else "float32", max_batch=batch)
     cams_dev = ann.scene.cams_tensor(cams)
     setup_s = time.time() - t0
 
@@ -70,7 +72,8 @@ def run(name):
         "frames_per_s": frames / (ms / 1000.0), "ms_per_job": ms,
         "raster_us_per_frame": 1000.0 * raster / frames, "fuse_us_per_frame": 1000.0 * fuse / frames,
         "fuse_gbs": b_frame * frames / (fuse / 1000.0) / 1e9, "setup_s": round(setup_s, 1),
-        "fuse_kernel": "k_fuse_fast<VEC>" if c % 4 == 0 else "k_fuse_fast<scalar quads>",
+        "fuse_kernel": ("k_fuse<double> (general)" if name.endswith("f64") else
+                        "k_fuse_fast<VEC>" if c % 4 == 0 else "k_fuse_fast<scalar quads>"),
     }), flush=True)
     del ann, maps, probs
     torch.cuda.empty_cache()
