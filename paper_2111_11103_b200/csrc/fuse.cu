@@ -38,7 +38,7 @@ namespace tfb {
 namespace {
 
 #ifndef TFB_FUSE_WARPS
-#define TFB_FUSE_WARPS 4
+#define TFB_FUSE_WARPS 8
 #endif
 #ifndef TFB_FUSE_NS
 #define TFB_FUSE_NS 2
