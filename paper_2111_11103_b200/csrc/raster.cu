@@ -605,9 +605,12 @@ __global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc
                                                     int H, int TX, int ntiles, Work w) {
   const int f = blockIdx.y;
   __shared__ Cam cam;
+  const uint32_t na = w.fcnt[4 * f + 2], ncand = na + w.fcnt[4 * f + 3];
+  // the grid is sized for a generous survivor fraction: blocks past the frame's
+  // survivors leave before staging the camera
+  if ((uint64_t)blockIdx.x * kThreads * kSetupPer >= ncand) return;
   load_cam(cam, cams, f);
   __syncthreads();
-  const uint32_t na = w.fcnt[4 * f + 2], ncand = na + w.fcnt[4 * f + 3];
   const int64_t mc = w.rs / 2;  // survivor list length (m)
   const uint4 *cl = w.cand + (int64_t)f * mc;
   // candidate prologue: triangle, vertex ids, outcodes -> 1 record slot if no vertex is
