@@ -14,63 +14,92 @@ __device__ __forceinline__ bool better(float a, int ia, float b, int ib) {
   return a > b || (a == b && ia < ib);
 }
 
-template <typename AccT>
+// One group of L lanes per texel (L = 8 when c <= 64, so four texels per warp
+// are in flight; L = 32 above).  The exponentials of the product rule are kept
+// in registers between the sum and the rows (up to kKeep per lane).
+constexpr int kKeep = 8;
+
+template <typename AccT, int L>
 __global__ void __launch_bounds__(256) k_finalize(const AccT *__restrict__ accum, int64_t stride,
                                                   const uint32_t *__restrict__ counts, int64_t n_x, int c, int agg,
                                                   float *rows_out, uint8_t *unobs_out, int32_t *labels_out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n_x; i += nwarps) {
-    const AccT *a = accum + i * stride;
-    const bool zero_count = counts[i] == 0u;
+  const int sub = threadIdx.x & (L - 1);
+  const int64_t ngroups = (int64_t)gridDim.x * (blockDim.x / L);
+  const int64_t first = (int64_t)blockIdx.x * (blockDim.x / L) + (threadIdx.x / L);
+  // every lane runs the same number of iterations (shuffles stay converged)
+  const int64_t iters = (n_x + ngroups - 1) / ngroups;
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t i = first + it * ngroups;
+    const bool live = i < n_x;
+    const AccT *a = accum + (live ? i : 0) * stride;
+    const bool zero_count = live ? counts[i] == 0u : true;
     bool unobs;
     double scale, shift = 0.0;
+    double ex[kKeep];
     if (agg == TFB_AGG_MUL) {
       // rows = exp(accum - rowmax) / sum  (fusion.py:196-200)
       double mx = -INFINITY;
-      for (int k = lane; k < c; k += 32) mx = fmax(mx, (double)a[k]);
+      for (int k = sub; k < c; k += L) mx = fmax(mx, (double)a[k]);
 #pragma unroll
-      for (int d = 16; d; d >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d));
-      double s = 0.0;
-      for (int k = lane; k < c; k += 32) s += exp((double)a[k] - mx);
+      for (int d = L / 2; d; d >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d, L));
+      double sacc = 0.0;
 #pragma unroll
-      for (int d = 16; d; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+      for (int kk = 0; kk < kKeep; ++kk) {
+        const int k = sub + kk * L;
+        ex[kk] = k < c ? exp((double)a[k] - mx) : 0.0;
+        sacc += ex[kk];
+      }
+      for (int k = sub + kKeep * L; k < c; k += L) sacc += exp((double)a[k] - mx);
+#pragma unroll
+      for (int d = L / 2; d; d >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, d, L);
       shift = mx;
-      scale = s;
+      scale = sacc;
       unobs = zero_count;
     } else {
       // rows = accum / L1 norm; zero mass counts as unobserved (fusion.py:202-205)
-      double s = 0.0;
-      for (int k = lane; k < c; k += 32) s += (double)a[k];
+      double sacc = 0.0;
+      for (int k = sub; k < c; k += L) sacc += (double)a[k];
 #pragma unroll
-      for (int d = 16; d; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
-      unobs = zero_count || !(s > 0.0);
-      scale = s > 0.0 ? s : 1.0;
+      for (int d = L / 2; d; d >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, d, L);
+      unobs = zero_count || !(sacc > 0.0);
+      scale = sacc > 0.0 ? sacc : 1.0;
     }
     const float uni = (float)(1.0 / c);
     float bv = 0.f;
     int bi = 0x7fffffff;
-    for (int k = lane; k < c; k += 32) {
+    for (int k = sub, kk = 0; k < c; k += L, ++kk) {
       float v;
-      if (unobs) v = uni;
-      else if (agg == TFB_AGG_MUL) v = (float)(exp((double)a[k] - shift) / scale);
-      else v = (float)((double)a[k] / scale);
-      if (rows_out) rows_out[i * c + k] = v;
+      if (unobs) {
+        v = uni;
+      } else if (agg == TFB_AGG_MUL) {
+        double e;
+        if (kk < kKeep) {
+          e = 0.0;
+#pragma unroll
+          for (int q = 0; q < kKeep; ++q) e = q == kk ? ex[q] : e;
+        } else {
+          e = exp((double)a[k] - shift);
+        }
+        v = (float)(e / scale);
+      } else {
+        v = (float)((double)a[k] / scale);
+      }
+      if (rows_out && live) rows_out[i * c + k] = v;
       if (bi == 0x7fffffff || better(v, k, bv, bi)) {
         bv = v;
         bi = k;
       }
     }
 #pragma unroll
-    for (int d = 16; d; d >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, d);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, d);
+    for (int d = L / 2; d; d >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, d, L);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, d, L);
       if (oi != 0x7fffffff && (bi == 0x7fffffff || better(ov, oi, bv, bi))) {
         bv = ov;
         bi = oi;
       }
     }
-    if (lane == 0) {
+    if (sub == 0 && live) {
       if (unobs_out) unobs_out[i] = unobs ? 1 : 0;
       if (labels_out) labels_out[i] = unobs ? -1 : bi;
     }
@@ -122,16 +151,28 @@ extern "C" int tfb_finalize(const void *accum, int accum_is_f64, int64_t accum_s
   TFB_REQUIRE(accum && counts, TFB_ERR_DATA, "tfb_finalize: null accum or counts");
   if (total_texels <= 0) return TFB_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int64_t blocks = (total_texels + 7) / 8;
+  const bool narrow = num_classes <= 64;  // 8 lanes per texel
+  const int64_t per_block = narrow ? 32 : 8;
+  int64_t blocks = (total_texels + per_block - 1) / per_block;
   if (blocks > 148 * 64) blocks = 148 * 64;
-  if (accum_is_f64)
-    k_finalize<double><<<(unsigned)blocks, 256, 0, st>>>(static_cast<const double *>(accum), accum_stride, counts,
-                                                          total_texels, num_classes, aggregator, rows_out,
-                                                          unobserved_out, labels_out);
-  else
-    k_finalize<float><<<(unsigned)blocks, 256, 0, st>>>(static_cast<const float *>(accum), accum_stride, counts,
-                                                         total_texels, num_classes, aggregator, rows_out,
-                                                         unobserved_out, labels_out);
+  const unsigned g = (unsigned)blocks;
+  if (accum_is_f64) {
+    const double *a = static_cast<const double *>(accum);
+    if (narrow)
+      k_finalize<double, 8><<<g, 256, 0, st>>>(a, accum_stride, counts, total_texels, num_classes, aggregator,
+                                               rows_out, unobserved_out, labels_out);
+    else
+      k_finalize<double, 32><<<g, 256, 0, st>>>(a, accum_stride, counts, total_texels, num_classes, aggregator,
+                                                rows_out, unobserved_out, labels_out);
+  } else {
+    const float *a = static_cast<const float *>(accum);
+    if (narrow)
+      k_finalize<float, 8><<<g, 256, 0, st>>>(a, accum_stride, counts, total_texels, num_classes, aggregator,
+                                              rows_out, unobserved_out, labels_out);
+    else
+      k_finalize<float, 32><<<g, 256, 0, st>>>(a, accum_stride, counts, total_texels, num_classes, aggregator,
+                                               rows_out, unobserved_out, labels_out);
+  }
   return check_launch("tfb_finalize");
 }
 
