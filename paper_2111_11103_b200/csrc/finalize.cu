@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) k_finalize(const AccT *__restrict__ accum
       for (int k = sub; k < c; k += L) sacc += (double)a[k];
 #pragma unroll
       for (int d = L / 2; d; d >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, d, L);
-      unobs = zero_count || !(sacc > 0.0);
+      unobs = zero_count || sacc <= 0.0;  // a NaN mass stays observed, rows = accum / 1 (fusion.py:203-205)
       scale = sacc > 0.0 ? sacc : 1.0;
     }
     const float uni = (float)(1.0 / c);
