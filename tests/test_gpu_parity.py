@@ -446,3 +446,33 @@ def test_raster_odd_image_sizes_vs_oracle():
                               want_uv=False)
             np.testing.assert_array_equal(rows[k], O.pixel_rows(layout.offsets, ref["triangle"],
                                                                 ref["texel"]).ravel(), err_msg="%dx%d" % (W, H))
+
+
+@pytest.mark.parametrize("agg", ["sum", "maxsum", "mul"])
+@pytest.mark.parametrize("accum_dtype", ["float32", "float64"])
+def test_accumulate_frame_explicit_random_weights_vs_oracle(agg, accum_dtype):
+    """accumulate_frame with a caller-provided per-pixel weight array that
+    varies inside texel runs (the scatter-add's per-pixel weight path), and
+    probabilities hitting the clip bounds, vs the float64 oracle."""
+    v, t = make_room((6.0, 5.0, 3.0), 12)
+    mesh = Mesh.from_arrays(v, t)
+    layout = uniform_layout(mesh, 2)
+    intr = Intrinsics(100.0, 100.0, 63.5, 47.5, 128, 96)
+    frames = random_room_trajectory(3, intr, seed=8)
+    rng = np.random.default_rng(3)
+    tex = init_texture(layout, 5, agg, accum_dtype=accum_dtype)
+    acc = np.zeros((layout.total_texels, 5))
+    cnt = np.zeros(layout.total_texels, np.int64)
+    for fr in frames:
+        ids = rasterize(mesh, layout, fr)
+        p = rng.dirichlet(np.ones(5), size=(96, 128)).astype(np.float32)
+        p[::7, ::5, 1] = 0.0
+        p[::11, ::3, 2] = 1.0
+        w = rng.uniform(0.0, 3.0, size=(96, 128))
+        accumulate_frame(tex, ids, p, w)
+        O.accumulate_frame(acc, cnt, layout.offsets, ids.triangle, ids.texel, p, w, agg)
+    got = tex.accum
+    np.testing.assert_array_equal(tex.counts, cnt)
+    tol = 1e-5 if accum_dtype == "float32" else 1e-12
+    scale = np.abs(acc).max(axis=1, keepdims=True) + 1e-30
+    assert (np.abs(got - acc) / scale).max() < tol
