@@ -51,3 +51,20 @@ def test_finalize_vs_oracle(c, agg, dtype):
     np.testing.assert_array_equal(unobs.cpu().numpy().astype(bool), ref_unobs)
     np.testing.assert_allclose(rows.cpu().numpy(), ref_rows, rtol=1e-6, atol=1e-7)
     np.testing.assert_array_equal(labels.cpu().numpy(), O.texel_argmax(ref_rows, ref_unobs))
+
+
+@pytest.mark.parametrize("c", [1, 2, 13, 40])
+def test_probs_argmax_matches_numpy(c):
+    """tfb_probs_argmax (the network-argmax fallback, cli.py:293): NumPy's
+    first-maximum / first-NaN rule, ties and negative values included."""
+    rng = np.random.default_rng(c)
+    p = rng.integers(0, 4, size=(997, c)).astype(np.float32) / 3.0  # many ties
+    p[::13, -1] = np.nan
+    p[::29, 0] = -1.0
+    p[5] = np.nan
+    d = torch.as_tensor(p, device="cuda")
+    out = torch.empty(len(p), dtype=torch.int32, device="cuda")
+    N.check(N.load().tfb_probs_argmax(P(d.data_ptr()), len(p), c, P(out.data_ptr()),
+                                      P(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.cpu().numpy(), p.argmax(axis=1))
