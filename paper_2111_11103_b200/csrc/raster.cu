@@ -596,6 +596,9 @@ __global__ void __launch_bounds__(kThreads) k_ccands(tfb_scene sc, const double 
 #define TFB_SETUP_PER 2
 #endif
 constexpr int kSetupPer = TFB_SETUP_PER;  // candidates per k_setup thread (their bin appends are batched)
+#ifndef TFB_SETUP_FLAT
+#define TFB_SETUP_FLAT 1
+#endif
 #ifndef TFB_SETUP_WIDE
 #define TFB_SETUP_WIDE 8
 #endif
@@ -699,6 +702,87 @@ __global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc
 #pragma unroll
     for (int e = 0; e < 2 * kSetupPer; ++e)
       pos[e] = __shfl_sync(act, pos[e], __ffs(peers[e]) - 1) + __popc(peers[e] & ((1u << lane) - 1u));
+#if TFB_SETUP_FLAT
+    if (act == 0xffffffffu) {
+      // Full warp: the (record, further tile) pairs of all its pending records are
+      // numbered warp-wide and dealt round-robin to the lanes, so every lane has
+      // at most ceil(pairs / 32) append round trips in flight one after another
+      // instead of a thread walking its own records' tiles serially.
+      uint32_t ext = 0, ext01 = 0, ext23 = 0;  // further tiles per record (16-bit packed)
+#pragma unroll
+      for (int e = 0; e < 2 * kSetupPer; ++e) {
+        uint32_t n = 0;
+        if (p[e].valid) {
+          const uint32_t nx = (p[e].tx >> 16) - (p[e].tx & 0xffffu) + 1u, ny = (p[e].ty >> 16) - (p[e].ty & 0xffffu) + 1u;
+          n = nx * ny - 1u;
+          bin_put(w, f, ntiles, (int)(p[e].ty & 0xffffu) * TX + (int)(p[e].tx & 0xffffu), pos[e], p[e].slot);
+        }
+        n = min(n, 0xffffu);  // records over > 65535 tiles: the rest below
+        if (e < 2) ext01 |= n << (16 * e);
+        else ext23 |= n << (16 * (e - 2));
+        ext += n;
+      }
+      uint32_t incl = ext;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      for (uint32_t q0 = 0; q0 < total; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        // owner: the first lane whose inclusive prefix exceeds q
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step; step >>= 1) {
+          const uint32_t v = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+          if (v <= q) lo += step;
+        }
+        const uint32_t o_incl = __shfl_sync(0xffffffffu, incl, lo), o_ext = __shfl_sync(0xffffffffu, ext, lo);
+        const uint32_t o01 = __shfl_sync(0xffffffffu, ext01, lo), o23 = __shfl_sync(0xffffffffu, ext23, lo);
+        uint32_t rtx[2 * kSetupPer], rty[2 * kSetupPer], rslot[2 * kSetupPer];
+#pragma unroll
+        for (int e = 0; e < 2 * kSetupPer; ++e) {
+          rtx[e] = __shfl_sync(0xffffffffu, p[e].tx, lo);
+          rty[e] = __shfl_sync(0xffffffffu, p[e].ty, lo);
+          rslot[e] = __shfl_sync(0xffffffffu, p[e].slot, lo);
+        }
+        if (q < total) {
+          uint32_t r = q - (o_incl - o_ext);  // index among the owner's further tiles
+          uint32_t tx = 0, ty = 0, slot = 0, k = 0;
+          bool found = false;
+#pragma unroll
+          for (int e = 0; e < 2 * kSetupPer; ++e) {
+            const uint32_t n = ((e < 2 ? o01 : o23) >> (16 * (e & 1))) & 0xffffu;
+            if (!found && r < n) {
+              tx = rtx[e];
+              ty = rty[e];
+              slot = rslot[e];
+              k = r + 1u;  // tile k of the record's box (0 = the first, appended above)
+              found = true;
+            } else if (!found) {
+              r -= n;
+            }
+          }
+          const uint32_t x0 = tx & 0xffffu, nx = (tx >> 16) - x0 + 1u, y0 = ty & 0xffffu;
+          const int tile = (int)((y0 + k / nx) * (uint32_t)TX + x0 + k % nx);
+          bin_put(w, f, ntiles, tile, atomicAdd(tc + tile, 1u), slot);
+        }
+      }
+      // a record over more than 65536 tiles (only with absurd image sizes) keeps its own loop
+#pragma unroll
+      for (int e = 0; e < 2 * kSetupPer; ++e) {
+        if (!p[e].valid) continue;
+        const int x0 = (int)(p[e].tx & 0xffffu), nx = (int)(p[e].tx >> 16) - x0 + 1;
+        const int y0 = (int)(p[e].ty & 0xffffu), ny = (int)(p[e].ty >> 16) - y0 + 1;
+        for (int i = 0x10000; i < nx * ny; ++i) {
+          const int tile = (y0 + i / nx) * TX + x0 + i % nx;
+          bin_put(w, f, ntiles, tile, atomicAdd(tc + tile, 1u), p[e].slot);
+        }
+      }
+      continue;
+    }
+#endif
     // the other tiles: a thread appends its own small records (a few round trips);
     // a record over more than kSetupWide tiles is appended by the whole warp, one
     // atomic per lane in flight at a time (a large triangle spans tens of tiles)
