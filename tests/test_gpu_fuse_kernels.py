@@ -107,7 +107,7 @@ def _scale(rows, probs, n_x, agg, wm, alpha):
 
 
 @pytest.mark.parametrize("fast", [True, False])
-@pytest.mark.parametrize("c", [3, 4, 13, 19, 20, 40, 132, 300, 601])
+@pytest.mark.parametrize("c", [3, 4, 7, 13, 19, 20, 23, 40, 41, 99, 132, 300, 601])
 @pytest.mark.parametrize("agg", ["sum", "maxsum", "mul"])
 def test_fuse_kernels_vs_oracle(fast, c, agg):
     rng = np.random.default_rng(1000 + c)
