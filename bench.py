@@ -9,10 +9,17 @@ c = 40 classes, softmax(N(0, 2^2)) float32 probability maps, aggregator mul
 (the paper default), weights images_iid, float32 accumulator.
 
 One step = one whole fusion job: zero the texture, rasterize + weight +
-scatter-add all 2000 frames (batches of --batch frames), finalize + argmax;
+scatter-add the rank's frames (batches of --batch frames), finalize + argmax;
 with N > 1 the accumulator rows are sum-reduce-scattered (NCCL), each rank
 finalizes its slice and the int32 labels are all-gathered.  `value` = frames of all
-ranks / max-over-ranks device time (weak scaling: 2000 frames per GPU).
+ranks / max-over-ranks device time.  --scaling strong (default; BASELINE
+configs[2]: "same ScanNet-scale scene frame-sharded at 2/4/8 B200") splits the
+2000-frame trajectory into N contiguous blocks; --scaling weak gives every
+rank its own 2000 frames.
+
+Multi-GPU: `python bench.py --gpus N` re-executes itself under
+torch.distributed.run with N ranks (one per GPU) unless it already runs under
+torchrun, in which case WORLD_SIZE must equal N (exit code 2 otherwise).
 Inputs are larger than L2: the frames cycle a pool of 8 distinct maps per
 GPU (8 x 49.2 MB = 393 MB > 126 MB L2), so every frame's probabilities are
 streamed from HBM.
@@ -22,8 +29,10 @@ probability maps in pinned HOST memory: every step copies all 2000 maps
 host→device and reads the texel labels back.
 
 `--impl reference` times the CPU reference path (the oracle's C port of the
-reference's rasterize → weights → accumulate loop, frame-parallel over all
-host threads) on a bounded sample of the same workload.
+reference's rasterize → weights → accumulate → finalize loop, frame-parallel
+over all host threads, parallel reduction and finalize) on a bounded sample
+of the same workload: exactly the function and sample size of the
+`cpu_baseline` leg, so the two agree.
 """
 
 import argparse
@@ -59,10 +68,16 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _frames_per_rank(args, n):
+    return args.frames if args.scaling == "weak" else -(-args.frames // n)
+
+
 def _config(args, n):
-    return {"workload": "cfg2: room 299,568 tris, %d frames/GPU 640x480, c=40, %s, %s, steps=1 layout"
-                        % (args.frames, AGG, WMODE),
-            "frames_per_gpu": args.frames, "triangles": 299568, "texels": 299568, "classes": C,
+    total = args.frames * (n if args.scaling == "weak" else 1)
+    return {"workload": "cfg%s: room 299,568 tris, %d frames 640x480 (%s scaling over %d GPU), c=40, %s, %s, "
+                        "steps=1 layout" % ("2" if n == 1 else "3", total, args.scaling, n, AGG, WMODE),
+            "frames_total": total, "frames_per_gpu": _frames_per_rank(args, n), "scaling": args.scaling,
+            "triangles": 299568, "texels": 299568, "classes": C,
             "aggregator": AGG, "weights": WMODE, "accum": "float32", "batch": args.batch, "overlap": bool(args.overlap),
             "parallelism": "frame-sharded dp%d" % n,
             "l2": "inputs larger than L2: 8-map pool per GPU (393 MB) cycled, accumulator 47.9 MB"}
@@ -154,29 +169,61 @@ def cpu_reference(args, frames_sample, threads, scene=None):
     return frames_sample / dt, dt
 
 
+CPU_FRAMES_PER_THREAD = 32  # bounded sample: ~3-6 s of CPU work per sample on 16-64 threads
+
+
+def _host_cpu():
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)), "model": model}
+
+
+def _cpu_threads():
+    return min(len(os.sched_getaffinity(0)), 64)
+
+
+def _cpu_sample_desc(sample, threads, dt=None):
+    return ("%d cfg2 frames (rasterize + images_iid weights + mul accumulate into float64, then finalize + "
+            "argmax), oracle C port of the reference loop, frame-parallel over %d host threads with a "
+            "row-parallel reduction%s" % (sample, threads, "" if dt is None else ", %.1f s" % dt))
+
+
 def run_reference(args):
     world, rank, _ = _dist_env()
     if rank != 0:
         return
-    threads = min(len(os.sched_getaffinity(0)), 64)
-    sample = 8 * threads
+    world = max(world, args.gpus)
+    threads = _cpu_threads()
+    sample = CPU_FRAMES_PER_THREAD * threads
+    from paper_2111_11103_b200.geometry import Mesh, uniform_layout
+    from paper_2111_11103_b200.synth import make_room
+
+    v, t = make_room((6.0, 5.0, 3.0), TESS)
+    mesh = Mesh.from_arrays(v, t)
+    scene = (mesh, uniform_layout(mesh, 1))
     for _ in range(args.warmup):
-        cpu_reference(args, threads, threads)
+        cpu_reference(args, threads, threads, scene=scene)
     vals = []
     t_total = 0.0
     for _ in range(args.steps):
-        v, dt = cpu_reference(args, sample, threads)
-        vals.append(v)
+        val, dt = cpu_reference(args, sample, threads, scene=scene)
+        vals.append(val)
         t_total += dt
     value = statistics.median(vals)
+    cfg = _config(args, world)
+    cfg["reference_sample_frames_per_step"] = sample
     line = {"metric": METRIC, "value": value, "unit": "frames/s", "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * t_total / max(args.steps, 1),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config(args, world),
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": cfg, "host_cpu": _host_cpu(),
             "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port",
-                             "sample": "%d cfg2 frames per step (rasterize+images_iid+mul accumulate), "
-                                       "frame-parallel C port of the reference loop over %d threads, "
-                                       "plus finalize" % (sample, threads)},
+                             "sample": _cpu_sample_desc(sample, threads) + " per step"},
             "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -186,22 +233,37 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2111_11103_b200 import MeshAnnotation
+    from paper_2111_11103_b200.dist import shard_bounds
     from paper_2111_11103_b200.geometry import Mesh, pack_camera, uniform_layout
     from paper_2111_11103_b200.synth import make_room, random_room_trajectory, scannet_intrinsics, softmax_maps
 
     world, rank, local = _dist_env()
+    if world > torch.cuda.device_count():
+        raise SystemExit("bench.py: %d ranks but only %d visible GPUs" % (world, torch.cuda.device_count()))
     torch.cuda.set_device(local)  # before the process group, so NCCL binds this rank's GPU
     dev = torch.device("cuda", local)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", init_method="env://", device_id=dev)
+        probe = torch.ones(1, device=dev)
+        dist.all_reduce(probe)  # forces communicator creation; every rank must contribute
+        comm = {"backend": dist.get_backend(), "world_size": dist.get_world_size(), "nranks_seen": int(probe.item()),
+                "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version())}
+        if int(probe.item()) != world:
+            raise SystemExit("bench.py: NCCL communicator saw %d ranks, expected %d" % (int(probe.item()), world))
 
     v, t = make_room((6.0, 5.0, 3.0), TESS)
     mesh = Mesh.from_arrays(v, t)
     layout = uniform_layout(mesh, 1)
-    frames = random_room_trajectory(args.frames, scannet_intrinsics(), seed=1000 + rank)
+    if args.scaling == "weak":
+        frames = random_room_trajectory(args.frames, scannet_intrinsics(), seed=1000 + rank)
+    else:  # strong: one 2000-frame trajectory, contiguous block per rank (dist.shard_bounds)
+        lo, hi = shard_bounds(args.frames, rank, world)
+        frames = random_room_trajectory(args.frames, scannet_intrinsics(), seed=1000)[lo:hi]
+    nf = len(frames)
     cams_dev = torch.as_tensor(np.stack([pack_camera(f) for f in frames])).to(dev)
     pool = softmax_maps(POOL, H, W, C, seed=rank, device=dev)
-    probs_list = [pool[i % POOL] for i in range(args.frames)]
+    probs_list = [pool[i % POOL] for i in range(nf)]
     ann = MeshAnnotation(mesh, layout, num_classes=C, aggregator=AGG, weight_mode=WMODE, accum_dtype="float32",
                          max_batch=args.batch, device=dev, overlap=args.overlap,
                          fuse_ctas_per_sm=args.fuse_ctas if args.fuse_ctas >= 0 else None)
@@ -235,10 +297,13 @@ def run_ours(args):
     prof, ann.profile = ann.profile, None
     ms = t_start.elapsed_time(t_end)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    frames_t = torch.tensor([float(nf)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(frames_t, op=dist.ReduceOp.SUM)
     ms_max = float(ms_t.item())
-    value = world * args.frames * args.steps / (ms_max / 1000.0)
+    frames_all = int(frames_t.item())
+    value = frames_all * args.steps / (ms_max / 1000.0)
 
     raster_ms = sum(r0.elapsed_time(r1) for _, r0, r1, _, _ in prof)
     fuse_ms = sum(f0.elapsed_time(f1) for _, _, _, f0, f1 in prof)
@@ -248,7 +313,7 @@ def run_ours(args):
     # our kernels per timed step: per batch k_ccull, k_ccands (k_verts, k_cull without scene clusters),
     # k_setup, k_raster, k_raster_big + the k_fuse launches (the hit-count reset is a dense torch
     # memset here), + k_finalize once
-    batches = [min(args.batch, args.frames - b0) for b0 in range(0, args.frames, args.batch)]
+    batches = [min(args.batch, nf - b0) for b0 in range(0, nf, args.batch)]
     gpu_launches = args.steps * (sum(5 + (b + 255) // 256 for b in batches) + 1)
     peak, peak_kind = _peaks()
     achieved = B_FRAME * fuse_frames / (fuse_ms / 1000.0) / 1e9
@@ -260,12 +325,39 @@ def run_ours(args):
     except Exception:
         pass
 
+    # ---- secondary: the same job with the float64 accumulator (the reference's arithmetic) ----
+    f64 = None
+    if not args.no_f64:
+        ann64 = MeshAnnotation(mesh, layout, num_classes=C, aggregator=AGG, weight_mode=WMODE,
+                               accum_dtype="float64", max_batch=args.batch, device=dev)
+
+        def step64():
+            ann64.reset()
+            ann64.add_batch(probs_list, cams_dev, width=W, height=H)
+            if world > 1:
+                ann64.finalize_distributed()
+            ann64.labels()
+
+        step64()
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        step64()
+        a1.record(stream)
+        barrier()
+        f_ms = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(f_ms, op=dist.ReduceOp.MAX)
+        f64 = {"value": frames_all / (float(f_ms.item()) / 1000.0), "unit": "frames/s", "steps": 1,
+               "accum": "float64 (atomicAdd f64; the reference's accumulator precision)"}
+        del ann64
+
     # ---- e2e through the public API with host (pinned) inputs --------------------------------
     e2e = None
     if not args.no_e2e:
         host_pool = [pool[i].cpu().pin_memory() for i in range(POOL)]
-        host_list = [host_pool[i % POOL] for i in range(args.frames)]
-        cams_host = [frames[i] for i in range(args.frames)]
+        host_list = [host_pool[i % POOL] for i in range(nf)]
+        cams_host = [frames[i] for i in range(nf)]
 
         def e2e_step():
             ann.reset()
@@ -287,37 +379,60 @@ def run_ours(args):
         e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * args.frames * ksteps / (float(e_ms.item()) / 1000.0), "unit": "frames/s",
-               "h2d_bytes_per_step": args.frames * (H * W * C * 4 + 16 * 8),
+        e2e = {"value": frames_all * ksteps / (float(e_ms.item()) / 1000.0), "unit": "frames/s",
+               "h2d_bytes_per_step": nf * (H * W * C * 4 + 16 * 8),
                "d2h_bytes_per_step": int(labels_host.nbytes), "steps": ksteps,
-               "api": "MeshAnnotation.add_batch(pinned host maps) + labels(host=True)"}
+               "api": "MeshAnnotation.add_batch(pinned host maps) + labels(host=True)",
+               "note": "bytes per rank; every rank copies its own frames"}
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        threads = min(len(os.sched_getaffinity(0)), 64)
-        sample = 64 * threads
+        threads = _cpu_threads()
+        sample = CPU_FRAMES_PER_THREAD * threads
         val, dt = cpu_reference(args, sample, threads, scene=(mesh, layout))
         cpu = {"value": val, "unit": "frames/s", "cores": threads, "kind": "port",
-               "sample": "%d cfg2 frames (rasterize+images_iid+mul accumulate+finalize), oracle C port, "
-                         "frame-parallel over %d host threads, %.1f s" % (sample, threads, dt)}
+               "sample": _cpu_sample_desc(sample, threads, dt), "host_cpu": _host_cpu()}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": _config(args, world),
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": _config(args, world),
             "roofline": {"bound": "hbm", "kernel": "k_fuse (tfb_fuse)", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                         "frac_vs_8tbs_nominal": achieved / 8000.0,
                          "bytes_per_frame": B_FRAME,
                          "launch_ms_avg": fuse_ms / max(n_launch_fuse, 1),
                          "frames_per_launch": fuse_frames / max(n_launch_fuse, 1)},
             "breakdown_ms_per_step": {"raster": raster_ms / args.steps, "fuse": fuse_ms / args.steps,
                                       "other": ms_max / args.steps - (raster_ms + fuse_ms) / args.steps},
-            "clocks": clocks.summary(), "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": gpu_launches,
+            "clocks": clocks.summary(), "e2e": e2e, "f64_accumulator": f64, "cpu_baseline": cpu,
+            "gpu_launches": gpu_launches, "comm": comm,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _free_port():
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _spawn_ranks(args):
+    """Re-execute this script under torch.distributed.run with --gpus ranks (one per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator size / NVLS selection visible in the log
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -326,14 +441,28 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--frames", type=int, default=FRAMES)
+    ap.add_argument("--frames", type=int, default=FRAMES, help="trajectory length (per rank with --scaling weak)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--overlap", type=int, default=0)
     ap.add_argument("--fuse-ctas", type=int, default=-1, help="cap on resident scatter-add CTAs per SM (-1: auto)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-f64", action="store_true")
     args = ap.parse_args()
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0:  # not under torchrun
+        if args.gpus > 1 and args.impl == "ours":
+            sys.exit(_spawn_ranks(args))
+        os.environ.setdefault("WORLD_SIZE", "1")
+    elif world != args.gpus:
+        print("bench.py: --gpus %d but WORLD_SIZE=%d" % (args.gpus, world), file=sys.stderr)
+        sys.exit(2)
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     if args.impl == "reference":
         run_reference(args)
     else:

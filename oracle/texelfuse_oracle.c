@@ -229,10 +229,19 @@ int tfo_fuse_frames(const double *verts, int64_t nv, const int32_t *tris, int64_
 #else
   nthreads = 1;
 #endif
+  /* private accumulators of every thread, summed row-block-parallel at the end */
+  double **accs = (double **)calloc((size_t)nthreads, sizeof(double *));
+  int64_t **cnts = (int64_t **)calloc((size_t)nthreads, sizeof(int64_t *));
+  if (!accs || !cnts) { free(accs); free(cnts); return 1; }
 #pragma omp parallel num_threads(nthreads)
   {
     double *acc = (double *)calloc((size_t)(n_x * c), sizeof(double));
     int64_t *cnt = (int64_t *)calloc((size_t)n_x, sizeof(int64_t));
+#ifdef _OPENMP
+    int me = omp_get_thread_num(), team = omp_get_num_threads();
+#else
+    int me = 0, team = 1;
+#endif
     int32_t *frame_cnt = (int32_t *)calloc((size_t)n_x, sizeof(int32_t));
     int32_t *tri = (int32_t *)malloc(sizeof(int32_t) * npx);
     int32_t *tex = (int32_t *)malloc(sizeof(int32_t) * npx);
@@ -278,22 +287,32 @@ int tfo_fuse_frames(const double *verts, int64_t nv, const int32_t *tris, int64_
       for (int64_t p = 0; p < npx; ++p)
         if (rows[p] >= 0) frame_cnt[rows[p]] = 0;
     }
-    if (ok) {
-#pragma omp critical
-      {
-        for (int64_t i = 0; i < n_x * c; ++i) accum[i] += acc[i];
-        for (int64_t i = 0; i < n_x; ++i) counts[i] += cnt[i];
-      }
+    accs[me] = ok ? acc : NULL;
+    cnts[me] = ok ? cnt : NULL;
+#pragma omp barrier
+    /* thread me sums texel rows [lo, hi) over all private accumulators, in thread order */
+    int64_t lo = n_x * me / team, hi = n_x * (me + 1) / team;
+    for (int q = 0; q < team; ++q) {
+      if (!accs[q]) continue;
+      const double *aq = accs[q];
+      const int64_t *cq = cnts[q];
+      for (int64_t i = lo * c; i < hi * c; ++i) accum[i] += aq[i];
+      for (int64_t i = lo; i < hi; ++i) counts[i] += cq[i];
     }
+#pragma omp barrier
     free(acc); free(cnt); free(frame_cnt); free(tri); free(tex); free(dep); free(rows); free(contrib);
   }
+  free(accs); free(cnts);
   return err;
 }
 
 /* fusion.py:186-222 — finalize + argmax.  rows (n_x*c float32) may be NULL. */
 void tfo_finalize(const double *accum, const int64_t *counts, int64_t n_x, int c, int agg,
                   float *rows, uint8_t *unobserved, int32_t *labels) {
+#pragma omp parallel
+  {
   float *tmp = (float *)malloc(sizeof(float) * c);
+#pragma omp for schedule(static)
   for (int64_t i = 0; i < n_x; ++i) {
     const double *a = accum + i * c;
     int unobs;
@@ -321,6 +340,7 @@ void tfo_finalize(const double *accum, const int64_t *counts, int64_t n_x, int c
     labels[i] = unobs ? -1 : best;
   }
   free(tmp);
+  }
 }
 
 /* ------------------------------------------------------------------------

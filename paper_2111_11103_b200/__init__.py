@@ -47,7 +47,21 @@ from .formats import (
 )
 from .meshio import load_mesh, load_trajectory, save_ply, save_trajectory
 from .rasterizer import IdImage, pixel_world_points, project_point, rasterize
-from .renderback import render_labels
+from .renderback import (
+    EvalReport,
+    colorize_labels,
+    default_palette,
+    export_colored_mesh,
+    load_palette,
+    merge_reports,
+    pixel_accuracy,
+    read_label_png,
+    render_labels,
+    save_palette,
+    select_frames,
+    write_label_png,
+)
+from .synth import NoiseModel, corrupt, make_orbit_trajectory
 
 __version__ = "0.1.0"
 
@@ -73,4 +87,8 @@ __all__ = [
     "finalize", "finalize_and_render", "init_texture", "load_mesh", "load_trajectory", "open_session",
     "parse_weight_mode", "pixel_world_points", "project_point", "rasterize", "render_labels", "save_ply",
     "save_trajectory", "texel_argmax", "texel_count", "texel_id", "texture_nbytes", "uniform_layout",
+    "EvalReport", "NoiseModel", "colorize_labels", "corrupt", "default_palette", "export_colored_mesh",
+    "load_palette", "make_orbit_trajectory", "merge_reports", "pixel_accuracy", "read_label_png",
+    "read_probability_header", "read_probability_image", "read_texture", "save_palette", "select_frames",
+    "write_label_png", "write_probability_image", "write_texture",
 ]

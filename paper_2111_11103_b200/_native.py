@@ -114,6 +114,8 @@ def ptr_array(addrs):
 
 
 def stream_handle(stream=None):
+    """cudaStream_t of ``stream``, else of the current stream of the current device
+    (callers that own tensors on another device enter ``torch.cuda.device`` first)."""
     import torch
 
     s = stream if stream is not None else torch.cuda.current_stream()

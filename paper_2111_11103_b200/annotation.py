@@ -2,8 +2,8 @@
 
 The batched, device-resident front end of the hot path (BASELINE north star):
 for each batch of up to ``max_batch`` frames of one size it issues the
-stream-ordered launches of tfb_rasterize (vertex outcodes, cull, setup +
-tile binning, tile raster with the per-frame texel hit counts fused into its
+stream-ordered launches of tfb_rasterize (cluster cull, setup + tile
+binning, tile raster with the per-frame texel hit counts fused into its
 epilogue), one tfb_fuse scatter-add and the hit-counter reset, and never
 synchronizes with the host.  Host inputs are copied on a separate stream
 into double-buffered device staging, overlapping the previous batch's
@@ -13,18 +13,34 @@ rows; ``render`` rasterizes the requested cameras and gathers labels
 ``finalize_distributed()`` (reduce-scatter, slice finalize, label
 all-gather) or ``allreduce()`` (then ``get()``).
 
+Per-frame calls run at batched speed: ``add(probs, camera)`` (and the
+session's ``add_frame``, bindings/__init__.py:85-115) only queue the frame;
+the queue is folded as one batch when it reaches ``max_batch`` frames, when
+the frame size changes, and before anything reads the texture (``get``,
+``labels``, ``render``, ``texture``, checkpoints, the exchange).  Host
+inputs are copied to the device when queued (so the caller may reuse its
+array at once, as with the reference's copy at bindings/__init__.py:101);
+device float32 tensors are used in place and must not be modified before
+the queue is folded -- an in-place write is detected through the tensor's
+version counter and raises instead of fusing changed data.
+
 It is a thin layer over the same ProbabilityTexture the reference-compatible
 functions use (fusion.py / session.py), so textures and results interchange.
 """
+
+import weakref
 
 import numpy as np
 import torch
 
 from . import _native as N
 from .device import scene_for
+from .errors import DataError
 from .fusion import init_texture, parse_weight_mode
 from .geometry import pack_camera, uniform_layout
 from .renderback import render_labels_device
+
+MAX_BATCH_CAP = 256  # tfb_fuse carries at most 256 frames per launch
 
 
 def _cams_array(cameras):
@@ -44,28 +60,122 @@ def _sizes(cameras, width, height):
     return int(cam0.width), int(cam0.height)
 
 
+def _device_ready(p, device):
+    """True for tensors the scatter-add can read in place."""
+    return (isinstance(p, torch.Tensor) and p.is_cuda and p.device == device and p.dtype == torch.float32
+            and p.is_contiguous() and p.data_ptr() % 16 == 0)
+
+
+class _Pending:
+    """A queued frame: device probabilities, packed camera, and what to report back."""
+
+    __slots__ = ("probs", "cam", "version", "ids", "ready", "fallback_key", "count")
+
+    def __init__(self, probs, cam, version, ids=None, ready=None, fallback_key=None, count=None):
+        self.probs = probs
+        self.cam = cam
+        self.version = version
+        self.ids = ids
+        self.ready = ready
+        self.fallback_key = fallback_key
+        self.count = count
+
+
+class FrameCount:
+    """Covered pixels of one queued frame (the int add_frame returns,
+    bindings/__init__.py:113), resolved when read: reading it folds the queue."""
+
+    __slots__ = ("_owner", "_t", "_i", "_v")
+
+    def __init__(self, owner):
+        self._owner = owner
+        self._t = None
+        self._i = 0
+        self._v = None
+
+    def _set(self, tensor, index):
+        self._t, self._i = tensor, index
+
+    def __int__(self):
+        if self._v is None:
+            if self._t is None:
+                owner = self._owner()
+                if owner is not None:
+                    owner.flush()
+            if self._t is None:
+                raise RuntimeError("the frame was discarded before it was folded (reset())")
+            self._v = int(self._t[self._i].item())
+            self._t = None
+        return self._v
+
+    __index__ = __int__
+
+    def __eq__(self, o):
+        return int(self) == int(o)
+
+    def __ne__(self, o):
+        return int(self) != int(o)
+
+    def __lt__(self, o):
+        return int(self) < o
+
+    def __le__(self, o):
+        return int(self) <= o
+
+    def __gt__(self, o):
+        return int(self) > o
+
+    def __ge__(self, o):
+        return int(self) >= o
+
+    def __hash__(self):
+        return hash(int(self))
+
+    def __add__(self, o):
+        return int(self) + o
+
+    __radd__ = __add__
+
+    def __sub__(self, o):
+        return int(self) - o
+
+    def __rsub__(self, o):
+        return o - int(self)
+
+    def __repr__(self):
+        return repr(int(self))
+
+
 class MeshAnnotation:
     """Fuse per-frame class probabilities onto a mesh's texels on the GPU."""
 
     def __init__(self, mesh, layout=None, num_classes=None, aggregator="mul", weight_mode="images_iid",
-                 accum_dtype="float32", max_batch=8, device=None, memory_budget=None, overlap=False,
-                 fuse_ctas_per_sm=None):
-        if num_classes is None:
+                 accum_dtype="float32", max_batch=None, device=None, memory_budget=None, overlap=False,
+                 fuse_ctas_per_sm=None, texture=None):
+        if texture is None and num_classes is None:
             raise ValueError("num_classes is required")
         self.mesh = mesh
-        self.layout = layout if layout is not None else uniform_layout(mesh, 1)
-        self.num_classes = int(num_classes)
+        self.layout = layout if layout is not None else (texture.layout if texture is not None
+                                                          else uniform_layout(mesh, 1))
         self.weight_mode, self.alpha = parse_weight_mode(weight_mode)
-        budget = memory_budget if memory_budget is not None else float("inf")
-        self.texture = init_texture(self.layout, self.num_classes, aggregator, budget, accum_dtype, device)
-        self.scene = scene_for(mesh, self.layout, self.texture.device)
+        if texture is None:
+            budget = memory_budget if memory_budget is not None else float("inf")
+            texture = init_texture(self.layout, int(num_classes), aggregator, budget, accum_dtype, device)
+        self._tex = texture
+        self.num_classes = int(texture.num_classes)
+        self.scene = scene_for(mesh, self.layout, texture.device)
         self.device = self.scene.device
-        self.max_batch = int(max_batch)
+        # None: sized per frame size from the free device memory (_batch_for)
+        self.max_batch = None if max_batch is None else max(1, min(int(max_batch), MAX_BATCH_CAP))
+        self._auto_batch = {}
         self._staging = [None, None]  # device staging for host inputs (double-buffered)
         self._stage_free = [None, None]
         self._stage_slot = 0
         self._copy_stream = None
         self.frames_added = 0
+        self._pending = []
+        self._pending_size = None
+        texture._flush_hook = weakref.WeakMethod(self.flush)
         # Overlap mode: batch k+1 is rasterized on a side stream while batch k
         # is scatter-added on the caller's stream (double-buffered row / hit
         # images); the scatter kernel is capped at fuse_ctas_per_sm resident
@@ -79,15 +189,41 @@ class MeshAnnotation:
         # optional list receiving (frames, ev_raster_start, ev_raster_end, ev_fuse_start, ev_fuse_end)
         self.profile = None
 
+    @property
+    def texture(self):
+        """The fused ProbabilityTexture (queued frames are folded first)."""
+        self.flush()
+        return self._tex
+
     @staticmethod
     def _event(stream):
         e = torch.cuda.Event(enable_timing=True)
         e.record(stream)
         return e
 
+    def _batch_for(self, W, H):
+        """Frames per batch: max_batch, or what a quarter of the free device
+        memory holds (raster workspace + row image + hit counts + host staging)."""
+        if self.max_batch is not None:
+            return self.max_batch
+        b = self._auto_batch.get((W, H))
+        if b is None:
+            lib = N.load()
+            nv, m = int(self.scene.struct.num_vertices), self.scene.num_triangles
+            ws1 = lib.tfb_raster_workspace_bytes(nv, m, W, H, 1, 0)
+            ws2 = lib.tfb_raster_workspace_bytes(nv, m, W, H, 2, 0)
+            per = (ws2 - ws1) + W * H * 4 * (2 + self.num_classes) + max(self._tex.total_texels, 1) * 4
+            free, _total = torch.cuda.mem_get_info(self.device)
+            b = int(max(1, min(MAX_BATCH_CAP, (free // 4 - ws1) // max(per, 1))))
+            self._auto_batch[(W, H)] = b
+        return b
+
     def reset(self):
-        """Zero the accumulator and counts for a new fusion job (same layout)."""
-        tex = self.texture
+        """Zero the accumulator and counts for a new fusion job (same layout);
+        frames still queued belong to the old job and are dropped."""
+        self._pending = []
+        self._pending_size = None
+        tex = self._tex
         tex._accum.zero_()
         tex._counts.zero_()
         tex.finalized = False
@@ -122,9 +258,7 @@ class MeshAnnotation:
         layout, class count, aggregator and weight mode (DataError otherwise);
         per-rank checkpoints of a sharded job can be loaded on their ranks and
         reduced as usual."""
-        from .errors import DataError
-
-        tex = self.texture
+        tex = self._tex
         with np.load(path, allow_pickle=False) as z:
             if int(z["version"]) != self.CHECKPOINT_VERSION:
                 raise DataError("checkpoint version %d is not supported" % int(z["version"]))
@@ -147,12 +281,14 @@ class MeshAnnotation:
             self.frames_added = int(z["frames_added"])
 
     # -- accumulation ------------------------------------------------------------------
-    def _probs_batch(self, probs, b, H, W):
+    def _probs_batch(self, probs, b, H, W, cur, cap):
         """Per-frame device pointers for b frames.  Contiguous float32 device
-        tensors are used in place; anything else (host arrays, pinned host
-        tensors) is copied into one of two device staging buffers on a copy
-        stream, so the copy of batch k+1 overlaps the kernels of batch k.
-        Returns (pointers, keep-alive list, copy-done event or None, staging slot)."""
+        tensors are used in place; other device tensors (float16, permuted,
+        unaligned) are converted on the caller's stream ``cur``, where they were
+        produced; host arrays / tensors are copied into one of two device
+        staging buffers on a copy stream, so the copy of batch k+1 overlaps the
+        kernels of batch k.  Returns (pointers, keep-alive list, copy-done event
+        or None, staging slot)."""
         c = self.num_classes
         if isinstance(probs, (list, tuple)):
             items = list(probs)
@@ -160,16 +296,19 @@ class MeshAnnotation:
             items = [probs[i] for i in range(b)] if probs.ndim == 4 else [probs]
         for p in items:
             if tuple(p.shape) != (H, W, c):
-                from .errors import DataError
-
                 raise DataError("probability array shape %s does not match expected %s"
                                 % (tuple(p.shape), (H, W, c)))
-        need_stage = [i for i, p in enumerate(items) if not (isinstance(p, torch.Tensor) and p.is_cuda
-                                                             and p.dtype == torch.float32 and p.is_contiguous()
-                                                             and p.data_ptr() % 16 == 0)]
+        for i, p in enumerate(items):
+            if isinstance(p, torch.Tensor) and p.is_cuda and not _device_ready(p, self.device):
+                with torch.cuda.stream(cur):
+                    q = p.detach().to(device=self.device, dtype=torch.float32).contiguous()
+                    if q.data_ptr() % 16 or q.data_ptr() == p.data_ptr():
+                        q = q.clone()
+                items[i] = q
+        need_stage = [i for i, p in enumerate(items) if not (isinstance(p, torch.Tensor) and p.is_cuda)]
         ready, slot = None, None
         if need_stage:
-            shape = (self.max_batch, H, W, c)
+            shape = (cap, H, W, c)
             slot = self._stage_slot
             self._stage_slot ^= 1
             if self._staging[slot] is None or tuple(self._staging[slot].shape) != shape:
@@ -180,8 +319,8 @@ class MeshAnnotation:
             if self._stage_free[slot] is not None:
                 cs.wait_event(self._stage_free[slot])  # the scatter that last read this buffer is done
             with torch.cuda.stream(cs):
-                for i in need_stage:
-                    p, dst = items[i], self._staging[slot][i]
+                for k, i in enumerate(need_stage):
+                    p, dst = items[i], self._staging[slot][k]
                     if isinstance(p, torch.Tensor):
                         dst.copy_(p, non_blocking=True)
                     else:
@@ -196,19 +335,28 @@ class MeshAnnotation:
         cameras a list of CameraFrame or a (B, 16) camera array/tensor.
         fallback_out (optional (B, H*W) int32 device tensor) receives each
         frame's network argmax."""
-        tex = self.texture
+        self.flush()
+        with torch.cuda.device(self.device):
+            W, H = _sizes(cameras, width, height)
+            cur = stream if stream is not None else torch.cuda.current_stream(self.device)
+            with torch.cuda.stream(cur):
+                cams_all = _cams_array(cameras).to(self.device, non_blocking=True)
+            self._fold(probs, cams_all, W, H, fallback_out, cur)
+
+    def _fold(self, probs, cams_all, W, H, fallback_out, cur, on_rows=None, ready=()):
+        """The batched pipeline over B frames with device cameras ``cams_all``."""
+        tex = self._tex
         if tex.finalized:
             raise RuntimeError("texture is already finalized")
-        W, H = _sizes(cameras, width, height)
-        cur = stream if stream is not None else torch.cuda.current_stream(self.device)
-        with torch.cuda.stream(cur):
-            cams_all = _cams_array(cameras).to(self.device, non_blocking=True)
         B = int(cams_all.shape[0])
         hw = H * W
         tex._push_host()
+        for ev in ready:
+            cur.wait_event(ev)
         needs_hits = self.weight_mode != "pixels_iid"
         nslots = 2 if self.overlap else 1
-        mb = self.max_batch
+        mb = self._batch_for(W, H) if B > 1 else 1
+        mb = min(mb, B) if self.max_batch is None else mb
         rows_all = self.scene.buffer("rows", (nslots, mb, hw), torch.int32)
         hits_all = (self.scene.buffer("hits2", (nslots, mb, max(tex.total_texels, 1)), torch.int32, zero=True)
                     if needs_hits else None)
@@ -220,7 +368,7 @@ class MeshAnnotation:
             b = min(mb, B - b0)
             slot = i % nslots
             chunk = probs[b0:b0 + b]
-            ptrs, keep, copied, sslot = self._probs_batch(chunk, b, H, W)
+            ptrs, keep, copied, sslot = self._probs_batch(chunk, b, H, W, cur, mb)
             rows = rows_all[slot, :b]
             hits = hits_all[slot, :b] if needs_hits else None
             if self.overlap and self._free[slot] is not None:
@@ -230,11 +378,14 @@ class MeshAnnotation:
             self.scene.rasterize(cams_all[b0:b0 + b], W, H, rows, hits=hits, stream=side)
             r1 = self._event(side) if prof is not None else None
             if self.overlap:
-                ready = torch.cuda.Event()
-                ready.record(side)
-                cur.wait_event(ready)
+                ev = torch.cuda.Event()
+                ev.record(side)
+                cur.wait_event(ev)
             if copied is not None:
                 cur.wait_event(copied)
+            if on_rows is not None:
+                with torch.cuda.stream(cur):
+                    on_rows(b0, b, rows)
             f0 = self._event(cur) if prof is not None else None
             parr, _k = N.ptr_array(ptrs)
             fb = fallback_out[b0:b0 + b] if fallback_out is not None else None
@@ -259,13 +410,152 @@ class MeshAnnotation:
                 ev = torch.cuda.Event()
                 ev.record(cur)
                 self._free[slot] = ev
+            for p in keep:  # inputs converted or staged on other streams stay valid until read
+                if isinstance(p, torch.Tensor) and p.is_cuda:
+                    p.record_stream(cur)
             del keep
         tex._h_accum = tex._h_counts = None
         self.frames_added += B
 
+    # -- per-frame queue ---------------------------------------------------------------
+    def _stage_one(self, probs, H, W, cur):
+        """Device float32 copy (or the tensor itself) of one frame's probabilities, and
+        the version to check at fold time (None when the copy is ours)."""
+        c = self.num_classes
+        shape = tuple(probs.shape) if hasattr(probs, "shape") else np.shape(probs)
+        if shape != (H, W, c):
+            raise DataError("probability array shape %s does not match expected %s" % (shape, (H, W, c)))
+        if _device_ready(probs, self.device):
+            return probs.detach(), probs._version, None
+        if isinstance(probs, torch.Tensor) and probs.is_cuda:
+            with torch.cuda.stream(cur):
+                q = probs.detach().to(device=self.device, dtype=torch.float32).contiguous()
+                if q.data_ptr() % 16 or q.data_ptr() == probs.data_ptr():
+                    q = q.clone()
+            return q, None, None
+        # host input: copied now (the caller may reuse its array), on the copy stream
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(self.device)
+        cs = self._copy_stream
+        if isinstance(probs, torch.Tensor):
+            src = probs.detach()
+            if src.dtype != torch.float32 or not src.is_contiguous():
+                src = src.to(torch.float32).contiguous()
+            pinned = src.is_pinned()
+        else:
+            src = torch.from_numpy(np.ascontiguousarray(probs, dtype=np.float32))
+            pinned = False
+        with torch.cuda.stream(cs):
+            q = torch.empty((H, W, c), dtype=torch.float32, device=self.device)
+            q.copy_(src, non_blocking=pinned)
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        q.record_stream(cur)
+        return q, None, ev
+
+    def _enqueue(self, probs, camera, ids=None, fallback_key=None, want_count=False):
+        tex = self._tex
+        if tex.finalized:
+            raise RuntimeError("texture is already finalized")
+        W, H = int(camera.width), int(camera.height)
+        if self._pending and self._pending_size != (W, H):
+            self.flush()
+        with torch.cuda.device(self.device):
+            cur = torch.cuda.current_stream(self.device)
+            p, version, ready = self._stage_one(probs, H, W, cur)
+        count = FrameCount(weakref.ref(self)) if want_count else None
+        self._pending.append(_Pending(p, pack_camera(camera), version, ids, ready, fallback_key, count))
+        self._pending_size = (W, H)
+        if len(self._pending) >= self._batch_for(W, H):
+            self.flush()
+        return count
+
     def add(self, probs, camera, **kw):
-        """Fold one (H, W, c) probability map seen from ``camera``."""
-        self.add_batch([probs], [camera] if not isinstance(camera, (list, tuple)) else camera, **kw)
+        """Queue one (H, W, c) probability map seen from ``camera``; it is folded
+        with the frames queued next to it as one batch (see the module doc).
+        With keyword arguments (width/height/fallback_out/stream) the frame is
+        folded at once through add_batch."""
+        if kw or isinstance(camera, (list, tuple)):
+            cams = list(camera) if isinstance(camera, (list, tuple)) else [camera]
+            self.add_batch([probs], cams, **kw)
+            return
+        self._enqueue(probs, camera)
+
+    # session hooks (session.py): results of queued frames ------------------------------
+    fallbacks = None  # dict key -> (H*W,) int32 device network argmax, when a session asks for it
+
+    def flush(self):
+        """Fold the queued frames (one batched pass per max_batch frames)."""
+        pend = self._pending
+        if not pend:
+            return
+        self._pending = []
+        W, H = self._pending_size
+        self._pending_size = None
+        for k, it in enumerate(pend):
+            if it.version is not None and it.probs._version != it.version:
+                raise RuntimeError("the probability tensor of queued frame %d was modified in place before the "
+                                   "queue was folded; pass a copy, or call flush() before reusing the buffer" % k)
+        hw = H * W
+        with torch.cuda.device(self.device):
+            cur = torch.cuda.current_stream(self.device)
+            # frames whose IdImage came from some other rasterization (a hook returning a
+            # prepared IdImage) fold with their own row image, one at a time
+            own = [it for it in pend if it.ids is None or self._ids_from_camera(it.ids)]
+            other = [it for it in pend if not (it.ids is None or self._ids_from_camera(it.ids))]
+            fb = None
+            if self.fallbacks is not None and own:
+                fb = torch.empty((len(own), hw), dtype=torch.int32, device=self.device)
+            counts = None
+            if any(it.count is not None for it in own):
+                counts = torch.empty(len(own), dtype=torch.int64, device=self.device)
+
+                def on_rows(b0, b, rows, counts=counts):
+                    torch.sum(rows >= 0, dim=1, out=counts[b0:b0 + b])
+            else:
+                on_rows = None
+            if own:
+                with torch.cuda.stream(cur):
+                    cams = torch.as_tensor(np.stack([it.cam for it in own])).to(self.device, non_blocking=True)
+                ready = [it.ready for it in own if it.ready is not None]
+                self._fold([it.probs for it in own], cams, W, H, fb, cur, on_rows=on_rows, ready=ready)
+                for k, it in enumerate(own):
+                    if fb is not None:
+                        self.fallbacks[it.fallback_key] = fb[k]
+                    if it.count is not None:
+                        it.count._set(counts, k)
+            for it in other:
+                self._fold_rows(it, W, H, cur)
+
+    def _ids_from_camera(self, ids):
+        src = getattr(ids, "_source", None)
+        return src is not None and (src[0] is self.scene or src[0].matches(self.mesh, self.layout))
+
+    def _fold_rows(self, it, W, H, cur):
+        """One frame with an explicit IdImage (its rows on this layout)."""
+        tex = self._tex
+        tex._push_host()
+        hw = H * W
+        rows = it.ids.rows_on(self.scene).view(1, hw)
+        if it.ready is not None:
+            cur.wait_event(it.ready)
+        hits = None
+        if self.weight_mode != "pixels_iid":
+            hits = self.scene.hits(1)
+            N.call("tfb_count_hits", N.ptr(rows), hw, 1, tex.total_texels, N.ptr(hits), N.stream_handle(cur))
+        fb = torch.empty(hw, dtype=torch.int32, device=self.device) if self.fallbacks is not None else None
+        parr, _keep = N.ptr_array([it.probs.data_ptr()])
+        N.call("tfb_fuse", N.ptr(rows), hw, 1, parr, self.num_classes, N.ptr(hits), None, tex.total_texels,
+               N.AGG_IDS[tex.aggregator], N.WMODE_IDS[self.weight_mode], float(self.alpha or 0.0),
+               N.ptr(tex._accum), int(tex.is_f64), tex.stride, N.ptr(tex._counts), N.ptr(fb), N.stream_handle(cur))
+        if hits is not None:
+            N.call("tfb_clear_hits", N.ptr(rows), hw, 1, tex.total_texels, N.ptr(hits), N.stream_handle(cur))
+        if fb is not None:
+            self.fallbacks[it.fallback_key] = fb
+        if it.count is not None:
+            it.count._set((rows >= 0).sum(dim=1), 0)
+        tex._h_accum = tex._h_counts = None
+        self.frames_added += 1
 
     # -- exchange ------------------------------------------------------------------------
     def allreduce(self, group=None):
@@ -295,10 +585,12 @@ class MeshAnnotation:
             labels = torch.empty(n, dtype=torch.int32, device=acc.device)
             unobs = torch.empty(n, dtype=torch.uint8, device=acc.device)
             N.call("tfb_finalize", N.ptr(acc), int(tex.is_f64), tex.stride, N.ptr(cnt), n, c,
-                   N.AGG_IDS[tex.aggregator], None, N.ptr(unobs), N.ptr(labels), N.stream_handle())
+                   N.AGG_IDS[tex.aggregator], None, N.ptr(unobs), N.ptr(labels),
+                   N.stream_handle(torch.cuda.current_stream(acc.device)))
             return labels
 
-        tex._labels = reduce_scatter_finalize(tex._accum, tex._counts, finalize_slice, group)
+        with torch.cuda.device(self.device):
+            tex._labels = reduce_scatter_finalize(tex._accum, tex._counts, finalize_slice, group)
         tex._rows = None
         tex._unobs = None
         tex.finalized = True
@@ -308,34 +600,41 @@ class MeshAnnotation:
     def _finalize(self):
         from .fusion import finalize
 
-        if not self.texture.finalized:
-            finalize(self.texture)
+        tex = self.texture
+        if not tex.finalized:
+            with torch.cuda.device(self.device):
+                finalize(tex)
 
     def get(self, host=False):
         """Finalize once; per-texel class distributions (n_x, c) float32."""
         self._finalize()
-        return self.texture.rows if host else self.texture.rows_device
+        return self._tex.rows if host else self._tex.rows_device
 
     def labels(self, host=False):
         self._finalize()
-        return self.texture.labels_device.cpu().numpy() if host else self.texture.labels_device
+        return self._tex.labels_device.cpu().numpy() if host else self._tex.labels_device
 
     def render(self, cameras, width=None, height=None, fallback=None, host=False, stream=None):
         """Label images (B, H, W) int32 for the given cameras (renderback.py:28-56)."""
         self._finalize()
         W, H = _sizes(cameras, width, height)
-        cams = _cams_array(cameras).to(self.device, non_blocking=True)
-        B = int(cams.shape[0])
-        hw = H * W
-        out = torch.empty((B, hw), dtype=torch.int32, device=self.device)
-        labels = self.texture.labels_device
-        for b0 in range(0, B, self.max_batch):
-            b = min(self.max_batch, B - b0)
-            rows = self.scene.buffer("render_rows", (self.max_batch, hw), torch.int32)[:b]
-            self.scene.rasterize(cams[b0:b0 + b], W, H, rows, stream=stream)
-            fb = None
-            if fallback is not None:
-                fb = torch.as_tensor(fallback).to(self.device, torch.int32).reshape(B, hw)[b0:b0 + b].contiguous()
-            render_labels_device(labels, rows, hw, b, fb, out[b0:b0 + b], stream)
+        with torch.cuda.device(self.device):
+            cur = stream if stream is not None else torch.cuda.current_stream(self.device)
+            with torch.cuda.stream(cur):
+                cams = _cams_array(cameras).to(self.device, non_blocking=True)
+                B = int(cams.shape[0])
+                hw = H * W
+                out = torch.empty((B, hw), dtype=torch.int32, device=self.device)
+                fb_all = None
+                if fallback is not None:
+                    fb_all = torch.as_tensor(fallback).to(self.device, torch.int32).reshape(B, hw)
+            labels = self._tex.labels_device
+            mb = self._batch_for(W, H)
+            for b0 in range(0, B, mb):
+                b = min(mb, B - b0)
+                rows = self.scene.buffer("render_rows", (mb, hw), torch.int32)[:b]
+                self.scene.rasterize(cams[b0:b0 + b], W, H, rows, stream=cur)
+                fb = fb_all[b0:b0 + b].contiguous() if fb_all is not None else None
+                render_labels_device(labels, rows, hw, b, fb, out[b0:b0 + b], cur)
         out = out.view(B, H, W)
         return out.cpu().numpy() if host else out

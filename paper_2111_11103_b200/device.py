@@ -195,9 +195,12 @@ class DeviceScene:
         if self.mesh is None:
             raise RuntimeError("layout-only scene cannot rasterize")
         ws = self.workspace(width, height, B)
-        N.call("tfb_rasterize", self.sref, N.ptr(cams), B, int(width), int(height), N.ptr(ws), ws.numel(), 0,
-               N.ptr(rows), N.ptr(hits), N.ptr(tri), N.ptr(texel), N.ptr(depth), N.ptr(u), N.ptr(v),
-               N.stream_handle(stream))
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device):  # launches go to this scene's GPU, whatever is current
+            N.call("tfb_rasterize", self.sref, N.ptr(cams), B, int(width), int(height), N.ptr(ws), ws.numel(), 0,
+                   N.ptr(rows), N.ptr(hits), N.ptr(tri), N.ptr(texel), N.ptr(depth), N.ptr(u), N.ptr(v),
+                   N.stream_handle(stream))
 
     def cams_tensor(self, frames):
         arr = np.stack([pack_camera(f) for f in frames]) if frames else np.zeros((0, 16))

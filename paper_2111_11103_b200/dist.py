@@ -9,8 +9,9 @@ rank-local.  After the exchange every rank holds the fused texture and can
 re-render its own frames with no further communication.
 
 Backend: NCCL over NVLink/NVSwitch on GPUs (torch.distributed "nccl"); the
-same code runs on "gloo" with CPU tensors, which is how the host logic is
-tested without GPUs (tests/test_dist_gloo.py).
+same calls (reduce_scatter_tensor, all_gather_into_tensor, all_reduce) run on
+"gloo" with CPU tensors, which is how the exchange is tested without GPUs
+(tests/test_dist_gloo.py, world sizes 2 and 3: with and without padding).
 """
 
 import os
@@ -53,8 +54,34 @@ def allreduce_sum_(tensors, group=None):
     return tensors
 
 
-def _supports_reduce_scatter(group):
-    return dist.get_backend(group) == "nccl"
+def _padded(t, rows):
+    """``t`` itself when it already has ``rows`` rows, else a zero-padded copy
+    (reduce-scatter needs equal slices; n % P == 0 at every BASELINE config)."""
+    if int(t.shape[0]) == rows:
+        return t
+    pad = torch.zeros((rows,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    pad[: int(t.shape[0])] = t
+    return pad
+
+
+def reduce_scatter_rows(tensors, group=None):
+    """Sum reduce-scatter of each tensor's leading (texel-row) dimension.
+
+    Rank r receives the summed rows [r*k, (r+1)*k) of every tensor, k =
+    ceil(n/P); rows past n are padding.  One ``reduce_scatter_tensor`` per
+    tensor (NCCL ring / NVLS on the GPU box, gloo's implementation on the
+    CPU tests: the same call either way).  Returns (slices, (lo, hi))."""
+    rank, world_size = dist.get_rank(group), dist.get_world_size(group)
+    n = int(tensors[0].shape[0])
+    k = (n + world_size - 1) // world_size
+    lo, hi = min(n, rank * k), min(n, (rank + 1) * k)
+    out = []
+    for t in tensors:
+        src = _padded(t if t.is_contiguous() else t.contiguous(), k * world_size)
+        mine = torch.empty((k,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        dist.reduce_scatter_tensor(mine, src, op=dist.ReduceOp.SUM, group=group)
+        out.append(mine[: hi - lo])
+    return out, (lo, hi)
 
 
 def reduce_scatter_finalize(accum, counts, finalize_slice, group=None):
@@ -66,38 +93,19 @@ def reduce_scatter_finalize(accum, counts, finalize_slice, group=None):
     slice (``finalize_slice(acc_slice, counts_slice) -> int32 labels``) and
     the int32 labels are all-gathered (4 B per texel instead of the 4c-byte
     rows).  Returns the (n,) int32 labels, identical on every rank.
-
-    NCCL runs reduce-scatter; on backends without it (gloo, used by the CPU
-    tests) the rows are all-reduced and sliced locally, with the same result.
     """
-    rank, world_size = (dist.get_rank(group), dist.get_world_size(group)) if (
-        dist.is_available() and dist.is_initialized()) else (0, 1)
+    world_size = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
     n = int(accum.shape[0])
     if world_size == 1:
         return finalize_slice(accum, counts)
     k = (n + world_size - 1) // world_size
-    lo, hi = min(n, rank * k), min(n, (rank + 1) * k)
-    if _supports_reduce_scatter(group):
-        acc_pad = torch.zeros((k * world_size,) + tuple(accum.shape[1:]), dtype=accum.dtype, device=accum.device)
-        acc_pad[:n] = accum
-        cnt_pad = torch.zeros(k * world_size, dtype=counts.dtype, device=counts.device)
-        cnt_pad[:n] = counts
-        acc_mine = torch.empty((k,) + tuple(accum.shape[1:]), dtype=accum.dtype, device=accum.device)
-        cnt_mine = torch.empty(k, dtype=counts.dtype, device=counts.device)
-        dist.reduce_scatter_tensor(acc_mine, acc_pad, op=dist.ReduceOp.SUM, group=group)
-        dist.reduce_scatter_tensor(cnt_mine, cnt_pad, op=dist.ReduceOp.SUM, group=group)
-        acc_mine, cnt_mine = acc_mine[: hi - lo], cnt_mine[: hi - lo]
-    else:
-        acc_all, cnt_all = accum.clone(), counts.clone()
-        dist.all_reduce(acc_all, op=dist.ReduceOp.SUM, group=group)
-        dist.all_reduce(cnt_all, op=dist.ReduceOp.SUM, group=group)
-        acc_mine, cnt_mine = acc_all[lo:hi], cnt_all[lo:hi]
+    (acc_mine, cnt_mine), (lo, hi) = reduce_scatter_rows([accum, counts], group)
     mine = torch.full((k,), -1, dtype=torch.int32, device=accum.device)
     if hi > lo:
         mine[: hi - lo] = finalize_slice(acc_mine.contiguous(), cnt_mine.contiguous())
-    parts = [torch.empty_like(mine) for _ in range(world_size)]
-    dist.all_gather(parts, mine, group=group)
-    return torch.cat(parts)[:n]
+    labels = torch.empty((k * world_size,), dtype=torch.int32, device=accum.device)
+    dist.all_gather_into_tensor(labels, mine, group=group)
+    return labels[:n]
 
 
 def init_from_env(backend=None):

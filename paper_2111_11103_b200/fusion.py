@@ -63,6 +63,14 @@ class ProbabilityTexture:
         self._h_counts = None
         self._h_rows = None
         self._h_unobs = None
+        self._flush_hook = None  # weak method of a MeshAnnotation / session holding queued frames
+
+    def _flush_pending(self):
+        hook = self._flush_hook
+        if hook is not None:
+            fn = hook()
+            if fn is not None:
+                fn()
 
     @property
     def total_texels(self):
@@ -75,6 +83,7 @@ class ProbabilityTexture:
     # -- host views (reference fields) ---------------------------------------------
     @property
     def accum(self):
+        self._flush_pending()
         if self._h_accum is None:
             self._h_accum = self._accum[:, : self.num_classes].to(torch.float64).cpu().numpy()
         return self._h_accum
@@ -85,6 +94,7 @@ class ProbabilityTexture:
 
     @property
     def counts(self):
+        self._flush_pending()
         if self._h_counts is None:
             self._h_counts = self._counts.to(torch.int64).cpu().numpy()
         return self._h_counts
@@ -120,15 +130,19 @@ class ProbabilityTexture:
         return self._labels
 
     def accum_device(self):
+        self._flush_pending()
         self._push_host()
         return self._accum
 
     def counts_device(self):
+        self._flush_pending()
         self._push_host()
         return self._counts
 
     def _push_host(self):
-        """Upload host mirrors (which callers may have written) before device work."""
+        """Fold queued frames, then upload host mirrors (which callers may have
+        written) before device work."""
+        self._flush_pending()
         if self._h_accum is not None:
             a = np.asarray(self._h_accum, dtype=np.float64)
             if a.shape != (self.total_texels, self.num_classes):
@@ -181,38 +195,15 @@ def _check_mode(mode, alpha):
         raise ValueError("blend weight mode needs alpha in [0, 1]")
 
 
-class PixelWeights:
-    """compute_pixel_weights result: an (H, W) float64 image that stays symbolic
-    (mode + IdImage) so accumulate_frame can derive the weights on the device;
-    behaves as a NumPy array when read (``np.asarray``, indexing, ``.shape``)."""
+class PixelWeights(np.ndarray):
+    """compute_pixel_weights result: an (H, W) float64 ndarray (fusion.py:114-142)
+    computed on the device, read-only, that remembers how it was derived so
+    accumulate_frame can rebuild the same weights on the device from the frame's
+    hit counts instead of uploading them.  Arrays derived from it (views,
+    arithmetic, copies) are plain writable weights and take the explicit path."""
 
-    def __init__(self, ids, mode, alpha):
-        self.ids = ids
-        self.mode = mode
-        self.alpha = alpha
-        self._host = None
-
-    shape = property(lambda self: (self.ids.height, self.ids.width))
-    dtype = np.dtype(np.float64)
-    ndim = 2
-
-    def _materialize(self):
-        if self._host is None:
-            self._host = _weights_on_device(self.ids, self.mode, self.alpha).cpu().numpy().reshape(self.shape)
-        return self._host
-
-    def __array__(self, dtype=None, copy=None):
-        a = self._materialize()
-        return a.astype(dtype) if dtype is not None else a
-
-    def __getitem__(self, idx):
-        return self._materialize()[idx]
-
-    def __eq__(self, other):
-        return self._materialize() == np.asarray(other)
-
-    def __repr__(self):
-        return "PixelWeights(%s)" % (self._materialize(),)
+    def __array_finalize__(self, obj):
+        self._spec = None
 
 
 def _virtual_rows(ids, device):
@@ -233,6 +224,7 @@ def _virtual_rows(ids, device):
 def _weights_on_device(ids, mode, alpha):
     import torch as _t
 
+    ids._ensure_device()
     dev = ids._rows.device if ids._rows is not None else _t.device("cuda", _t.cuda.current_device())
     rows, n = _virtual_rows(ids, dev)
     hw = ids.width * ids.height
@@ -250,7 +242,11 @@ def compute_pixel_weights(ids, mode, alpha=None):
     """Per-pixel fusion weight for one frame (fusion.py:114-142)."""
     _check_mode(mode, alpha)
     N.require_cuda()
-    return PixelWeights(ids, mode, alpha)
+    host = _weights_on_device(ids, mode, alpha).cpu().numpy().reshape(ids.height, ids.width)
+    w = host.view(PixelWeights)
+    w._spec = (ids, mode, alpha)
+    w.flags.writeable = False
+    return w
 
 
 def _probs_device(probs, H, W, c, device):
@@ -272,6 +268,23 @@ def _probs_device(probs, H, W, c, device):
     return t.view(H * W, c)
 
 
+def _on_texture_device(fn):
+    """Run a texture operation with the texture's GPU current, so the C ABI
+    launches there and N.stream_handle() names that device's stream."""
+    import functools
+
+    @functools.wraps(fn)
+    def run(tex, *args, **kw):
+        dev = getattr(tex, "device", None)
+        if isinstance(dev, torch.device) and dev.type == "cuda":
+            with torch.cuda.device(dev):
+                return fn(tex, *args, **kw)
+        return fn(tex, *args, **kw)
+
+    return run
+
+
+@_on_texture_device
 def accumulate_frame(tex, ids, probs, weights):
     """Fold one frame's class distributions into the texture (fusion.py:145-183)."""
     if tex.finalized:
@@ -292,17 +305,15 @@ def accumulate_frame(tex, ids, probs, weights):
     hw = H * W
     hits = None
     wdev = None
-    if isinstance(weights, PixelWeights) and weights.ids is ids and weights._host is None:
-        mode = weights.mode
-        alpha = weights.alpha
+    spec = getattr(weights, "_spec", None) if isinstance(weights, PixelWeights) else None
+    if spec is not None and spec[0] is ids and not weights.flags.writeable:
+        mode, alpha = spec[1], spec[2]
         if mode != "pixels_iid":
             hits = scene.hits(1)
             N.call("tfb_count_hits", N.ptr(rows), hw, 1, tex.total_texels, N.ptr(hits), N.stream_handle())
     else:
         mode, alpha = "explicit", 0.0
         w = weights
-        if isinstance(w, PixelWeights):
-            w = w._materialize()
         if isinstance(w, torch.Tensor):
             wdev = w.detach().to(device=tex.device, dtype=torch.float64).contiguous().view(-1)
         else:
@@ -318,6 +329,7 @@ def accumulate_frame(tex, ids, probs, weights):
     return tex
 
 
+@_on_texture_device
 def finalize(tex):
     """Normalize accumulated rows into per-texel distributions (fusion.py:186-210)."""
     if tex.finalized:

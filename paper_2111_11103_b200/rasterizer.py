@@ -1,9 +1,13 @@
 """Per-frame correspondences (rasterizer.py:93-202) on the GPU.
 
-``rasterize`` returns an IdImage whose planes live in device memory; the
-host views ``triangle``/``texel``/``depth``/``u``/``v`` are materialized on
-first access (depth/u/v by a second, bit-identical rasterization that also
-writes those float64 planes — only tests and debugging read them).
+``rasterize`` returns an IdImage that is lazy: it records the camera, and the
+frame is rasterized on the device when something needs its planes (the row
+image for fusion or render, or a host view).  A session / MeshAnnotation that
+receives such an IdImage rasterizes it inside its batched fold instead, with
+the texel hit counts fused in.  The host views ``triangle``/``texel``/
+``depth``/``u``/``v`` are materialized on first access (depth/u/v by a
+second, bit-identical rasterization that also writes those float64 planes —
+only tests and debugging read them).
 IdImages can also be built on the host from arrays, as the reference's test
 helpers do (tests/helpers.py:45-61); they are uploaded when first used.
 """
@@ -14,6 +18,7 @@ import torch
 from . import _native as N
 from .device import scene_for
 from .errors import DataError
+from .geometry import pack_camera
 
 DEPTH_TIE = 1e-9  # rasterizer.py:18
 NONE = -1  # rasterizer.py:20
@@ -40,27 +45,46 @@ class IdImage:
 
     # -- construction from the device path -------------------------------------
     @classmethod
-    def _from_device(cls, frame_id, width, height, scene, cam, rows, tri=None, texel=None):
+    def _from_camera(cls, frame_id, width, height, scene, cam):
+        """Lazy IdImage of ``scene`` seen from the packed camera ``cam`` ((16,) float64)."""
         ids = cls(frame_id, width, height)
-        ids._rows = rows
-        ids._rows_scene = scene
-        ids._dev_tri = tri
-        ids._dev_texel = texel
-        ids._source = (scene, cam)
+        ids._source = (scene, np.asarray(cam, dtype=np.float64).reshape(16))
         return ids
+
+    def _cam_device(self):
+        scene, cam = self._source
+        return torch.as_tensor(cam.reshape(1, 16)).to(scene.device, non_blocking=True)
+
+    def _ensure_device(self):
+        """Rasterize a lazy IdImage once: row image + triangle / texel planes."""
+        if self._rows is not None or self._source is None:
+            return
+        scene, _cam = self._source
+        hw = self.width * self.height
+        d = scene.device
+        rows = torch.empty((1, hw), dtype=torch.int32, device=d)
+        tri = torch.empty((1, hw), dtype=torch.int32, device=d)
+        tex = torch.empty((1, hw), dtype=torch.int32, device=d)
+        with torch.cuda.device(d):
+            scene.rasterize(self._cam_device(), self.width, self.height, rows, tri=tri, texel=tex)
+        self._rows, self._rows_scene = rows.view(-1), scene
+        self._dev_tri, self._dev_texel = tri.view(-1), tex.view(-1)
 
     # -- reference field access ---------------------------------------------------
     def _materialize(self, name):
         if name in self._host:
             return self._host[name]
         H, W = self.height, self.width
+        if name in ("triangle", "texel"):
+            self._ensure_device()
         if name in ("triangle", "texel") and self._dev_tri is not None:
             self._host["triangle"] = self._dev_tri.view(H, W).cpu().numpy()
             self._host["texel"] = self._dev_texel.view(H, W).cpu().numpy()
             return self._host[name]
         if self._source is None:
             raise AttributeError("IdImage has no %s plane" % name)
-        scene, cam = self._source
+        scene, _cam = self._source
+        cam = self._cam_device()
         d = scene.device
         rows = torch.empty((1, H * W), dtype=torch.int32, device=d)
         tri = torch.empty((1, H * W), dtype=torch.int32, device=d)
@@ -68,7 +92,8 @@ class IdImage:
         dep = torch.empty((1, H * W), dtype=torch.float64, device=d)
         uu = torch.empty((1, H * W), dtype=torch.float64, device=d)
         vv = torch.empty((1, H * W), dtype=torch.float64, device=d)
-        scene.rasterize(cam, W, H, rows, tri=tri, texel=tex, depth=dep, u=uu, v=vv)
+        with torch.cuda.device(d):
+            scene.rasterize(cam, W, H, rows, tri=tri, texel=tex, depth=dep, u=uu, v=vv)
         for key, t in (("triangle", tri), ("texel", tex), ("depth", dep), ("u", uu), ("v", vv)):
             self._host.setdefault(key, t.view(H, W).cpu().numpy())
         return self._host[name]
@@ -86,6 +111,8 @@ class IdImage:
     # -- device rows ----------------------------------------------------------------
     def rows_on(self, scene):
         """(H*W,) int32 device tensor of global texel rows (offsets[t] + texel, -1 uncovered)."""
+        if self._source is not None and not self._host:
+            self._ensure_device()
         if self._rows is not None and self._rows_scene is not None and (
                 self._rows_scene is scene or self._rows_scene.same_layout(scene.layout)):
             return self._rows
@@ -107,18 +134,12 @@ class IdImage:
 
 
 def rasterize(mesh, layout, frame, device=None):
-    """Render triangle/texel correspondences for one frame (rasterizer.py:93-132)."""
+    """Render triangle/texel correspondences for one frame (rasterizer.py:93-132).
+    Lazy: the device rasterization runs when the IdImage is first used."""
     if layout.num_triangles != mesh.num_triangles:
         raise DataError("layout covers %d triangles but mesh has %d" % (layout.num_triangles, mesh.num_triangles))
     scene = scene_for(mesh, layout, device)
-    W, H = int(frame.width), int(frame.height)
-    cam = scene.cams_tensor([frame])
-    d = scene.device
-    rows = torch.empty((1, H * W), dtype=torch.int32, device=d)
-    tri = torch.empty((1, H * W), dtype=torch.int32, device=d)
-    tex = torch.empty((1, H * W), dtype=torch.int32, device=d)
-    scene.rasterize(cam, W, H, rows, tri=tri, texel=tex)
-    return IdImage._from_device(frame.frame_id, W, H, scene, cam, rows.view(-1), tri.view(-1), tex.view(-1))
+    return IdImage._from_camera(frame.frame_id, int(frame.width), int(frame.height), scene, pack_camera(frame))
 
 
 def project_point(frame, point):

@@ -2,10 +2,14 @@
 
 Public surface, names and error behaviour of the reference bindings:
 ``open_session`` / ``add_frame`` / ``finalize_and_render``.  A session keeps
-mesh, layout and texture in device memory; ``add_frame`` runs the device
-rasterizer, the fused scatter-add and the network-argmax fallback in one
-pass and does not synchronize with the host: it returns a lazily evaluated
-count of the pixel observations added.
+mesh, layout and texture in device memory.  ``add_frame`` validates the frame,
+takes its correspondence through the ``rasterize`` hook (lazy: no device work
+yet) and queues the frame on the session's MeshAnnotation, which folds queued
+frames as one batch (rasterization with fused hit counts, one scatter-add
+launch that also writes each frame's network-argmax fallback) when the batch
+is full or anything reads the texture.  It returns the covered-pixel count as
+an int-like FrameCount resolved when read, so nothing synchronizes per
+frame.
 """
 
 import threading
@@ -13,68 +17,14 @@ import threading
 import numpy as np
 import torch
 
-from . import _native as N
+from .annotation import MeshAnnotation
 from .device import scene_for
 from .errors import DataError
 from .fusion import finalize, init_texture, parse_weight_mode
 from .geometry import build_texel_layout, compute_worst_case_areas
 from .meshio import load_mesh, load_trajectory
-from .renderback import render_labels_device
 
 __all__ = ["open_session", "add_frame", "finalize_and_render"]
-
-
-class LazyCount:
-    """An int-like observation count that syncs with the device only when read."""
-
-    __slots__ = ("_t", "_v")
-
-    def __init__(self, tensor):
-        self._t = tensor
-        self._v = None
-
-    def __int__(self):
-        if self._v is None:
-            self._v = int(self._t.item())
-            self._t = None
-        return self._v
-
-    __index__ = __int__
-
-    def __eq__(self, o):
-        return int(self) == int(o)
-
-    def __ne__(self, o):
-        return int(self) != int(o)
-
-    def __lt__(self, o):
-        return int(self) < o
-
-    def __le__(self, o):
-        return int(self) <= o
-
-    def __gt__(self, o):
-        return int(self) > o
-
-    def __ge__(self, o):
-        return int(self) >= o
-
-    def __hash__(self):
-        return hash(int(self))
-
-    def __add__(self, o):
-        return int(self) + o
-
-    __radd__ = __add__
-
-    def __sub__(self, o):
-        return int(self) - o
-
-    def __rsub__(self, o):
-        return o - int(self)
-
-    def __repr__(self):
-        return repr(int(self))
 
 
 class _FusionSession:
@@ -87,9 +37,15 @@ class _FusionSession:
         self.texture = texture
         self.weight_mode = weight_mode
         self.alpha = alpha
-        self.fallbacks = {}  # frame_id -> (H*W,) int32 device tensor (the frame's own argmax)
         self.scene = scene_for(mesh, layout, texture.device)
+        self.ann = MeshAnnotation(mesh, layout, weight_mode=_spec(weight_mode, alpha), texture=texture,
+                                  device=texture.device)
+        self.ann.fallbacks = {}  # frame_id -> (H*W,) int32 device tensor (the frame's own argmax)
         self._gate = threading.Lock()
+
+    @property
+    def fallbacks(self):
+        return self.ann.fallbacks
 
     @property
     def num_texels(self):
@@ -102,6 +58,10 @@ class _FusionSession:
     @property
     def finalized(self):
         return bool(self.texture.finalized)
+
+
+def _spec(mode, alpha):
+    return "blend:%r" % alpha if mode == "blend" else mode
 
 
 def open_session(mesh_path, trajectory_path, gamma, aggregator, weight_mode, num_classes,
@@ -140,32 +100,8 @@ def add_frame(session, frame_id, probabilities):
         tex = session.texture
         if tex.finalized:
             raise RuntimeError("texture is already finalized")
-        ids = rasterize(session.mesh, session.layout, frame)
-        scene = session.scene
-        H, W, c = want
-        hw = H * W
-        if isinstance(probabilities, torch.Tensor):
-            p = probabilities.detach().to(device=tex.device, dtype=torch.float32).contiguous()
-        else:
-            p = torch.as_tensor(np.ascontiguousarray(probabilities, dtype=np.float32)).to(tex.device)
-        if p.data_ptr() % 16:
-            p = p.clone()
-        rows = ids.rows_on(scene)
-        tex._push_host()
-        hits = None
-        if session.weight_mode != "pixels_iid":
-            hits = scene.hits(1)
-            N.call("tfb_count_hits", N.ptr(rows), hw, 1, tex.total_texels, N.ptr(hits), N.stream_handle())
-        fb = torch.empty(hw, dtype=torch.int32, device=tex.device)
-        parr, _keep = N.ptr_array([p.data_ptr()])
-        N.call("tfb_fuse", N.ptr(rows), hw, 1, parr, c, N.ptr(hits), None, tex.total_texels,
-               N.AGG_IDS[tex.aggregator], N.WMODE_IDS[session.weight_mode], float(session.alpha or 0.0),
-               N.ptr(tex._accum), int(tex.is_f64), tex.stride, N.ptr(tex._counts), N.ptr(fb), N.stream_handle())
-        if hits is not None:
-            N.call("tfb_clear_hits", N.ptr(rows), hw, 1, tex.total_texels, N.ptr(hits), N.stream_handle())
-        tex._h_accum = tex._h_counts = None
-        session.fallbacks[frame_id] = fb
-        return LazyCount((rows >= 0).sum())
+        ids = rasterize(session.mesh, session.layout, frame)  # lazy IdImage: the fold rasterizes it
+        return session.ann._enqueue(probabilities, frame, ids=ids, fallback_key=frame_id, want_count=True)
     finally:
         session._gate.release()
 
@@ -178,15 +114,24 @@ def finalize_and_render(session, frame_ids=()):
     if missing:
         raise DataError("frame ids not in the trajectory: %s" % missing)
     tex = finalize(session.texture)
-    labels = tex.labels_device
     rows = np.ascontiguousarray(tex.rows.copy())
     if not frame_ids:
         return rows
-    images = []
-    for fid in frame_ids:
+    # one batched rasterize + gather per frame size (renderback.py:28-56 with the
+    # session's cached network argmax as fallback, bindings/__init__.py:136-141)
+    images = [None] * len(frame_ids)
+    by_size = {}
+    for k, fid in enumerate(frame_ids):
         fr = session.frames[fid]
-        ids = rasterize(session.mesh, session.layout, fr)
-        hw = fr.width * fr.height
-        out = render_labels_device(labels, ids.rows_on(session.scene), hw, 1, session.fallbacks.get(fid))
-        images.append(out.view(fr.height, fr.width).cpu().numpy())
+        by_size.setdefault((fr.width, fr.height), []).append(k)
+    for (W, H), ks in by_size.items():
+        frs = [session.frames[frame_ids[k]] for k in ks]
+        fbs = [session.fallbacks.get(frame_ids[k]) for k in ks]
+        fb = None
+        if any(f is not None for f in fbs):
+            fb = torch.stack([f if f is not None else torch.full((H * W,), -1, dtype=torch.int32,
+                                                                 device=tex.device) for f in fbs])
+        out = session.ann.render(frs, fallback=fb, host=True)
+        for k, img in zip(ks, out):
+            images[k] = np.ascontiguousarray(img)
     return images, rows

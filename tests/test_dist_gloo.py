@@ -108,15 +108,22 @@ def _rs_worker(rank, world, port, agg, out):
         rows, unobs = O.finalize(a.numpy(), c.numpy(), agg)
         return torch.from_numpy(O.texel_argmax(rows, unobs).astype(np.int32))
 
-    labels = D.reduce_scatter_finalize(torch.from_numpy(acc), torch.from_numpy(cnt), finalize_slice)
+    ta, tc = torch.from_numpy(acc), torch.from_numpy(cnt.astype(np.int32))  # the product's count dtype
+    (sa, sc), (lo, hi) = D.reduce_scatter_rows([ta, tc])
+    np.save(out + "_slice%d.npy" % rank, np.concatenate([sa.numpy(), sc.numpy()[:, None]], axis=1))
+    np.save(out + "_bounds%d.npy" % rank, np.array([lo, hi]))
+    labels = D.reduce_scatter_finalize(ta, tc, finalize_slice)
+    assert labels.dtype == torch.int32 and labels.shape == (acc.shape[0],)
     np.save(out + "_labels%d.npy" % rank, labels.numpy())
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_reduce_scatter_finalize_equals_single_rank_labels(tmp_path, world):
-    """Slice-wise finalize after the exchange + label all-gather == one-rank labels (uneven slices for 3)."""
+    """The product exchange (dist.reduce_scatter_rows + reduce_scatter_finalize: reduce_scatter_tensor,
+    slice-wise finalize, all_gather_into_tensor) == one-rank labels.  cfg1 has 13,468 texels: world 2
+    and 4 divide it (no padding copy), world 3 does not (padded last slice)."""
     out = str(tmp_path / "rs")
     mp.spawn(_rs_worker, args=(world, _free_port(), "mul", out), nprocs=world, join=True)
     import oracle as O
@@ -125,7 +132,13 @@ def test_reduce_scatter_finalize_equals_single_rank_labels(tmp_path, world):
     acc1, cnt1 = _fold(z, probs, range(len(z["cams"])), "mul")
     rows, unobs = O.finalize(acc1, cnt1, "mul")
     ref = O.texel_argmax(rows, unobs)
+    k = (len(cnt1) + world - 1) // world
     for r in range(world):
+        lo, hi = np.load(out + "_bounds%d.npy" % r)
+        assert (lo, hi) == (min(len(cnt1), r * k), min(len(cnt1), (r + 1) * k))
+        sl = np.load(out + "_slice%d.npy" % r)
+        np.testing.assert_allclose(sl[:, :-1], acc1[lo:hi], rtol=1e-12, atol=1e-12)
+        np.testing.assert_array_equal(sl[:, -1], cnt1[lo:hi])
         got = np.load(out + "_labels%d.npy" % r)
         decided = np.ones(len(ref), bool)
         top2 = np.sort(rows, axis=1)[:, -2:]

@@ -4,6 +4,7 @@ loop (rasterize -> compute_pixel_weights -> accumulate_frame), device maps.
 
     python tools/bench_session.py [frames]
 """
+import json
 import os
 import sys
 import tempfile
@@ -14,42 +15,59 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from paper_2111_11103_b200 import (Mesh, accumulate_frame, compute_pixel_weights, finalize,  # noqa: E402
+from paper_2111_11103_b200 import (Mesh, MeshAnnotation, accumulate_frame, compute_pixel_weights, finalize,  # noqa: E402
                                    init_texture, rasterize, save_ply, save_trajectory, uniform_layout)
 from paper_2111_11103_b200.session import add_frame, finalize_and_render, open_session  # noqa: E402
 from paper_2111_11103_b200.synth import make_room, random_room_trajectory, scannet_intrinsics, softmax_maps  # noqa: E402
 
 
 def main():
-    n = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
     v, t = make_room((6.0, 5.0, 3.0), 158)
     mesh = Mesh.from_arrays(v, t)
     frames = random_room_trajectory(n, scannet_intrinsics(), seed=0)
     maps = softmax_maps(8, 480, 640, 40, seed=0)
+    out = {"frames": n}
     with tempfile.TemporaryDirectory() as d:
         mp, tp = os.path.join(d, "m.ply"), os.path.join(d, "t.txt")
         save_ply(mp, mesh)
         save_trajectory(tp, frames)
-        s = open_session(mp, tp, 0.0, "mul", "images_iid", 40, accum_dtype="float32")
-        add_frame(s, frames[0].frame_id, maps[0])
-        torch.cuda.synchronize()
-        t0 = time.time()
-        for i, fr in enumerate(frames):
-            add_frame(s, fr.frame_id, maps[i % 8])
-        torch.cuda.synchronize()
-        dt = time.time() - t0
-        finalize_and_render(s, [frames[0].frame_id])
-    print("session add_frame: %.0f frames/s (%d frames, wall clock)" % (n / dt, n))
-    layout = uniform_layout(mesh, 1)
-    tex = init_texture(layout, 40, "mul", accum_dtype="float32")
+        for acc in ("float32", "float64"):
+            s = open_session(mp, tp, 0.0, "mul", "images_iid", 40, accum_dtype=acc)
+            add_frame(s, frames[0].frame_id, maps[0])
+            s.ann.flush()
+            torch.cuda.synchronize()
+            t0 = time.time()
+            for i, fr in enumerate(frames):
+                add_frame(s, fr.frame_id, maps[i % 8])
+            s.ann.flush()
+            torch.cuda.synchronize()
+            dt = time.time() - t0
+            finalize_and_render(s, [frames[0].frame_id])
+            out["session_add_frame_%s" % acc] = round(n / dt)
+    ann = MeshAnnotation(mesh, uniform_layout(mesh, 1), num_classes=40, aggregator="mul")
+    ann.add(maps[0], frames[0])
+    ann.flush()
     torch.cuda.synchronize()
     t0 = time.time()
     for i, fr in enumerate(frames):
+        ann.add(maps[i % 8], fr)
+    ann.labels()
+    torch.cuda.synchronize()
+    out["meshannotation_add_float32"] = round(n / (time.time() - t0))
+    layout = uniform_layout(mesh, 1)
+    tex = init_texture(layout, 40, "mul", accum_dtype="float32")
+    m = min(n, 300)
+    torch.cuda.synchronize()
+    t0 = time.time()
+    for i, fr in enumerate(frames[:m]):
         ids = rasterize(mesh, layout, fr)
         accumulate_frame(tex, ids, maps[i % 8], compute_pixel_weights(ids, "images_iid"))
     finalize(tex)
     torch.cuda.synchronize()
-    print("library loop: %.0f frames/s (%d frames, wall clock)" % (n / (time.time() - t0), n))
+    out["library_loop_float32"] = round(m / (time.time() - t0))
+    out["note"] = "wall clock, device maps (8-map pool), cfg2 scene, frames/s; library loop over %d frames" % m
+    print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":
