@@ -48,6 +48,12 @@ extern "C" {
 #define TFB_W_BLEND 2
 #define TFB_W_EXPLICIT 3 /* caller-provided per-pixel weights (fusion.py:145 `weights`) */
 
+/* accumulator element kinds (tfb_fuse / tfb_finalize `accum_kind`) */
+#define TFB_ACCUM_F32 0   /* float32: red.global.add.v4.f32, the throughput mode */
+#define TFB_ACCUM_F64 1   /* float64: atomicAdd(double), the reference's precision */
+#define TFB_ACCUM_FIXED 2 /* int64 fixed point, value * 2^32: integer atomics are order-free, so
+                             reruns are bit-identical (the CLI's deterministic=true, SPEC criterion 9) */
+
 /* Mesh + texel layout resident on the device (geometry.py:31-77, 208-232). */
 typedef struct tfb_scene {
   const double *vertices;   /* (num_vertices, 3) float64, world metres     */
@@ -137,20 +143,23 @@ int tfb_pixel_weights(const int32_t *rows, int64_t hw, int nframes, const uint32
  * accumulators and count-derived weights take the specialised kernel; any
  * class count up to ~880 is accepted.  weight_mode TFB_W_EXPLICIT reads `weights`
  * (nframes*H*W float64), the other modes derive w from `texel_hits`.
- * accum: (total_texels, accum_stride) float32 (accum_is_f64 = 0; stride a
- * multiple of 4) or float64 (accum_is_f64 = 1); log-space for TFB_AGG_MUL.
+ * accum: (total_texels, accum_stride) float32 (accum_kind TFB_ACCUM_F32; stride
+ * a multiple of 4), float64 (TFB_ACCUM_F64) or int64 fixed point in units of
+ * 2^-32 (TFB_ACCUM_FIXED: each piece of equal-row pixels is summed in float64
+ * in a fixed order, rounded once and added with an integer atomic, so the
+ * result does not depend on scheduling); log-space for TFB_AGG_MUL.
  * counts: (total_texels,) u32 observation counts.  fallback_out (optional,
  * nframes*H*W int32): the per-pixel network argmax probs.argmax(axis=2)
  * (cli.py:293, bindings/__init__.py:112), fused into the same pass. */
 int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const float *const *probs, int num_classes,
              const uint32_t *texel_hits, const double *weights, int64_t total_texels, int aggregator,
-             int weight_mode, double alpha, void *accum, int accum_is_f64, int64_t accum_stride,
+             int weight_mode, double alpha, void *accum, int accum_kind, int64_t accum_stride,
              uint32_t *counts, int32_t *fallback_out, void *stream);
 
 /* finalize + texel_argmax (fusion.py:186-222).  rows_out (total_texels*c
  * float32), unobserved_out (u8) and labels_out (int32, UNKNOWN = -1) are each
  * optional. */
-int tfb_finalize(const void *accum, int accum_is_f64, int64_t accum_stride, const uint32_t *counts,
+int tfb_finalize(const void *accum, int accum_kind, int64_t accum_stride, const uint32_t *counts,
                  int64_t total_texels, int num_classes, int aggregator, float *rows_out,
                  uint8_t *unobserved_out, int32_t *labels_out, void *stream);
 

@@ -235,13 +235,14 @@ int tfo_fuse_frames(const double *verts, int64_t nv, const int32_t *tris, int64_
   if (!accs || !cnts) { free(accs); free(cnts); return 1; }
 #pragma omp parallel num_threads(nthreads)
   {
-    double *acc = (double *)calloc((size_t)(n_x * c), sizeof(double));
-    int64_t *cnt = (int64_t *)calloc((size_t)n_x, sizeof(int64_t));
 #ifdef _OPENMP
     int me = omp_get_thread_num(), team = omp_get_num_threads();
 #else
     int me = 0, team = 1;
 #endif
+    /* a team of one folds straight into the caller's arrays (no private copy: large layouts) */
+    double *acc = team == 1 ? accum : (double *)calloc((size_t)(n_x * c), sizeof(double));
+    int64_t *cnt = team == 1 ? counts : (int64_t *)calloc((size_t)n_x, sizeof(int64_t));
     int32_t *frame_cnt = (int32_t *)calloc((size_t)n_x, sizeof(int32_t));
     int32_t *tri = (int32_t *)malloc(sizeof(int32_t) * npx);
     int32_t *tex = (int32_t *)malloc(sizeof(int32_t) * npx);
@@ -292,7 +293,7 @@ int tfo_fuse_frames(const double *verts, int64_t nv, const int32_t *tris, int64_
 #pragma omp barrier
     /* thread me sums texel rows [lo, hi) over all private accumulators, in thread order */
     int64_t lo = n_x * me / team, hi = n_x * (me + 1) / team;
-    for (int q = 0; q < team; ++q) {
+    for (int q = 0; q < team && team > 1; ++q) {
       if (!accs[q]) continue;
       const double *aq = accs[q];
       const int64_t *cq = cnts[q];
@@ -300,7 +301,8 @@ int tfo_fuse_frames(const double *verts, int64_t nv, const int32_t *tris, int64_
       for (int64_t i = lo; i < hi; ++i) counts[i] += cq[i];
     }
 #pragma omp barrier
-    free(acc); free(cnt); free(frame_cnt); free(tri); free(tex); free(dep); free(rows); free(contrib);
+    if (team > 1) { free(acc); free(cnt); }
+    free(frame_cnt); free(tri); free(tex); free(dep); free(rows); free(contrib);
   }
   free(accs); free(cnts);
   return err;

@@ -46,7 +46,7 @@ from .formats import (
     write_texture,
 )
 from .meshio import load_mesh, load_trajectory, save_ply, save_trajectory
-from .rasterizer import IdImage, pixel_world_points, project_point, rasterize
+from .rasterizer import IdImage, dump_debug_images, pixel_world_points, project_point, rasterize
 from .renderback import (
     EvalReport,
     colorize_labels,
@@ -61,7 +61,15 @@ from .renderback import (
     select_frames,
     write_label_png,
 )
-from .synth import NoiseModel, corrupt, make_orbit_trajectory
+from .synthgen import (
+    NoiseModel,
+    SyntheticScene,
+    corrupt,
+    make_orbit_trajectory,
+    make_scene,
+    render_ground_truth,
+    write_scene_dir,
+)
 
 __version__ = "0.1.0"
 
@@ -90,5 +98,6 @@ __all__ = [
     "EvalReport", "NoiseModel", "colorize_labels", "corrupt", "default_palette", "export_colored_mesh",
     "load_palette", "make_orbit_trajectory", "merge_reports", "pixel_accuracy", "read_label_png",
     "read_probability_header", "read_probability_image", "read_texture", "save_palette", "select_frames",
-    "write_label_png", "write_probability_image", "write_texture",
+    "write_label_png", "write_probability_image", "write_texture", "SyntheticScene", "make_scene",
+    "render_ground_truth", "write_scene_dir",
 ]

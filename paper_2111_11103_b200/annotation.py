@@ -69,43 +69,33 @@ def _device_ready(p, device):
 class _Pending:
     """A queued frame: device probabilities, packed camera, and what to report back."""
 
-    __slots__ = ("probs", "cam", "version", "ids", "ready", "fallback_key", "count")
+    __slots__ = ("probs", "cam", "version", "ids", "ready", "fallback_key")
 
-    def __init__(self, probs, cam, version, ids=None, ready=None, fallback_key=None, count=None):
+    def __init__(self, probs, cam, version, ids=None, ready=None, fallback_key=None):
         self.probs = probs
         self.cam = cam
         self.version = version
         self.ids = ids
         self.ready = ready
         self.fallback_key = fallback_key
-        self.count = count
 
 
 class FrameCount:
     """Covered pixels of one queued frame (the int add_frame returns,
-    bindings/__init__.py:113), resolved when read: reading it folds the queue."""
+    bindings/__init__.py:113), computed only when read -- from the frame's lazy
+    IdImage, so reading it neither folds the queue nor costs the unread ones."""
 
-    __slots__ = ("_owner", "_t", "_i", "_v")
+    __slots__ = ("_ids", "_scene", "_v")
 
-    def __init__(self, owner):
-        self._owner = owner
-        self._t = None
-        self._i = 0
+    def __init__(self, ids, scene):
+        self._ids = ids
+        self._scene = scene
         self._v = None
-
-    def _set(self, tensor, index):
-        self._t, self._i = tensor, index
 
     def __int__(self):
         if self._v is None:
-            if self._t is None:
-                owner = self._owner()
-                if owner is not None:
-                    owner.flush()
-            if self._t is None:
-                raise RuntimeError("the frame was discarded before it was folded (reset())")
-            self._v = int(self._t[self._i].item())
-            self._t = None
+            self._v = int((self._ids.rows_on(self._scene) >= 0).sum().item())
+            self._ids = self._scene = None
         return self._v
 
     __index__ = __int__
@@ -146,6 +136,39 @@ class FrameCount:
         return repr(int(self))
 
 
+class FallbackMap(dict):
+    """key -> (H*W,) int32 device network argmax of a folded frame; entries are
+    stored as (batch buffer, index) and viewed on access (no per-frame views).
+    ``reserve`` pre-sizes one arena per frame size (a session knows its
+    trajectory), so folds take rows from it instead of allocating per batch."""
+
+    def __init__(self):
+        super().__init__()
+        self._arena = {}  # (W, H) -> [tensor (n, H*W) int32 or None, capacity, next free row]
+
+    def reserve(self, size, nframes):
+        self._arena[size] = [None, int(nframes), 0]
+
+    def rows_for(self, size, b, device):
+        """(b, H*W) int32 device rows for the network argmax of b frames."""
+        a = self._arena.get(size)
+        hw = size[0] * size[1]
+        if a is not None and a[2] + b <= a[1]:
+            if a[0] is None:
+                a[0] = torch.empty((a[1], hw), dtype=torch.int32, device=device)
+            out = a[0][a[2]:a[2] + b]
+            a[2] += b
+            return out
+        return torch.empty((b, hw), dtype=torch.int32, device=device)
+
+    def __getitem__(self, key):
+        buf, k = dict.__getitem__(self, key)
+        return buf[k]
+
+    def get(self, key, default=None):
+        return self[key] if key in self else default
+
+
 class MeshAnnotation:
     """Fuse per-frame class probabilities onto a mesh's texels on the GPU."""
 
@@ -165,6 +188,7 @@ class MeshAnnotation:
         self.num_classes = int(texture.num_classes)
         self.scene = scene_for(mesh, self.layout, texture.device)
         self.device = self.scene.device
+        self._dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         # None: sized per frame size from the free device memory (_batch_for)
         self.max_batch = None if max_batch is None else max(1, min(int(max_batch), MAX_BATCH_CAP))
         self._auto_batch = {}
@@ -175,6 +199,7 @@ class MeshAnnotation:
         self.frames_added = 0
         self._pending = []
         self._pending_size = None
+        self._cam_ring = None
         texture._flush_hook = weakref.WeakMethod(self.flush)
         # Overlap mode: batch k+1 is rasterized on a side stream while batch k
         # is scatter-added on the caller's stream (double-buffered row / hit
@@ -245,7 +270,7 @@ class MeshAnnotation:
         tex._push_host()
         torch.cuda.synchronize(self.device)
         np.savez(path, version=np.int64(self.CHECKPOINT_VERSION),
-                 accum=tex._accum[:, : self.num_classes].cpu().numpy(), counts=tex._counts.cpu().numpy(),
+                 accum=tex.accum_values().cpu().numpy(), counts=tex._counts.cpu().numpy(),
                  frames_added=np.int64(self.frames_added), num_classes=np.int64(self.num_classes),
                  aggregator=np.array(tex.aggregator), weight_mode=np.array(self.weight_mode),
                  alpha=np.float64(self.alpha or 0.0), total_texels=np.int64(tex.total_texels),
@@ -276,7 +301,7 @@ class MeshAnnotation:
             if accum.shape != (tex.total_texels, self.num_classes) or counts.shape != (tex.total_texels,):
                 raise DataError("checkpoint arrays have the wrong shape")
             self.reset()
-            tex._accum[:, : self.num_classes].copy_(torch.as_tensor(accum).to(self.device, tex.dtype))
+            tex._accum[:, : self.num_classes].copy_(tex.accum_from_values(accum))
             tex._counts.copy_(torch.as_tensor(counts).to(self.device, tex._counts.dtype))
             self.frames_added = int(z["frames_added"])
 
@@ -304,7 +329,7 @@ class MeshAnnotation:
                     q = p.detach().to(device=self.device, dtype=torch.float32).contiguous()
                     if q.data_ptr() % 16 or q.data_ptr() == p.data_ptr():
                         q = q.clone()
-                items[i] = q
+                items[i] = q  # made on cur, read on cur: no cross-stream lifetime to track
         need_stage = [i for i, p in enumerate(items) if not (isinstance(p, torch.Tensor) and p.is_cuda)]
         ready, slot = None, None
         if need_stage:
@@ -343,7 +368,7 @@ class MeshAnnotation:
                 cams_all = _cams_array(cameras).to(self.device, non_blocking=True)
             self._fold(probs, cams_all, W, H, fallback_out, cur)
 
-    def _fold(self, probs, cams_all, W, H, fallback_out, cur, on_rows=None, ready=()):
+    def _fold(self, probs, cams_all, W, H, fallback_out, cur, ready=()):
         """The batched pipeline over B frames with device cameras ``cams_all``."""
         tex = self._tex
         if tex.finalized:
@@ -383,15 +408,12 @@ class MeshAnnotation:
                 cur.wait_event(ev)
             if copied is not None:
                 cur.wait_event(copied)
-            if on_rows is not None:
-                with torch.cuda.stream(cur):
-                    on_rows(b0, b, rows)
             f0 = self._event(cur) if prof is not None else None
             parr, _k = N.ptr_array(ptrs)
             fb = fallback_out[b0:b0 + b] if fallback_out is not None else None
             N.call("tfb_fuse", N.ptr(rows), hw, b, parr, self.num_classes, N.ptr(hits), None, tex.total_texels,
                    N.AGG_IDS[tex.aggregator], N.WMODE_IDS[self.weight_mode], float(self.alpha or 0.0),
-                   N.ptr(tex._accum), int(tex.is_f64), tex.stride, N.ptr(tex._counts), N.ptr(fb),
+                   N.ptr(tex._accum), tex.accum_kind, tex.stride, N.ptr(tex._counts), N.ptr(fb),
                    N.stream_handle(cur))
             if prof is not None:
                 prof.append((b, r0, r1, f0, self._event(cur)))
@@ -410,9 +432,6 @@ class MeshAnnotation:
                 ev = torch.cuda.Event()
                 ev.record(cur)
                 self._free[slot] = ev
-            for p in keep:  # inputs converted or staged on other streams stay valid until read
-                if isinstance(p, torch.Tensor) and p.is_cuda:
-                    p.record_stream(cur)
             del keep
         tex._h_accum = tex._h_counts = None
         self.frames_added += B
@@ -457,18 +476,27 @@ class MeshAnnotation:
         tex = self._tex
         if tex.finalized:
             raise RuntimeError("texture is already finalized")
-        W, H = int(camera.width), int(camera.height)
+        intr = camera.intrinsics
+        W, H = int(intr.width), int(intr.height)
         if self._pending and self._pending_size != (W, H):
             self.flush()
-        with torch.cuda.device(self.device):
-            cur = torch.cuda.current_stream(self.device)
-            p, version, ready = self._stage_one(probs, H, W, cur)
-        count = FrameCount(weakref.ref(self)) if want_count else None
-        self._pending.append(_Pending(p, pack_camera(camera), version, ids, ready, fallback_key, count))
+        src = getattr(ids, "_source", None)
+        cam = src[1] if src is not None else pack_camera(camera)
+        if (type(probs) is torch.Tensor and probs.is_cuda and probs.dtype is torch.float32
+                and probs.get_device() == self._dev_index and probs.is_contiguous() and not probs.data_ptr() & 15):
+            if probs.shape != (H, W, self.num_classes):
+                raise DataError("probability array shape %s does not match expected %s"
+                                % (tuple(probs.shape), (H, W, self.num_classes)))
+            item = _Pending(probs, cam, probs._version, ids, None, fallback_key)
+        else:
+            with torch.cuda.device(self.device):
+                p, version, ready = self._stage_one(probs, H, W, torch.cuda.current_stream(self.device))
+            item = _Pending(p, cam, version, ids, ready, fallback_key)
+        self._pending.append(item)
         self._pending_size = (W, H)
         if len(self._pending) >= self._batch_for(W, H):
             self.flush()
-        return count
+        return FrameCount(ids, self.scene) if want_count else None
 
     def add(self, probs, camera, **kw):
         """Queue one (H, W, c) probability map seen from ``camera``; it is folded
@@ -482,7 +510,7 @@ class MeshAnnotation:
         self._enqueue(probs, camera)
 
     # session hooks (session.py): results of queued frames ------------------------------
-    fallbacks = None  # dict key -> (H*W,) int32 device network argmax, when a session asks for it
+    fallbacks = None  # FallbackMap key -> (H*W,) int32 device network argmax, when a session asks for it
 
     def flush(self):
         """Fold the queued frames (one batched pass per max_batch frames)."""
@@ -505,27 +533,38 @@ class MeshAnnotation:
             other = [it for it in pend if not (it.ids is None or self._ids_from_camera(it.ids))]
             fb = None
             if self.fallbacks is not None and own:
-                fb = torch.empty((len(own), hw), dtype=torch.int32, device=self.device)
-            counts = None
-            if any(it.count is not None for it in own):
-                counts = torch.empty(len(own), dtype=torch.int64, device=self.device)
-
-                def on_rows(b0, b, rows, counts=counts):
-                    torch.sum(rows >= 0, dim=1, out=counts[b0:b0 + b])
-            else:
-                on_rows = None
+                fb = self.fallbacks.rows_for((W, H), len(own), self.device)
             if own:
-                with torch.cuda.stream(cur):
-                    cams = torch.as_tensor(np.stack([it.cam for it in own])).to(self.device, non_blocking=True)
+                cams = self._upload_cams([it.cam for it in own], cur)
                 ready = [it.ready for it in own if it.ready is not None]
-                self._fold([it.probs for it in own], cams, W, H, fb, cur, on_rows=on_rows, ready=ready)
-                for k, it in enumerate(own):
-                    if fb is not None:
-                        self.fallbacks[it.fallback_key] = fb[k]
-                    if it.count is not None:
-                        it.count._set(counts, k)
+                self._fold([it.probs for it in own], cams, W, H, fb, cur, ready=ready)
+                if fb is not None:
+                    for k, it in enumerate(own):
+                        self.fallbacks[it.fallback_key] = (fb, k)
             for it in other:
                 self._fold_rows(it, W, H, cur)
+
+    def _upload_cams(self, rows, cur):
+        """(B, 16) device cameras through a reusable pinned host ring: a copy from
+        pageable memory would wait for the stream, stalling the host behind the
+        batches already queued instead of overlapping them."""
+        ring = self._cam_ring
+        if ring is None or ring[0].shape[1] < len(rows):
+            n = max(len(rows), MAX_BATCH_CAP)
+            ring = self._cam_ring = (torch.empty((2, n, 16), dtype=torch.float64).pin_memory(), [None, None], [0])
+        host, done, nxt = ring
+        slot = nxt[0]
+        nxt[0] ^= 1
+        if done[slot] is not None:
+            done[slot].synchronize()  # the copy that last read this slot has finished
+        buf = host[slot, : len(rows)]
+        buf.numpy()[:] = np.stack(rows)
+        with torch.cuda.stream(cur):
+            cams = buf.to(self.device, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        done[slot] = ev
+        return cams
 
     def _ids_from_camera(self, ids):
         src = getattr(ids, "_source", None)
@@ -547,13 +586,11 @@ class MeshAnnotation:
         parr, _keep = N.ptr_array([it.probs.data_ptr()])
         N.call("tfb_fuse", N.ptr(rows), hw, 1, parr, self.num_classes, N.ptr(hits), None, tex.total_texels,
                N.AGG_IDS[tex.aggregator], N.WMODE_IDS[self.weight_mode], float(self.alpha or 0.0),
-               N.ptr(tex._accum), int(tex.is_f64), tex.stride, N.ptr(tex._counts), N.ptr(fb), N.stream_handle(cur))
+               N.ptr(tex._accum), tex.accum_kind, tex.stride, N.ptr(tex._counts), N.ptr(fb), N.stream_handle(cur))
         if hits is not None:
             N.call("tfb_clear_hits", N.ptr(rows), hw, 1, tex.total_texels, N.ptr(hits), N.stream_handle(cur))
         if fb is not None:
-            self.fallbacks[it.fallback_key] = fb
-        if it.count is not None:
-            it.count._set((rows >= 0).sum(dim=1), 0)
+            self.fallbacks[it.fallback_key] = (fb.view(1, hw), 0)
         tex._h_accum = tex._h_counts = None
         self.frames_added += 1
 
@@ -584,7 +621,7 @@ class MeshAnnotation:
             n = int(acc.shape[0])
             labels = torch.empty(n, dtype=torch.int32, device=acc.device)
             unobs = torch.empty(n, dtype=torch.uint8, device=acc.device)
-            N.call("tfb_finalize", N.ptr(acc), int(tex.is_f64), tex.stride, N.ptr(cnt), n, c,
+            N.call("tfb_finalize", N.ptr(acc), tex.accum_kind, tex.stride, N.ptr(cnt), n, c,
                    N.AGG_IDS[tex.aggregator], None, N.ptr(unobs), N.ptr(labels),
                    N.stream_handle(torch.cuda.current_stream(acc.device)))
             return labels

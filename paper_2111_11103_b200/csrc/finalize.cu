@@ -19,6 +19,11 @@ __device__ __forceinline__ bool better(float a, int ia, float b, int ib) {
 // in registers between the sum and the rows (up to kKeep per lane).
 constexpr int kKeep = 8;
 
+// accumulator element as float64 (TFB_ACCUM_FIXED elements are value * 2^32)
+__device__ __forceinline__ double acc_val(float x) { return (double)x; }
+__device__ __forceinline__ double acc_val(double x) { return x; }
+__device__ __forceinline__ double acc_val(long long x) { return (double)x * 2.3283064365386963e-10; }
+
 template <typename AccT, int L>
 __global__ void __launch_bounds__(256) k_finalize(const AccT *__restrict__ accum, int64_t stride,
                                                   const uint32_t *__restrict__ counts, int64_t n_x, int c, int agg,
@@ -39,17 +44,17 @@ __global__ void __launch_bounds__(256) k_finalize(const AccT *__restrict__ accum
     if (agg == TFB_AGG_MUL) {
       // rows = exp(accum - rowmax) / sum  (fusion.py:196-200)
       double mx = -INFINITY;
-      for (int k = sub; k < c; k += L) mx = fmax(mx, (double)a[k]);
+      for (int k = sub; k < c; k += L) mx = fmax(mx, acc_val(a[k]));
 #pragma unroll
       for (int d = L / 2; d; d >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, d, L));
       double sacc = 0.0;
 #pragma unroll
       for (int kk = 0; kk < kKeep; ++kk) {
         const int k = sub + kk * L;
-        ex[kk] = k < c ? exp((double)a[k] - mx) : 0.0;
+        ex[kk] = k < c ? exp(acc_val(a[k]) - mx) : 0.0;
         sacc += ex[kk];
       }
-      for (int k = sub + kKeep * L; k < c; k += L) sacc += exp((double)a[k] - mx);
+      for (int k = sub + kKeep * L; k < c; k += L) sacc += exp(acc_val(a[k]) - mx);
 #pragma unroll
       for (int d = L / 2; d; d >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, d, L);
       shift = mx;
@@ -58,7 +63,7 @@ __global__ void __launch_bounds__(256) k_finalize(const AccT *__restrict__ accum
     } else {
       // rows = accum / L1 norm; zero mass counts as unobserved (fusion.py:202-205)
       double sacc = 0.0;
-      for (int k = sub; k < c; k += L) sacc += (double)a[k];
+      for (int k = sub; k < c; k += L) sacc += acc_val(a[k]);
 #pragma unroll
       for (int d = L / 2; d; d >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, d, L);
       unobs = zero_count || sacc <= 0.0;  // a NaN mass stays observed, rows = accum / 1 (fusion.py:203-205)
@@ -78,11 +83,11 @@ __global__ void __launch_bounds__(256) k_finalize(const AccT *__restrict__ accum
 #pragma unroll
           for (int q = 0; q < kKeep; ++q) e = q == kk ? ex[q] : e;
         } else {
-          e = exp((double)a[k] - shift);
+          e = exp(acc_val(a[k]) - shift);
         }
         v = (float)(e / scale);
       } else {
-        v = (float)((double)a[k] / scale);
+        v = (float)(acc_val(a[k]) / scale);
       }
       if (rows_out && live) rows_out[i * c + k] = v;
       if (bi == 0x7fffffff || better(v, k, bv, bi)) {
@@ -143,7 +148,7 @@ unsigned grid_for(int64_t n) {
 
 using namespace tfb;
 
-extern "C" int tfb_finalize(const void *accum, int accum_is_f64, int64_t accum_stride, const uint32_t *counts,
+extern "C" int tfb_finalize(const void *accum, int accum_kind, int64_t accum_stride, const uint32_t *counts,
                             int64_t total_texels, int num_classes, int aggregator, float *rows_out,
                             uint8_t *unobserved_out, int32_t *labels_out, void *stream) {
   TFB_REQUIRE(aggregator >= 0 && aggregator <= 2, TFB_ERR_VALUE, "unknown aggregator id %d", aggregator);
@@ -156,7 +161,17 @@ extern "C" int tfb_finalize(const void *accum, int accum_is_f64, int64_t accum_s
   int64_t blocks = (total_texels + per_block - 1) / per_block;
   if (blocks > 148 * 64) blocks = 148 * 64;
   const unsigned g = (unsigned)blocks;
-  if (accum_is_f64) {
+  TFB_REQUIRE(accum_kind >= TFB_ACCUM_F32 && accum_kind <= TFB_ACCUM_FIXED, TFB_ERR_VALUE,
+              "unknown accumulator kind %d", accum_kind);
+  if (accum_kind == TFB_ACCUM_FIXED) {
+    const long long *a = static_cast<const long long *>(accum);
+    if (narrow)
+      k_finalize<long long, 8><<<g, 256, 0, st>>>(a, accum_stride, counts, total_texels, num_classes, aggregator,
+                                                  rows_out, unobserved_out, labels_out);
+    else
+      k_finalize<long long, 32><<<g, 256, 0, st>>>(a, accum_stride, counts, total_texels, num_classes, aggregator,
+                                                   rows_out, unobserved_out, labels_out);
+  } else if (accum_kind == TFB_ACCUM_F64) {
     const double *a = static_cast<const double *>(accum);
     if (narrow)
       k_finalize<double, 8><<<g, 256, 0, st>>>(a, accum_stride, counts, total_texels, num_classes, aggregator,
@@ -178,8 +193,8 @@ extern "C" int tfb_finalize(const void *accum, int accum_is_f64, int64_t accum_s
 
 extern "C" int tfb_render(const int32_t *rows, int64_t hw, int nframes, const int32_t *texel_labels,
                           int64_t total_texels, const int32_t *fallback, int32_t *out, void *stream) {
-  (void)total_texels;
-  TFB_REQUIRE(rows && texel_labels && out, TFB_ERR_DATA, "tfb_render: null argument");
+  // an empty layout has no labels (every row is -1): texel_labels may then be NULL
+  TFB_REQUIRE(rows && out && (texel_labels || total_texels == 0), TFB_ERR_DATA, "tfb_render: null argument");
   const int64_t n = hw * (int64_t)nframes;
   if (n <= 0) return TFB_OK;
   k_render<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(rows, n, texel_labels, fallback, out);

@@ -243,7 +243,12 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
   return *reinterpret_cast<float2 *>(&r);
 }
 
-template <typename AccT, int AGG, bool EQW>
+// fixed-point accumulator element (TFB_ACCUM_FIXED): value * 2^32, round to nearest
+__device__ __forceinline__ unsigned long long to_fixed(double x) {
+  return (unsigned long long)__double2ll_rn(x * 4294967296.0);
+}
+
+template <typename AccT, int AGG, bool EQW, bool FIX = false>
 __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ FuseParams p) {
   // product rule in float32 with weights constant per run: fold w*log(prod p)
   constexpr bool kProd = (AGG == TFB_AGG_MUL) && EQW && sizeof(AccT) == 4;
@@ -418,7 +423,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              if (k0 + k < c) atomicAdd(dst + k, v[k]);
+              if (k0 + k < c) {
+                if (FIX)  // integer adds commute exactly: the sum is independent of the atomic order
+                  atomicAdd(reinterpret_cast<unsigned long long *>(dst) + k, to_fixed(v[k]));
+                else
+                  atomicAdd(dst + k, v[k]);
+              }
           }
         };
 #pragma unroll 2
@@ -898,10 +908,10 @@ int launch_persistent(Kern kern, LaunchCache &lc, size_t per_warp, const FusePar
   return check_launch("tfb_fuse");
 }
 
-template <typename AccT, int AGG, bool EQW>
+template <typename AccT, int AGG, bool EQW, bool FIX = false>
 int launch_fuse(const FuseParams &p, cudaStream_t st) {
   static LaunchCache lc;
-  return launch_persistent(k_fuse<AccT, AGG, EQW>, lc, warp_layout(p.c, p.NS, (int)sizeof(AccT)).total, p, st);
+  return launch_persistent(k_fuse<AccT, AGG, EQW, FIX>, lc, warp_layout(p.c, p.NS, (int)sizeof(AccT)).total, p, st);
 }
 
 template <int AGG, bool VEC, int CC = 0>
@@ -926,9 +936,10 @@ int launch_fuse_fast_c(const FuseParams &p, bool vec, cudaStream_t st) {
   return vec ? launch_fuse_fast<AGG, true>(p, st) : launch_fuse_fast<AGG, false>(p, st);
 }
 
-template <typename AccT, int AGG>
+template <typename AccT, int AGG, bool FIX = false>
 int launch_fuse_w(const FuseParams &p, cudaStream_t st) {
-  return p.wmode == TFB_W_EXPLICIT ? launch_fuse<AccT, AGG, false>(p, st) : launch_fuse<AccT, AGG, true>(p, st);
+  return p.wmode == TFB_W_EXPLICIT ? launch_fuse<AccT, AGG, false, FIX>(p, st)
+                                   : launch_fuse<AccT, AGG, true, FIX>(p, st);
 }
 
 __global__ void k_rows_from_ids(const int32_t *tri, const int32_t *texel, int64_t npix, tfb_scene sc, int32_t *rows,
@@ -1003,8 +1014,11 @@ using namespace tfb;
 
 extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const float *const *probs, int num_classes,
                         const uint32_t *texel_hits, const double *weights, int64_t total_texels, int aggregator,
-                        int weight_mode, double alpha, void *accum, int accum_is_f64, int64_t accum_stride,
+                        int weight_mode, double alpha, void *accum, int accum_kind, int64_t accum_stride,
                         uint32_t *counts, int32_t *fallback_out, void *stream) {
+  TFB_REQUIRE(accum_kind >= TFB_ACCUM_F32 && accum_kind <= TFB_ACCUM_FIXED, TFB_ERR_VALUE,
+              "unknown accumulator kind %d", accum_kind);
+  const bool wide = accum_kind != TFB_ACCUM_F32;  // 8-byte accumulator elements
   TFB_REQUIRE(aggregator >= 0 && aggregator <= 2, TFB_ERR_VALUE, "unknown aggregator id %d", aggregator);
   TFB_REQUIRE(weight_mode >= 0 && weight_mode <= 3, TFB_ERR_VALUE, "unknown weight mode id %d", weight_mode);
   TFB_REQUIRE(num_classes >= 1, TFB_ERR_VALUE, "num_classes must be >= 1");
@@ -1014,7 +1028,7 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
               "tfb_fuse: weight mode needs per-frame texel hit counts");
   TFB_REQUIRE(accum_stride >= num_classes, TFB_ERR_DATA, "tfb_fuse: accum stride %lld < classes %d",
               (long long)accum_stride, num_classes);
-  TFB_REQUIRE(accum_is_f64 || (accum_stride % 4 == 0 && ((uintptr_t)accum & 15) == 0), TFB_ERR_DATA,
+  TFB_REQUIRE(wide || (accum_stride % 4 == 0 && ((uintptr_t)accum & 15) == 0), TFB_ERR_DATA,
               "tfb_fuse: float32 accumulator rows must be 16-byte aligned (stride multiple of 4)");
   if (nframes <= 0 || hw <= 0) return TFB_OK;
   TFB_REQUIRE(hw + kChunk < (1LL << 31), TFB_ERR_CAPACITY, "tfb_fuse: %lld pixels per frame is too many",
@@ -1027,7 +1041,7 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
               (long long)accum_stride);
   const size_t stage = (size_t)kChunk * num_classes * 4;
   const int NS = stage <= 2048 ? 4 : TFB_FUSE_NS;
-  TFB_REQUIRE(warp_layout(num_classes, NS, accum_is_f64 ? 8 : 4).total <= kSmemBudget &&
+  TFB_REQUIRE(warp_layout(num_classes, NS, wide ? 8 : 4).total <= kSmemBudget &&
                   fast_layout(num_classes, NS).total <= kSmemBudget,
               TFB_ERR_CAPACITY, "tfb_fuse: %d classes exceed the shared-memory staging budget of one warp",
               num_classes);
@@ -1058,7 +1072,7 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
     p.fallback = fallback_out ? fallback_out + (int64_t)f0 * hw : nullptr;
     p.nframes = nf;
     p.nitems = p.cpf * nf;
-    bool fast = !accum_is_f64 && weight_mode != TFB_W_EXPLICIT && g_fuse_fast;
+    bool fast = !wide && weight_mode != TFB_W_EXPLICIT && g_fuse_fast;
     for (int i = 0; i < nf && fast; ++i) fast = ((uintptr_t)p.probs[i] & 15) == 0;
     const bool vec = num_classes % 4 == 0;
     int rc;
@@ -1074,7 +1088,13 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
           rc = launch_fuse_fast_c<TFB_AGG_MUL>(p, vec, st);
           break;
       }
-    } else if (accum_is_f64) {
+    } else if (accum_kind == TFB_ACCUM_FIXED) {
+      switch (aggregator) {
+        case TFB_AGG_SUM: rc = launch_fuse_w<double, TFB_AGG_SUM, true>(p, st); break;
+        case TFB_AGG_MAXSUM: rc = launch_fuse_w<double, TFB_AGG_MAXSUM, true>(p, st); break;
+        default: rc = launch_fuse_w<double, TFB_AGG_MUL, true>(p, st); break;
+      }
+    } else if (wide) {
       switch (aggregator) {
         case TFB_AGG_SUM: rc = launch_fuse_w<double, TFB_AGG_SUM>(p, st); break;
         case TFB_AGG_MAXSUM: rc = launch_fuse_w<double, TFB_AGG_MAXSUM>(p, st); break;

@@ -603,6 +603,8 @@ constexpr int kSetupPer = TFB_SETUP_PER;  // candidates per k_setup thread (thei
 #define TFB_SETUP_WIDE 8
 #endif
 constexpr int kSetupWide = TFB_SETUP_WIDE;  // records over more tiles are binned by the whole warp
+// the flat deal packs each record's further-tile count into 16-bit halves of two words
+static_assert(!TFB_SETUP_FLAT || kSetupPer == 2, "TFB_SETUP_FLAT packs exactly two records per thread");
 
 __global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc, const double *__restrict__ cams, int W,
                                                     int H, int TX, int ntiles, Work w) {

@@ -10,8 +10,12 @@ the next device operation, so the reference's own tests that poke the
 texture keep working).
 
 Accumulator precision: ``accum_dtype="float64"`` (default here, matching the
-reference's float64 fold and its 1e-6 row tests) or ``"float32"`` (the
-throughput mode; red.global.add.v4.f32, within 1e-5 relative).
+reference's float64 fold and its 1e-6 row tests), ``"float32"`` (the
+throughput mode; red.global.add.v4.f32, within 1e-5 relative) or
+``"fixed64"`` (int64 fixed point in units of 2^-32: every piece of equal-row
+pixels is summed in float64 in a fixed order and added with an integer
+atomic, so reruns are bit-identical whatever the scheduling -- the CLI's
+``deterministic=true`` and the session API use it).
 """
 
 import numpy as np
@@ -29,7 +33,10 @@ DEFAULT_MEMORY_BUDGET = 4 * 1024 ** 3  # fusion.py:44
 DEFAULT_ACCUM_DTYPE = "float64"
 
 _DTYPES = {"float32": torch.float32, "float64": torch.float64, torch.float32: torch.float32,
-           torch.float64: torch.float64, np.float32: torch.float32, np.float64: torch.float64}
+           torch.float64: torch.float64, np.float32: torch.float32, np.float64: torch.float64,
+           "fixed64": torch.int64, torch.int64: torch.int64}
+FIXED_SCALE = 2.0 ** 32  # TFB_ACCUM_FIXED: accumulator element = round(value * 2^32)
+ACCUM_KIND = {torch.float32: 0, torch.float64: 1, torch.int64: 2}  # TFB_ACCUM_F32 / F64 / FIXED
 
 
 def texture_nbytes(total_texels, num_classes):
@@ -38,7 +45,7 @@ def texture_nbytes(total_texels, num_classes):
 
 
 def accum_stride(num_classes, dtype):
-    return num_classes if dtype == torch.float64 else (num_classes + 3) // 4 * 4
+    return (num_classes + 3) // 4 * 4 if dtype == torch.float32 else num_classes
 
 
 class ProbabilityTexture:
@@ -51,6 +58,8 @@ class ProbabilityTexture:
         self.finalized = False
         self._scene = layout_scene(layout, device)
         self.device = self._scene.device
+        if accum_dtype not in _DTYPES:
+            raise ValueError("accum_dtype must be float32, float64 or fixed64, got %r" % (accum_dtype,))
         self.dtype = _DTYPES[accum_dtype]
         self.stride = accum_stride(self.num_classes, self.dtype)
         n = max(int(layout.total_texels), 0)
@@ -80,12 +89,31 @@ class ProbabilityTexture:
     def is_f64(self):
         return self.dtype == torch.float64
 
+    @property
+    def accum_kind(self):
+        """C ABI accumulator kind: TFB_ACCUM_F32 (0), TFB_ACCUM_F64 (1), TFB_ACCUM_FIXED (2)."""
+        return ACCUM_KIND[self.dtype]
+
+    def accum_values(self, t=None):
+        """Accumulator elements (device) as float64 values."""
+        t = self._accum[:, : self.num_classes] if t is None else t
+        if self.dtype == torch.int64:
+            return t.to(torch.float64) / FIXED_SCALE
+        return t.to(torch.float64)
+
+    def accum_from_values(self, a):
+        """(n_x, c) float64 values → accumulator elements of this texture's kind (device)."""
+        t = torch.as_tensor(np.asarray(a, dtype=np.float64)).to(self.device)
+        if self.dtype == torch.int64:
+            return torch.round(t * FIXED_SCALE).to(torch.int64)
+        return t.to(self.dtype)
+
     # -- host views (reference fields) ---------------------------------------------
     @property
     def accum(self):
         self._flush_pending()
         if self._h_accum is None:
-            self._h_accum = self._accum[:, : self.num_classes].to(torch.float64).cpu().numpy()
+            self._h_accum = self.accum_values().cpu().numpy()
         return self._h_accum
 
     @accum.setter
@@ -147,7 +175,7 @@ class ProbabilityTexture:
             a = np.asarray(self._h_accum, dtype=np.float64)
             if a.shape != (self.total_texels, self.num_classes):
                 raise DataError("accumulator shape %s does not match texture" % (a.shape,))
-            self._accum[:, : self.num_classes].copy_(torch.as_tensor(a).to(self.device, self.dtype))
+            self._accum[:, : self.num_classes].copy_(self.accum_from_values(a))
             self._h_accum = None
         if self._h_counts is not None:
             self._counts.copy_(torch.as_tensor(np.asarray(self._h_counts, dtype=np.int64)).to(self.device,
@@ -320,7 +348,7 @@ def accumulate_frame(tex, ids, probs, weights):
             wdev = torch.as_tensor(np.ascontiguousarray(w, dtype=np.float64)).to(tex.device).view(-1)
     ptrs, _keep = N.ptr_array([p.data_ptr()])
     N.call("tfb_fuse", N.ptr(rows), hw, 1, ptrs, c, N.ptr(hits), N.ptr(wdev), tex.total_texels,
-           N.AGG_IDS[tex.aggregator], N.WMODE_IDS[mode], float(alpha or 0.0), N.ptr(tex._accum), int(tex.is_f64),
+           N.AGG_IDS[tex.aggregator], N.WMODE_IDS[mode], float(alpha or 0.0), N.ptr(tex._accum), tex.accum_kind,
            tex.stride, N.ptr(tex._counts), None, N.stream_handle())
     if hits is not None:
         N.call("tfb_clear_hits", N.ptr(rows), hw, 1, tex.total_texels, N.ptr(hits), N.stream_handle())
@@ -340,7 +368,7 @@ def finalize(tex):
     tex._rows = torch.empty((n, c), dtype=torch.float32, device=d)
     tex._unobs = torch.empty(n, dtype=torch.uint8, device=d)
     tex._labels = torch.empty(n, dtype=torch.int32, device=d)
-    N.call("tfb_finalize", N.ptr(tex._accum), int(tex.is_f64), tex.stride, N.ptr(tex._counts), n, c,
+    N.call("tfb_finalize", N.ptr(tex._accum), tex.accum_kind, tex.stride, N.ptr(tex._counts), n, c,
            N.AGG_IDS[tex.aggregator], N.ptr(tex._rows), N.ptr(tex._unobs), N.ptr(tex._labels), N.stream_handle())
     tex.finalized = True
     tex._h_rows = tex._h_unobs = None

@@ -120,11 +120,11 @@ class CameraFrame:
 
 
 def pack_camera(frame):
-    out = np.empty(16, dtype=np.float64)
-    out[0:9] = np.asarray(frame.rotation, dtype=np.float64).reshape(9)
-    out[9:12] = np.asarray(frame.translation, dtype=np.float64).reshape(3)
-    out[12], out[13], out[14], out[15] = frame.fx, frame.fy, frame.cx, frame.cy
-    return out
+    """The 16-float64 camera record of the C ABI: R (row-major), t, fx, fy, cx, cy."""
+    i = frame.intrinsics
+    return np.concatenate((np.asarray(frame.rotation, dtype=np.float64).reshape(9),
+                           np.asarray(frame.translation, dtype=np.float64).reshape(3),
+                           np.array((i.fx, i.fy, i.cx, i.cy), dtype=np.float64)))
 
 
 def to_camera(frame, points):

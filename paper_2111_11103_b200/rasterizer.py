@@ -163,3 +163,29 @@ def pixel_world_points(mesh, layout, ids):
     w[r, (o + 1) % 3] = u - v
     w[r, (o + 2) % 3] = v
     return np.einsum("nk,nkd->nd", w, mesh.vertices[mesh.triangles[tri]])
+
+
+def dump_debug_images(ids, prefix):
+    """16-bit grayscale PNGs of an IdImage for eyeballing correspondences
+    (rasterizer.py:227-254): hashed triangle id, texel id + 1 and depth
+    rescaled to [1, 65535]; 0 marks uncovered pixels.  Returns the paths."""
+    from PIL import Image
+
+    cov = ids.covered
+    tri = ids.triangle.astype(np.int64)
+    planes = {
+        "triangle": np.where(cov, (tri + 1) * 2654435761 % 65535 + 1, 0),
+        "texel": np.where(cov, ids.texel.astype(np.int64) % 65535 + 1, 0),
+        "depth": np.zeros(cov.shape, np.int64),
+    }
+    if cov.any():
+        d = ids.depth[cov]
+        lo, hi = float(d.min()), float(d.max())
+        planes["depth"][cov] = ((d - lo) * (65534.0 / (hi - lo) if hi > lo else 0.0)).astype(np.int64) + 1
+    paths = []
+    for name in ("triangle", "texel", "depth"):
+        path = "%s_%s.png" % (prefix, name)
+        img = planes[name].astype("<u2")
+        Image.frombytes("I;16", (img.shape[1], img.shape[0]), img.tobytes()).save(path)
+        paths.append(path)
+    return paths

@@ -17,7 +17,7 @@ import threading
 import numpy as np
 import torch
 
-from .annotation import MeshAnnotation
+from .annotation import FallbackMap, MeshAnnotation
 from .device import scene_for
 from .errors import DataError
 from .fusion import finalize, init_texture, parse_weight_mode
@@ -40,7 +40,12 @@ class _FusionSession:
         self.scene = scene_for(mesh, layout, texture.device)
         self.ann = MeshAnnotation(mesh, layout, weight_mode=_spec(weight_mode, alpha), texture=texture,
                                   device=texture.device)
-        self.ann.fallbacks = {}  # frame_id -> (H*W,) int32 device tensor (the frame's own argmax)
+        self.ann.fallbacks = FallbackMap()  # frame_id -> (H*W,) int32 device tensor (the frame's own argmax)
+        sizes = {}
+        for f in frames:
+            sizes[(f.width, f.height)] = sizes.get((f.width, f.height), 0) + 1
+        for size, n in sizes.items():  # one add per trajectory frame fits without allocating per batch
+            self.ann.fallbacks.reserve(size, n)
         self._gate = threading.Lock()
 
     @property
@@ -65,9 +70,11 @@ def _spec(mode, alpha):
 
 
 def open_session(mesh_path, trajectory_path, gamma, aggregator, weight_mode, num_classes,
-                 accum_dtype="float64", device=None):
+                 accum_dtype="fixed64", device=None):
     """Load the scene; size the texture from the worst-case projected footprints
-    computed on the GPU (bindings/__init__.py:68-82)."""
+    computed on the GPU (bindings/__init__.py:68-82).  The default fixed64
+    accumulator makes a session's outputs independent of scheduling, so they
+    equal the fuse command's in deterministic mode bit for bit (criterion 11)."""
     mesh = load_mesh(mesh_path)
     frames = load_trajectory(trajectory_path)
     mode, alpha = parse_weight_mode(weight_mode)
@@ -77,11 +84,8 @@ def open_session(mesh_path, trajectory_path, gamma, aggregator, weight_mode, num
     return _FusionSession(mesh, frames, layout, texture, mode, alpha)
 
 
-def rasterize(mesh, layout, frame):
-    """Module-level hook (the reference tests monkeypatch bindings.rasterize)."""
-    from .rasterizer import rasterize as _r
-
-    return _r(mesh, layout, frame)
+# module-level hook, as in the reference bindings (its tests monkeypatch bindings.rasterize)
+from .rasterizer import rasterize  # noqa: E402
 
 
 def add_frame(session, frame_id, probabilities):

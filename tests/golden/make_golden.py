@@ -220,14 +220,41 @@ def write_cfg2_frame(path):
     print("cfg2 frame golden in %.1f s" % (time.time() - t0))
 
 
+def write_cfg2_areas(path):
+    """compute_worst_case_areas + build_texel_layout (geometry.py:257-380) on the BASELINE
+    configs[1] mesh over 4 seeded in-room cameras (paper_2111_11103_b200.synth's
+    random_room_trajectory poses), at gamma 0.2 and 1.0."""
+    t0 = time.time()
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_2111_11103_b200.synth import random_room_trajectory, scannet_intrinsics
+
+    scene = synthgen.make_room(size=(6.0, 5.0, 3.0), tess=158, num_classes=40)
+    mesh = scene.mesh
+    intr = tf.Intrinsics(fx=577.87, fy=577.87, cx=319.5, cy=239.5, width=640, height=480)
+    poses = random_room_trajectory(4, scannet_intrinsics(), seed=21)
+    frames = [tf.CameraFrame(frame_id=k, intrinsics=intr, rotation=p.rotation, translation=p.translation)
+              for k, p in enumerate(poses)]
+    areas = tf.compute_worst_case_areas(mesh, frames)
+    out = {"cams": np.stack([cam16(f) for f in frames]), "areas": areas}
+    for gamma in (0.2, 1.0):
+        lay = tf.build_texel_layout(mesh, areas, gamma)
+        out["steps_%g" % gamma] = lay.steps.astype(np.int32)
+        out["origins_%g" % gamma] = lay.origins.astype(np.int8)
+        out["total_%g" % gamma] = np.int64(lay.total_texels)
+    np.savez_compressed(path, **out)
+    print("cfg2 areas golden in %.1f s" % (time.time() - t0))
+
+
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["raster", "cfg1", "cfg2"]
+    what = sys.argv[1:] or ["raster", "cfg1", "cfg2", "cfg2areas"]
     if "raster" in what:
         write_raster_cases(os.path.join(HERE, "raster_cases.npz"))
     if "cfg1" in what:
         write_cfg1(os.path.join(HERE, "cfg1.npz"))
     if "cfg2" in what:
         write_cfg2_frame(os.path.join(HERE, "cfg2_frame.npz"))
+    if "cfg2areas" in what:
+        write_cfg2_areas(os.path.join(HERE, "cfg2_areas.npz"))
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -121,3 +121,26 @@ def test_render_and_eval_match_reference_cli(tmp_path):
                      "output=%s" % ev, "ignore=0"]) == 0
     assert (ev / "report.txt").read_text() == open(os.path.join(REF, "eval", "report.txt")).read()
     assert (ev / "report.json").read_text() == open(os.path.join(REF, "eval", "report.json")).read()
+
+
+def test_deterministic_needs_fixed_accumulator(tmp_path):
+    assert cli.main(["fuse"] + _fuse_args(tmp_path / "o", deterministic="true", accum="float32")) == 2
+    assert cli.main(["fuse"] + _fuse_args(tmp_path / "o", accum="float16")) == 2
+
+
+@pytest.mark.gpu
+def test_criterion_09_deterministic_reruns_are_byte_identical(tmp_path):
+    """test_acceptance.py:373-399: two `fuse ... deterministic=true` runs write
+    byte-identical texture.smtx and label PNGs (fixed64 accumulator)."""
+    outs = []
+    for name in ("a", "b"):
+        out = tmp_path / name
+        assert cli.main(["fuse"] + _fuse_args(out, aggregator="mul", deterministic="true", batch=3 if name == "a"
+                                              else 64)) == 0
+        outs.append(out)
+    a, b = outs
+    assert (a / "texture.smtx").read_bytes() == (b / "texture.smtx").read_bytes()
+    pngs = sorted(os.listdir(a / "labels"))
+    assert pngs
+    for f in pngs:
+        assert (a / "labels" / f).read_bytes() == (b / "labels" / f).read_bytes()

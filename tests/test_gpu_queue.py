@@ -138,7 +138,9 @@ def test_session_add_frame_queue_counts_and_fallbacks(tmp_path):
     assert s.ann.frames_added == 0  # all queued
     for k, fr in enumerate(frames):
         ids = rasterize(s.mesh, s.layout, fr)
-        assert int(counts[k]) == int((ids.triangle >= 0).sum())
+        assert int(counts[k]) == int((ids.triangle >= 0).sum())  # resolved without folding the queue
+    assert s.ann.frames_added == 0
+    assert s.texture.counts.sum() == sum(int(n) for n in counts)  # reading the texture folds it
     assert s.ann.frames_added == len(frames)
     labels, rows = finalize_and_render(s, [fr.frame_id for fr in frames])
     for k, fr in enumerate(frames):

@@ -155,3 +155,16 @@ def test_oracle_areas_and_layout_cfg1(cfg1):
     areas = O.worst_case_areas(z["verts"], z["tris"], z["cams"], sizes)
     np.testing.assert_array_equal(areas, z["areas"])
     np.testing.assert_array_equal(O.build_steps(areas, 0.2), z["steps"])
+
+
+def test_oracle_areas_cfg2_golden():
+    """The C restatement of compute_worst_case_areas on the configs[1] mesh (300k triangles,
+    4 cameras) equals the reference's output bit for bit (fixture: make_golden.py cfg2areas)."""
+    import oracle as O
+    from paper_2111_11103_b200.synth import make_room
+
+    z = np.load(os.path.join(GOLD, "cfg2_areas.npz"))
+    v, t = make_room((6.0, 5.0, 3.0), 158)
+    sizes = np.tile(np.array([[640, 480]], np.int32), (len(z["cams"]), 1))
+    areas = O.worst_case_areas(v, t, z["cams"], sizes)
+    np.testing.assert_array_equal(areas, z["areas"])
