@@ -156,6 +156,29 @@ int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const float *const *p
              int weight_mode, double alpha, void *accum, int accum_kind, int64_t accum_stride,
              uint32_t *counts, int32_t *fallback_out, void *stream);
 
+/* tfb_fuse with an item order from tfb_fuse_order (NULL: frame-major, as tfb_fuse).
+ * The order is honoured by the float32 fast path when the call is one launch
+ * (nframes <= 256) and fallback_out is NULL; otherwise every item is processed in
+ * frame-major order.  n_items is a DEVICE pointer (written by tfb_fuse_order). */
+int tfb_fuse_ordered(const int32_t *rows, int64_t hw, int nframes, const float *const *probs, int num_classes,
+                     const uint32_t *texel_hits, const double *weights, int64_t total_texels, int aggregator,
+                     int weight_mode, double alpha, void *accum, int accum_kind, int64_t accum_stride,
+                     uint32_t *counts, int32_t *fallback_out, const uint32_t *item_order, const uint32_t *n_items,
+                     void *stream);
+
+/* Row-block item order for accumulators larger than L2 (configs[3]: 1.73 GB): the
+ * (frame, 32-pixel chunk) items of one tfb_fuse launch (nframes <= 256) sorted by
+ * the accumulator row block (row >> shift) of their first covered pixel, by a
+ * counting sort; chunks with no covered pixel are left out.  The scatter-add then
+ * walks the accumulator block by block, so the rows in flight stay in L2 and each
+ * is read and written back about once per batch instead of once per frame
+ * (fusion.py:180-181 semantics unchanged: the fold is a sum).
+ * order_out: nframes*ceil(hw/32) uint32 (frame << 24 | chunk); n_out: one device
+ * uint32 (number of items); workspace: tfb_fuse_order_workspace_bytes(). */
+size_t tfb_fuse_order_workspace_bytes(int64_t hw, int nframes, int64_t total_texels, int shift);
+int tfb_fuse_order(const int32_t *rows, int64_t hw, int nframes, int64_t total_texels, int shift,
+                   void *workspace, size_t workspace_bytes, uint32_t *order_out, uint32_t *n_out, void *stream);
+
 /* finalize + texel_argmax (fusion.py:186-222).  rows_out (total_texels*c
  * float32), unobserved_out (u8) and labels_out (int32, UNKNOWN = -1) are each
  * optional. */

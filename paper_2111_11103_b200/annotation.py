@@ -174,7 +174,7 @@ class MeshAnnotation:
 
     def __init__(self, mesh, layout=None, num_classes=None, aggregator="mul", weight_mode="images_iid",
                  accum_dtype="float32", max_batch=None, device=None, memory_budget=None, overlap=False,
-                 fuse_ctas_per_sm=None, texture=None):
+                 fuse_ctas_per_sm=None, texture=None, order_items=None):
         if texture is None and num_classes is None:
             raise ValueError("num_classes is required")
         self.mesh = mesh
@@ -200,6 +200,9 @@ class MeshAnnotation:
         self._pending = []
         self._pending_size = None
         self._cam_ring = None
+        # row-block item order for the scatter-add (tfb_fuse_order): None = when the
+        # accumulator exceeds half the L2 (configs[3]), True / False to force it
+        self.order_items = order_items
         texture._flush_hook = weakref.WeakMethod(self.flush)
         # Overlap mode: batch k+1 is rasterized on a side stream while batch k
         # is scatter-added on the caller's stream (double-buffered row / hit
@@ -411,10 +414,11 @@ class MeshAnnotation:
             f0 = self._event(cur) if prof is not None else None
             parr, _k = N.ptr_array(ptrs)
             fb = fallback_out[b0:b0 + b] if fallback_out is not None else None
-            N.call("tfb_fuse", N.ptr(rows), hw, b, parr, self.num_classes, N.ptr(hits), None, tex.total_texels,
-                   N.AGG_IDS[tex.aggregator], N.WMODE_IDS[self.weight_mode], float(self.alpha or 0.0),
-                   N.ptr(tex._accum), tex.accum_kind, tex.stride, N.ptr(tex._counts), N.ptr(fb),
-                   N.stream_handle(cur))
+            order, n_order = self._item_order(rows, hw, b, fb, cur)
+            N.call("tfb_fuse_ordered", N.ptr(rows), hw, b, parr, self.num_classes, N.ptr(hits), None,
+                   tex.total_texels, N.AGG_IDS[tex.aggregator], N.WMODE_IDS[self.weight_mode],
+                   float(self.alpha or 0.0), N.ptr(tex._accum), tex.accum_kind, tex.stride, N.ptr(tex._counts),
+                   N.ptr(fb), N.ptr(order), N.ptr(n_order), N.stream_handle(cur))
             if prof is not None:
                 prof.append((b, r0, r1, f0, self._event(cur)))
             if sslot is not None:
@@ -435,6 +439,37 @@ class MeshAnnotation:
             del keep
         tex._h_accum = tex._h_counts = None
         self.frames_added += B
+
+    ORDER_SHIFT = 10  # item-order key = accumulator row block of 1024 rows
+
+    def _use_order(self):
+        """Auto: the float32 fast path (the kernel that walks an order) with 16-byte class
+        quads (c % 4 == 0), when the accumulator exceeds half the L2.  Measured at
+        configs[3] (1.73 GB): scatter-add 32.9 -> 15.3 us/frame.  The c % 4 != 0 kernel is
+        issue-bound rather than bound by accumulator traffic, and the order's extra work
+        makes it slower (configs[4], c = 19: 47.0 -> 55.2 us/frame), so it walks
+        frame-major."""
+        if self.order_items is not None:
+            return bool(self.order_items)
+        tex = self._tex
+        if tex.accum_kind != 0 or self.num_classes % 4:
+            return False
+        l2 = torch.cuda.get_device_properties(self.device).L2_cache_size
+        return tex.total_texels * tex.stride * 4 > l2 // 2
+
+    def _item_order(self, rows, hw, b, fb, cur):
+        """(order, count) device buffers from tfb_fuse_order, or (None, None)."""
+        if fb is not None or not self._use_order():
+            return None, None
+        tex = self._tex
+        lib = N.load()
+        nbytes = lib.tfb_fuse_order_workspace_bytes(hw, b, tex.total_texels, self.ORDER_SHIFT)
+        ws = self.scene.buffer("order_ws", (nbytes,), torch.uint8)
+        order = self.scene.buffer("order", (b * ((hw + 31) // 32),), torch.int32)
+        n_order = self.scene.buffer("order_n", (1,), torch.int32)
+        N.call("tfb_fuse_order", N.ptr(rows), hw, b, tex.total_texels, self.ORDER_SHIFT, N.ptr(ws), nbytes,
+               N.ptr(order), N.ptr(n_order), N.stream_handle(cur))
+        return order, n_order
 
     # -- per-frame queue ---------------------------------------------------------------
     def _stage_one(self, probs, H, W, cur):

@@ -72,6 +72,10 @@ struct FuseParams {
   int NS;
   int64_t cpf;     // chunks per frame
   int64_t nitems;  // nframes * cpf
+  // optional item order (tfb_fuse_order): items as (frame << 24 | chunk), sorted by the
+  // accumulator row block they touch; *norder of them (empty chunks are left out)
+  const uint32_t *order;
+  const uint32_t *norder;
 };
 
 struct Geo {
@@ -163,9 +167,10 @@ __device__ __forceinline__ bool tma_ok(const float *src, int npix, int c) {
   return (bytes % 16 == 0) && (((uintptr_t)src & 15) == 0) && bytes > 0;
 }
 
-// (frame, chunk) of a work item, advanced by the warp-grid stride without divisions
+// (frame, chunk) of a work item, advanced by the warp-grid stride without divisions;
+// i is the item's index in the launch's item order when there is one
 struct Pos {
-  int f, ch;
+  int f, ch, i;
 };
 
 __device__ __forceinline__ void advance(Pos &q, int dF, int dC, int cpf) {
@@ -176,6 +181,25 @@ __device__ __forceinline__ void advance(Pos &q, int dF, int dC, int cpf) {
     ++q.f;
   }
 }
+
+// The warp-grid walk over a launch's items: frame-major (ORD = false), or through the
+// row-block order of tfb_fuse_order (ORD = true), which keeps the accumulator rows the
+// in-flight items touch inside L2 when the whole accumulator does not fit.
+template <bool ORD>
+struct Walk {
+  int dF, dC, cpf, GW, n, nframes;
+  const uint32_t *order;
+  __device__ __forceinline__ Pos at(int i) const {
+    if (i >= n) return Pos{nframes, 0, i};
+    const uint32_t it = __ldg(order + i);
+    return Pos{(int)(it >> 24), (int)(it & 0xffffffu), i};
+  }
+  __device__ __forceinline__ Pos first(int gw) const { return ORD ? at(gw) : Pos{gw / cpf, gw % cpf, gw}; }
+  __device__ __forceinline__ void next(Pos &q) const {
+    if (ORD) q = at(q.i + GW);
+    else advance(q, dF, dC, cpf);
+  }
+};
 
 __device__ __forceinline__ int32_t row_at(const FuseParams &p, Pos q, int lane) {
   if (q.f >= p.nframes) return -1;
@@ -288,7 +312,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
       bulk_g2s(stages + (size_t)s * L.stage_floats, src, bytes, bar + s, policy);
     }
   };
-  Pos cur{gw / cpf, gw % cpf};
+  Pos cur{gw / cpf, gw % cpf, gw};
   if (lane == 0) {
     Pos q = cur;
     for (int s = 0; s < NS && q.f < p.nframes; ++s) {
@@ -492,15 +516,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
         flush();
       }
     }
+    // stage s, table and side arrays are free again: every lane orders its generic-proxy reads
+    // of the stage before the async-proxy refill, then the warp converges
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
-    // stage s, table and side arrays are free again
     if (lane == 0) {
       Pos ahead = cur;
       for (int k = 0; k < NS; ++k) advance(ahead, dF, dC, cpf);
-      if (ahead.f < p.nframes) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(ahead, s);
-      }
+      if (ahead.f < p.nframes) issue(ahead, s);
     }
     cur = nxt;
     nxt = nn;
@@ -601,7 +624,7 @@ __device__ __forceinline__ void sts4(float *p, float4 v, int nv) {
   if (nv > 3) p[3] = v.w;
 }
 
-template <int AGG, bool VEC, int CC>
+template <int AGG, bool VEC, int CC, bool ORD = false>
 __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant__ FuseParams p) {
   constexpr bool kProd = AGG == TFB_AGG_MUL;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -622,6 +645,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
   const int cpf = (int)p.cpf, hw = (int)p.hw;
   const int dF = GW / cpf, dC = GW - dF * cpf;
   const float wa = p.wa, wb = p.wb;
+  const Walk<ORD> wk{dF, dC, cpf, GW, ORD ? (int)*p.norder : 0, p.nframes, p.order};
 
   uint64_t policy = 0;
   if (lane == 0) {
@@ -641,16 +665,16 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
     if (bytes)
       bulk_g2s(stages + (size_t)s * L.stage_floats, p.probs[q.f] + (size_t)start * c, bytes, bar + s, policy);
   };
-  Pos cur{gw / cpf, gw % cpf};
+  Pos cur = wk.first(gw);
   Pos ahead = cur;  // next item to stage
   for (int s = 0; s < NS && ahead.f < p.nframes; ++s) {
     if (lane == 0) issue(ahead, s);
-    advance(ahead, dF, dC, cpf);
+    wk.next(ahead);
   }
   Pos nxt = cur, nn = cur;
-  advance(nxt, dF, dC, cpf);
-  advance(nn, dF, dC, cpf);
-  advance(nn, dF, dC, cpf);
+  wk.next(nxt);
+  nn = nxt;
+  wk.next(nn);
 
   const unsigned upto = (2u << lane) - 1u;  // lanes <= this one
   const int g = lane / geo.QW, qi0 = lane - g * geo.QW;
@@ -838,17 +862,18 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
       }
       __syncwarp();
     }
-    // stage s is free again
+    // stage s is free again.  Every lane read it and wrote folded quads into it through the
+    // generic proxy: each orders those accesses before the async-proxy refill, then the warp
+    // converges and one lane issues the bulk copy (the CUTLASS producer convention).
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
     if (ahead.f < p.nframes) {
-      if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(ahead, s);
-      }
-      advance(ahead, dF, dC, cpf);
+      if (lane == 0) issue(ahead, s);
+      wk.next(ahead);
     }
     cur = nxt;
     nxt = nn;
-    advance(nn, dF, dC, cpf);
+    wk.next(nn);
     r_cur = r_nxt;
     n_cur = n_nxt;
     r_nxt = r_nn;
@@ -916,6 +941,10 @@ int launch_fuse(const FuseParams &p, cudaStream_t st) {
 
 template <int AGG, bool VEC, int CC = 0>
 int launch_fuse_fast(const FuseParams &p, cudaStream_t st) {
+  if (p.order) {
+    static LaunchCache lco;
+    return launch_persistent(k_fuse_fast<AGG, VEC, CC, true>, lco, fast_layout(p.c, p.NS).total, p, st);
+  }
   static LaunchCache lc;
   return launch_persistent(k_fuse_fast<AGG, VEC, CC>, lc, fast_layout(p.c, p.NS).total, p, st);
 }
@@ -940,6 +969,71 @@ template <typename AccT, int AGG, bool FIX = false>
 int launch_fuse_w(const FuseParams &p, cudaStream_t st) {
   return p.wmode == TFB_W_EXPLICIT ? launch_fuse<AccT, AGG, false, FIX>(p, st)
                                    : launch_fuse<AccT, AGG, true, FIX>(p, st);
+}
+
+// ---- item order for accumulators beyond L2 (tfb_fuse_order) ------------------------------
+// key of item (f, ch) = accumulator row block (row >> shift) of its first covered pixel,
+// -1 when no pixel of the chunk is covered.  One thread per item: pixel 0's row (one sector
+// per item) decides for nearly every chunk; only chunks starting on an uncovered pixel scan
+// on.  Consecutive items mostly share a key, so the histogram adds are warp-aggregated.
+__global__ void k_item_keys(const int32_t *rows, int64_t hw, int cpf, int64_t nitems, int shift, int32_t *keys,
+                            uint32_t *hist) {
+  const int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int32_t key = -1;
+  if (item < nitems) {
+    const int64_t f = item / cpf, ch = item - f * cpf;
+    const int64_t p0 = ch * kChunk, n = min((int64_t)kChunk, hw - p0);
+    const int32_t *r = rows + f * hw + p0;
+    int32_t row = __ldg(r);
+    for (int64_t k = 1; row < 0 && k < n; ++k) row = __ldg(r + k);
+    key = row >= 0 ? (row >> shift) : -1;
+    keys[item] = key;
+  }
+  const unsigned act = __ballot_sync(0xffffffffu, key >= 0);
+  if (key >= 0) {
+    const unsigned peers = __match_any_sync(act, key);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(hist + key, (uint32_t)__popc(peers));
+  }
+}
+
+// exclusive scan of the key histogram in place (one CTA), total item count to *n
+__global__ void __launch_bounds__(1024) k_key_scan(uint32_t *hist, int64_t nkeys, uint32_t *n) {
+  __shared__ uint32_t part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (nkeys + 1023) / 1024, lo = t * per, hi = min(nkeys, lo + per);
+  uint32_t sum = 0;
+  for (int64_t k = lo; k < hi; ++k) sum += hist[k];
+  part[t] = sum;
+  __syncthreads();
+  for (int d = 1; d < 1024; d <<= 1) {  // Hillis-Steele inclusive scan of the thread sums
+    const uint32_t v = t >= d ? part[t - d] : 0u;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  uint32_t run = part[t] - sum;
+  for (int64_t k = lo; k < hi; ++k) {
+    const uint32_t h = hist[k];
+    hist[k] = run;
+    run += h;
+  }
+  if (t == 1023) *n = part[1023];
+}
+
+// every covered item to its key's next slot: order = items grouped by ascending key
+// (warp-aggregated slot claims; the order inside a key is arbitrary -- the fold is a sum)
+__global__ void k_key_scatter(const int32_t *keys, int64_t nitems, int cpf, uint32_t *cursor, uint32_t *order) {
+  const int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int32_t key = item < nitems ? keys[item] : -1;
+  const unsigned act = __ballot_sync(0xffffffffu, key >= 0);
+  if (key < 0) return;
+  const unsigned peers = __match_any_sync(act, key);
+  const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(cursor + key, (uint32_t)__popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  const int64_t f = item / cpf, ch = item - f * cpf;
+  order[base + __popc(peers & ((1u << lane) - 1u))] = (uint32_t)(f << 24) | (uint32_t)ch;
 }
 
 __global__ void k_rows_from_ids(const int32_t *tri, const int32_t *texel, int64_t npix, tfb_scene sc, int32_t *rows,
@@ -1012,10 +1106,50 @@ unsigned grid_for(int64_t n) {
 
 using namespace tfb;
 
+extern "C" size_t tfb_fuse_order_workspace_bytes(int64_t hw, int nframes, int64_t total_texels, int shift) {
+  const int64_t cpf = (hw + kChunk - 1) / kChunk;
+  const int64_t nkeys = (total_texels >> shift) + 1;
+  return (size_t)(cpf * nframes) * 4 + (size_t)nkeys * 4 + 256;
+}
+
+extern "C" int tfb_fuse_order(const int32_t *rows, int64_t hw, int nframes, int64_t total_texels, int shift,
+                              void *workspace, size_t workspace_bytes, uint32_t *order_out, uint32_t *n_out,
+                              void *stream) {
+  TFB_REQUIRE(rows && workspace && order_out && n_out, TFB_ERR_DATA, "tfb_fuse_order: null argument");
+  TFB_REQUIRE(shift >= 0 && shift < 31, TFB_ERR_VALUE, "tfb_fuse_order: bad row-block shift %d", shift);
+  TFB_REQUIRE(nframes >= 0 && nframes <= kMaxFrames, TFB_ERR_DATA, "tfb_fuse_order: %d frames > %d per launch",
+              nframes, kMaxFrames);
+  TFB_REQUIRE(workspace_bytes >= tfb_fuse_order_workspace_bytes(hw, nframes, total_texels, shift), TFB_ERR_CAPACITY,
+              "tfb_fuse_order: workspace too small");
+  const int64_t cpf = (hw + kChunk - 1) / kChunk;
+  TFB_REQUIRE(cpf < (1 << 24), TFB_ERR_CAPACITY, "tfb_fuse_order: %lld chunks per frame", (long long)cpf);
+  const int64_t nitems = cpf * nframes, nkeys = (total_texels >> shift) + 1;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t *keys = static_cast<int32_t *>(workspace);
+  uint32_t *hist = reinterpret_cast<uint32_t *>(static_cast<char *>(workspace) + ((nitems * 4 + 255) / 256) * 256);
+  if (cudaMemsetAsync(hist, 0, (size_t)nkeys * 4, st) != cudaSuccess) return check_launch("tfb_fuse_order");
+  if (nitems == 0) return cudaMemsetAsync(n_out, 0, 4, st) == cudaSuccess ? TFB_OK : check_launch("tfb_fuse_order");
+  const unsigned blocks = (unsigned)((nitems + 255) / 256);
+  k_item_keys<<<blocks, 256, 0, st>>>(rows, hw, (int)cpf, nitems, shift, keys, hist);
+  k_key_scan<<<1, 1024, 0, st>>>(hist, nkeys, n_out);
+  k_key_scatter<<<blocks, 256, 0, st>>>(keys, nitems, (int)cpf, hist, order_out);
+  return check_launch("tfb_fuse_order");
+}
+
 extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const float *const *probs, int num_classes,
                         const uint32_t *texel_hits, const double *weights, int64_t total_texels, int aggregator,
                         int weight_mode, double alpha, void *accum, int accum_kind, int64_t accum_stride,
                         uint32_t *counts, int32_t *fallback_out, void *stream) {
+  return tfb_fuse_ordered(rows, hw, nframes, probs, num_classes, texel_hits, weights, total_texels, aggregator,
+                          weight_mode, alpha, accum, accum_kind, accum_stride, counts, fallback_out, nullptr, nullptr,
+                          stream);
+}
+
+extern "C" int tfb_fuse_ordered(const int32_t *rows, int64_t hw, int nframes, const float *const *probs,
+                                int num_classes, const uint32_t *texel_hits, const double *weights,
+                                int64_t total_texels, int aggregator, int weight_mode, double alpha, void *accum,
+                                int accum_kind, int64_t accum_stride, uint32_t *counts, int32_t *fallback_out,
+                                const uint32_t *item_order, const uint32_t *n_items, void *stream) {
   TFB_REQUIRE(accum_kind >= TFB_ACCUM_F32 && accum_kind <= TFB_ACCUM_FIXED, TFB_ERR_VALUE,
               "unknown accumulator kind %d", accum_kind);
   const bool wide = accum_kind != TFB_ACCUM_F32;  // 8-byte accumulator elements
@@ -1072,6 +1206,10 @@ extern "C" int tfb_fuse(const int32_t *rows, int64_t hw, int nframes, const floa
     p.fallback = fallback_out ? fallback_out + (int64_t)f0 * hw : nullptr;
     p.nframes = nf;
     p.nitems = p.cpf * nf;
+    // the item order covers one launch and leaves out chunks with no covered pixel, so it is
+    // used only when every item is in it or nothing per pixel is written (no fallback output)
+    p.order = (item_order && nframes <= fpl && !fallback_out) ? item_order : nullptr;
+    p.norder = p.order ? n_items : nullptr;
     bool fast = !wide && weight_mode != TFB_W_EXPLICIT && g_fuse_fast;
     for (int i = 0; i < nf && fast; ++i) fast = ((uintptr_t)p.probs[i] & 15) == 0;
     const bool vec = num_classes % 4 == 0;

@@ -151,3 +151,21 @@ def test_session_add_frame_queue_counts_and_fallbacks(tmp_path):
         np.testing.assert_array_equal(labels[k][hole], fb[hole])
     assert rows.shape == (s.num_texels, 12)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("agg", ["mul", "sum"])
+def test_row_block_item_order_equals_frame_major(agg):
+    """tfb_fuse_order + tfb_fuse_ordered (the configs[3] path for accumulators beyond L2) fold
+    the same contributions as the frame-major walk: counts exact, float32 sums to rounding."""
+    from paper_2111_11103_b200 import MeshAnnotation
+
+    mesh, layout, frames, probs = _scene(n=10)
+    a = MeshAnnotation(mesh, layout, num_classes=12, aggregator=agg, max_batch=4, order_items=True)
+    b = MeshAnnotation(mesh, layout, num_classes=12, aggregator=agg, max_batch=4, order_items=False)
+    a.ORDER_SHIFT = 4  # many row blocks on this small layout
+    a.add_batch(probs, frames)
+    b.add_batch(probs, frames)
+    acc_a, cnt_a = _state(a)
+    acc_b, cnt_b = _state(b)
+    np.testing.assert_array_equal(cnt_a, cnt_b)
+    np.testing.assert_allclose(acc_a, acc_b, rtol=1e-5, atol=1e-5)

@@ -23,6 +23,7 @@ from paper_2111_11103_b200.synth import (make_furnished_room, make_room, random_
 CONFIGS = {
     # name: (tess, width, height, fx, classes, frames, aggregator, layout steps, batch, pool)
     "cfg1": (32, 160, 120, 160.0, 13, 20, "sum", 1, 20, 4),
+    "cfg2": (158, 640, 480, 577.87, 40, 2000, "mul", 1, 256, 8),
     "cfg2sum": (158, 640, 480, 577.87, 40, 2000, "sum", 1, 256, 8),
     "cfg4": (158, 640, 480, 577.87, 40, 2000, "mul", 8, 256, 8),
     "cfg5": (646, 1920, 1080, 1728.0, 19, 500, "mul", 1, 32, 4),  # one GPU's share of the 8-GPU job
@@ -43,7 +44,8 @@ def run(name):
     cams = random_room_trajectory(frames, intr, seed=0)
     maps = softmax_maps(pool, H, W, c, seed=0, device="cuda")
     probs = [maps[i % pool] for i in range(frames)]
-    ann = MeshAnnotation(mesh, layout, num_classes=c, aggregator=agg, weight_mode="images_iid",
+    order = {"1": True, "0": False}.get(os.environ.get("TFB_ORDER", ""))  # force the item order on / off
+    ann = MeshAnnotation(mesh, layout, num_classes=c, aggregator=agg, weight_mode="images_iid", order_items=order,
                          accum_dtype="float64" if name.endswith("f64") else "float32", max_batch=batch)
     cams_dev = ann.scene.cams_tensor(cams)
     setup_s = time.time() - t0
@@ -72,6 +74,7 @@ def run(name):
         "frames_per_s": frames / (ms / 1000.0), "ms_per_job": ms,
         "raster_us_per_frame": 1000.0 * raster / frames, "fuse_us_per_frame": 1000.0 * fuse / frames,
         "fuse_gbs": b_frame * frames / (fuse / 1000.0) / 1e9, "setup_s": round(setup_s, 1),
+        "order_items": ann._use_order(),
         "fuse_kernel": ("k_fuse<double> (general)" if name.endswith("f64") else
                         "k_fuse_fast<VEC>" if c % 4 == 0 else "k_fuse_fast<scalar quads>"),
     }), flush=True)
