@@ -272,6 +272,34 @@ __device__ __forceinline__ unsigned long long to_fixed(double x) {
   return (unsigned long long)__double2ll_rn(x * 4294967296.0);
 }
 
+// NumPy argmax / max of one pixel's c staged classes, in class order (first NaN wins,
+// else the first maximum; cli.py:293, fusion.py:174).  Lanes hold different pixels, c
+// words apart: with c % 4 == 0 the classes move as 16-byte quads (the 4c-byte pixel
+// stride puts the quads of 8 lanes on at most 2-way conflicting banks, where scalar
+// reads at a stride of 40 words would be 8-way); an odd c is conflict-free as scalars.
+template <bool VEC>
+__device__ __forceinline__ void pixel_argmax(const float *pp, int c, float &best, int &bi) {
+  best = pp[0];
+  bi = 0;
+  auto take = [&](float v, int k) {
+    if (!isnan(best) && (isnan(v) || v > best)) {
+      best = v;
+      bi = k;
+    }
+  };
+  if (VEC) {
+    for (int k = 0; k < c; k += 4) {
+      const float4 v = *reinterpret_cast<const float4 *>(pp + k);
+      take(v.x, k);
+      take(v.y, k + 1);
+      take(v.z, k + 2);
+      take(v.w, k + 3);
+    }
+  } else {
+    for (int k = 1; k < c; ++k) take(pp[k], k);
+  }
+}
+
 template <typename AccT, int AGG, bool EQW, bool FIX = false>
 __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ FuseParams p) {
   // product rule in float32 with weights constant per run: fold w*log(prod p)
@@ -383,16 +411,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
     // per-pixel maximum (maxsum, fusion.py:174) and network argmax fallback (cli.py:293)
     if (AGG == TFB_AGG_MAXSUM || p.fallback) {
       if (lane < npix) {
-        const float *pp = st + (size_t)lane * c;
-        float best = pp[0];
-        int bi = 0;
-        for (int k = 1; k < c; ++k) {
-          const float v = pp[k];
-          if (!isnan(best) && (isnan(v) || v > best)) {
-            best = v;
-            bi = k;
-          }
-        }
+        float best;
+        int bi;
+        if (vec_ok) pixel_argmax<true>(st + (size_t)lane * c, c, best, bi);
+        else pixel_argmax<false>(st + (size_t)lane * c, c, best, bi);
         smax[lane] = best;
         if (p.fallback) p.fallback[(int64_t)cur.f * p.hw + start + lane] = bi;
       }
@@ -624,7 +646,7 @@ __device__ __forceinline__ void sts4(float *p, float4 v, int nv) {
   if (nv > 3) p[3] = v.w;
 }
 
-template <int AGG, bool VEC, int CC, bool ORD = false>
+template <int AGG, bool VEC, int CC, bool ORD = false, bool FIX = false>
 __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant__ FuseParams p) {
   constexpr bool kProd = AGG == TFB_AGG_MUL;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -736,16 +758,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
 
     if (AGG == TFB_AGG_MAXSUM || p.fallback) {  // fusion.py:174, cli.py:293
       if (lane < npix) {
-        const float *pp = st + (size_t)lane * c;
-        float best = pp[0];
-        int bi = 0;
-        for (int k = 1; k < c; ++k) {
-          const float v = pp[k];
-          if (!isnan(best) && (isnan(v) || v > best)) {
-            best = v;
-            bi = k;
-          }
-        }
+        float best;
+        int bi;
+        pixel_argmax<VEC>(st + (size_t)lane * c, c, best, bi);
         smax[lane] = best;
         if (p.fallback) p.fallback[(int64_t)cur.f * p.hw + cur.ch * kChunk + lane] = bi;
       }
@@ -856,9 +871,20 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
         const float wv = __int_as_float(h.y);
         const float2 o01 = mul2(make_float2(b0, b1), make_float2(wv, wv));
         const float2 o23 = mul2(make_float2(b2, b3), make_float2(wv, wv));
-        if (ok)
-          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(accq + h.x), "f"(o01.x), "f"(o01.y),
-                       "f"(o23.x), "f"(o23.y));
+        if (ok) {
+          if (FIX) {
+            // fixed-point accumulator (TFB_ACCUM_FIXED): the piece's float32 value, rounded
+            // once to 2^-32 units; integer adds make the sum independent of their order
+            unsigned long long *dq = reinterpret_cast<unsigned long long *>(p.accum) + h.x + 4 * q;
+            atomicAdd(dq, to_fixed(o01.x));
+            if (nv > 1) atomicAdd(dq + 1, to_fixed(o01.y));
+            if (nv > 2) atomicAdd(dq + 2, to_fixed(o23.x));
+            if (nv > 3) atomicAdd(dq + 3, to_fixed(o23.y));
+          } else {
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(accq + h.x), "f"(o01.x), "f"(o01.y),
+                         "f"(o23.x), "f"(o23.y));
+          }
+        }
       }
       __syncwarp();
     }
@@ -940,7 +966,11 @@ int launch_fuse(const FuseParams &p, cudaStream_t st) {
 }
 
 template <int AGG, bool VEC, int CC = 0>
-int launch_fuse_fast(const FuseParams &p, cudaStream_t st) {
+int launch_fuse_fast(const FuseParams &p, cudaStream_t st, bool fix) {
+  if (fix) {
+    static LaunchCache lcf;
+    return launch_persistent(k_fuse_fast<AGG, VEC, CC, false, true>, lcf, fast_layout(p.c, p.NS).total, p, st);
+  }
   if (p.order) {
     static LaunchCache lco;
     return launch_persistent(k_fuse_fast<AGG, VEC, CC, true>, lco, fast_layout(p.c, p.NS).total, p, st);
@@ -952,17 +982,17 @@ int launch_fuse_fast(const FuseParams &p, cudaStream_t st) {
 // Common class counts get their own instantiation (NYU40, ScanNet 20,
 // Cityscapes 19, NYU13): 3-4 % faster than the runtime-c kernel at c = 40.
 template <int AGG>
-int launch_fuse_fast_c(const FuseParams &p, bool vec, cudaStream_t st) {
+int launch_fuse_fast_c(const FuseParams &p, bool vec, cudaStream_t st, bool fix) {
 #if TFB_FUSE_CSPEC
   switch (p.c) {
-    case 40: return launch_fuse_fast<AGG, true, 40>(p, st);
-    case 20: return launch_fuse_fast<AGG, true, 20>(p, st);
-    case 19: return launch_fuse_fast<AGG, false, 19>(p, st);
-    case 13: return launch_fuse_fast<AGG, false, 13>(p, st);
+    case 40: return launch_fuse_fast<AGG, true, 40>(p, st, fix);
+    case 20: return launch_fuse_fast<AGG, true, 20>(p, st, fix);
+    case 19: return launch_fuse_fast<AGG, false, 19>(p, st, fix);
+    case 13: return launch_fuse_fast<AGG, false, 13>(p, st, fix);
     default: break;
   }
 #endif
-  return vec ? launch_fuse_fast<AGG, true>(p, st) : launch_fuse_fast<AGG, false>(p, st);
+  return vec ? launch_fuse_fast<AGG, true>(p, st, fix) : launch_fuse_fast<AGG, false>(p, st, fix);
 }
 
 template <typename AccT, int AGG, bool FIX = false>
@@ -1210,20 +1240,23 @@ extern "C" int tfb_fuse_ordered(const int32_t *rows, int64_t hw, int nframes, co
     // used only when every item is in it or nothing per pixel is written (no fallback output)
     p.order = (item_order && nframes <= fpl && !fallback_out) ? item_order : nullptr;
     p.norder = p.order ? n_items : nullptr;
-    bool fast = !wide && weight_mode != TFB_W_EXPLICIT && g_fuse_fast;
+    // the specialised kernel serves float32 and fixed-point accumulators (the latter with
+    // float32 piece arithmetic); float64 keeps the reference's per-pixel double arithmetic
+    const bool fix = accum_kind == TFB_ACCUM_FIXED;
+    bool fast = (!wide || fix) && weight_mode != TFB_W_EXPLICIT && g_fuse_fast;
     for (int i = 0; i < nf && fast; ++i) fast = ((uintptr_t)p.probs[i] & 15) == 0;
     const bool vec = num_classes % 4 == 0;
     int rc;
     if (fast) {
       switch (aggregator) {
         case TFB_AGG_SUM:
-          rc = launch_fuse_fast_c<TFB_AGG_SUM>(p, vec, st);
+          rc = launch_fuse_fast_c<TFB_AGG_SUM>(p, vec, st, fix);
           break;
         case TFB_AGG_MAXSUM:
-          rc = launch_fuse_fast_c<TFB_AGG_MAXSUM>(p, vec, st);
+          rc = launch_fuse_fast_c<TFB_AGG_MAXSUM>(p, vec, st, fix);
           break;
         default:
-          rc = launch_fuse_fast_c<TFB_AGG_MUL>(p, vec, st);
+          rc = launch_fuse_fast_c<TFB_AGG_MUL>(p, vec, st, fix);
           break;
       }
     } else if (accum_kind == TFB_ACCUM_FIXED) {

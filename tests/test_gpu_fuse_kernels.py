@@ -165,3 +165,23 @@ def test_fuse_fast_products_at_the_clip_floor():
         ref, cref = _oracle(rows, probs, hw // 160, agg, "images_iid", 0.0)
         np.testing.assert_array_equal(cnt, cref)
         _check(got, ref, _scale(rows, probs, hw // 160, agg, "images_iid", 0.0))
+
+
+@pytest.mark.parametrize("fast", [True, False])
+@pytest.mark.parametrize("c", [7, 8, 19, 40])
+def test_fused_argmax_ties_and_nan(fast, c):
+    """The fused network argmax / per-pixel maximum (cli.py:293, fusion.py:174), read as 16-byte
+    quads when c % 4 == 0: NumPy's rule must hold -- the first NaN wins, else the FIRST maximum
+    (many exact ties here)."""
+    rng = np.random.default_rng(77 + c)
+    nframes, hw, n_x = 2, 32 * 23 + 9, 50
+    rows = _rows(rng, nframes, hw, n_x)
+    probs = (np.round(rng.random((nframes, hw, c)) * 4) / 4).astype(np.float32)  # values in {0, .25, ..., 1}
+    flat = probs.reshape(-1)
+    flat[rng.choice(flat.size, size=flat.size // 97, replace=False)] = np.nan
+    for agg in ("sum", "maxsum"):
+        got, cnt, fb = _run(rows, probs, n_x, agg, "pixels_iid", 0.0, fast)
+        np.testing.assert_array_equal(fb, probs.argmax(axis=2))
+        ref, cref = _oracle(rows, probs, n_x, agg, "pixels_iid", 0.0)
+        np.testing.assert_array_equal(cnt, cref)
+        _check(got, ref, _scale(rows, probs, n_x, agg, "pixels_iid", 0.0))

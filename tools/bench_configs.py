@@ -29,8 +29,10 @@ CONFIGS = {
     "cfg5": (646, 1920, 1080, 1728.0, 19, 500, "mul", 1, 32, 4),  # one GPU's share of the 8-GPU job
     # cfg2 with furniture (SURVEY §7 hard part 9): 10 boxes, +1.4 % triangles, occlusion / overdraw
     "cfg2furn": (158, 640, 480, 577.87, 40, 2000, "mul", 1, 256, 8),
-    # cfg2 with the float64 accumulator (the library / session API default, the reference's precision)
+    # cfg2 with the float64 accumulator (the library API default, the reference's precision)
     "cfg2f64": (158, 640, 480, 577.87, 40, 2000, "mul", 1, 256, 8),
+    # cfg2 with the fixed-point accumulator (the session default and deterministic=true)
+    "cfg2fix": (158, 640, 480, 577.87, 40, 2000, "mul", 1, 256, 8),
 }
 
 
@@ -46,7 +48,8 @@ def run(name):
     probs = [maps[i % pool] for i in range(frames)]
     order = {"1": True, "0": False}.get(os.environ.get("TFB_ORDER", ""))  # force the item order on / off
     ann = MeshAnnotation(mesh, layout, num_classes=c, aggregator=agg, weight_mode="images_iid", order_items=order,
-                         accum_dtype="float64" if name.endswith("f64") else "float32", max_batch=batch)
+                         accum_dtype=("float64" if name.endswith("f64") else "fixed64" if name.endswith("fix")
+                                      else "float32"), max_batch=batch)
     cams_dev = ann.scene.cams_tensor(cams)
     setup_s = time.time() - t0
 
@@ -75,7 +78,7 @@ def run(name):
         "raster_us_per_frame": 1000.0 * raster / frames, "fuse_us_per_frame": 1000.0 * fuse / frames,
         "fuse_gbs": b_frame * frames / (fuse / 1000.0) / 1e9, "setup_s": round(setup_s, 1),
         "order_items": ann._use_order(),
-        "fuse_kernel": ("k_fuse<double> (general)" if name.endswith("f64") else
+        "fuse_kernel": ("k_fuse<double> (general)" if name.endswith(("f64", "fix")) else
                         "k_fuse_fast<VEC>" if c % 4 == 0 else "k_fuse_fast<scalar quads>"),
     }), flush=True)
     del ann, maps, probs

@@ -27,7 +27,7 @@ def main():
         mp, tp = os.path.join(d, "m.ply"), os.path.join(d, "t.txt")
         save_ply(mp, mesh)
         save_trajectory(tp, frames)
-        s = open_session(mp, tp, 0.0, "mul", "images_iid", 40, accum_dtype="float32")
+        s = open_session(mp, tp, 0.0, "mul", "images_iid", 40)
         for fr in frames[:300]:
             add_frame(s, fr.frame_id, views[0])
         s.ann.flush()
@@ -39,7 +39,8 @@ def main():
         s.ann.flush()
         torch.cuda.synchronize()
         pr.disable()
-    pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+    pstats.Stats(pr).sort_stats("tottime").print_stats(30)
+    pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
 
 
 if __name__ == "__main__":
