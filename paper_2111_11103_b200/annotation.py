@@ -241,8 +241,11 @@ class MeshAnnotation:
             ws1 = lib.tfb_raster_workspace_bytes(nv, m, W, H, 1, 0)
             ws2 = lib.tfb_raster_workspace_bytes(nv, m, W, H, 2, 0)
             per = (ws2 - ws1) + W * H * 4 * (2 + self.num_classes) + max(self._tex.total_texels, 1) * 4
+            # what is free plus what the caching allocator holds unused (blocks of earlier
+            # jobs count as used to the driver but are ours to reuse)
             free, _total = torch.cuda.mem_get_info(self.device)
-            b = int(max(1, min(MAX_BATCH_CAP, (free // 4 - ws1) // max(per, 1))))
+            cached = torch.cuda.memory_reserved(self.device) - torch.cuda.memory_allocated(self.device)
+            b = int(max(1, min(MAX_BATCH_CAP, ((free + cached) // 4 - ws1) // max(per, 1))))
             self._auto_batch[(W, H)] = b
         return b
 

@@ -23,6 +23,7 @@ from paper_2111_11103_b200.synth import make_room, random_room_trajectory, scann
 
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
+    only = sys.argv[2].split(",") if len(sys.argv) > 2 else ["fixed64", "float32", "float64", "ann", "lib"]
     v, t = make_room((6.0, 5.0, 3.0), 158)
     mesh = Mesh.from_arrays(v, t)
     frames = random_room_trajectory(n, scannet_intrinsics(), seed=0)
@@ -32,21 +33,44 @@ def main():
         mp, tp = os.path.join(d, "m.ply"), os.path.join(d, "t.txt")
         save_ply(mp, mesh)
         save_trajectory(tp, frames)
-        for acc in ("fixed64", "float32", "float64"):
+        for rep, acc in enumerate(only):
+            if acc not in ("fixed64", "float32", "float64"):
+                continue
             s = open_session(mp, tp, 0.0, "mul", "images_iid", 40, accum_dtype=acc)
-            add_frame(s, frames[0].frame_id, maps[0])
+            for fr in frames[:300]:  # warm-up: the GPU leaves its idle clocks, buffers are allocated
+                add_frame(s, fr.frame_id, maps[0])
             s.ann.flush()
             torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t0 = time.time()
+            e0.record()
+            s.ann.profile = []
             for i, fr in enumerate(frames):
                 add_frame(s, fr.frame_id, maps[i % 8])
+            t_py = time.time() - t0
             s.ann.flush()
+            e1.record()
             torch.cuda.synchronize()
             dt = time.time() - t0
+            out["s%d_%s_host_us" % (rep, acc)] = round(1e6 * t_py / n, 1)
+            out["s%d_%s_device_us" % (rep, acc)] = round(1e3 * e0.elapsed_time(e1) / n, 1)
+            out["s%d_%s_batch" % (rep, acc)] = s.ann._batch_for(640, 480)
+            prof, s.ann.profile = s.ann.profile, None
+            out["s%d_%s_raster_fuse_us" % (rep, acc)] = [
+                round(1e3 * sum(a.elapsed_time(b) for _, a, b, _, _ in prof) / n, 1),
+                round(1e3 * sum(a.elapsed_time(b) for _, _, _, a, b in prof) / n, 1)]
+            import gc
+            out["session_%s_rep%d" % (acc, rep)] = round(n / dt)
             finalize_and_render(s, [frames[0].frame_id])
             out["session_add_frame_%s%s" % (acc, " (default)" if acc == "fixed64" else "")] = round(n / dt)
+            del s
+            gc.collect()
+    if "ann" not in only:
+        print(json.dumps(out), flush=True)
+        return
     ann = MeshAnnotation(mesh, uniform_layout(mesh, 1), num_classes=40, aggregator="mul")
-    ann.add(maps[0], frames[0])
+    for fr in frames[:300]:
+        ann.add(maps[0], fr)
     ann.flush()
     torch.cuda.synchronize()
     t0 = time.time()
