@@ -71,12 +71,23 @@ def run(name):
     raster = sum(r0.elapsed_time(r1) for _, r0, r1, _, _ in prof)
     fuse = sum(f0.elapsed_time(f1) for _, _, _, f0, f1 in prof)
     b_frame = H * W * (4 * c + 8)
+    # the accumulator read-modify-write term, reported on its own (never folded into
+    # the headline bytes): T_frame distinct texels touched per frame x stride x 4 B x 2
+    touched = []
+    for k in range(0, min(frames, 64), 8):
+        ann.reset()
+        ann.add_batch(probs[k:k + 1], cams_dev[k:k + 1], width=W, height=H)
+        touched.append(int((ann.texture.counts_device() > 0).sum().item()))
+    t_frame = sum(touched) / len(touched)
     print(json.dumps({
         "config": name, "triangles": mesh.num_triangles, "texels": layout.total_texels, "size": [W, H],
         "classes": c, "aggregator": agg, "frames": frames, "batch": batch,
         "frames_per_s": frames / (ms / 1000.0), "ms_per_job": ms,
         "raster_us_per_frame": 1000.0 * raster / frames, "fuse_us_per_frame": 1000.0 * fuse / frames,
         "fuse_gbs": b_frame * frames / (fuse / 1000.0) / 1e9, "setup_s": round(setup_s, 1),
+        "bytes_per_frame_maps": b_frame, "texels_touched_per_frame": round(t_frame),
+        "accum_rmw_bytes_per_frame": int(t_frame * ann.texture.stride * (8 if ann.texture.accum_kind else 4) * 2),
+        "accum_bytes": int(layout.total_texels * ann.texture.stride * (8 if ann.texture.accum_kind else 4)),
         "order_items": ann._use_order(),
         "fuse_kernel": ("k_fuse<double> (general)" if name.endswith(("f64", "fix")) else
                         "k_fuse_fast<VEC>" if c % 4 == 0 else "k_fuse_fast<scalar quads>"),
