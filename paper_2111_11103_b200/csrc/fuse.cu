@@ -156,11 +156,14 @@ __device__ __forceinline__ float clip_mul(float x) {
   return y;
 }
 
-__device__ __forceinline__ double np_clip(double x, double lo, double hi) {
-  if (isnan(x)) return x;
-  x = x > lo ? x : lo;
-  return x < hi ? x : hi;
+// np.clip((double)v, 1e-7, 1) for a float32 v, compared in float: no float lies in
+// [1e-7, kMulClampF) (kMulClampF is the float just above 1e-7), so v < 1e-7 as a double
+// exactly when v < kMulClampF.  NaN fails every comparison and passes through.
+__device__ __forceinline__ double clip_mul64(float v) {
+  return v < kMulClampF ? kMulClamp : (v > 1.0f ? 1.0 : (double)v);
 }
+
+
 
 __device__ __forceinline__ bool tma_ok(const float *src, int npix, int c) {
   const size_t bytes = (size_t)npix * c * 4;
@@ -502,10 +505,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
           if (kProd64) {
             // float64 parity mode, product rule with one weight per piece: the
             // clipped values multiply in double, one log per piece and class
-            d01.x *= np_clip((double)v0, kMulClamp, 1.0);
-            d01.y *= np_clip((double)v1, kMulClamp, 1.0);
-            d23.x *= np_clip((double)v2, kMulClamp, 1.0);
-            d23.y *= np_clip((double)v3, kMulClamp, 1.0);
+            d01.x *= clip_mul64(v0);
+            d01.y *= clip_mul64(v1);
+            d23.x *= clip_mul64(v2);
+            d23.y *= clip_mul64(v3);
           } else if (kProd) {
             m01 = mul2(m01, make_float2(clip_mul(v0), clip_mul(v1)));
             m23 = mul2(m23, make_float2(clip_mul(v2), clip_mul(v3)));
@@ -530,7 +533,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
             for (int k = 0; k < 4; ++k) {
               if (AGG == TFB_AGG_SUM) tt[k] = (double)vv[k];
               else if (AGG == TFB_AGG_MAXSUM) tt[k] = vv[k] == smax[i] ? (double)vv[k] : 0.0;
-              else tt[k] = log(np_clip((double)vv[k], kMulClamp, 1.0));
+              else tt[k] = log(clip_mul64(vv[k]));
             }
             a0 += wi * tt[0]; a1 += wi * tt[1]; a2 += wi * tt[2]; a3 += wi * tt[3];
           }
@@ -909,6 +912,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
 
 std::atomic<int> g_fuse_ctas_per_sm{0};  // 0 = as many as fit (tfb_set_option(TFB_OPT_FUSE_CTAS_PER_SM))
 std::atomic<int> g_fuse_fast{1};         // tfb_set_option(TFB_OPT_FUSE_FAST): 0 routes everything through k_fuse
+
 
 // Per-device launch configuration of one kernel (dynamic shared memory attribute,
 // occupancy), computed once per device and size; entry points stay re-entrant.

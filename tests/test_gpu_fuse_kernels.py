@@ -185,3 +185,55 @@ def test_fused_argmax_ties_and_nan(fast, c):
         ref, cref = _oracle(rows, probs, n_x, agg, "pixels_iid", 0.0)
         np.testing.assert_array_equal(cnt, cref)
         _check(got, ref, _scale(rows, probs, n_x, agg, "pixels_iid", 0.0))
+
+
+def _run64(rows, probs, n_x, agg, wm, alpha, weights=None):
+    """tfb_fuse into a float64 accumulator (the reference's precision, fusion.py:145-183)."""
+    lib = N.load()
+    nframes, hw = rows.shape
+    c = probs.shape[2]
+    dev = torch.device("cuda")
+    rows_d = torch.as_tensor(rows, device=dev)
+    pd = [torch.as_tensor(probs[f], device=dev).contiguous() for f in range(nframes)]
+    ptrs = (P * nframes)(*[t.data_ptr() for t in pd])
+    hits = torch.zeros((nframes, n_x), dtype=torch.int32, device=dev)
+    acc = torch.zeros((n_x, c), dtype=torch.float64, device=dev)
+    cnt = torch.zeros(n_x, dtype=torch.int32, device=dev)
+    wd = torch.as_tensor(weights, device=dev) if weights is not None else None
+    stream = P(torch.cuda.current_stream().cuda_stream)
+    N.check(lib.tfb_count_hits(P(rows_d.data_ptr()), hw, nframes, n_x, P(hits.data_ptr()), stream))
+    N.check(lib.tfb_fuse(P(rows_d.data_ptr()), hw, nframes, ctypes.cast(ptrs, P), c, P(hits.data_ptr()),
+                         P(wd.data_ptr()) if wd is not None else None, n_x, N.AGG_IDS[agg],
+                         N.WMODE_IDS["explicit" if wd is not None else wm], alpha, P(acc.data_ptr()), 1, c,
+                         P(cnt.data_ptr()), None, stream))
+    torch.cuda.synchronize()
+    return acc.cpu().numpy(), cnt.cpu().numpy()
+
+
+@pytest.mark.parametrize("c", [5, 19, 40])
+def test_float64_accumulator_log_within_1e12(c):
+    """The float64 accumulator's per-piece log and float-domain clip (fuse.cu clip_mul64)
+    against NumPy's log(clip(p, 1e-7, 1)) (fusion.py:177): 1e-12 relative, with values at and
+    around 1, at the clip floor, below it, above 1 and NaN; piecewise products (count weights)
+    and per-pixel terms (explicit weights)."""
+    rng = np.random.default_rng(500 + c)
+    nframes, hw, n_x = 2, 32 * 41 + 3, 120
+    rows = _rows(rng, nframes, hw, n_x)
+    probs = _probs(rng, nframes, hw, c, special=True)
+    flat = probs.reshape(-1)
+    flat[rng.choice(flat.size, size=flat.size // 40, replace=False)] = np.float32(1e-7)
+    flat[rng.choice(flat.size, size=flat.size // 40, replace=False)] = np.float32(0.99999994)
+    flat[rng.choice(flat.size, size=flat.size // 40, replace=False)] = np.nextafter(np.float32(1e-7), np.float32(0))
+    for wm, alpha in (("images_iid", 0.0), ("blend", 0.25)):
+        got, cnt = _run64(rows, probs, n_x, "mul", wm, alpha)
+        ref, cref = _oracle(rows, probs, n_x, "mul", wm, alpha)
+        np.testing.assert_array_equal(cnt, cref)
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+    w = rng.uniform(0.1, 3.0, size=(nframes, hw))
+    got, _ = _run64(rows, probs, n_x, "mul", "explicit", 0.0, weights=w)
+    ref = np.zeros((n_x, c))
+    cref = np.zeros(n_x, np.int64)
+    for f in range(nframes):
+        O.accumulate_frame(ref, cref, np.arange(n_x, dtype=np.int64), rows[f], np.zeros_like(rows[f]), probs[f],
+                           w[f], "mul")
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
