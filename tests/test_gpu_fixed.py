@@ -69,3 +69,28 @@ def test_fixed_accumulator_host_views_and_checkpoint(tmp_path):
     np.testing.assert_array_equal(b.texture.accum, acc)  # float64 values round-trip exactly (multiples of 2^-32)
     b.texture.accum = acc * 0.5  # reference-style host write, uploaded before the next device op
     np.testing.assert_allclose(b.texture.accum, acc * 0.5, atol=2 ** -32)
+
+
+def test_fixed_accumulator_library_path_explicit_weights():
+    """accumulate_frame with caller weights (the general kernel's fixed-point landing) through the
+    library API: equal to the float64 texture to 2^-32 resolution, and order-free."""
+    from paper_2111_11103_b200 import accumulate_frame, finalize, init_texture, rasterize, texel_argmax
+
+    mesh, layout, frames, probs = _scene(n=5)
+    rng = np.random.default_rng(3)
+    ws = [rng.uniform(0.2, 2.0, size=(96, 128)) for _ in frames]
+    texs = {}
+    for kind, order in (("fixed64", range(5)), ("fixed64r", reversed(range(5))), ("float64", range(5))):
+        tex = init_texture(layout, 7, "mul", accum_dtype=kind.rstrip("r"))
+        for k in order:
+            ids = rasterize(mesh, layout, frames[k])
+            accumulate_frame(tex, ids, probs[k].cpu().numpy(), ws[k])
+        texs[kind] = tex
+    a, b, ref = texs["fixed64"], texs["fixed64r"], texs["float64"]
+    np.testing.assert_array_equal(a.accum, b.accum)  # bit-identical in any order
+    np.testing.assert_array_equal(a.counts, ref.counts)
+    np.testing.assert_allclose(a.accum, ref.accum, rtol=0, atol=1e-8)
+    for t in (a, ref):
+        finalize(t)
+    np.testing.assert_allclose(a.rows, ref.rows, atol=1e-6)
+    assert (texel_argmax(a) == texel_argmax(ref)).mean() > 0.999
