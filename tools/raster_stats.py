@@ -35,6 +35,9 @@ def main():
         lib = build_variant(["-DTFB_RASTER_STATS"])
     os.environ["TFB_LIB"] = lib
     sys.path.insert(0, ROOT)
+    from paper_2111_11103_b200 import _native as N  # build_variant imported the package already:
+    N._lib = None                                     # bind the stats variant explicitly
+    N.load(lib)
     import torch
     from paper_2111_11103_b200 import Mesh, MeshAnnotation, uniform_layout
     from paper_2111_11103_b200.synth import make_room, random_room_trajectory, scannet_intrinsics, softmax_maps
