@@ -169,3 +169,33 @@ def test_row_block_item_order_equals_frame_major(agg):
     acc_b, cnt_b = _state(b)
     np.testing.assert_array_equal(cnt_a, cnt_b)
     np.testing.assert_allclose(acc_a, acc_b, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("accum", ["float32", "fixed64"])
+def test_odd_frame_size_queue_order_and_fixed(accum):
+    """61x37 frames (a partial last 32-pixel chunk, H*W odd), some frames looking away from
+    everything: the queue, the row-block item order and the fixed-point landing agree with a
+    frame-major float64 fold."""
+    from paper_2111_11103_b200 import Mesh, MeshAnnotation, uniform_layout
+    from paper_2111_11103_b200.geometry import CameraFrame, Intrinsics
+    from paper_2111_11103_b200.synth import make_room, random_room_trajectory, softmax_maps
+
+    v, t = make_room((6.0, 5.0, 3.0), 16)
+    mesh = Mesh.from_arrays(v, t)
+    layout = uniform_layout(mesh, 3)
+    intr = Intrinsics(50.0, 50.0, 30.5, 18.5, 61, 37)
+    frames = random_room_trajectory(7, intr, seed=8)
+    # a camera outside the room looking away: no covered pixel at all
+    frames.append(CameraFrame(99, intr, np.eye(3), np.array([0.0, 0.0, 50.0])))
+    probs = softmax_maps(8, 37, 61, 9, seed=4)
+    ref = MeshAnnotation(mesh, layout, num_classes=9, aggregator="mul", accum_dtype="float64", max_batch=8)
+    ref.add_batch(probs, frames)
+    a = MeshAnnotation(mesh, layout, num_classes=9, aggregator="mul", accum_dtype=accum, max_batch=3,
+                       order_items=True)
+    a.ORDER_SHIFT = 3
+    for k, fr in enumerate(frames):
+        a.add(probs[k], fr)
+    np.testing.assert_array_equal(a.texture.counts, ref.texture.counts)
+    got, want = a.texture.accum, ref.texture.accum
+    err = np.abs(got - want) / np.maximum(np.abs(want), 1e-3)
+    assert err.max() < 1e-5, err.max()
