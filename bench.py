@@ -431,7 +431,7 @@ def run_ours(args):
         del out_imgs
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline is an N=1 figure
         threads = _cpu_threads()
         sample = CPU_FRAMES_PER_THREAD * threads
         val, dt = cpu_reference(args, sample, threads, scene=(mesh, layout))
