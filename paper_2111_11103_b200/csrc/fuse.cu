@@ -229,10 +229,12 @@ __device__ __forceinline__ AccT weight_from(const FuseParams &p, double src, int
 }
 
 // log of a (product of) clipped probabilities, x in [1e-28, 1]: MUFU lg2 (2 ulp
-// below 1/2, 2^-22.6 absolute above).  Where that absolute error would be
-// large relative to |log x| (x > 0.9) the log1p series in t = x - 1 (exact)
-// is used instead, truncation t^7/7 < 1.5e-7 relative.  In log4 the series
-// runs behind a warp vote, so warps with no such value skip it.
+// below 1/2, 2^-22.6 absolute above: at most 5.4e-6 relative for x <= 0.98, where
+// |log2 x| >= 0.029).  Above kNear1 that absolute error would be large relative to
+// |log x|, so the log1p series in t = x - 1 (exact) is used instead: |t| < 0.02,
+// truncation t^5/5 below 3.2e-8 relative.  In log4 the series runs behind a warp
+// vote, so warps with no such value skip it.
+constexpr float kNear1 = 0.98f;
 __device__ __forceinline__ float lg2_ln(float x) {
   float l;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(x));
@@ -241,7 +243,7 @@ __device__ __forceinline__ float lg2_ln(float x) {
 
 __device__ __forceinline__ float log1p_series(float x) {
   const float t = x - 1.0f;
-  return t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, fmaf(t, -1.0f / 6.0f, 1.0f / 5.0f), -0.25f), 1.0f / 3.0f), -0.5f), 1.0f);
+  return t * fmaf(t, fmaf(t, fmaf(t, -0.25f, 1.0f / 3.0f), -0.5f), 1.0f);
 }
 
 __device__ __forceinline__ void log4(float &a0, float &a1, float &a2, float &a3) {
@@ -250,16 +252,16 @@ __device__ __forceinline__ void log4(float &a0, float &a1, float &a2, float &a3)
   a1 = lg2_ln(x1);
   a2 = lg2_ln(x2);
   a3 = lg2_ln(x3);
-  const bool near1 = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3)) > 0.9f;
+  const bool near1 = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3)) > kNear1;
   if (__any_sync(__activemask(), near1)) {
-    if (x0 > 0.9f) a0 = log1p_series(x0);
-    if (x1 > 0.9f) a1 = log1p_series(x1);
-    if (x2 > 0.9f) a2 = log1p_series(x2);
-    if (x3 > 0.9f) a3 = log1p_series(x3);
+    if (x0 > kNear1) a0 = log1p_series(x0);
+    if (x1 > kNear1) a1 = log1p_series(x1);
+    if (x2 > kNear1) a2 = log1p_series(x2);
+    if (x3 > kNear1) a3 = log1p_series(x3);
   }
 }
 
-__device__ __forceinline__ float log_prob(float x) { return x > 0.9f ? log1p_series(x) : lg2_ln(x); }
+__device__ __forceinline__ float log_prob(float x) { return x > kNear1 ? log1p_series(x) : lg2_ln(x); }
 
 // packed float32x2 multiply (sm_100 FMUL2)
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
@@ -602,11 +604,11 @@ __device__ __forceinline__ float lg2_approx(float x) {
   return l;
 }
 
-// log2(x) for x in (0.9, 1] from the log1p series in t = x - 1 (exact), scaled by 1/ln2
+// log2(x) for x in (kNear1, 1] from the log1p series in t = x - 1 (exact), scaled by 1/ln2
 __device__ __forceinline__ float log2_series(float x) {
   const float t = x - 1.0f;
   constexpr float k = 1.4426950408889634f;
-  return t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, fmaf(t, -k / 6.0f, k / 5.0f), -k / 4.0f), k / 3.0f), -k / 2.0f), k);
+  return t * fmaf(t, fmaf(t, fmaf(t, -k / 4.0f, k / 3.0f), -k / 2.0f), k);
 }
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -863,12 +865,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
           b1 = lg2_approx(m.y);
           b2 = lg2_approx(m.z);
           b3 = lg2_approx(m.w);
-          const bool near1 = fmaxf(fmaxf(m.x, m.y), fmaxf(m.z, m.w)) > 0.9f;
+          const bool near1 = fmaxf(fmaxf(m.x, m.y), fmaxf(m.z, m.w)) > kNear1;
           if (__any_sync(0xffffffffu, near1)) {
-            if (m.x > 0.9f) b0 = log2_series(m.x);
-            if (m.y > 0.9f) b1 = log2_series(m.y);
-            if (m.z > 0.9f) b2 = log2_series(m.z);
-            if (m.w > 0.9f) b3 = log2_series(m.w);
+            if (m.x > kNear1) b0 = log2_series(m.x);
+            if (m.y > kNear1) b1 = log2_series(m.y);
+            if (m.z > kNear1) b2 = log2_series(m.z);
+            if (m.w > kNear1) b3 = log2_series(m.w);
           }
         }
         const float wv = __int_as_float(h.y);
