@@ -237,3 +237,22 @@ def test_float64_accumulator_log_within_1e12(c):
         O.accumulate_frame(ref, cref, np.arange(n_x, dtype=np.int64), rows[f], np.zeros_like(rows[f]), probs[f],
                            w[f], "mul")
     np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("c", [7, 19, 40, 41])
+@pytest.mark.parametrize("agg", ["sum", "maxsum", "mul"])
+def test_fuse_piece_per_pixel_chunks(c, agg):
+    """Chunks where nearly every pixel is its own piece (tiny triangles: configs[4]), mixed with
+    long-run chunks in the same launch, special values included."""
+    rng = np.random.default_rng(900 + c)
+    nframes, hw, n_x = 2, 32 * 50 + 13, 5000
+    rows = rng.integers(0, n_x, size=(nframes, hw)).astype(np.int32)  # a new row at every pixel
+    rows[:, ::17] = -1
+    rows[:, 32 * 10: 32 * 20] = np.repeat(np.arange(40, dtype=np.int32), 8)[None, :]  # long runs too
+    probs = _probs(rng, nframes, hw, c, special=True)
+    for wm, alpha in (("images_iid", 0.0), ("blend", 0.3)):
+        got, cnt, fb = _run(rows, probs, n_x, agg, wm, alpha, True)
+        ref, cref = _oracle(rows, probs, n_x, agg, wm, alpha)
+        np.testing.assert_array_equal(cnt, cref)
+        _check(got, ref, _scale(rows, probs, n_x, agg, wm, alpha))
+    np.testing.assert_array_equal(fb, probs.argmax(axis=2))
