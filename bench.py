@@ -238,13 +238,18 @@ def run_ours(args):
     from paper_2111_11103_b200.synth import make_room, random_room_trajectory, scannet_intrinsics, softmax_maps
 
     world, rank, local = _dist_env()
-    if world > torch.cuda.device_count():
+    if world > torch.cuda.device_count() and not args.share_gpu:
         raise SystemExit("bench.py: %d ranks but only %d visible GPUs" % (world, torch.cuda.device_count()))
+    if args.share_gpu:  # functional self-test of the multi-rank code path only (never a measurement)
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)  # before the process group, so NCCL binds this rank's GPU
     dev = torch.device("cuda", local)
     comm = None
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", init_method="env://", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend, init_method="env://")
         probe = torch.ones(1, device=dev)
         dist.all_reduce(probe)  # forces communicator creation; every rank must contribute
         comm = {"backend": dist.get_backend(), "world_size": dist.get_world_size(), "nranks_seen": int(probe.item()),
@@ -256,14 +261,16 @@ def run_ours(args):
     mesh = Mesh.from_arrays(v, t)
     layout = uniform_layout(mesh, 1)
     if args.scaling == "weak":
+        lo = 0
         frames = random_room_trajectory(args.frames, scannet_intrinsics(), seed=1000 + rank)
     else:  # strong: one 2000-frame trajectory, contiguous block per rank (dist.shard_bounds)
         lo, hi = shard_bounds(args.frames, rank, world)
         frames = random_room_trajectory(args.frames, scannet_intrinsics(), seed=1000)[lo:hi]
     nf = len(frames)
     cams_dev = torch.as_tensor(np.stack([pack_camera(f) for f in frames])).to(dev)
-    pool = softmax_maps(POOL, H, W, C, seed=rank, device=dev)
-    probs_list = [pool[i % POOL] for i in range(nf)]
+    # strong scaling: frame g gets map g % POOL whatever the rank count, so every N fuses the same job
+    pool = softmax_maps(POOL, H, W, C, seed=rank if args.scaling == "weak" else 0, device=dev)
+    probs_list = [pool[(lo + i) % POOL] for i in range(nf)]
     ann = MeshAnnotation(mesh, layout, num_classes=C, aggregator=AGG, weight_mode=WMODE, accum_dtype="float32",
                          max_batch=args.batch, device=dev, overlap=args.overlap,
                          fuse_ctas_per_sm=args.fuse_ctas if args.fuse_ctas >= 0 else None)
@@ -295,6 +302,8 @@ def run_ours(args):
         t_end.record(stream)
         barrier()
     prof, ann.profile = ann.profile, None
+    if args.dump_labels and rank == 0:  # after the timed region: the fused labels, for cross-N checks
+        np.save(args.dump_labels, ann.labels(host=True))
     ms = t_start.elapsed_time(t_end)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     frames_t = torch.tensor([float(nf)], dtype=torch.float64, device=dev)
@@ -455,6 +464,9 @@ def run_ours(args):
             "clocks": clocks.summary(), "e2e": e2e, "f64_accumulator": f64, "render": render, "cpu_baseline": cpu,
             "gpu_launches": gpu_launches, "comm": comm,
         }
+        if args.share_gpu:
+            line["functional_test"] = "ranks shared %d GPU(s) over %s: a code-path check, not a measurement" % (
+                torch.cuda.device_count(), args.dist_backend)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -496,6 +508,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-f64", action="store_true")
     ap.add_argument("--no-render", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: functional tests of the multi-rank path only")
+    ap.add_argument("--dump-labels", default=None, help="rank 0 saves the fused labels (.npy) after the timed steps")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="functional test: more ranks than GPUs (ranks share them); never a measurement")
     ap.add_argument("--no-pageable", action="store_true")
     args = ap.parse_args()
     if args.gpus < 1:
