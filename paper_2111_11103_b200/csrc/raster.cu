@@ -54,6 +54,9 @@ constexpr int kThreads = 256;              // setup-side kernels
 #ifndef TFB_FIRST_FAST
 #define TFB_FIRST_FAST 1
 #endif
+#ifndef TFB_PAIR_WIN
+#define TFB_PAIR_WIN 1  // k_raster pair phase in warp windows (0: per-thread contiguous pair runs)
+#endif
 #ifndef TFB_RASTER_MINB
 #define TFB_RASTER_MINB 9  // k_raster CTAs per SM the register budget must allow (56 regs, 36 warps)
 #endif
@@ -865,8 +868,9 @@ struct AosRec {  // one RecGeom (global memory or AoS shared memory)
 // Record j of a tile staged field-major (lanes reading different records hit
 // different banks).  Only xs, ys, zs and |area2| are staged (kStaged fields);
 // the edge deltas are re-derived on read exactly as expand_derived forms them.
-constexpr int kStaged = 10;
-constexpr int kSA2 = 9;  // staged slot of |area2|
+constexpr int kStaged = 11;
+constexpr int kSA2 = 9;   // staged slot of |area2|
+constexpr int kSThr = 10;  // staged slot of the sole-candidate threshold (first_win_threshold)
 struct SoaRec {
   const double *base;
   int j;
@@ -976,6 +980,18 @@ __device__ __forceinline__ bool first_wins_without_divisions(const R &g, const d
   const double zmax = fmax(fmax(z0, z1), z2);
   const double emax = fmax(fmax(e[0], e[1]), e[2]);
   return zok && a2 >= 1e-100 && a2 <= 1e100 && emax <= 1e100 && emax >= __dmul_rn(__dmul_rn(a2, zmax), 1e-50);
+}
+
+// first_wins_without_divisions with the record-only part folded into one number per
+// record, formed when the record is staged: a2 * max z_k * 1e-50 when steps = 1 and the
+// z_k and a2 ranges hold, else NaN (every comparison against it fails).  A covering
+// pixel's sole record then wins without divisions iff max e_k <= 1e100 && max e_k >= thr.
+__device__ __forceinline__ double first_win_threshold(const double zs[3], double a2, uint32_t flags) {
+  const double z0 = zs[0], z1 = zs[1], z2 = zs[2];
+  const bool zok = z0 >= 1e-100 && z0 <= 1e100 && z1 >= 1e-100 && z1 <= 1e100 && z2 >= 1e-100 && z2 <= 1e100;
+  const double zmax = fmax(fmax(z0, z1), z2);
+  const bool ok = (flags >> 16) == 1u && zok && a2 >= 1e-100 && a2 <= 1e100;
+  return ok ? __dmul_rn(__dmul_rn(a2, zmax), 1e-50) : __longlong_as_double(0x7ff8000000000000LL);
 }
 
 __device__ __forceinline__ void emit_pixel(const tfb_scene &sc, const Outs &o, int f, int64_t pix, int32_t t,
@@ -1170,6 +1186,7 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
 #pragma unroll
     for (int q = 0; q < 9; ++q) sg[q * kFS + tid] = v[2 + q];
     sg[kSA2 * kFS + tid] = a2;
+    sg[kSThr * kFS + tid] = first_win_threshold(v + 8, a2, mt.flags);
     skey[tid] = key;
     sflags[tid] = mt.flags;
     soff[tid] = mt.off;
@@ -1215,6 +1232,79 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
   }
 
   if (tid == 0) RSTAT(32 + min(total / 256u, 15u));
+#if TFB_PAIR_WIN
+  // pair-parallel edge tests in warp windows: a window is 32 consecutive (record, pixel of
+  // its bbox) pairs, lane l taking pair base + l, and each warp walks a contiguous range of
+  // windows.  The records starting inside a window come from one shared-memory load per
+  // lane and a warp OR-reduction, so a lane finds its record with a popcount (no per-lane
+  // search), and all lanes run the same straight-line test (no per-lane row / record
+  // refills diverging across the warp).
+  {
+    const uint32_t nwin = (total + 31u) >> 5;
+    const uint32_t wper = (nwin + (kTP / 32) - 1) / (kTP / 32);
+    const uint32_t wbeg = (uint32_t)warp * wper, wend = min(wbeg + wper, nwin);
+    if (wbeg < wend) {
+      const unsigned upto = (2u << lane) - 1u;
+      // jb: the record holding pair base - 1 (areas are >= 1: every binned bbox meets the
+      // tile), i.e. the number of records starting at or before it, less one
+      int jb = -1;
+      if (wbeg > 0u) {
+        const uint32_t q = (wbeg << 5) - 1u;
+        for (int r0 = 0; r0 < (int)n; r0 += 32)
+          jb += __popc(__ballot_sync(0xffffffffu, r0 + lane < (int)n && spre[r0 + lane] <= q));
+      }
+      for (uint32_t wi = wbeg; wi < wend; ++wi) {
+        const uint32_t base = wi << 5;
+        const int jc = jb + 1 + lane;
+        unsigned bit = 0u;
+        if (jc < (int)n) {
+          const uint32_t st = spre[jc];
+          if (st < base + 32u) bit = 1u << (st - base);
+        }
+        const unsigned starts = __reduce_or_sync(0xffffffffu, bit);
+        const int j = jb + __popc(starts & upto);
+        jb += __popc(starts);
+        const uint32_t p = base + (uint32_t)lane;
+        if (p < total) {
+          const uint32_t b = sbox[j];
+          const int local = (int)(p - spre[j]);
+          const int bw = (int)((b >> 16) & 0xffu);
+          // local / bw (local < 2^15, bw <= 255): (local + 0.5) / bw sits >= 0.5 / bw from an
+          // integer, far above the error of the approximate reciprocal and the product
+          float rbw;
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rbw) : "f"((float)bw));
+          const int ly = (int)(((float)local + 0.5f) * rbw);
+          const int lx = local - ly * bw;
+          const int pxl = (int)(b & 0xffu) + lx, pyl = (int)((b >> 8) & 0xffu) + ly;
+          const SoaRec R{sg, j};
+          const double x0 = R.at(kFXs), x1 = R.at(kFXs + 1), x2 = R.at(kFXs + 2);
+          const double y0 = R.at(kFYs), y1 = R.at(kFYs + 1), y2 = R.at(kFYs + 2);
+          const uint32_t fl = sflags[j];
+          const double px = (double)(tx0 + pxl) + 0.5, py = (double)(ty0 + pyl) + 0.5;
+          // rasterizer.py:161-162, dX / dY exactly as expand_derived forms them
+          const double e0 = __dsub_rn(__dmul_rn(__dsub_rn(x2, x1), __dsub_rn(py, y1)),
+                                      __dmul_rn(__dsub_rn(y2, y1), __dsub_rn(px, x1)));
+          const double e1 = __dsub_rn(__dmul_rn(__dsub_rn(x0, x2), __dsub_rn(py, y2)),
+                                      __dmul_rn(__dsub_rn(y0, y2), __dsub_rn(px, x2)));
+          const double e2 = __dsub_rn(__dmul_rn(__dsub_rn(x1, x0), __dsub_rn(py, y0)),
+                                      __dmul_rn(__dsub_rn(y1, y0), __dsub_rn(px, x0)));
+          if ((e0 > 0.0 || (e0 == 0.0 && (fl & 1u))) && (e1 > 0.0 || (e1 == 0.0 && (fl & 2u))) &&
+              (e2 > 0.0 || (e2 == 0.0 && (fl & 4u)))) {
+            const int pix = pyl * kTW + pxl;
+            const uint32_t idx = atomicAdd(pcnt + pix, 1u);
+            if (idx < (uint32_t)kPC) pc[idx][pix] = j;
+            if (idx == 0u) {  // used only when this is the pixel's sole candidate
+              pe[0][pix] = e0;
+              pe[1][pix] = e1;
+              pe[2][pix] = e2;
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+#else
   // pair-parallel edge tests: thread handles pairs [p0, p1)
   const uint32_t ppt = (total + kTP - 1) / kTP;
   const uint32_t p0 = tid * ppt, p1 = min(p0 + ppt, total);
@@ -1284,6 +1374,7 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
     }
   }
   __syncthreads();
+#endif
 
   // one thread per pixel: fold its covering records in ascending key order
   const int pxl = tid & (kTW - 1), pyl = tid / kTW;
@@ -1299,7 +1390,9 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
     const double e[3] = {pe[0][tid], pe[1][tid], pe[2][tid]};
     if (o.depth) {
       fd.step_e(SoaRec{sg, j}, e, j);
-    } else if (TFB_FIRST_FAST && (sflags[j] >> 16) == 1u && first_wins_without_divisions(SoaRec{sg, j}, e)) {
+    } else if (TFB_FIRST_FAST && e[0] <= 1e100 && e[1] <= 1e100 && e[2] <= 1e100 &&
+               (e[0] >= sg[kSThr * kFS + j] || e[1] >= sg[kSThr * kFS + j] || e[2] >= sg[kSThr * kFS + j])) {
+      // (max e_k <= 1e100 && max e_k >= thr, the e_k of a covering pair being no NaN)
       // One texel per triangle (steps = 1) and no float planes: the sole covering
       // record wins, and u in [0, 1], v in [0, u] give i = min(int(u), 0) = 0,
       // j = min(int(v), 0) = 0 (rasterizer.py:196-198), so the texel is 0 whatever
