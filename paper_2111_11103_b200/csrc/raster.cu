@@ -994,6 +994,14 @@ __device__ __forceinline__ double first_win_threshold(const double zs[3], double
   return ok ? __dmul_rn(__dmul_rn(a2, zmax), 1e-50) : __longlong_as_double(0x7ff8000000000000LL);
 }
 
+// max e_k <= 1e100 && max e_k >= thr for the (non-NaN) edge values of a covering pair,
+// evaluated without branches
+__device__ __forceinline__ bool first_fast(const double e[3], double thr) {
+  const bool lo = (e[0] <= 1e100) & (e[1] <= 1e100) & (e[2] <= 1e100);
+  const bool hi = (e[0] >= thr) | (e[1] >= thr) | (e[2] >= thr);
+  return lo & hi;
+}
+
 __device__ __forceinline__ void emit_pixel(const tfb_scene &sc, const Outs &o, int f, int64_t pix, int32_t t,
                                            int32_t texel, int32_t row);
 
@@ -1147,7 +1155,7 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
   // the bin entry this thread would stage is read speculatively, in flight together
   // with the tile's count (entries past the count are stale and ignored)
   const uint32_t *src = w.list + ((int64_t)f * ntiles + tile) * w.bincap;
-  const uint32_t key_spec = (int64_t)tid < w.bincap ? src[tid] : 0u;
+  const uint32_t key_spec = tid < (int)min(w.bincap, (int64_t)kTP) ? src[tid] : 0u;
   const uint32_t n = w.tile_count[(int64_t)f * ntiles + tile];
   if (n > (uint64_t)w.bincap || n > (uint32_t)kTP) {
     if (tid == 0) w.big[atomicAdd(w.fcnt + 1, 1u)] = (uint32_t)(f * ntiles + tile);
@@ -1390,9 +1398,7 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
     const double e[3] = {pe[0][tid], pe[1][tid], pe[2][tid]};
     if (o.depth) {
       fd.step_e(SoaRec{sg, j}, e, j);
-    } else if (TFB_FIRST_FAST && e[0] <= 1e100 && e[1] <= 1e100 && e[2] <= 1e100 &&
-               (e[0] >= sg[kSThr * kFS + j] || e[1] >= sg[kSThr * kFS + j] || e[2] >= sg[kSThr * kFS + j])) {
-      // (max e_k <= 1e100 && max e_k >= thr, the e_k of a covering pair being no NaN)
+    } else if (TFB_FIRST_FAST && first_fast(e, sg[kSThr * kFS + j])) {
       // One texel per triangle (steps = 1) and no float planes: the sole covering
       // record wins, and u in [0, 1], v in [0, u] give i = min(int(u), 0) = 0,
       // j = min(int(v), 0) = 0 (rasterizer.py:196-198), so the texel is 0 whatever
