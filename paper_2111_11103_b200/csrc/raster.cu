@@ -54,9 +54,10 @@ constexpr int kThreads = 256;              // setup-side kernels
 #ifndef TFB_FIRST_FAST
 #define TFB_FIRST_FAST 1
 #endif
-#ifndef TFB_PAIR_WIN
-#define TFB_PAIR_WIN 1  // k_raster pair phase in warp windows (0: per-thread contiguous pair runs)
+#ifndef TFB_RASTER_NT
+#define TFB_RASTER_NT 64  // k_raster threads per tile (= staged record capacity); kTP: one tier
 #endif
+constexpr int kRasterNT = TFB_RASTER_NT;
 #ifndef TFB_RASTER_MINB
 #define TFB_RASTER_MINB 9  // k_raster CTAs per SM the register budget must allow (56 regs, 36 warps)
 #endif
@@ -145,7 +146,10 @@ struct Work {
   uint32_t *fcnt;       // fcnt[1]: big-tile count
   uint32_t *tile_count; // per frame per tile
   uint32_t *list;
-  uint32_t *big;  // (frame, tile) codes handed to k_raster_big; count in fcnt[1]
+  uint32_t *big;  // (frame, tile) codes handed to k_raster_big (count in fcnt[1]) from the front, and
+                  // to the kTP-thread second tier (count *t2cnt) from the back
+  uint32_t *t2cnt;
+  int64_t bigcap;  // entries of big (nframes x ntiles: a tile is in at most one list)
   uint32_t *csurv;  // per frame: surviving cluster ids (count fcnt[4f]); ncl entries per frame
   int64_t ncl;
   int64_t rs;   // record slots per frame (2m)
@@ -169,7 +173,7 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
   size_t o_rec = take(sizeof(RecStore) * rs * nframes);
   size_t o_cand = take(sizeof(uint4) * (size_t)(rs / 2) * nframes);
   size_t o_vcode = take((size_t)(nv > 0 ? nv : 1) * nframes);
-  size_t o_fcnt = take(sizeof(uint32_t) * 4 * nframes);
+  size_t o_fcnt = take(sizeof(uint32_t) * 4 * (nframes + 1));
   size_t o_tc = take(sizeof(uint32_t) * ntiles * nframes);
   size_t o_list = take(sizeof(uint32_t) * (size_t)bincap * ntiles * nframes);
   size_t o_big = take(sizeof(uint32_t) * ntiles * nframes);
@@ -183,6 +187,8 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
   w.vcode = reinterpret_cast<uint8_t *>(b + o_vcode);
   w.nv = nv > 0 ? nv : 1;
   w.fcnt = reinterpret_cast<uint32_t *>(b + o_fcnt);
+  w.t2cnt = w.fcnt + 4 * (int64_t)nframes;
+  w.bigcap = (int64_t)ntiles * nframes;
   w.tile_count = reinterpret_cast<uint32_t *>(b + o_tc);
   w.list = reinterpret_cast<uint32_t *>(b + o_list);
   w.big = reinterpret_cast<uint32_t *>(b + o_big);
@@ -858,7 +864,6 @@ struct Outs {
 enum { kFXs = 0, kFYs = 3, kFZs = 6, kFDX = 9, kFDY = 12, kFA2 = 15, kFields = 16 };
 constexpr int kPC = 8;        // covering slots kept per pixel by the pair phase (more: selection by key)
 static_assert(kPC >= 4, "the fold's 4-input network reads four kept slots");
-constexpr int kFS = kTP + 1;  // field stride of the staged (SoA) tile records, +1 double: fields on distinct banks
 
 struct AosRec {  // one RecGeom (global memory or AoS shared memory)
   const RecGeom *g;
@@ -871,10 +876,11 @@ struct AosRec {  // one RecGeom (global memory or AoS shared memory)
 constexpr int kStaged = 11;
 constexpr int kSA2 = 9;   // staged slot of |area2|
 constexpr int kSThr = 10;  // staged slot of the sole-candidate threshold (first_win_threshold)
-struct SoaRec {
+template <int FS>
+struct SoaRecT {
   const double *base;
   int j;
-  __device__ __forceinline__ double at(int q) const { return base[q * kFS + j]; }
+  __device__ __forceinline__ double at(int q) const { return base[q * FS + j]; }
   __device__ __forceinline__ double f(int k) const {
     if (k < kFDX) return at(k);
     if (k == kFA2) return at(kSA2);
@@ -1118,19 +1124,23 @@ __device__ __forceinline__ void emit_pixel(const tfb_scene &sc, const Outs &o, i
   }
 }
 
+// Shared memory of one tile staged by a CTA of NT threads (at most NT records).
+template <int NT>
 struct TileSmem {
-  double g[kStaged * kFS];          // staged records, field-major (SoA): g[q * kFS + j]
-  double pe[3][kTP];                // edge values of a pixel's (single) covering pair
-  int32_t pc[kPC][kTP];             // per pixel: slots of its first kPC covering pairs (arrival order)
-  uint32_t flags[kTP];              // RecMeta::flags
-  int32_t off[kTP];                 // offsets[t] of the record's triangle (n_x < 2^31)
+  static constexpr int FS = NT + 1;  // field stride: the fields of lanes on different records on distinct banks
+  double g[kStaged * FS];            // staged records, field-major (SoA): g[q * FS + j]
+  double pe[3][kTP];                 // edge values of a pixel's (single) covering pair
+  uint8_t pc[kPC][kTP];              // per pixel: slots of its first kPC covering pairs (arrival order)
+  uint32_t flags[NT];                // RecMeta::flags
+  int32_t off[NT];                   // offsets[t] of the record's triangle (n_x < 2^31)
   Cam cam;
-  uint32_t key[kTP];
-  uint32_t box[kTP];                // tile-relative bbox: x0 | y0 << 8 | w << 16 | h << 24
-  uint32_t pre[kTP];                // exclusive prefix of bbox areas
+  uint32_t key[NT];
+  uint32_t box[NT];                  // tile-relative bbox: x0 | y0 << 8 | w << 16 | h << 24
+  uint32_t pre[NT];                  // exclusive prefix of bbox areas
   uint32_t pcnt[kTP];
-  uint32_t wtot[kTP / 32];
+  uint32_t wtot[NT / 32];
 };
+static_assert(kTP <= 256, "covering slots are stored as bytes");
 
 // One CTA of kTP threads per kTW x kTH tile with at most kTP records (the common case).
 //  1. The tile's records are staged in shared memory in list order (all
@@ -1146,34 +1156,42 @@ struct TileSmem {
 //     smallest covering key above the last folded one — the reference's
 //     ascending sequential fold (rasterizer.py:108, 170-171) without sorting.
 //  Larger or overflowed tiles are handed to k_raster_big.
-__global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, const double *__restrict__ cams, int W, int H,
-                                                        int TX, int ntiles, Work w, Outs o) {
-  const int f = blockIdx.z;
-  const int tile = blockIdx.y * TX + blockIdx.x;
-  const int tx0 = blockIdx.x * kTW, ty0 = blockIdx.y * kTH;
+template <int NT>
+__device__ __forceinline__ void raster_tile(const tfb_scene &sc, const double *__restrict__ cams, int W, int H, int TX,
+                                            int ntiles, const Work &w, const Outs &o, int f, int tx, int ty,
+                                            unsigned char *raster_smem) {
+  static_assert(NT % 32 == 0 && NT <= kTP && kTP % NT == 0, "whole warps, whole pixel passes");
+  constexpr int FS = TileSmem<NT>::FS;
+  using Rec = SoaRecT<FS>;
+  const int tile = ty * TX + tx;
+  const int tx0 = tx * kTW, ty0 = ty * kTH;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // the bin entry this thread would stage is read speculatively, in flight together
   // with the tile's count (entries past the count are stale and ignored)
   const uint32_t *src = w.list + ((int64_t)f * ntiles + tile) * w.bincap;
-  const uint32_t key_spec = tid < (int)min(w.bincap, (int64_t)kTP) ? src[tid] : 0u;
+  const uint32_t key_spec = tid < (int)min(w.bincap, (int64_t)NT) ? src[tid] : 0u;
   const uint32_t n = w.tile_count[(int64_t)f * ntiles + tile];
-  if (n > (uint64_t)w.bincap || n > (uint32_t)kTP) {
-    if (tid == 0) w.big[atomicAdd(w.fcnt + 1, 1u)] = (uint32_t)(f * ntiles + tile);
-    if (tid == 0) RSTAT(48);
+  if (n > (uint64_t)w.bincap || n > (uint32_t)NT) {
+    if (tid == 0) {
+      const uint32_t code = (uint32_t)(f * ntiles + tile);
+      if (NT < kTP && n <= (uint64_t)w.bincap && n <= (uint32_t)kTP) w.big[w.bigcap - 1 - atomicAdd(w.t2cnt, 1u)] = code;
+      else w.big[atomicAdd(w.fcnt + 1, 1u)] = code;
+      RSTAT(48);
+    }
     return;
   }
   if (tid == 0) RSTAT(min(n / 32u, 15u));
-  extern __shared__ __align__(16) unsigned char raster_smem[];
-  TileSmem &S = *reinterpret_cast<TileSmem *>(raster_smem);
+  TileSmem<NT> &S = *reinterpret_cast<TileSmem<NT> *>(raster_smem);
   double *sg = S.g;
   uint32_t *sflags = S.flags;
   int32_t *soff = S.off;
   uint32_t *skey = S.key, *sbox = S.box, *spre = S.pre, *pcnt = S.pcnt, *wtot = S.wtot;
-  int32_t(*pc)[kTP] = S.pc;
+  uint8_t(*pc)[kTP] = S.pc;
   double(*pe)[kTP] = S.pe;
   Cam &cam = S.cam;
   load_cam(cam, cams, f);
-  pcnt[tid] = 0u;
+#pragma unroll
+  for (int q = tid; q < kTP; q += NT) pcnt[q] = 0u;
   const RecStore *recs = w.rec + (int64_t)f * w.rs;
   uint32_t area = 0;
   if (tid < n) {
@@ -1192,9 +1210,9 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
     double dX[3], dY[3], a2;
     expand_derived(v + 2, v + 5, dX, dY, a2);
 #pragma unroll
-    for (int q = 0; q < 9; ++q) sg[q * kFS + tid] = v[2 + q];
-    sg[kSA2 * kFS + tid] = a2;
-    sg[kSThr * kFS + tid] = first_win_threshold(v + 8, a2, mt.flags);
+    for (int q = 0; q < 9; ++q) sg[q * FS + tid] = v[2 + q];
+    sg[kSA2 * FS + tid] = a2;
+    sg[kSThr * FS + tid] = first_win_threshold(v + 8, a2, mt.flags);
     skey[tid] = key;
     sflags[tid] = mt.flags;
     soff[tid] = mt.off;
@@ -1230,7 +1248,7 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
     __syncthreads();
     uint32_t wbase = 0;
 #pragma unroll
-    for (int i = 0; i < kTP / 32; ++i) {
+    for (int i = 0; i < NT / 32; ++i) {
       const uint32_t v = wtot[i];
       wbase += i < warp ? v : 0u;
       total += v;
@@ -1240,7 +1258,6 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
   }
 
   if (tid == 0) RSTAT(32 + min(total / 256u, 15u));
-#if TFB_PAIR_WIN
   // pair-parallel edge tests in warp windows: a window is 32 consecutive (record, pixel of
   // its bbox) pairs, lane l taking pair base + l, and each warp walks a contiguous range of
   // windows.  The records starting inside a window come from one shared-memory load per
@@ -1249,7 +1266,7 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
   // refills diverging across the warp).
   {
     const uint32_t nwin = (total + 31u) >> 5;
-    const uint32_t wper = (nwin + (kTP / 32) - 1) / (kTP / 32);
+    const uint32_t wper = (nwin + (NT / 32) - 1) / (NT / 32);
     const uint32_t wbeg = (uint32_t)warp * wper, wend = min(wbeg + wper, nwin);
     if (wbeg < wend) {
       const unsigned upto = (2u << lane) - 1u;
@@ -1284,7 +1301,7 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
           const int ly = (int)(((float)local + 0.5f) * rbw);
           const int lx = local - ly * bw;
           const int pxl = (int)(b & 0xffu) + lx, pyl = (int)((b >> 8) & 0xffu) + ly;
-          const SoaRec R{sg, j};
+          const Rec R{sg, j};
           const double x0 = R.at(kFXs), x1 = R.at(kFXs + 1), x2 = R.at(kFXs + 2);
           const double y0 = R.at(kFYs), y1 = R.at(kFYs + 1), y2 = R.at(kFYs + 2);
           const uint32_t fl = sflags[j];
@@ -1300,7 +1317,7 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
               (e2 > 0.0 || (e2 == 0.0 && (fl & 4u)))) {
             const int pix = pyl * kTW + pxl;
             const uint32_t idx = atomicAdd(pcnt + pix, 1u);
-            if (idx < (uint32_t)kPC) pc[idx][pix] = j;
+            if (idx < (uint32_t)kPC) pc[idx][pix] = (uint8_t)j;
             if (idx == 0u) {  // used only when this is the pixel's sole candidate
               pe[0][pix] = e0;
               pe[1][pix] = e1;
@@ -1312,93 +1329,24 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
     }
   }
   __syncthreads();
-#else
-  // pair-parallel edge tests: thread handles pairs [p0, p1)
-  const uint32_t ppt = (total + kTP - 1) / kTP;
-  const uint32_t p0 = tid * ppt, p1 = min(p0 + ppt, total);
-  if (p0 < p1) {
-    int lo = 0, hi = (int)n - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (spre[mid] <= p0) lo = mid;
-      else hi = mid - 1;
-    }
-    int j = lo;
-    uint32_t b = sbox[j];
-    int bw = (b >> 16) & 0xff, bh = b >> 24;
-    const int local = (int)(p0 - spre[j]);
-    int ly = local / bw, lx = local - ly * bw;
-    // the record's edge coefficients stay in registers while its pairs are walked, and
-    // the row terms dX[k] * (py - ys[a]) of edges_at are formed once per bbox row
-    double dX0, dX1, dX2, dY0, dY1, dY2, xa0, xa1, xa2, A0, A1, A2;
-    uint32_t fl;
-    auto load_rec = [&]() {
-      const SoaRec R{sg, j};
-      dX0 = R.f(kFDX); dX1 = R.f(kFDX + 1); dX2 = R.f(kFDX + 2);
-      dY0 = R.f(kFDY); dY1 = R.f(kFDY + 1); dY2 = R.f(kFDY + 2);
-      xa0 = R.f(kFXs + 1); xa1 = R.f(kFXs + 2); xa2 = R.f(kFXs);
-      fl = sflags[j];
-    };
-    auto load_row = [&]() {
-      const SoaRec R{sg, j};
-      const double py = (double)(ty0 + (int)((b >> 8) & 0xffu) + ly) + 0.5;
-      A0 = __dmul_rn(dX0, __dsub_rn(py, R.f(kFYs + 1)));
-      A1 = __dmul_rn(dX1, __dsub_rn(py, R.f(kFYs + 2)));
-      A2 = __dmul_rn(dX2, __dsub_rn(py, R.f(kFYs)));
-    };
-    load_rec();
-    load_row();
-    for (uint32_t p = p0; p < p1; ++p) {
-      const int pxl = (int)(b & 0xffu) + lx, pyl = (int)((b >> 8) & 0xffu) + ly;
-      const double px = (double)(tx0 + pxl) + 0.5;
-      const double e0 = __dsub_rn(A0, __dmul_rn(dY0, __dsub_rn(px, xa0)));  // rasterizer.py:161-162
-      const double e1 = __dsub_rn(A1, __dmul_rn(dY1, __dsub_rn(px, xa1)));
-      const double e2 = __dsub_rn(A2, __dmul_rn(dY2, __dsub_rn(px, xa2)));
-      if ((e0 > 0.0 || (e0 == 0.0 && (fl & 1u))) && (e1 > 0.0 || (e1 == 0.0 && (fl & 2u))) &&
-          (e2 > 0.0 || (e2 == 0.0 && (fl & 4u)))) {
-        const int pix = pyl * kTW + pxl;
-        const uint32_t idx = atomicAdd(pcnt + pix, 1u);
-        if (idx < (uint32_t)kPC) pc[idx][pix] = j;
-        if (idx == 0u) {  // used only when this is the pixel's sole candidate
-          pe[0][pix] = e0;
-          pe[1][pix] = e1;
-          pe[2][pix] = e2;
-        }
-      }
-      if (++lx == bw) {
-        lx = 0;
-        if (++ly == bh) {
-          ly = 0;
-          ++j;
-          if (j < (int)n && p + 1 < p1) {
-            b = sbox[j];
-            bw = (b >> 16) & 0xff;
-            bh = b >> 24;
-            load_rec();
-          }
-        }
-        if (p + 1 < p1) load_row();
-      }
-    }
-  }
-  __syncthreads();
-#endif
 
-  // one thread per pixel: fold its covering records in ascending key order
-  const int pxl = tid & (kTW - 1), pyl = tid / kTW;
+  // one thread per pixel (NT < kTP: kTP / NT pixels per thread): fold its covering
+  // records in ascending key order
+  auto fold_pixel = [&](const int pt) {
+  const int pxl = pt & (kTW - 1), pyl = pt / kTW;
   const int px_i = tx0 + pxl, py_i = ty0 + pyl;
   if (px_i >= W || py_i >= H) return;
   const double px = (double)px_i + 0.5, py = (double)py_i + 0.5;
-  const uint32_t cnt = pcnt[tid];
+  const uint32_t cnt = pcnt[pt];
   RSTAT(16 + min(cnt, 15u));
   Fold fd;
   fd.init();
   if (cnt == 1u) {
-    const int j = pc[0][tid];
-    const double e[3] = {pe[0][tid], pe[1][tid], pe[2][tid]};
+    const int j = pc[0][pt];
+    const double e[3] = {pe[0][pt], pe[1][pt], pe[2][pt]};
     if (o.depth) {
-      fd.step_e(SoaRec{sg, j}, e, j);
-    } else if (TFB_FIRST_FAST && first_fast(e, sg[kSThr * kFS + j])) {
+      fd.step_e(Rec{sg, j}, e, j);
+    } else if (TFB_FIRST_FAST && first_fast(e, sg[kSThr * FS + j])) {
       // One texel per triangle (steps = 1) and no float planes: the sole covering
       // record wins, and u in [0, 1], v in [0, u] give i = min(int(u), 0) = 0,
       // j = min(int(v), 0) = 0 (rasterizer.py:196-198), so the texel is 0 whatever
@@ -1407,19 +1355,19 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
       emit_pixel(sc, o, f, (int64_t)f * W * H + (int64_t)(py_i * W + px_i), (int32_t)(skey[j] >> 1), 0, soff[j]);
       return;
     } else {
-      fd.first_e(SoaRec{sg, j}, e, j);
+      fd.first_e(Rec{sg, j}, e, j);
     }
   } else if (cnt == 2u) {  // both slots known: fold in ascending key order
-    int j0 = pc[0][tid], j1 = pc[1][tid];
+    int j0 = pc[0][pt], j1 = pc[1][pt];
     if (skey[j1] < skey[j0]) {
       const int tmp = j0;
       j0 = j1;
       j1 = tmp;
     }
-    fd.step(SoaRec{sg, j0}, sflags[j0], px, py, j0);
-    fd.step(SoaRec{sg, j1}, sflags[j1], px, py, j1);
+    fd.step(Rec{sg, j0}, sflags[j0], px, py, j0);
+    fd.step(Rec{sg, j1}, sflags[j1], px, py, j1);
   } else if (cnt > 2u && cnt <= 4u) {  // 3 or 4 slots known: sort by key (a 4-input network) and fold
-    int j0 = pc[0][tid], j1 = pc[1][tid], j2 = pc[2][tid], j3 = cnt > 3u ? pc[3][tid] : 0;
+    int j0 = pc[0][pt], j1 = pc[1][pt], j2 = pc[2][pt], j3 = cnt > 3u ? pc[3][pt] : 0;
     uint32_t k0 = skey[j0], k1 = skey[j1], k2 = skey[j2], k3 = cnt > 3u ? skey[j3] : 0xffffffffu;
     auto cx = [](uint32_t &ka, int &ja, uint32_t &kb, int &jb) {
       if (kb < ka) {
@@ -1436,24 +1384,24 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
     cx(k0, j0, k2, j2);
     cx(k1, j1, k3, j3);
     cx(k1, j1, k2, j2);
-    fd.step(SoaRec{sg, j0}, sflags[j0], px, py, j0);
-    fd.step(SoaRec{sg, j1}, sflags[j1], px, py, j1);
-    fd.step(SoaRec{sg, j2}, sflags[j2], px, py, j2);
-    if (cnt > 3u) fd.step(SoaRec{sg, j3}, sflags[j3], px, py, j3);
+    fd.step(Rec{sg, j0}, sflags[j0], px, py, j0);
+    fd.step(Rec{sg, j1}, sflags[j1], px, py, j1);
+    fd.step(Rec{sg, j2}, sflags[j2], px, py, j2);
+    if (cnt > 3u) fd.step(Rec{sg, j3}, sflags[j3], px, py, j3);
   } else if (cnt > 4u && cnt <= (uint32_t)kPC) {  // 5..8 slots known: ascending selection among them
     int64_t last = -1;
     for (uint32_t k = 0; k < cnt; ++k) {
       uint32_t bk = 0xffffffffu;
       int bj = 0;
       for (uint32_t i = 0; i < cnt; ++i) {
-        const int ji = pc[i][tid];
+        const int ji = pc[i][pt];
         const uint32_t ki = skey[ji];
         if ((int64_t)ki > last && ki < bk) {
           bk = ki;
           bj = ji;
         }
       }
-      fd.step(SoaRec{sg, bj}, sflags[bj], px, py, bj);
+      fd.step(Rec{sg, bj}, sflags[bj], px, py, bj);
       last = bk;
     }
   } else if (cnt > (uint32_t)kPC) {  // deeper stacks: repeated smallest-key selection over the tile's records
@@ -1469,10 +1417,10 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
         const unsigned long long cand = ((unsigned long long)key << 32) | i;
         if (cand >= best) continue;
         double e[3];
-        if (edges_at(SoaRec{sg, (int)i}, sflags[i], px, py, e)) best = cand;
+        if (edges_at(Rec{sg, (int)i}, sflags[i], px, py, e)) best = cand;
       }
       const int j = (int)(best & 0xffffffffu);
-      fd.step(SoaRec{sg, j}, sflags[j], px, py, j);
+      fd.step(Rec{sg, j}, sflags[j], px, py, j);
       last = (int64_t)(best >> 32);
     }
   }
@@ -1480,6 +1428,40 @@ __global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster(tfb_scene sc, c
   const int32_t t = fd.win >= 0 ? (int32_t)(skey[fd.win] >> 1) : -1;
   const int64_t off = fd.win >= 0 ? soff[fd.win] : 0;
   write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, off);
+  };
+  if constexpr (NT == kTP) {
+    fold_pixel(tid);
+  } else {
+#pragma unroll 1
+    for (int pt = tid; pt < kTP; pt += NT) fold_pixel(pt);
+  }
+}
+
+// One CTA of NT threads per tile.  With NT < kTP (the default 64 for 16 x 8 tiles) a
+// tile's staging (one record per thread) holds NT records and its shared memory is about
+// half the kTP-record layout, so twice the tiles are in flight per SM with the same warp
+// count: the latency chain of a tile (bin entry -> records -> staging barrier) is hidden by
+// more independent tiles.  Tiles with NT < n <= kTP records go to k_raster_t2, larger or
+// overflowed ones to k_raster_big.
+template <int NT>
+__global__ void __launch_bounds__(NT, TFB_RASTER_MINB * kTP / NT) k_raster(tfb_scene sc, const double *__restrict__ cams,
+                                                                          int W, int H, int TX, int ntiles, Work w, Outs o) {
+  extern __shared__ __align__(16) unsigned char raster_smem[];
+  raster_tile<NT>(sc, cams, W, H, TX, ntiles, w, o, blockIdx.z, blockIdx.x, blockIdx.y, raster_smem);
+}
+
+// The second tier: the tiles k_raster<NT < kTP> passed on (NT < n <= kTP records), kTP
+// threads each, a persistent grid walking the list.
+__global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster_t2(tfb_scene sc, const double *__restrict__ cams, int W,
+                                                                    int H, int TX, int ntiles, Work w, Outs o) {
+  extern __shared__ __align__(16) unsigned char raster_smem[];
+  const uint32_t cnt = *w.t2cnt;
+  for (uint32_t i = blockIdx.x; i < cnt; i += gridDim.x) {
+    __syncthreads();  // the previous tile's fold is done with the shared memory
+    const uint32_t code = w.big[w.bigcap - 1 - i];
+    const int f = (int)(code / (uint32_t)ntiles), tile = (int)(code % (uint32_t)ntiles);
+    raster_tile<kTP>(sc, cams, W, H, TX, ntiles, w, o, f, tile % TX, tile / TX, raster_smem);
+  }
 }
 
 // Tiles with more than kTP records, or whose bin overflowed (then every
@@ -1634,7 +1616,7 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
     set_error("tfb_rasterize: workspace of %zu bytes is smaller than the %zu required", workspace_bytes, need);
     return TFB_ERR_CAPACITY;
   }
-  cudaMemsetAsync(w.fcnt, 0, sizeof(uint32_t) * 4 * nframes, st);
+  cudaMemsetAsync(w.fcnt, 0, sizeof(uint32_t) * 4 * (nframes + 1), st);
   cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ntiles * nframes, st);
   tfb_scene sc = *scene;
   const bool clustered = sc.num_clusters > 0 && sc.clusters;
@@ -1672,16 +1654,23 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
     std::lock_guard<std::mutex> guard(mu);
     if (dev >= 0 && dev < 64) {
       if (!smem_set[dev]) {
-        cudaFuncSetAttribute(k_raster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem));
+        cudaFuncSetAttribute(k_raster<kRasterNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(TileSmem<kRasterNT>));
+        cudaFuncSetAttribute(k_raster_t2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem<kTP>));
         cudaDeviceGetAttribute(&num_sms[dev], cudaDevAttrMultiProcessorCount, dev);
         smem_set[dev] = true;
       }
       sms = num_sms[dev];
     } else {
-      cudaFuncSetAttribute(k_raster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem));
+      cudaFuncSetAttribute(k_raster<kRasterNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(TileSmem<kRasterNT>));
+      cudaFuncSetAttribute(k_raster_t2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem<kTP>));
     }
   }
-  k_raster<<<dim3(TX, TY, nframes), kTP, sizeof(TileSmem), st>>>(sc, cams, width, height, TX, ntiles, w, o);
+  k_raster<kRasterNT><<<dim3(TX, TY, nframes), kRasterNT, sizeof(TileSmem<kRasterNT>), st>>>(sc, cams, width, height,
+                                                                                            TX, ntiles, w, o);
+  if (kRasterNT < kTP)
+    k_raster_t2<<<sms * TFB_RASTER_MINB, kTP, sizeof(TileSmem<kTP>), st>>>(sc, cams, width, height, TX, ntiles, w, o);
   k_raster_big<<<sms * (256 / kTP), kTP, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
   return check_launch("tfb_rasterize");
 }
