@@ -58,6 +58,12 @@ constexpr int kThreads = 256;              // setup-side kernels
 #define TFB_RASTER_NT 64  // k_raster threads per tile (= staged record capacity); kTP: one tier
 #endif
 constexpr int kRasterNT = TFB_RASTER_NT;
+#ifndef TFB_KEEP_PE
+#define TFB_KEEP_PE 0  // 1: keep a sole covering pair's edge values in shared memory (else recomputed)
+#endif
+#ifndef TFB_RASTER_MINB1
+#define TFB_RASTER_MINB1 20  // k_raster<64> CTAs per SM the register budget must allow (48 registers)
+#endif
 #ifndef TFB_RASTER_MINB
 #define TFB_RASTER_MINB 9  // k_raster CTAs per SM the register budget must allow (56 regs, 36 warps)
 #endif
@@ -1129,7 +1135,9 @@ template <int NT>
 struct TileSmem {
   static constexpr int FS = NT + 1;  // field stride: the fields of lanes on different records on distinct banks
   double g[kStaged * FS];            // staged records, field-major (SoA): g[q * FS + j]
+#if TFB_KEEP_PE
   double pe[3][kTP];                 // edge values of a pixel's (single) covering pair
+#endif
   uint8_t pc[kPC][kTP];              // per pixel: slots of its first kPC covering pairs (arrival order)
   uint32_t flags[NT];                // RecMeta::flags
   int32_t off[NT];                   // offsets[t] of the record's triangle (n_x < 2^31)
@@ -1187,7 +1195,9 @@ __device__ __forceinline__ void raster_tile(const tfb_scene &sc, const double *_
   int32_t *soff = S.off;
   uint32_t *skey = S.key, *sbox = S.box, *spre = S.pre, *pcnt = S.pcnt, *wtot = S.wtot;
   uint8_t(*pc)[kTP] = S.pc;
+#if TFB_KEEP_PE
   double(*pe)[kTP] = S.pe;
+#endif
   Cam &cam = S.cam;
   load_cam(cam, cams, f);
 #pragma unroll
@@ -1317,12 +1327,23 @@ __device__ __forceinline__ void raster_tile(const tfb_scene &sc, const double *_
               (e2 > 0.0 || (e2 == 0.0 && (fl & 4u)))) {
             const int pix = pyl * kTW + pxl;
             const uint32_t idx = atomicAdd(pcnt + pix, 1u);
+#if TFB_KEEP_PE
             if (idx < (uint32_t)kPC) pc[idx][pix] = (uint8_t)j;
             if (idx == 0u) {  // used only when this is the pixel's sole candidate
               pe[0][pix] = e0;
               pe[1][pix] = e1;
               pe[2][pix] = e2;
             }
+#else
+            // the first covering pair also records whether, should it stay the pixel's
+            // only one, it wins without divisions (bit 7; record slots are < 128)
+            uint32_t v = (uint32_t)j;
+            if (idx == 0u && TFB_FIRST_FAST && !o.depth) {
+              const double e[3] = {e0, e1, e2};
+              if (first_fast(e, sg[kSThr * FS + j])) v |= 0x80u;
+            }
+            if (idx < (uint32_t)kPC) pc[idx][pix] = (uint8_t)v;
+#endif
           }
         }
       }
@@ -1333,6 +1354,7 @@ __device__ __forceinline__ void raster_tile(const tfb_scene &sc, const double *_
   // one thread per pixel (NT < kTP: kTP / NT pixels per thread): fold its covering
   // records in ascending key order
   auto fold_pixel = [&](const int pt) {
+#define PCJ(i) ((int)(pc[(i)][pt] & 0x7f))
   const int pxl = pt & (kTW - 1), pyl = pt / kTW;
   const int px_i = tx0 + pxl, py_i = ty0 + pyl;
   if (px_i >= W || py_i >= H) return;
@@ -1342,11 +1364,19 @@ __device__ __forceinline__ void raster_tile(const tfb_scene &sc, const double *_
   Fold fd;
   fd.init();
   if (cnt == 1u) {
+#if TFB_KEEP_PE
     const int j = pc[0][pt];
     const double e[3] = {pe[0][pt], pe[1][pt], pe[2][pt]};
+    const bool fast = TFB_FIRST_FAST && !o.depth && first_fast(e, sg[kSThr * FS + j]);
+#else
+    const int j = pc[0][pt] & 0x7f;
+    const bool fast = (pc[0][pt] & 0x80) != 0;
+    double e[3];
+    if (!fast) edges_at(Rec{sg, j}, sflags[j], px, py, e);  // the pair phase's values, bit for bit
+#endif
     if (o.depth) {
       fd.step_e(Rec{sg, j}, e, j);
-    } else if (TFB_FIRST_FAST && first_fast(e, sg[kSThr * FS + j])) {
+    } else if (fast) {
       // One texel per triangle (steps = 1) and no float planes: the sole covering
       // record wins, and u in [0, 1], v in [0, u] give i = min(int(u), 0) = 0,
       // j = min(int(v), 0) = 0 (rasterizer.py:196-198), so the texel is 0 whatever
@@ -1358,7 +1388,7 @@ __device__ __forceinline__ void raster_tile(const tfb_scene &sc, const double *_
       fd.first_e(Rec{sg, j}, e, j);
     }
   } else if (cnt == 2u) {  // both slots known: fold in ascending key order
-    int j0 = pc[0][pt], j1 = pc[1][pt];
+    int j0 = PCJ(0), j1 = PCJ(1);
     if (skey[j1] < skey[j0]) {
       const int tmp = j0;
       j0 = j1;
@@ -1367,7 +1397,7 @@ __device__ __forceinline__ void raster_tile(const tfb_scene &sc, const double *_
     fd.step(Rec{sg, j0}, sflags[j0], px, py, j0);
     fd.step(Rec{sg, j1}, sflags[j1], px, py, j1);
   } else if (cnt > 2u && cnt <= 4u) {  // 3 or 4 slots known: sort by key (a 4-input network) and fold
-    int j0 = pc[0][pt], j1 = pc[1][pt], j2 = pc[2][pt], j3 = cnt > 3u ? pc[3][pt] : 0;
+    int j0 = PCJ(0), j1 = PCJ(1), j2 = PCJ(2), j3 = cnt > 3u ? PCJ(3) : 0;
     uint32_t k0 = skey[j0], k1 = skey[j1], k2 = skey[j2], k3 = cnt > 3u ? skey[j3] : 0xffffffffu;
     auto cx = [](uint32_t &ka, int &ja, uint32_t &kb, int &jb) {
       if (kb < ka) {
@@ -1394,7 +1424,7 @@ __device__ __forceinline__ void raster_tile(const tfb_scene &sc, const double *_
       uint32_t bk = 0xffffffffu;
       int bj = 0;
       for (uint32_t i = 0; i < cnt; ++i) {
-        const int ji = pc[i][pt];
+        const int ji = PCJ(i);
         const uint32_t ki = skey[ji];
         if ((int64_t)ki > last && ki < bk) {
           bk = ki;
@@ -1428,6 +1458,7 @@ __device__ __forceinline__ void raster_tile(const tfb_scene &sc, const double *_
   const int32_t t = fd.win >= 0 ? (int32_t)(skey[fd.win] >> 1) : -1;
   const int64_t off = fd.win >= 0 ? soff[fd.win] : 0;
   write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, off);
+#undef PCJ
   };
   if constexpr (NT == kTP) {
     fold_pixel(tid);
@@ -1444,7 +1475,7 @@ __device__ __forceinline__ void raster_tile(const tfb_scene &sc, const double *_
 // more independent tiles.  Tiles with NT < n <= kTP records go to k_raster_t2, larger or
 // overflowed ones to k_raster_big.
 template <int NT>
-__global__ void __launch_bounds__(NT, TFB_RASTER_MINB * kTP / NT) k_raster(tfb_scene sc, const double *__restrict__ cams,
+__global__ void __launch_bounds__(NT, NT < kTP ? TFB_RASTER_MINB1 : TFB_RASTER_MINB) k_raster(tfb_scene sc, const double *__restrict__ cams,
                                                                           int W, int H, int TX, int ntiles, Work w, Outs o) {
   extern __shared__ __align__(16) unsigned char raster_smem[];
   raster_tile<NT>(sc, cams, W, H, TX, ntiles, w, o, blockIdx.z, blockIdx.x, blockIdx.y, raster_smem);
