@@ -541,7 +541,10 @@ __global__ void __launch_bounds__(kThreads) k_ccull(tfb_scene sc, const double *
 // time and stride over the frame's survivors.
 constexpr int kCV = 128;  // vertex slots per cluster (tfb_cluster::verts)
 
-__global__ void __launch_bounds__(kThreads) k_ccands(tfb_scene sc, const double *__restrict__ cams, int W, int H,
+#ifndef TFB_CCANDS_MINB
+#define TFB_CCANDS_MINB 8  // 32 registers: 8 blocks (64 warps) per SM hide the cluster -> vertex -> append chain
+#endif
+__global__ void __launch_bounds__(kThreads, TFB_CCANDS_MINB) k_ccands(tfb_scene sc, const double *__restrict__ cams, int W, int H,
                                                      Work w) {
   const int f = blockIdx.y;
   constexpr int kPer = kThreads / kCluster;
