@@ -58,6 +58,9 @@ constexpr int kThreads = 256;              // setup-side kernels
 #define TFB_RASTER_NT 64  // k_raster threads per tile (= staged record capacity); kTP: one tier
 #endif
 constexpr int kRasterNT = TFB_RASTER_NT;
+#ifndef TFB_FAST_LO
+#define TFB_FAST_LO 0  // 1: test max e_k <= 1e100 per pixel instead of bounding the record's coordinates
+#endif
 #ifndef TFB_KEEP_PE
 #define TFB_KEEP_PE 0  // 1: keep a sole covering pair's edge values in shared memory (else recomputed)
 #endif
@@ -1001,19 +1004,29 @@ __device__ __forceinline__ bool first_wins_without_divisions(const R &g, const d
 // record, formed when the record is staged: a2 * max z_k * 1e-50 when steps = 1 and the
 // z_k and a2 ranges hold, else NaN (every comparison against it fails).  A covering
 // pixel's sole record then wins without divisions iff max e_k <= 1e100 && max e_k >= thr.
-__device__ __forceinline__ double first_win_threshold(const double zs[3], double a2, uint32_t flags) {
+//
+// With TFB_FAST_LO = 0 the record also requires |x|, |y| <= 1e40 for its projected
+// vertices: every edge value at a pixel centre (|px|, |py| < 2^15) is then a difference of
+// two products below 2e40 * (1e40 + 2^15), far under 1e100 even after rounding, so the
+// max e_k <= 1e100 half of the test holds by construction and is not evaluated per pixel.
+__device__ __forceinline__ double first_win_threshold(const double xs[3], const double ys[3], const double zs[3],
+                                                      double a2, uint32_t flags) {
   const double z0 = zs[0], z1 = zs[1], z2 = zs[2];
   const bool zok = z0 >= 1e-100 && z0 <= 1e100 && z1 >= 1e-100 && z1 <= 1e100 && z2 >= 1e-100 && z2 <= 1e100;
   const double zmax = fmax(fmax(z0, z1), z2);
-  const bool ok = (flags >> 16) == 1u && zok && a2 >= 1e-100 && a2 <= 1e100;
+  bool ok = (flags >> 16) == 1u && zok && a2 >= 1e-100 && a2 <= 1e100;
+  if (!TFB_FAST_LO)
+    ok = ok && fabs(xs[0]) <= 1e40 && fabs(xs[1]) <= 1e40 && fabs(xs[2]) <= 1e40 && fabs(ys[0]) <= 1e40 &&
+         fabs(ys[1]) <= 1e40 && fabs(ys[2]) <= 1e40;
   return ok ? __dmul_rn(__dmul_rn(a2, zmax), 1e-50) : __longlong_as_double(0x7ff8000000000000LL);
 }
 
 // max e_k <= 1e100 && max e_k >= thr for the (non-NaN) edge values of a covering pair,
-// evaluated without branches
+// evaluated without branches (the first half only with TFB_FAST_LO, see above)
 __device__ __forceinline__ bool first_fast(const double e[3], double thr) {
-  const bool lo = (e[0] <= 1e100) & (e[1] <= 1e100) & (e[2] <= 1e100);
   const bool hi = (e[0] >= thr) | (e[1] >= thr) | (e[2] >= thr);
+  if (!TFB_FAST_LO) return hi;
+  const bool lo = (e[0] <= 1e100) & (e[1] <= 1e100) & (e[2] <= 1e100);
   return lo & hi;
 }
 
@@ -1225,7 +1238,7 @@ __device__ __forceinline__ void raster_tile(const tfb_scene &sc, const double *_
 #pragma unroll
     for (int q = 0; q < 9; ++q) sg[q * FS + tid] = v[2 + q];
     sg[kSA2 * FS + tid] = a2;
-    sg[kSThr * FS + tid] = first_win_threshold(v + 8, a2, mt.flags);
+    sg[kSThr * FS + tid] = first_win_threshold(v + 2, v + 5, v + 8, a2, mt.flags);
     skey[tid] = key;
     sflags[tid] = mt.flags;
     soff[tid] = mt.off;
