@@ -1371,109 +1371,109 @@ __device__ __forceinline__ void raster_tile(const tfb_scene &sc, const double *_
   // records in ascending key order
   auto fold_pixel = [&](const int pt) {
 #define PCJ(i) ((int)(pc[(i)][pt] & 0x7f))
-  const int pxl = pt & (kTW - 1), pyl = pt / kTW;
-  const int px_i = tx0 + pxl, py_i = ty0 + pyl;
-  if (px_i >= W || py_i >= H) return;
-  const double px = (double)px_i + 0.5, py = (double)py_i + 0.5;
-  const uint32_t cnt = pcnt[pt];
-  RSTAT(16 + min(cnt, 15u));
-  Fold fd;
-  fd.init();
-  if (cnt == 1u) {
+    const int pxl = pt & (kTW - 1), pyl = pt / kTW;
+    const int px_i = tx0 + pxl, py_i = ty0 + pyl;
+    if (px_i >= W || py_i >= H) return;
+    const double px = (double)px_i + 0.5, py = (double)py_i + 0.5;
+    const uint32_t cnt = pcnt[pt];
+    RSTAT(16 + min(cnt, 15u));
+    Fold fd;
+    fd.init();
+    if (cnt == 1u) {
 #if TFB_KEEP_PE
-    const int j = pc[0][pt];
-    const double e[3] = {pe[0][pt], pe[1][pt], pe[2][pt]};
-    const bool fast = TFB_FIRST_FAST && !o.depth && first_fast(e, sg[kSThr * FS + j]);
+      const int j = pc[0][pt];
+      const double e[3] = {pe[0][pt], pe[1][pt], pe[2][pt]};
+      const bool fast = TFB_FIRST_FAST && !o.depth && first_fast(e, sg[kSThr * FS + j]);
 #else
-    const int j = pc[0][pt] & 0x7f;
-    const bool fast = (pc[0][pt] & 0x80) != 0;
-    double e[3];
-    if (!fast) edges_at(Rec{sg, j}, sflags[j], px, py, e);  // the pair phase's values, bit for bit
+      const int j = pc[0][pt] & 0x7f;
+      const bool fast = (pc[0][pt] & 0x80) != 0;
+      double e[3];
+      if (!fast) edges_at(Rec{sg, j}, sflags[j], px, py, e);  // the pair phase's values, bit for bit
 #endif
-    if (o.depth) {
-      fd.step_e(Rec{sg, j}, e, j);
-    } else if (fast) {
-      // One texel per triangle (steps = 1) and no float planes: the sole covering
-      // record wins, and u in [0, 1], v in [0, u] give i = min(int(u), 0) = 0,
-      // j = min(int(v), 0) = 0 (rasterizer.py:196-198), so the texel is 0 whatever
-      // the barycentrics are.  They are finite for a winner: w_k >= 0 with
-      // 0 < wsum < inf, and the b rows sum to about wsum / wsum, so b.sum() > 0.
-      emit_pixel(sc, o, f, (int64_t)f * W * H + (int64_t)(py_i * W + px_i), (int32_t)(skey[j] >> 1), 0, soff[j]);
-      return;
-    } else {
-      fd.first_e(Rec{sg, j}, e, j);
-    }
-  } else if (cnt == 2u) {  // both slots known: fold in ascending key order
-    int j0 = PCJ(0), j1 = PCJ(1);
-    if (skey[j1] < skey[j0]) {
-      const int tmp = j0;
-      j0 = j1;
-      j1 = tmp;
-    }
-    fd.step(Rec{sg, j0}, sflags[j0], px, py, j0);
-    fd.step(Rec{sg, j1}, sflags[j1], px, py, j1);
-  } else if (cnt > 2u && cnt <= 4u) {  // 3 or 4 slots known: sort by key (a 4-input network) and fold
-    int j0 = PCJ(0), j1 = PCJ(1), j2 = PCJ(2), j3 = cnt > 3u ? PCJ(3) : 0;
-    uint32_t k0 = skey[j0], k1 = skey[j1], k2 = skey[j2], k3 = cnt > 3u ? skey[j3] : 0xffffffffu;
-    auto cx = [](uint32_t &ka, int &ja, uint32_t &kb, int &jb) {
-      if (kb < ka) {
-        const uint32_t tk = ka;
-        ka = kb;
-        kb = tk;
-        const int tj = ja;
-        ja = jb;
-        jb = tj;
+      if (o.depth) {
+        fd.step_e(Rec{sg, j}, e, j);
+      } else if (fast) {
+        // One texel per triangle (steps = 1) and no float planes: the sole covering
+        // record wins, and u in [0, 1], v in [0, u] give i = min(int(u), 0) = 0,
+        // j = min(int(v), 0) = 0 (rasterizer.py:196-198), so the texel is 0 whatever
+        // the barycentrics are.  They are finite for a winner: w_k >= 0 with
+        // 0 < wsum < inf, and the b rows sum to about wsum / wsum, so b.sum() > 0.
+        emit_pixel(sc, o, f, (int64_t)f * W * H + (int64_t)(py_i * W + px_i), (int32_t)(skey[j] >> 1), 0, soff[j]);
+        return;
+      } else {
+        fd.first_e(Rec{sg, j}, e, j);
       }
-    };
-    cx(k0, j0, k1, j1);
-    cx(k2, j2, k3, j3);
-    cx(k0, j0, k2, j2);
-    cx(k1, j1, k3, j3);
-    cx(k1, j1, k2, j2);
-    fd.step(Rec{sg, j0}, sflags[j0], px, py, j0);
-    fd.step(Rec{sg, j1}, sflags[j1], px, py, j1);
-    fd.step(Rec{sg, j2}, sflags[j2], px, py, j2);
-    if (cnt > 3u) fd.step(Rec{sg, j3}, sflags[j3], px, py, j3);
-  } else if (cnt > 4u && cnt <= (uint32_t)kPC) {  // 5..8 slots known: ascending selection among them
-    int64_t last = -1;
-    for (uint32_t k = 0; k < cnt; ++k) {
-      uint32_t bk = 0xffffffffu;
-      int bj = 0;
-      for (uint32_t i = 0; i < cnt; ++i) {
-        const int ji = PCJ(i);
-        const uint32_t ki = skey[ji];
-        if ((int64_t)ki > last && ki < bk) {
-          bk = ki;
-          bj = ji;
+    } else if (cnt == 2u) {  // both slots known: fold in ascending key order
+      int j0 = PCJ(0), j1 = PCJ(1);
+      if (skey[j1] < skey[j0]) {
+        const int tmp = j0;
+        j0 = j1;
+        j1 = tmp;
+      }
+      fd.step(Rec{sg, j0}, sflags[j0], px, py, j0);
+      fd.step(Rec{sg, j1}, sflags[j1], px, py, j1);
+    } else if (cnt > 2u && cnt <= 4u) {  // 3 or 4 slots known: sort by key (a 4-input network) and fold
+      int j0 = PCJ(0), j1 = PCJ(1), j2 = PCJ(2), j3 = cnt > 3u ? PCJ(3) : 0;
+      uint32_t k0 = skey[j0], k1 = skey[j1], k2 = skey[j2], k3 = cnt > 3u ? skey[j3] : 0xffffffffu;
+      auto cx = [](uint32_t &ka, int &ja, uint32_t &kb, int &jb) {
+        if (kb < ka) {
+          const uint32_t tk = ka;
+          ka = kb;
+          kb = tk;
+          const int tj = ja;
+          ja = jb;
+          jb = tj;
         }
+      };
+      cx(k0, j0, k1, j1);
+      cx(k2, j2, k3, j3);
+      cx(k0, j0, k2, j2);
+      cx(k1, j1, k3, j3);
+      cx(k1, j1, k2, j2);
+      fd.step(Rec{sg, j0}, sflags[j0], px, py, j0);
+      fd.step(Rec{sg, j1}, sflags[j1], px, py, j1);
+      fd.step(Rec{sg, j2}, sflags[j2], px, py, j2);
+      if (cnt > 3u) fd.step(Rec{sg, j3}, sflags[j3], px, py, j3);
+    } else if (cnt > 4u && cnt <= (uint32_t)kPC) {  // 5..8 slots known: ascending selection among them
+      int64_t last = -1;
+      for (uint32_t k = 0; k < cnt; ++k) {
+        uint32_t bk = 0xffffffffu;
+        int bj = 0;
+        for (uint32_t i = 0; i < cnt; ++i) {
+          const int ji = PCJ(i);
+          const uint32_t ki = skey[ji];
+          if ((int64_t)ki > last && ki < bk) {
+            bk = ki;
+            bj = ji;
+          }
+        }
+        fd.step(Rec{sg, bj}, sflags[bj], px, py, bj);
+        last = bk;
       }
-      fd.step(Rec{sg, bj}, sflags[bj], px, py, bj);
-      last = bk;
-    }
-  } else if (cnt > (uint32_t)kPC) {  // deeper stacks: repeated smallest-key selection over the tile's records
-    int64_t last = -1;  // key of the last folded record
-    for (uint32_t k = 0; k < cnt; ++k) {
-      unsigned long long best = ~0ull;
-      for (uint32_t i = 0; i < n; ++i) {
-        const uint32_t key = skey[i];
-        if ((int64_t)key <= last) continue;
-        const uint32_t bb = sbox[i];
-        const int bx = bb & 0xff, by = (bb >> 8) & 0xff;
-        if (pxl < bx || pxl >= bx + (int)((bb >> 16) & 0xff) || pyl < by || pyl >= by + (int)(bb >> 24)) continue;
-        const unsigned long long cand = ((unsigned long long)key << 32) | i;
-        if (cand >= best) continue;
-        double e[3];
-        if (edges_at(Rec{sg, (int)i}, sflags[i], px, py, e)) best = cand;
+    } else if (cnt > (uint32_t)kPC) {  // deeper stacks: repeated smallest-key selection over the tile's records
+      int64_t last = -1;  // key of the last folded record
+      for (uint32_t k = 0; k < cnt; ++k) {
+        unsigned long long best = ~0ull;
+        for (uint32_t i = 0; i < n; ++i) {
+          const uint32_t key = skey[i];
+          if ((int64_t)key <= last) continue;
+          const uint32_t bb = sbox[i];
+          const int bx = bb & 0xff, by = (bb >> 8) & 0xff;
+          if (pxl < bx || pxl >= bx + (int)((bb >> 16) & 0xff) || pyl < by || pyl >= by + (int)(bb >> 24)) continue;
+          const unsigned long long cand = ((unsigned long long)key << 32) | i;
+          if (cand >= best) continue;
+          double e[3];
+          if (edges_at(Rec{sg, (int)i}, sflags[i], px, py, e)) best = cand;
+        }
+        const int j = (int)(best & 0xffffffffu);
+        fd.step(Rec{sg, j}, sflags[j], px, py, j);
+        last = (int64_t)(best >> 32);
       }
-      const int j = (int)(best & 0xffffffffu);
-      fd.step(Rec{sg, j}, sflags[j], px, py, j);
-      last = (int64_t)(best >> 32);
     }
-  }
-  const uint32_t flags = fd.win >= 0 ? sflags[fd.win] : 0u;
-  const int32_t t = fd.win >= 0 ? (int32_t)(skey[fd.win] >> 1) : -1;
-  const int64_t off = fd.win >= 0 ? soff[fd.win] : 0;
-  write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, off);
+    const uint32_t flags = fd.win >= 0 ? sflags[fd.win] : 0u;
+    const int32_t t = fd.win >= 0 ? (int32_t)(skey[fd.win] >> 1) : -1;
+    const int64_t off = fd.win >= 0 ? soff[fd.win] : 0;
+    write_pixel(sc, cam, o, f, W, H, px_i, py_i, fd, flags, t, off);
 #undef PCJ
   };
   if constexpr (NT == kTP) {
