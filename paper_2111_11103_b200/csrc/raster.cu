@@ -64,6 +64,9 @@ constexpr int kRasterNT = TFB_RASTER_NT;
 #ifndef TFB_KEEP_PE
 #define TFB_KEEP_PE 0  // 1: keep a sole covering pair's edge values in shared memory (else recomputed)
 #endif
+#ifndef TFB_RASTER_MINB32
+#define TFB_RASTER_MINB32 32  // k_raster<32> CTAs per SM (the per-SM CTA limit; 64 registers)
+#endif
 #ifndef TFB_RASTER_MINB1
 #define TFB_RASTER_MINB1 20  // k_raster<64> CTAs per SM the register budget must allow (48 registers)
 #endif
@@ -155,10 +158,10 @@ struct Work {
   uint32_t *fcnt;       // fcnt[1]: big-tile count
   uint32_t *tile_count; // per frame per tile
   uint32_t *list;
-  uint32_t *big;  // (frame, tile) codes handed to k_raster_big (count in fcnt[1]) from the front, and
-                  // to the kTP-thread second tier (count *t2cnt) from the back
-  uint32_t *t2cnt;
-  int64_t bigcap;  // entries of big (nframes x ntiles: a tile is in at most one list)
+  uint32_t *big;  // (frame, tile) codes handed to k_raster_big; count in fcnt[1]
+  uint32_t *tl;    // tier lists: [0, nframes x ntiles) tiles for the 64-thread tier, then the 128-thread tier
+  uint32_t *tcnt;  // their counts
+  int64_t tlcap;   // entries per tier list (nframes x ntiles)
   uint32_t *csurv;  // per frame: surviving cluster ids (count fcnt[4f]); ncl entries per frame
   int64_t ncl;
   int64_t rs;   // record slots per frame (2m)
@@ -186,6 +189,7 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
   size_t o_tc = take(sizeof(uint32_t) * ntiles * nframes);
   size_t o_list = take(sizeof(uint32_t) * (size_t)bincap * ntiles * nframes);
   size_t o_big = take(sizeof(uint32_t) * ntiles * nframes);
+  size_t o_tl = take(sizeof(uint32_t) * 2 * ntiles * nframes);
   const int64_t ncl = max_clusters(m);
   size_t o_csurv = take(sizeof(uint32_t) * (size_t)ncl * nframes);
   if (need_out) *need_out = off;
@@ -196,11 +200,12 @@ bool carve(void *ws, size_t ws_bytes, int64_t nv, int64_t m, int nframes, int nt
   w.vcode = reinterpret_cast<uint8_t *>(b + o_vcode);
   w.nv = nv > 0 ? nv : 1;
   w.fcnt = reinterpret_cast<uint32_t *>(b + o_fcnt);
-  w.t2cnt = w.fcnt + 4 * (int64_t)nframes;
-  w.bigcap = (int64_t)ntiles * nframes;
+  w.tcnt = w.fcnt + 4 * (int64_t)nframes;
+  w.tlcap = (int64_t)ntiles * nframes;
   w.tile_count = reinterpret_cast<uint32_t *>(b + o_tc);
   w.list = reinterpret_cast<uint32_t *>(b + o_list);
   w.big = reinterpret_cast<uint32_t *>(b + o_big);
+  w.tl = reinterpret_cast<uint32_t *>(b + o_tl);
   w.csurv = reinterpret_cast<uint32_t *>(b + o_csurv);
   w.ncl = ncl;
   w.rs = rs;
@@ -1198,8 +1203,12 @@ __device__ __forceinline__ void raster_tile(const tfb_scene &sc, const double *_
   if (n > (uint64_t)w.bincap || n > (uint32_t)NT) {
     if (tid == 0) {
       const uint32_t code = (uint32_t)(f * ntiles + tile);
-      if (NT < kTP && n <= (uint64_t)w.bincap && n <= (uint32_t)kTP) w.big[w.bigcap - 1 - atomicAdd(w.t2cnt, 1u)] = code;
-      else w.big[atomicAdd(w.fcnt + 1, 1u)] = code;
+      if (NT < kTP && n <= (uint64_t)w.bincap && n <= (uint32_t)kTP) {
+        const int tier = n <= 64u ? 0 : 1;  // the smallest wider CTA that stages them all
+        w.tl[tier * w.tlcap + atomicAdd(w.tcnt + tier, 1u)] = code;
+      } else {
+        w.big[atomicAdd(w.fcnt + 1, 1u)] = code;
+      }
       RSTAT(48);
     }
     return;
@@ -1484,30 +1493,40 @@ __device__ __forceinline__ void raster_tile(const tfb_scene &sc, const double *_
   }
 }
 
+// CTAs per SM the register budget must allow for a tile kernel of NT threads
+template <int NT>
+constexpr int raster_minb() {
+  return NT >= kTP ? TFB_RASTER_MINB : (NT >= 64 ? TFB_RASTER_MINB1 : TFB_RASTER_MINB32);
+}
+
 // One CTA of NT threads per tile.  With NT < kTP (the default 64 for 16 x 8 tiles) a
 // tile's staging (one record per thread) holds NT records and its shared memory is about
 // half the kTP-record layout, so twice the tiles are in flight per SM with the same warp
 // count: the latency chain of a tile (bin entry -> records -> staging barrier) is hidden by
-// more independent tiles.  Tiles with NT < n <= kTP records go to k_raster_t2, larger or
-// overflowed ones to k_raster_big.
+// more independent tiles.  Tiles with NT < n <= kTP records go to the tier kernels below,
+// larger or overflowed ones to k_raster_big.
 template <int NT>
-__global__ void __launch_bounds__(NT, NT < kTP ? TFB_RASTER_MINB1 : TFB_RASTER_MINB) k_raster(tfb_scene sc, const double *__restrict__ cams,
-                                                                          int W, int H, int TX, int ntiles, Work w, Outs o) {
+__global__ void __launch_bounds__(NT, raster_minb<NT>()) k_raster(tfb_scene sc, const double *__restrict__ cams, int W,
+                                                                  int H, int TX, int ntiles, Work w, Outs o) {
   extern __shared__ __align__(16) unsigned char raster_smem[];
   raster_tile<NT>(sc, cams, W, H, TX, ntiles, w, o, blockIdx.z, blockIdx.x, blockIdx.y, raster_smem);
 }
 
-// The second tier: the tiles k_raster<NT < kTP> passed on (NT < n <= kTP records), kTP
-// threads each, a persistent grid walking the list.
-__global__ void __launch_bounds__(kTP, TFB_RASTER_MINB) k_raster_t2(tfb_scene sc, const double *__restrict__ cams, int W,
-                                                                    int H, int TX, int ntiles, Work w, Outs o) {
+// The wider tiers: the tiles a narrower k_raster passed on (n <= 64 records for NT = 64,
+// n <= kTP for NT = kTP), NT threads each, a persistent grid walking the tier's list.
+template <int NT>
+__global__ void __launch_bounds__(NT, raster_minb<NT>()) k_raster_tier(tfb_scene sc, const double *__restrict__ cams,
+                                                                       int W, int H, int TX, int ntiles, Work w,
+                                                                       Outs o) {
   extern __shared__ __align__(16) unsigned char raster_smem[];
-  const uint32_t cnt = *w.t2cnt;
+  constexpr int tier = NT >= kTP ? 1 : 0;
+  const uint32_t cnt = w.tcnt[tier];
+  const uint32_t *list = w.tl + tier * w.tlcap;
   for (uint32_t i = blockIdx.x; i < cnt; i += gridDim.x) {
     __syncthreads();  // the previous tile's fold is done with the shared memory
-    const uint32_t code = w.big[w.bigcap - 1 - i];
+    const uint32_t code = list[i];
     const int f = (int)(code / (uint32_t)ntiles), tile = (int)(code % (uint32_t)ntiles);
-    raster_tile<kTP>(sc, cams, W, H, TX, ntiles, w, o, f, tile % TX, tile / TX, raster_smem);
+    raster_tile<NT>(sc, cams, W, H, TX, ntiles, w, o, f, tile % TX, tile / TX, raster_smem);
   }
 }
 
@@ -1699,25 +1718,31 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
     static bool smem_set[64] = {};
     static int num_sms[64] = {};
     std::lock_guard<std::mutex> guard(mu);
+    auto set_smem = [] {
+      cudaFuncSetAttribute(k_raster<kRasterNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(TileSmem<kRasterNT>));
+      cudaFuncSetAttribute(k_raster_tier<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem<64>));
+      cudaFuncSetAttribute(k_raster_tier<kTP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem<kTP>));
+    };
     if (dev >= 0 && dev < 64) {
       if (!smem_set[dev]) {
-        cudaFuncSetAttribute(k_raster<kRasterNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(TileSmem<kRasterNT>));
-        cudaFuncSetAttribute(k_raster_t2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem<kTP>));
+        set_smem();
         cudaDeviceGetAttribute(&num_sms[dev], cudaDevAttrMultiProcessorCount, dev);
         smem_set[dev] = true;
       }
       sms = num_sms[dev];
     } else {
-      cudaFuncSetAttribute(k_raster<kRasterNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sizeof(TileSmem<kRasterNT>));
-      cudaFuncSetAttribute(k_raster_t2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem<kTP>));
+      set_smem();
     }
   }
   k_raster<kRasterNT><<<dim3(TX, TY, nframes), kRasterNT, sizeof(TileSmem<kRasterNT>), st>>>(sc, cams, width, height,
                                                                                             TX, ntiles, w, o);
+  if (kRasterNT < 64)
+    k_raster_tier<64><<<sms * raster_minb<64>(), 64, sizeof(TileSmem<64>), st>>>(sc, cams, width, height, TX, ntiles,
+                                                                                w, o);
   if (kRasterNT < kTP)
-    k_raster_t2<<<sms * TFB_RASTER_MINB, kTP, sizeof(TileSmem<kTP>), st>>>(sc, cams, width, height, TX, ntiles, w, o);
+    k_raster_tier<kTP><<<sms * raster_minb<kTP>(), kTP, sizeof(TileSmem<kTP>), st>>>(sc, cams, width, height, TX,
+                                                                                    ntiles, w, o);
   k_raster_big<<<sms * (256 / kTP), kTP, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
   return check_launch("tfb_rasterize");
 }
