@@ -54,6 +54,9 @@ constexpr int kThreads = 256;              // setup-side kernels
 #ifndef TFB_FIRST_FAST
 #define TFB_FIRST_FAST 1
 #endif
+#ifndef TFB_FUSED_SETUP
+#define TFB_FUSED_SETUP 1  // clustered scenes: k_ccsetup (cull + record setup + binning in one pass)
+#endif
 #ifndef TFB_RASTER_NT
 #define TFB_RASTER_NT 64  // k_raster threads per tile (= staged record capacity); kTP: one tier
 #endif
@@ -393,6 +396,41 @@ __device__ __forceinline__ uint32_t vertex_code(const Cam &cam, const double P[3
          ((P[1] * cam.fy + (cam.cy - ((double)H - 0.25)) * z > 0.0) ? 16u : 0u);
 }
 
+// Record(s) of one surviving triangle t with camera-space vertices P (rasterizer.py:113-164):
+// one record at `slot` when no vertex is behind the near plane, else the clip fan's two
+// halves at slot and slot + 1 (holes where a half produces nothing).  p0 / p1 receive the
+// records' pending tile-bin appends.
+__device__ __forceinline__ void setup_candidate(const tfb_scene &sc, const Cam &cam, int W, int H, const Work &w, int f,
+                                                int64_t t, const double P[3][3], bool unclipped, uint32_t slot,
+                                                Pend &p0, Pend &p1) {
+  RecGeom g;
+  RecMeta mt;
+  const uint32_t tflags = ((uint32_t)__ldg(sc.origins + t) << 5) | ((uint32_t)__ldg(sc.steps + t) << 16);
+  const int32_t toff = (int32_t)__ldg(sc.offsets + t);
+  if (unclipped) {
+    if (build_record(cam, W, H, P, toff, false, 0, tflags, g, mt)) store_record(w, f, slot, (uint32_t)(2 * t), g, mt, p0);
+    else store_hole(w, f, slot);
+  } else {
+    double op[4][3], ob[4][3];
+    const int n = clip_near(P, op, ob);
+    for (int k = 1; k <= 2; ++k) {  // fan (0, k, k+1), rasterizer.py:119-122
+      bool ok = false;
+      if (k + 1 < n) {
+        double S[3][3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          S[0][q] = op[0][q];
+          S[1][q] = op[k][q];
+          S[2][q] = op[k + 1][q];
+        }
+        ok = build_record(cam, W, H, S, toff, true, k - 1, tflags, g, mt);
+      }
+      if (ok) store_record(w, f, slot + (k - 1), (uint32_t)(2 * t + (k - 1)), g, mt, k == 1 ? p0 : p1);
+      else store_hole(w, f, slot + (k - 1));
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_verts(tfb_scene sc, const double *__restrict__ cams, int W, int H,
                                                     Work w) {
   const int f = blockIdx.y;
@@ -669,40 +707,13 @@ __global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc
   auto one = [&](const Cand &c, Pend &p0, Pend &p1) {
     p0.valid = p1.valid = false;
     if (!c.nslot) return;
-    const uint32_t slot = c.slot;
-    const int64_t t = c.t;
     // camera-space vertices recomputed here (bit-identical to k_verts' transform): the
     // vertex array is L2-resident across frames, a per-frame camera-space copy is not
     double P[3][3];
     xform(cam, sc.vertices + 3 * c.i0, P[0]);
     xform(cam, sc.vertices + 3 * c.i1, P[1]);
     xform(cam, sc.vertices + 3 * c.i2, P[2]);
-    RecGeom g;
-    RecMeta mt;
-    const uint32_t tflags = ((uint32_t)__ldg(sc.origins + t) << 5) | ((uint32_t)__ldg(sc.steps + t) << 16);
-    const int32_t toff = (int32_t)__ldg(sc.offsets + t);
-    if (c.unclipped) {
-      if (build_record(cam, W, H, P, toff, false, 0, tflags, g, mt)) store_record(w, f, slot, (uint32_t)(2 * t), g, mt, p0);
-      else store_hole(w, f, slot);
-    } else {
-      double op[4][3], ob[4][3];
-      const int n = clip_near(P, op, ob);
-      for (int k = 1; k <= 2; ++k) {  // fan (0, k, k+1), rasterizer.py:119-122
-        bool ok = false;
-        if (k + 1 < n) {
-          double S[3][3];
-#pragma unroll
-          for (int q = 0; q < 3; ++q) {
-            S[0][q] = op[0][q];
-            S[1][q] = op[k][q];
-            S[2][q] = op[k + 1][q];
-          }
-          ok = build_record(cam, W, H, S, toff, true, k - 1, tflags, g, mt);
-        }
-        if (ok) store_record(w, f, slot + (k - 1), (uint32_t)(2 * t + (k - 1)), g, mt, k == 1 ? p0 : p1);
-        else store_hole(w, f, slot + (k - 1));
-      }
-    }
+    setup_candidate(sc, cam, W, H, w, f, c.t, P, c.unclipped, c.slot, p0, p1);
   };
   uint32_t *tc = w.tile_count + (int64_t)f * ntiles;
   const uint32_t stride = gridDim.x * kThreads * kSetupPer;
@@ -855,6 +866,157 @@ __global__ void __launch_bounds__(kThreads, TFB_SETUP_MINB) k_setup(tfb_scene sc
         bin_put(w, f, ntiles, tile, atomicAdd(tc + tile, 1u), bslot);
       }
     }
+  }
+}
+
+// Tile-bin appends of NP pending records per lane of a (possibly partial) warp: the
+// first-tile appends of all of them warp-aggregated (one atomic per distinct tile) and in
+// flight together, then each lane appends its small records' further tiles and the whole
+// warp those of records spanning more than kSetupWide tiles (k_setup's non-flat path).
+template <int NP>
+__device__ __forceinline__ void bin_pending(const Work &w, int f, int ntiles, int TX, uint32_t *tc, const Pend (&p)[NP],
+                                            unsigned act, int lane) {
+  uint32_t pos[NP];
+  unsigned peers[NP];
+#pragma unroll
+  for (int e = 0; e < NP; ++e) {
+    const int tile = p[e].valid ? (int)(p[e].ty & 0xffffu) * TX + (int)(p[e].tx & 0xffffu) : -1 - lane;
+    peers[e] = __match_any_sync(act, tile);
+    pos[e] = 0u;
+    if (p[e].valid && lane == __ffs(peers[e]) - 1) pos[e] = atomicAdd(tc + tile, (uint32_t)__popc(peers[e]));
+  }
+#pragma unroll
+  for (int e = 0; e < NP; ++e)
+    pos[e] = __shfl_sync(act, pos[e], __ffs(peers[e]) - 1) + __popc(peers[e] & ((1u << lane) - 1u));
+  unsigned wide = 0u;  // bit e: record e goes to the warp
+#pragma unroll
+  for (int e = 0; e < NP; ++e) {
+    if (!p[e].valid) continue;
+    const int x0 = (int)(p[e].tx & 0xffffu), x1 = (int)(p[e].tx >> 16);
+    const int y0 = (int)(p[e].ty & 0xffffu), y1 = (int)(p[e].ty >> 16);
+    bin_put(w, f, ntiles, y0 * TX + x0, pos[e], p[e].slot);
+    if ((x1 - x0 + 1) * (y1 - y0 + 1) > kSetupWide) {
+      wide |= 1u << e;
+      continue;
+    }
+    for (int ty = y0; ty <= y1; ++ty)
+      for (int tx = (ty == y0 ? x0 + 1 : x0); tx <= x1; ++tx) {
+        const int tile = ty * TX + tx;
+        bin_put(w, f, ntiles, tile, atomicAdd(tc + tile, 1u), p[e].slot);
+      }
+  }
+  for (unsigned todo = __ballot_sync(act, wide != 0u); todo; todo = __ballot_sync(act, wide != 0u)) {
+    const int src = __ffs(todo) - 1;
+    const int e = __shfl_sync(act, wide ? __ffs(wide) - 1 : 0, src);
+    uint32_t mtx = 0, mty = 0, mslot = 0;
+#pragma unroll
+    for (int k = 0; k < NP; ++k)
+      if (k == e) {
+        mtx = p[k].tx;
+        mty = p[k].ty;
+        mslot = p[k].slot;
+      }
+    const uint32_t btx = __shfl_sync(act, mtx, src), bty = __shfl_sync(act, mty, src);
+    const uint32_t bslot = __shfl_sync(act, mslot, src);
+    if (lane == src) wide &= wide - 1u;
+    const int x0 = (int)(btx & 0xffffu), nx = (int)(btx >> 16) - x0 + 1;
+    const int y0 = (int)(bty & 0xffffu), ny = (int)(bty >> 16) - y0 + 1;
+    const int rank = __popc(act & ((1u << lane) - 1u)), nact = __popc(act);
+    for (int i = 1 + rank; i < nx * ny; i += nact) {
+      const int tile = (y0 + i / nx) * TX + x0 + i % nx;
+      bin_put(w, f, ntiles, tile, atomicAdd(tc + tile, 1u), bslot);
+    }
+  }
+}
+
+// k_ccsetup = k_ccands + k_setup in one pass (TFB_FUSED_SETUP): per (frame, surviving
+// cluster) the cluster's distinct vertices are transformed once into shared memory
+// (camera space, bit-identical to xform), the outcode test of k_ccands picks the
+// candidates, their record slots come from the same front / back appends, and each
+// candidate's thread builds its record(s) from the shared positions and bins them -- no
+// survivor list round trip through memory, no second gather and transform of the
+// vertices (a cluster's ~55 distinct vertices serve its 64 triangles).
+#ifndef TFB_CCSETUP_MINB
+#define TFB_CCSETUP_MINB 5  // 48 registers: 5 blocks (40 warps) per SM
+#endif
+__global__ void __launch_bounds__(kThreads, TFB_CCSETUP_MINB) k_ccsetup(tfb_scene sc, const double *__restrict__ cams,
+                                                                        int W, int H, int TX, int ntiles, Work w) {
+  const int f = blockIdx.y;
+  constexpr int kPer = kThreads / kCluster;
+  __shared__ Cam cam;
+  __shared__ uint8_t scode[kPer][kCV];
+  __shared__ double sP[kPer][3][kCV];  // camera-space positions, component-major
+  load_cam(cam, cams, f);
+  __syncthreads();
+  const uint32_t nsurv = w.fcnt[4 * f];
+  const uint32_t *cs = w.csurv + (int64_t)f * w.ncl;
+  uint32_t *tc = w.tile_count + (int64_t)f * ntiles;
+  const int64_t mc = w.rs / 2;
+  const int lane = threadIdx.x & 31, sub = threadIdx.x / kCluster, slot = threadIdx.x % kCluster;
+  for (uint32_t g0 = blockIdx.x * kPer; g0 < nsurv; g0 += gridDim.x * kPer) {
+    const uint32_t gi = g0 + sub;
+    const tfb_cluster *cl = gi < nsurv ? sc.clusters + __ldg(cs + gi) : nullptr;
+    int4 tr = make_int4(-1, 0, 0, 0);
+    uint32_t loc = 0;
+    if (cl) {
+      tr = __ldg(reinterpret_cast<const int4 *>(cl->tri[slot]));
+      loc = __ldg(cl->local + slot);
+      int32_t vid[kCV / kCluster];
+#pragma unroll
+      for (int k = 0; k < kCV / kCluster; ++k) vid[k] = __ldg(cl->verts + slot + k * kCluster);
+      const int nv = __ldg(&cl->nverts);
+#pragma unroll
+      for (int k = 0; k < kCV / kCluster; ++k) {
+        const int j = slot + k * kCluster;
+        if (j < nv) {
+          double P[3];
+          xform(cam, sc.vertices + 3 * (int64_t)vid[k], P);
+          scode[sub][j] = (uint8_t)vertex_code(cam, P, W, H);
+          sP[sub][0][j] = P[0];
+          sP[sub][1][j] = P[1];
+          sP[sub][2][j] = P[2];
+        }
+      }
+    }
+    __syncthreads();
+    bool cand = false, nc = false;
+    uint32_t l0 = 0, l1 = 0, l2 = 0;
+    if (tr.x >= 0) {
+      l0 = loc & 0xffu;
+      l1 = (loc >> 8) & 0xffu;
+      l2 = (loc >> 16) & 0xffu;
+      const uint32_t c0 = scode[sub][l0], c1 = scode[sub][l1], c2 = scode[sub][l2];
+      cand = (c0 & c1 & c2) == 0u;
+      nc = ((c0 | c1 | c2) & 1u) != 0u;
+    }
+    const unsigned ba = __ballot_sync(0xffffffffu, cand && !nc), bb = __ballot_sync(0xffffffffu, cand && nc);
+    uint32_t pa = 0, pb = 0;
+    if (lane == 0) {
+      if (ba) pa = atomicAdd(w.fcnt + 4 * f + 2, (uint32_t)__popc(ba));
+      if (bb) pb = atomicAdd(w.fcnt + 4 * f + 3, (uint32_t)__popc(bb));
+    }
+    pa = __shfl_sync(0xffffffffu, pa, 0);
+    pb = __shfl_sync(0xffffffffu, pb, 0);
+    Pend pd[2];
+    pd[0].valid = pd[1].valid = false;
+    if (cand) {
+      // record slots exactly as k_setup derives them from the survivor lists: the i-th
+      // unclipped survivor -> slot i, the near-clipped one at back index ci -> 2ci, 2ci + 1
+      const unsigned below = (1u << lane) - 1u;
+      const uint32_t rslot = nc ? (uint32_t)(2 * (mc - 1 - (int64_t)(pb + __popc(bb & below))))
+                                : pa + __popc(ba & below);
+      double P[3][3];
+      const uint32_t lk[3] = {l0, l1, l2};
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        P[k][0] = sP[sub][0][lk[k]];
+        P[k][1] = sP[sub][1][lk[k]];
+        P[k][2] = sP[sub][2][lk[k]];
+      }
+      setup_candidate(sc, cam, W, H, w, f, (int64_t)tr.x, P, !nc, rslot, pd[0], pd[1]);
+    }
+    bin_pending<2>(w, f, ntiles, TX, tc, pd, 0xffffffffu, lane);
+    __syncthreads();  // scode / sP reused by the next group
   }
 }
 
@@ -1696,7 +1858,10 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
     // more survivors are strided over
     const int64_t gb = (sc.num_clusters + 8 * (kThreads / kCluster) - 1) / (8 * (kThreads / kCluster));
     dim3 g1((unsigned)(gb < 1 ? 1 : gb), nframes);
-    k_ccands<<<g1, kThreads, 0, st>>>(sc, cams, width, height, w);
+    if (TFB_FUSED_SETUP)
+      k_ccsetup<<<g1, kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w);
+    else
+      k_ccands<<<g1, kThreads, 0, st>>>(sc, cams, width, height, w);
   } else if (m > 0) {
     if (sc.num_vertices > 0) {
       dim3 g0((unsigned)((sc.num_vertices + kThreads - 1) / kThreads), nframes);
@@ -1705,7 +1870,7 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
     dim3 g1((unsigned)((m + kThreads * kCullPer - 1) / (kThreads * kCullPer)), nframes);
     k_cull<<<g1, kThreads, 0, st>>>(sc, w);
   }
-  if (m > 0) {
+  if (m > 0 && !(clustered && TFB_FUSED_SETUP)) {
     int64_t sb = (m / 3 + kThreads * kSetupPer - 1) / (kThreads * kSetupPer);  // ~1/3 survive a typical cull
     dim3 g2((unsigned)(sb < 1 ? 1 : sb), nframes);
     k_setup<<<g2, kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w);
