@@ -149,9 +149,11 @@ class _PinnedStager:
         import os
         from concurrent.futures import ThreadPoolExecutor
 
-        # 8 threads measured best on a 16-core host (876 vs 832 frames/s with 16 at cfg2)
-        n = threads or int(os.environ.get("TFB_STAGE_THREADS", "0")) or max(
-            1, min(8, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count() or 2))
+        # 8 threads measured best on a 16-core host (876 vs 832 frames/s with 16 at cfg2);
+        # with several ranks per host (LOCAL_WORLD_SIZE, set by torchrun) they share the cores
+        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count() or 2
+        local = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1") or 1))
+        n = threads or int(os.environ.get("TFB_STAGE_THREADS", "0")) or max(1, min(8, cores // local))
         self.pool = ThreadPoolExecutor(max_workers=n, thread_name_prefix="tfb-stage")
         self.nthreads = n
         self.nslots = slots
