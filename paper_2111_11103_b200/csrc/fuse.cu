@@ -40,6 +40,9 @@ namespace {
 #ifndef TFB_FUSE_WARPS
 #define TFB_FUSE_WARPS 8
 #endif
+#ifndef TFB_FUSE_NS_SHALLOW
+#define TFB_FUSE_NS_SHALLOW 1
+#endif
 #ifndef TFB_FUSE_NS
 #define TFB_FUSE_NS 2
 #endif
@@ -1210,7 +1213,13 @@ extern "C" int tfb_fuse_ordered(const int32_t *rows, int64_t hw, int nframes, co
               "tfb_fuse: accumulator of %lld x %lld elements exceeds 32-bit row offsets", (long long)total_texels,
               (long long)accum_stride);
   const size_t stage = (size_t)kChunk * num_classes * 4;
-  const int NS = stage <= 2048 ? 4 : TFB_FUSE_NS;
+  // staging depth per warp: small stages keep four in flight; otherwise one, so twice the
+  // warps fit per SM (measured: cfg2 scatter -2 %, float64 -7 %), except where a warp needs
+  // its own look-ahead -- the row-block item order walks items out of address order, and
+  // the c % 4 != 0 kernel is issue-bound on few resident warps (2: configs[3] 20.7 -> 15.2
+  // us/frame, configs[4] 46.2 -> 45.7)
+  const bool deep = item_order != nullptr || num_classes % 4 != 0;
+  const int NS = stage <= 2048 ? 4 : (deep ? TFB_FUSE_NS : TFB_FUSE_NS_SHALLOW);
   TFB_REQUIRE(warp_layout(num_classes, NS, wide ? 8 : 4).total <= kSmemBudget &&
                   fast_layout(num_classes, NS).total <= kSmemBudget,
               TFB_ERR_CAPACITY, "tfb_fuse: %d classes exceed the shared-memory staging budget of one warp",
