@@ -267,6 +267,32 @@ def test_raster_dense_tiles_big_path_exact():
     assert cov.mean() > 0.1  # the 40x24-pixel window is covered
 
 
+@pytest.mark.parametrize("m", [60, 400, 700])
+def test_raster_tile_tiers_exact(m):
+    """Record densities that put the window's 16x8 tiles in each rasterizer tier:
+    <= 64 records (k_raster<64>), 64 < n <= 128 (the 128-thread tier kernel
+    walking its list) and beyond (k_raster_big), with overlapping stacks -- ids,
+    depth, u, v bit-exact vs the oracle."""
+    rng = np.random.default_rng(100 + m)
+    centers = np.column_stack([rng.uniform(-0.2, 0.2, m), rng.uniform(-0.12, 0.12, m),
+                               np.round(rng.uniform(1.9, 2.1, m), 2)])
+    offs = rng.uniform(-0.04, 0.04, size=(m, 3, 3))
+    offs[:, :, 2] *= 0.1
+    verts = (centers[:, None, :] + offs).reshape(-1, 3)
+    mesh = Mesh.from_arrays(verts, np.arange(3 * m, dtype=np.int32).reshape(m, 3))
+    layout = uniform_layout(mesh, 2)
+    W, H = 96, 64
+    fr = CameraFrame(0, Intrinsics(200.0, 200.0, 47.5, 31.5, W, H), np.eye(3), np.zeros(3))
+    ids = rasterize(mesh, layout, fr)
+    ref = O.rasterize(mesh.vertices, mesh.triangles, layout.steps, layout.origins, pack_camera(fr), W, H)
+    for key, plane in (("triangle", ids.triangle), ("texel", ids.texel), ("depth", ids.depth)):
+        np.testing.assert_array_equal(plane, ref[key], err_msg=key)
+    cov = ids.triangle >= 0
+    np.testing.assert_array_equal(ids.u[cov], ref["u"][cov])
+    np.testing.assert_array_equal(ids.v[cov], ref["v"][cov])
+    assert cov.mean() > 0.02
+
+
 def _raster_rows_hits(mesh, layout, frames, W, H, clusters, monkeypatch):
     from paper_2111_11103_b200.device import DeviceScene
 
