@@ -319,9 +319,9 @@ def run_ours(args):
     fuse_frames = sum(p_[0] for p_ in prof)
     # k_fuse launches: tfb_fuse carries at most 256 frames per launch
     n_launch_fuse = sum((p_[0] + 255) // 256 for p_ in prof)
-    # our kernels per timed step: per batch k_ccull, k_ccands (k_verts, k_cull without scene clusters),
-    # k_setup, k_raster, k_raster_big + the k_fuse launches (the hit-count reset is a dense torch
-    # memset here), + k_finalize once
+    # our kernels per timed step: per batch k_ccull, k_ccsetup, k_raster<64>, k_raster_tier<128>,
+    # k_raster_big + the k_fuse launches (the hit-count reset is a dense torch memset here),
+    # + k_finalize once
     batches = [min(args.batch, nf - b0) for b0 in range(0, nf, args.batch)]
     gpu_launches = args.steps * (sum(5 + (b + 255) // 256 for b in batches) + 1)
     peak, peak_kind = _peaks()
