@@ -179,6 +179,10 @@ size_t tfb_fuse_order_workspace_bytes(int64_t hw, int nframes, int64_t total_tex
 int tfb_fuse_order(const int32_t *rows, int64_t hw, int nframes, int64_t total_texels, int shift,
                    void *workspace, size_t workspace_bytes, uint32_t *order_out, uint32_t *n_out, void *stream);
 
+/* Test support: y[i] = the float64 natural log the float64-accumulator scatter-add
+ * uses (table-driven, csrc/log_f64.cuh) for device arrays x, y of n doubles. */
+int tfb_test_log_f64(const double *x, double *y, int64_t n, void *stream);
+
 /* finalize + texel_argmax (fusion.py:186-222).  rows_out (total_texels*c
  * float32), unobserved_out (u8) and labels_out (int32, UNKNOWN = -1) are each
  * optional. */

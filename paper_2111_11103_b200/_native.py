@@ -47,6 +47,7 @@ _SIGNATURES = {
     "tfb_fuse": ([_P, _I64, _I, _P, _I, _P, _P, _I64, _I, _I, _D, _P, _I, _I64, _P, _P, _P], _I),
     "tfb_fuse_ordered": ([_P, _I64, _I, _P, _I, _P, _P, _I64, _I, _I, _D, _P, _I, _I64, _P, _P, _P, _P, _P], _I),
     "tfb_fuse_order_workspace_bytes": ([_I64, _I, _I64, _I], _SZ),
+    "tfb_test_log_f64": ([_P, _P, _I64, _P], _I),
     "tfb_fuse_order": ([_P, _I64, _I, _I64, _I, _P, _SZ, _P, _P, _P], _I),
     "tfb_finalize": ([_P, _I, _I64, _P, _I64, _I, _I, _P, _P, _P, _P], _I),
     "tfb_render": ([_P, _I64, _I, _P, _I64, _P, _P, _P], _I),

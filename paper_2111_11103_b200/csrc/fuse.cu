@@ -33,6 +33,11 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "log_f64.cuh"
+
+#ifndef TFB_LOG_F64
+#define TFB_LOG_F64 1  // float64 logs through the table-driven tfb_log::log_f64 (else libdevice log)
+#endif
 
 namespace tfb {
 namespace {
@@ -315,6 +320,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
   constexpr bool kProd64 = (AGG == TFB_AGG_MUL) && EQW && sizeof(AccT) == 8;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the float64 log's reduction table, per CTA in shared memory (lanes index it divergently)
+  __shared__ double2 s_logtab[sizeof(AccT) == 8 && TFB_LOG_F64 ? 128 : 1];
+  if (sizeof(AccT) == 8 && TFB_LOG_F64) {
+    for (int t = threadIdx.x; t < 128; t += blockDim.x) s_logtab[t] = tfb_log::kTable[t];
+    __syncthreads();
+  }
+  auto log64 = [&](double x) -> double { return TFB_LOG_F64 ? tfb_log::log_f64(x, s_logtab) : log(x); };
   const int c = p.c, NS = p.NS;
   const Geo geo = geo_of(c);
   const WarpSmem L = warp_layout(c, NS, (int)sizeof(AccT));
@@ -470,10 +482,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
             double v[4] = {(double)a0, (double)a1, (double)a2, (double)a3};
             if (kProd64) {  // w * log(prod of the piece's clipped values) = sum of w * log(p)
               const double wv = (double)wrun;
-              v[0] = wv * log(d01.x);
-              v[1] = wv * log(d01.y);
-              v[2] = wv * log(d23.x);
-              v[3] = wv * log(d23.y);
+              v[0] = wv * log64(d01.x);
+              v[1] = wv * log64(d01.y);
+              v[2] = wv * log64(d23.x);
+              v[3] = wv * log64(d23.y);
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k)
@@ -538,7 +550,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
             for (int k = 0; k < 4; ++k) {
               if (AGG == TFB_AGG_SUM) tt[k] = (double)vv[k];
               else if (AGG == TFB_AGG_MAXSUM) tt[k] = vv[k] == smax[i] ? (double)vv[k] : 0.0;
-              else tt[k] = log(clip_mul64(vv[k]));
+              else tt[k] = log64(clip_mul64(vv[k]));
             }
             a0 += wi * tt[0]; a1 += wi * tt[1]; a2 += wi * tt[2]; a3 += wi * tt[3];
           }
@@ -1348,4 +1360,25 @@ extern "C" int tfb_pixel_weights(const int32_t *rows, int64_t hw, int nframes, c
   k_pixel_weights<<<dim3(grid_for(hw), nframes), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       rows, hw, hits, total_texels, weight_mode, alpha, out);
   return check_launch("tfb_pixel_weights");
+}
+
+namespace tfb {
+namespace {
+__global__ void k_test_log_f64(const double *x, double *y, int64_t n) {
+  __shared__ double2 tab[128];
+  for (int t = threadIdx.x; t < 128; t += blockDim.x) tab[t] = tfb_log::kTable[t];
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = tfb_log::log_f64(x[i], tab);
+}
+}  // namespace
+}  // namespace tfb
+
+extern "C" int tfb_test_log_f64(const double *x, double *y, int64_t n, void *stream) {
+  TFB_REQUIRE(n >= 0 && (n == 0 || (x && y)), TFB_ERR_DATA, "tfb_test_log_f64: bad arguments");
+  if (n == 0) return TFB_OK;
+  const int64_t blocks = (n + 255) / 256;
+  tfb::k_test_log_f64<<<(unsigned)(blocks < 1024 ? blocks : 1024), 256, 0, static_cast<cudaStream_t>(stream)>>>(x, y,
+                                                                                                              n);
+  return check_launch("tfb_test_log_f64");
 }

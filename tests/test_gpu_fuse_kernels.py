@@ -256,3 +256,44 @@ def test_fuse_piece_per_pixel_chunks(c, agg):
         np.testing.assert_array_equal(cnt, cref)
         _check(got, ref, _scale(rows, probs, n_x, agg, wm, alpha))
     np.testing.assert_array_equal(fb, probs.argmax(axis=2))
+
+
+def test_log_f64_against_numpy():
+    """The table-driven float64 log of the float64-accumulator scatter-add
+    (csrc/log_f64.cuh) against NumPy's log: within 2 ulp over random arguments
+    across the whole product range, around 1 (no cancellation), at powers of two
+    and at every reduction-interval boundary; special arguments (0, negative,
+    subnormal, inf, NaN) follow libdevice / NumPy."""
+    rng = np.random.default_rng(7)
+    xs = [np.exp(rng.uniform(np.log(1e-300), 0.0, 200000)),            # products of clipped probabilities
+          1.0 - np.exp(rng.uniform(np.log(1e-16), np.log(0.3), 20000)),  # just below 1
+          1.0 + np.exp(rng.uniform(np.log(1e-16), np.log(0.3), 20000)),  # just above 1
+          np.ldexp(1.0, np.arange(-1022, 1023)).astype(np.float64),
+          rng.uniform(1e-7, 1.0, 20000)]
+    # interval boundaries of z = x * 2^-k in [0.6875, 1.375) and their neighbours
+    edges = 0.6875 * (1.0 + np.arange(129) / 128.0)
+    edges = np.concatenate([edges[edges < 1.0], 1.0 + (np.arange(49) / 128.0)])
+    edges = np.concatenate([edges, np.nextafter(edges, 0.0), np.nextafter(edges, 2.0)])
+    for s in (-3, -1, 0, 1, 3):
+        xs.append(edges * 2.0 ** s)
+    x = np.concatenate(xs).astype(np.float64)
+    x = x[(x > 0) & np.isfinite(x)]
+    xd = torch.as_tensor(x, device="cuda")
+    yd = torch.empty_like(xd)
+    N.call("tfb_test_log_f64", N.ptr(xd), N.ptr(yd), x.size, N.stream_handle())
+    y = yd.cpu().numpy()
+    ref = np.log(x)
+    ulp = np.spacing(np.abs(ref))
+    err = np.abs(y - ref) / ulp
+    assert err.max() <= 2.0, (err.max(), x[np.argmax(err)])
+    assert np.all(y[x == 1.0] == 0.0)
+    special = np.array([0.0, -0.0, -1.0, 5e-324, 1e-310, np.inf, np.nan, 2.0 ** -1022], dtype=np.float64)
+    sd = torch.as_tensor(special, device="cuda")
+    so = torch.empty_like(sd)
+    N.call("tfb_test_log_f64", N.ptr(sd), N.ptr(so), special.size, N.stream_handle())
+    got = so.cpu().numpy()
+    with np.errstate(divide="ignore", invalid="ignore"):
+        want = np.log(special)
+    np.testing.assert_array_equal(np.isnan(got), np.isnan(want))
+    ok = ~np.isnan(want)
+    np.testing.assert_allclose(got[ok], want[ok], rtol=1e-15)
