@@ -270,7 +270,14 @@ def compute_pixel_weights(ids, mode, alpha=None):
     """Per-pixel fusion weight for one frame (fusion.py:114-142)."""
     _check_mode(mode, alpha)
     N.require_cuda()
-    host = _weights_on_device(ids, mode, alpha).cpu().numpy().reshape(ids.height, ids.width)
+    dev = _weights_on_device(ids, mode, alpha)
+    # read back through page-locked memory (torch's caching host allocator: no allocation
+    # after warm-up, a DMA at full PCIe rate instead of the driver's pageable staging);
+    # the returned array keeps its pinned buffer alive
+    pinned = torch.empty(dev.shape, dtype=dev.dtype, pin_memory=True)
+    pinned.copy_(dev, non_blocking=True)
+    torch.cuda.current_stream(dev.device).synchronize()
+    host = pinned.numpy().reshape(ids.height, ids.width)
     w = host.view(PixelWeights)
     w._spec = (ids, mode, alpha)
     w.flags.writeable = False
