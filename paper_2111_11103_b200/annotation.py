@@ -760,7 +760,7 @@ class MeshAnnotation:
 
     def labels(self, host=False):
         self._finalize()
-        return self._tex.labels_device.cpu().numpy() if host else self._tex.labels_device
+        return N.host_copy(self._tex.labels_device) if host else self._tex.labels_device
 
     def render(self, cameras, width=None, height=None, fallback=None, host=False, stream=None):
         """Label images (B, H, W) int32 for the given cameras (renderback.py:28-56)."""
@@ -785,4 +785,4 @@ class MeshAnnotation:
                 fb = fb_all[b0:b0 + b].contiguous() if fb_all is not None else None
                 render_labels_device(labels, rows, hw, b, fb, out[b0:b0 + b], cur)
         out = out.view(B, H, W)
-        return out.cpu().numpy() if host else out
+        return N.host_copy(out) if host else out

@@ -270,14 +270,7 @@ def compute_pixel_weights(ids, mode, alpha=None):
     """Per-pixel fusion weight for one frame (fusion.py:114-142)."""
     _check_mode(mode, alpha)
     N.require_cuda()
-    dev = _weights_on_device(ids, mode, alpha)
-    # read back through page-locked memory (torch's caching host allocator: no allocation
-    # after warm-up, a DMA at full PCIe rate instead of the driver's pageable staging);
-    # the returned array keeps its pinned buffer alive
-    pinned = torch.empty(dev.shape, dtype=dev.dtype, pin_memory=True)
-    pinned.copy_(dev, non_blocking=True)
-    torch.cuda.current_stream(dev.device).synchronize()
-    host = pinned.numpy().reshape(ids.height, ids.width)
+    host = N.host_copy(_weights_on_device(ids, mode, alpha)).reshape(ids.height, ids.width)
     w = host.view(PixelWeights)
     w._spec = (ids, mode, alpha)
     w.flags.writeable = False
@@ -386,4 +379,4 @@ def texel_argmax(tex):
     """Most probable class per texel, UNKNOWN where unobserved (fusion.py:213-222)."""
     if not tex.finalized:
         raise RuntimeError("texture must be finalized before argmax")
-    return tex._labels.cpu().numpy()
+    return N.host_copy(tex._labels)

@@ -78,8 +78,8 @@ class IdImage:
         if name in ("triangle", "texel"):
             self._ensure_device()
         if name in ("triangle", "texel") and self._dev_tri is not None:
-            self._host["triangle"] = self._dev_tri.view(H, W).cpu().numpy()
-            self._host["texel"] = self._dev_texel.view(H, W).cpu().numpy()
+            self._host["triangle"] = N.host_copy(self._dev_tri.view(H, W))
+            self._host["texel"] = N.host_copy(self._dev_texel.view(H, W))
             return self._host[name]
         if self._source is None:
             raise AttributeError("IdImage has no %s plane" % name)
@@ -95,7 +95,7 @@ class IdImage:
         with torch.cuda.device(d):
             scene.rasterize(cam, W, H, rows, tri=tri, texel=tex, depth=dep, u=uu, v=vv)
         for key, t in (("triangle", tri), ("texel", tex), ("depth", dep), ("u", uu), ("v", vv)):
-            self._host.setdefault(key, t.view(H, W).cpu().numpy())
+            self._host.setdefault(key, N.host_copy(t.view(H, W)))
         return self._host[name]
 
     triangle = property(lambda self: self._materialize("triangle"))
