@@ -45,6 +45,9 @@ namespace {
 #ifndef TFB_FUSE_WARPS
 #define TFB_FUSE_WARPS 8
 #endif
+#ifndef TFB_FUSE_REPACK
+#define TFB_FUSE_REPACK 0  // 1: compile-time c % 4 != 0 scans a 16-byte-quad repack of each stage (measured slower)
+#endif
 #ifndef TFB_FUSE_NS_SHALLOW
 #define TFB_FUSE_NS_SHALLOW 1
 #endif
@@ -300,13 +303,13 @@ __device__ __forceinline__ void pixel_argmax(const float *pp, int c, float &best
       bi = k;
     }
   };
-  if (VEC) {
+  if (VEC) {  // 16-byte quads; a padded last quad's extra lanes are not classes
     for (int k = 0; k < c; k += 4) {
       const float4 v = *reinterpret_cast<const float4 *>(pp + k);
       take(v.x, k);
-      take(v.y, k + 1);
-      take(v.z, k + 2);
-      take(v.w, k + 3);
+      if (k + 1 < c) take(v.y, k + 1);
+      if (k + 2 < c) take(v.z, k + 2);
+      if (k + 3 < c) take(v.w, k + 3);
     }
   } else {
     for (int k = 1; k < c; ++k) take(pp[k], k);
@@ -596,13 +599,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
 // product unchanged, as through np.clip + np.log).
 // ---------------------------------------------------------------------------
 struct FastSmem {
-  size_t stage_floats, o_head, o_max, o_bar, total;
+  size_t stage_floats, o_pad, o_head, o_max, o_bar, total;
 };
 
-__host__ __device__ inline FastSmem fast_layout(int c, int NS) {
+// cpad > 0: a per-warp working copy of the landed stage with the class stride padded
+// to cpad (a multiple of 4), so c % 4 != 0 rows move as 16-byte quads
+__host__ __device__ inline FastSmem fast_layout(int c, int NS, int cpad = 0) {
   FastSmem s;
   s.stage_floats = (size_t)kChunk * c;  // 128*c bytes: every stage starts 16-byte aligned
   size_t o = (size_t)NS * s.stage_floats * 4;
+  s.o_pad = o;
+  o += (size_t)kChunk * cpad * 4;
   s.o_head = o;  // int4 per valid piece: {accumulator offset, weight bits, first-pixel float offset, 0}
   o += (size_t)kChunk * 16;
   s.o_max = o;
@@ -674,10 +681,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
   // CC != 0: the class count is a compile-time constant (address steps and the
   // quad geometry fold into immediates); 0: read from the parameters
   const int c = CC ? CC : p.c, NS = p.NS;
+  // compile-time c % 4 != 0: each landed stage is repacked into a working copy with the
+  // class stride padded to a multiple of 4 (pad lanes = the fold identity), so the scan
+  // and the epilogue move 16-byte quads as for c % 4 == 0 (QV) instead of masked scalars
+  constexpr bool kPad = !VEC && TFB_FUSE_REPACK && CC != 0 && (CC % 4) != 0;
+  constexpr bool QV = VEC || kPad;
+  const int cs = kPad ? ((CC + 3) & ~3) : c;  // class stride of the working rows
   const Geo geo = geo_of(c);
-  const FastSmem L = fast_layout(c, NS);
+  const FastSmem L = fast_layout(c, NS, kPad ? cs : 0);
   unsigned char *ws = smem + (size_t)warp * L.total;
   float *stages = reinterpret_cast<float *>(ws);
+  float *padrows = reinterpret_cast<float *>(ws + L.o_pad);
   int4 *shead = reinterpret_cast<int4 *>(ws + L.o_head);
   float *smax = reinterpret_cast<float *>(ws + L.o_max);
   uint64_t *bar = reinterpret_cast<uint64_t *>(ws + L.o_bar);
@@ -763,7 +777,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
     }
     if (valid) {
       const float wv = kProd ? w * 0.693147180559945f : w;
-      shead[__popc(vmask & (upto >> 1))] = make_int4(r_cur * (int)p.stride, __float_as_int(wv), lane * c, 0);
+      shead[__popc(vmask & (upto >> 1))] = make_int4(r_cur * (int)p.stride, __float_as_int(wv), lane * cs, 0);
     }
     const int npv = __popc(vmask);
 
@@ -775,12 +789,30 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
       for (int i = done + lane; i < nfl; i += 32) st[i] = src[i];
     }
     __syncwarp();
+    float *wst = st;  // the rows the scan, the argmax and the epilogue read (stride cs)
+    if (kPad) {
+      // lane = pixel: its CC scalars at stride CC (odd CC: conflict-free), four-aligned
+      // 16-byte stores at stride cs, the pad lanes set to the fold identity
+      if (lane < npix) {
+        const float *sp = st + lane * CC;
+        float *dp = padrows + lane * cs;
+        const float one = kProd ? 1.0f : 0.0f;
+#pragma unroll
+        for (int q = 0; q < (CC + 3) / 4; ++q) {
+          const int k = 4 * q;
+          *reinterpret_cast<float4 *>(dp + k) = make_float4(
+              sp[k], k + 1 < CC ? sp[k + 1] : one, k + 2 < CC ? sp[k + 2] : one, k + 3 < CC ? sp[k + 3] : one);
+        }
+      }
+      __syncwarp();
+      wst = padrows;
+    }
 
     if (AGG == TFB_AGG_MAXSUM || p.fallback) {  // fusion.py:174, cli.py:293
       if (lane < npix) {
         float best;
         int bi;
-        pixel_argmax<VEC>(st + (size_t)lane * c, c, best, bi);
+        pixel_argmax<QV>(wst + (size_t)lane * cs, c, best, bi);
         smax[lane] = best;
         if (p.fallback) p.fallback[(int64_t)cur.f * p.hw + cur.ch * kChunk + lane] = bi;
       }
@@ -794,12 +826,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
       // ---- scan: fold each piece of this lane's group into its first pixel's slot.
       // Branch-free over the group's pixels: at a piece start the running value
       // is stored (one predicated STS.128) and reset by selects.
-      if (scan_lane && q < geo.nq && vmask != 0u) {
+      // pixels past npix (a frame's partial last chunk) hold stale stage data: not scanned
+      const int n = min(i1, npix) - i0;
+      if (scan_lane && q < geo.nq && vmask != 0u && n > 0) {
         const unsigned sm = smask >> i0;  // bit j: a piece starts at pixel i0 + j (bit 0 always set)
-        const int n = i1 - i0;
-        float *pp = st + (size_t)i0 * c + 4 * q;
+        float *pp = wst + (size_t)i0 * cs + 4 * q;
         float *ps = pp;
-        float4 v = lds4<VEC>(pp, nv, one);
+        float4 v = lds4<QV>(pp, nv, one);
         if (AGG == TFB_AGG_MAXSUM) {
           const float mx = smax[i0];
           v.x = v.x == mx ? v.x : 0.f; v.y = v.y == mx ? v.y : 0.f;
@@ -811,11 +844,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
         unsigned smr = sm >> 1;  // bit 0: does a piece start at the next pixel
 #pragma unroll 2
         for (int j = 1; j < n; ++j) {
-          pp += c;
-          v = lds4<VEC>(pp, nv, one);
+          pp += cs;
+          v = lds4<QV>(pp, nv, one);
           const bool start = smr & 1u;
           smr >>= 1;
-          if (start) sts4<VEC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
+          if (start) sts4<QV>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
           ps = start ? pp : ps;
           a01.x = start ? one : a01.x; a01.y = start ? one : a01.y;
           a23.x = start ? one : a23.x; a23.y = start ? one : a23.y;
@@ -836,20 +869,20 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
             a23 = add2(a23, make_float2(v.z, v.w));
           }
         }
-        sts4<VEC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
+        sts4<QV>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
         if (kProd && (fminf(mn01, mn23) < kMulClampF || fmaxf(mx01, mx23) > 1.0f)) {
           // rare: a value outside [1e-7, 1] in this group -> redo its pieces with
           // np.clip(p, 1e-7, 1) (fusion.py:177) from the global copy (the staged
           // first-pixel slots are already overwritten)
           const float *g4 = p.probs[cur.f] + ((size_t)cur.ch * kChunk + i0) * c + 4 * q;
-          pp = st + (size_t)i0 * c + 4 * q;
+          pp = wst + (size_t)i0 * cs + 4 * q;
           ps = pp;
           a01 = make_float2(1.f, 1.f);
           a23 = a01;
-          for (int j = 0; j < n; ++j, pp += c, g4 += c) {
+          for (int j = 0; j < n; ++j, pp += cs, g4 += c) {
             const bool start = (sm >> j) & 1u;
             if (start && j > 0) {
-              sts4<VEC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
+              sts4<QV>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
               ps = pp;
               a01 = make_float2(1.f, 1.f);
               a23 = a01;
@@ -858,13 +891,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
             a01 = mul2(a01, make_float2(clip_mul(u.x), clip_mul(u.y)));
             a23 = mul2(a23, make_float2(clip_mul(u.z), clip_mul(u.w)));
           }
-          sts4<VEC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
+          sts4<QV>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
         }
       }
       __syncwarp();
       // ---- epilogue (converged): lanes = (piece, quad), one red.v4 per pair (fusion.py:180-181)
       float *accq = reinterpret_cast<float *>(p.accum) + 4 * q;
-      const float *stq = st + 4 * q;
+      const float *stq = wst + 4 * q;
       const bool lane_ok = scan_lane && q < geo.nq;
       for (int P = g; P - g < npv; P += geo.G) {
         const bool ok = lane_ok && P < npv;
@@ -872,7 +905,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
         float4 m = make_float4(0.5f, 0.5f, 0.5f, 0.5f);  // idle lanes must not trip the near-1 vote
         if (ok) {
           h = shead[P];
-          m = lds4<VEC>(stq + h.z, nv, one);
+          m = lds4<QV>(stq + h.z, nv, one);
         }
         float b0 = m.x, b1 = m.y, b2 = m.z, b3 = m.w;
         if (kProd) {
@@ -988,16 +1021,19 @@ int launch_fuse(const FuseParams &p, cudaStream_t st) {
 
 template <int AGG, bool VEC, int CC = 0>
 int launch_fuse_fast(const FuseParams &p, cudaStream_t st, bool fix) {
+  // the padded working rows of k_fuse_fast's compile-time c % 4 != 0 repack
+  constexpr int kPadCs = (!VEC && TFB_FUSE_REPACK && CC != 0 && CC % 4 != 0) ? ((CC + 3) & ~3) : 0;
+  const size_t bytes = fast_layout(p.c, p.NS, kPadCs).total;
   if (fix) {
     static LaunchCache lcf;
-    return launch_persistent(k_fuse_fast<AGG, VEC, CC, false, true>, lcf, fast_layout(p.c, p.NS).total, p, st);
+    return launch_persistent(k_fuse_fast<AGG, VEC, CC, false, true>, lcf, bytes, p, st);
   }
   if (p.order) {
     static LaunchCache lco;
-    return launch_persistent(k_fuse_fast<AGG, VEC, CC, true>, lco, fast_layout(p.c, p.NS).total, p, st);
+    return launch_persistent(k_fuse_fast<AGG, VEC, CC, true>, lco, bytes, p, st);
   }
   static LaunchCache lc;
-  return launch_persistent(k_fuse_fast<AGG, VEC, CC>, lc, fast_layout(p.c, p.NS).total, p, st);
+  return launch_persistent(k_fuse_fast<AGG, VEC, CC>, lc, bytes, p, st);
 }
 
 // Common class counts get their own instantiation (NYU40, ScanNet 20,
@@ -1233,7 +1269,7 @@ extern "C" int tfb_fuse_ordered(const int32_t *rows, int64_t hw, int nframes, co
   const bool deep = item_order != nullptr || num_classes % 4 != 0;
   const int NS = stage <= 2048 ? 4 : (deep ? TFB_FUSE_NS : TFB_FUSE_NS_SHALLOW);
   TFB_REQUIRE(warp_layout(num_classes, NS, wide ? 8 : 4).total <= kSmemBudget &&
-                  fast_layout(num_classes, NS).total <= kSmemBudget,
+                  fast_layout(num_classes, NS, (num_classes + 3) & ~3).total <= kSmemBudget,
               TFB_ERR_CAPACITY, "tfb_fuse: %d classes exceed the shared-memory staging budget of one warp",
               num_classes);
   FuseParams p;
