@@ -13,6 +13,6 @@ timeout 300 python tools/fallback_cost.py > "$out/fallback_cost.json" 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file "$out/launches.csv" \
   python bench.py --frames 512 --steps 1 --warmup 1 --no-e2e --no-cpu --no-f64 > "$out/ncu_launch.log" 2>&1
 bash tools/ncu_red.sh "$out" > /dev/null 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_raster[^_]|k_ccsetup|k_fuse_fast" -s 3 -c 3 \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_raster[^_]|k_raster$|k_ccsetup|k_fuse_fast" -s 4 -c 4 \
   -o "$out/full" python bench.py --frames 256 --steps 1 --warmup 1 --no-e2e --no-cpu --no-f64 > "$out/ncu_full.log" 2>&1
 echo done
