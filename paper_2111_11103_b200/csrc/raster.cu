@@ -74,7 +74,7 @@ constexpr int kRasterNT = TFB_RASTER_NT;
 #define TFB_RASTER_MINB1 20  // k_raster<64> CTAs per SM the register budget must allow (48 registers)
 #endif
 #ifndef TFB_RASTER_MINB
-#define TFB_RASTER_MINB 9  // k_raster CTAs per SM the register budget must allow (56 regs, 36 warps)
+#define TFB_RASTER_MINB 12  // 128-thread tile CTAs per SM the register budget must allow (40 regs; 1 % faster than 56 on the furnished room despite spills)
 #endif
 static_assert(kTW % 8 == 0 && kTH % 4 == 0 && kTP >= 64 && kTP <= 256, "tile shape: 8x4-pixel warp blocks");
 constexpr int kCand = 8;
