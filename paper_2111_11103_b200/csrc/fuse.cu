@@ -59,6 +59,9 @@ constexpr int kWarps = TFB_FUSE_WARPS;  // warps per CTA (independent pipelines)
 #define TFB_FUSE_CSPEC 1
 #endif
 #ifndef TFB_PIECE
+#ifndef TFB_NEAR1_PACKED_C
+#define TFB_NEAR1_PACKED_C 32  // k_fuse_fast: compile-time class counts below this evaluate the near-1 series branch-free
+#endif
 #define TFB_PIECE 5  // k_fuse_fast product pieces: 5 clipped values >= 1e-7 multiply to >= 1e-35, a normal float
 #endif
 constexpr int kChunk = 32;       // pixels per work item = one per lane
@@ -633,6 +636,31 @@ __device__ __forceinline__ float log2_series(float x) {
   return t * fmaf(t, fmaf(t, fmaf(t, -k / 4.0f, k / 3.0f), -k / 2.0f), k);
 }
 
+// log2_series on two values at once (sm_100 packed f32x2 add / fma / mul): the same
+// operations in the same order per element, so each result is bit-identical to log2_series
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long ra = *reinterpret_cast<unsigned long long *>(&a);
+  unsigned long long rb = *reinterpret_cast<unsigned long long *>(&b);
+  unsigned long long rc = *reinterpret_cast<unsigned long long *>(&c);
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(ra), "l"(rb), "l"(rc));
+  return *reinterpret_cast<float2 *>(&r);
+}
+
+__device__ __forceinline__ float2 add2(float2 a, float2 b);
+__device__ __forceinline__ float2 log2_series2(float2 x) {
+  constexpr float k = 1.4426950408889634f;
+  const float2 t = add2(x, make_float2(-1.0f, -1.0f));  // x - 1, exact (Sterbenz) as in log2_series
+  float2 s = fma2(t, make_float2(-k / 4.0f, -k / 4.0f), make_float2(k / 3.0f, k / 3.0f));
+  s = fma2(t, s, make_float2(-k / 2.0f, -k / 2.0f));
+  s = fma2(t, s, make_float2(k, k));
+  unsigned long long rt = *reinterpret_cast<const unsigned long long *>(&t);
+  unsigned long long rs = *reinterpret_cast<unsigned long long *>(&s);
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(rt), "l"(rs));
+  return *reinterpret_cast<float2 *>(&r);
+}
+
 __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -676,6 +704,8 @@ __device__ __forceinline__ void sts4(float *p, float4 v, int nv) {
 template <int AGG, bool VEC, int CC, bool ORD = false, bool FIX = false>
 __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant__ FuseParams p) {
   constexpr bool kProd = AGG == TFB_AGG_MUL;
+  // compile-time c below TFB_NEAR1_PACKED_C: the near-1 log series without the warp vote
+  constexpr bool kNear1Packed = CC != 0 && CC < TFB_NEAR1_PACKED_C;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // CC != 0: the class count is a compile-time constant (address steps and the
@@ -913,8 +943,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
           b1 = lg2_approx(m.y);
           b2 = lg2_approx(m.z);
           b3 = lg2_approx(m.w);
-          const bool near1 = fmaxf(fmaxf(m.x, m.y), fmaxf(m.z, m.w)) > kNear1;
-          if (__any_sync(0xffffffffu, near1)) {
+          if (kNear1Packed) {
+            // small c and short pieces: some lane of nearly every warp holds a value above
+            // kNear1, so the series runs branch-free, two values per instruction
+            const float2 s01 = log2_series2(make_float2(m.x, m.y)), s23 = log2_series2(make_float2(m.z, m.w));
+            b0 = m.x > kNear1 ? s01.x : b0;
+            b1 = m.y > kNear1 ? s01.y : b1;
+            b2 = m.z > kNear1 ? s23.x : b2;
+            b3 = m.w > kNear1 ? s23.y : b3;
+          } else if (__any_sync(0xffffffffu, fmaxf(fmaxf(m.x, m.y), fmaxf(m.z, m.w)) > kNear1)) {
             if (m.x > kNear1) b0 = log2_series(m.x);
             if (m.y > kNear1) b1 = log2_series(m.y);
             if (m.z > kNear1) b2 = log2_series(m.z);

@@ -942,6 +942,9 @@ __device__ __forceinline__ void bin_pending(const Work &w, int f, int ntiles, in
 #ifndef TFB_CCSETUP_PER
 #define TFB_CCSETUP_PER 2  // clusters per k_ccsetup block (64 threads each; 2 measured 1 % ahead of 4 and 1)
 #endif
+#ifndef TFB_CCSETUP_EARLY
+#define TFB_CCSETUP_EARLY 0
+#endif
 constexpr int kCcsPer = TFB_CCSETUP_PER;
 __global__ void __launch_bounds__(kCcsPer * kCluster, TFB_CCSETUP_MINB * 4 / kCcsPer) k_ccsetup(
     tfb_scene sc, const double *__restrict__ cams, int W, int H, int TX, int ntiles, Work w) {
@@ -950,16 +953,36 @@ __global__ void __launch_bounds__(kCcsPer * kCluster, TFB_CCSETUP_MINB * 4 / kCc
   __shared__ Cam cam;
   __shared__ uint8_t scode[kPer][kCV];
   __shared__ double sP[kPer][3][kCV];  // camera-space positions, component-major
+  const uint32_t *cs = w.csurv + (int64_t)f * w.ncl;
+  const int lane = threadIdx.x & 31, sub = threadIdx.x / kCluster, slot = threadIdx.x % kCluster;
+#if TFB_CCSETUP_EARLY
+  // the survivor count (and, EARLY >= 2, this thread's first survivor entry, read
+  // speculatively: the list has ncl slots) is read in flight with the camera; blocks
+  // past the frame's survivors (the grid is sized for a generous fraction) leave first
+  const uint32_t nsurv = w.fcnt[4 * f];
+  uint32_t cid = 0;
+  if (TFB_CCSETUP_EARLY >= 2 && blockIdx.x * kPer + sub < (uint32_t)w.ncl) cid = __ldg(cs + blockIdx.x * kPer + sub);
+  if (blockIdx.x * kPer >= nsurv) return;
+  load_cam(cam, cams, f);
+  __syncthreads();
+#else
   load_cam(cam, cams, f);
   __syncthreads();
   const uint32_t nsurv = w.fcnt[4 * f];
-  const uint32_t *cs = w.csurv + (int64_t)f * w.ncl;
+#endif
   uint32_t *tc = w.tile_count + (int64_t)f * ntiles;
   const int64_t mc = w.rs / 2;
-  const int lane = threadIdx.x & 31, sub = threadIdx.x / kCluster, slot = threadIdx.x % kCluster;
   for (uint32_t g0 = blockIdx.x * kPer; g0 < nsurv; g0 += gridDim.x * kPer) {
     const uint32_t gi = g0 + sub;
+#if TFB_CCSETUP_EARLY >= 2
+    const tfb_cluster *cl = gi < nsurv ? sc.clusters + cid : nullptr;
+    {  // the next group's entry, in flight with this group's work
+      const uint32_t gn = gi + gridDim.x * kPer;
+      cid = gn < nsurv ? __ldg(cs + gn) : 0u;
+    }
+#else
     const tfb_cluster *cl = gi < nsurv ? sc.clusters + __ldg(cs + gi) : nullptr;
+#endif
     int4 tr = make_int4(-1, 0, 0, 0);
     uint32_t loc = 0;
     if (cl) {

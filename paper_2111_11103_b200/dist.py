@@ -84,7 +84,7 @@ def reduce_scatter_rows(tensors, group=None):
     return out, (lo, hi)
 
 
-def reduce_scatter_finalize(accum, counts, finalize_slice, group=None):
+def reduce_scatter_finalize(accum, counts, finalize_slice, group=None, exchange_single=False):
     """Exchange + finalize with the work split over ranks (fused variant).
 
     Instead of every rank receiving the whole summed accumulator, texel rows
@@ -93,10 +93,13 @@ def reduce_scatter_finalize(accum, counts, finalize_slice, group=None):
     slice (``finalize_slice(acc_slice, counts_slice) -> int32 labels``) and
     the int32 labels are all-gathered (4 B per texel instead of the 4c-byte
     rows).  Returns the (n,) int32 labels, identical on every rank.
+    ``exchange_single`` runs the collectives even in a one-rank group (tests drive
+    the NCCL calls on a single GPU with it).
     """
-    world_size = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
+    initialized = dist.is_available() and dist.is_initialized()
+    world_size = dist.get_world_size(group) if initialized else 1
     n = int(accum.shape[0])
-    if world_size == 1:
+    if world_size == 1 and not (exchange_single and initialized):
         return finalize_slice(accum, counts)
     k = (n + world_size - 1) // world_size
     (acc_mine, cnt_mine), (lo, hi) = reduce_scatter_rows([accum, counts], group)
