@@ -59,6 +59,9 @@ constexpr int kWarps = TFB_FUSE_WARPS;  // warps per CTA (independent pipelines)
 #define TFB_FUSE_CSPEC 1
 #endif
 #ifndef TFB_PIECE
+#ifndef TFB_QUAD_CSPEC
+#define TFB_QUAD_CSPEC 1  // k_fuse_fast: masked quads of a compile-time c % 4 != 0 read as 4 words + selects
+#endif
 #ifndef TFB_NEAR1_PACKED_C
 #define TFB_NEAR1_PACKED_C 32  // k_fuse_fast: compile-time class counts below this evaluate the near-1 series branch-free
 #endif
@@ -677,9 +680,22 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) {
 
 // quad access: 16-byte vectors when rows are 16-byte aligned (c % 4 == 0), else nv <= 4
 // valid scalars with `pad` (the fold identity) in the missing lanes
-template <bool VEC>
+// CC != 0 (compile-time c, c % 4 != 0): nv < 4 only on the last quad, where it is c % 4;
+// the four words are read unconditionally (past a pixel's last class they are the next
+// pixel's, or past the last stage the warp's head records: always inside the warp's shared
+// memory) and the missing classes replaced by the pad with selects
+template <bool VEC, int CC = 0>
 __device__ __forceinline__ float4 lds4(const float *p, int nv, float pad) {
   if (VEC) return *reinterpret_cast<const float4 *>(p);
+  if (CC != 0) {
+    constexpr int t = CC % 4;
+    float4 v = make_float4(p[0], p[1], p[2], p[3]);
+    const bool last = t != 0 && nv < 4;
+    if (t == 1) v.y = last ? pad : v.y;
+    if (t == 1 || t == 2) v.z = last ? pad : v.z;
+    v.w = last ? pad : v.w;
+    return v;
+  }
   return make_float4(p[0], nv > 1 ? p[1] : pad, nv > 2 ? p[2] : pad, nv > 3 ? p[3] : pad);
 }
 
@@ -689,10 +705,19 @@ __device__ __forceinline__ float4 ldg4(const float *p, int nv, float pad) {
   return make_float4(__ldg(p), nv > 1 ? __ldg(p + 1) : pad, nv > 2 ? __ldg(p + 2) : pad, nv > 3 ? __ldg(p + 3) : pad);
 }
 
-template <bool VEC>
+template <bool VEC, int CC = 0>
 __device__ __forceinline__ void sts4(float *p, float4 v, int nv) {
   if (VEC) {
     *reinterpret_cast<float4 *>(p) = v;
+    return;
+  }
+  if (CC != 0) {
+    constexpr int t = CC % 4;
+    const bool last = t != 0 && nv < 4;
+    p[0] = v.x;
+    if (t != 1 || !last) p[1] = v.y;
+    if ((t != 1 && t != 2) || !last) p[2] = v.z;
+    if (!last) p[3] = v.w;
     return;
   }
   p[0] = v.x;
@@ -706,6 +731,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
   constexpr bool kProd = AGG == TFB_AGG_MUL;
   // compile-time c below TFB_NEAR1_PACKED_C: the near-1 log series without the warp vote
   constexpr bool kNear1Packed = CC != 0 && CC < TFB_NEAR1_PACKED_C;
+#define TFB_QUAD_CC (TFB_QUAD_CSPEC ? CC : 0)
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // CC != 0: the class count is a compile-time constant (address steps and the
@@ -862,7 +888,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
         const unsigned sm = smask >> i0;  // bit j: a piece starts at pixel i0 + j (bit 0 always set)
         float *pp = wst + (size_t)i0 * cs + 4 * q;
         float *ps = pp;
-        float4 v = lds4<QV>(pp, nv, one);
+        float4 v = lds4<QV, TFB_QUAD_CC>(pp, nv, one);
         if (AGG == TFB_AGG_MAXSUM) {
           const float mx = smax[i0];
           v.x = v.x == mx ? v.x : 0.f; v.y = v.y == mx ? v.y : 0.f;
@@ -875,10 +901,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
 #pragma unroll 2
         for (int j = 1; j < n; ++j) {
           pp += cs;
-          v = lds4<QV>(pp, nv, one);
+          v = lds4<QV, TFB_QUAD_CC>(pp, nv, one);
           const bool start = smr & 1u;
           smr >>= 1;
-          if (start) sts4<QV>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
+          if (start) sts4<QV, TFB_QUAD_CC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
           ps = start ? pp : ps;
           a01.x = start ? one : a01.x; a01.y = start ? one : a01.y;
           a23.x = start ? one : a23.x; a23.y = start ? one : a23.y;
@@ -899,7 +925,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
             a23 = add2(a23, make_float2(v.z, v.w));
           }
         }
-        sts4<QV>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
+        sts4<QV, TFB_QUAD_CC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
         if (kProd && (fminf(mn01, mn23) < kMulClampF || fmaxf(mx01, mx23) > 1.0f)) {
           // rare: a value outside [1e-7, 1] in this group -> redo its pieces with
           // np.clip(p, 1e-7, 1) (fusion.py:177) from the global copy (the staged
@@ -912,7 +938,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
           for (int j = 0; j < n; ++j, pp += cs, g4 += c) {
             const bool start = (sm >> j) & 1u;
             if (start && j > 0) {
-              sts4<QV>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
+              sts4<QV, TFB_QUAD_CC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
               ps = pp;
               a01 = make_float2(1.f, 1.f);
               a23 = a01;
@@ -921,7 +947,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
             a01 = mul2(a01, make_float2(clip_mul(u.x), clip_mul(u.y)));
             a23 = mul2(a23, make_float2(clip_mul(u.z), clip_mul(u.w)));
           }
-          sts4<QV>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
+          sts4<QV, TFB_QUAD_CC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
         }
       }
       __syncwarp();
@@ -935,7 +961,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
         float4 m = make_float4(0.5f, 0.5f, 0.5f, 0.5f);  // idle lanes must not trip the near-1 vote
         if (ok) {
           h = shead[P];
-          m = lds4<QV>(stq + h.z, nv, one);
+          m = lds4<QV, TFB_QUAD_CC>(stq + h.z, nv, one);
         }
         float b0 = m.x, b1 = m.y, b2 = m.z, b3 = m.w;
         if (kProd) {
