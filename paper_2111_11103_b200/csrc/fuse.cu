@@ -59,6 +59,9 @@ constexpr int kWarps = TFB_FUSE_WARPS;  // warps per CTA (independent pipelines)
 #define TFB_FUSE_CSPEC 1
 #endif
 #ifndef TFB_PIECE
+#ifndef TFB_FUSE_FOLDBUF
+#define TFB_FUSE_FOLDBUF 1  // k_fuse_fast, compile-time c % 4 != 0: folded pieces through an aligned buffer (16-byte STS / LDS)
+#endif
 #ifndef TFB_QUAD_CSPEC
 #define TFB_QUAD_CSPEC 1  // k_fuse_fast: masked quads of a compile-time c % 4 != 0 read as 4 words + selects
 #endif
@@ -742,9 +745,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
   // and the epilogue move 16-byte quads as for c % 4 == 0 (QV) instead of masked scalars
   constexpr bool kPad = !VEC && TFB_FUSE_REPACK && CC != 0 && (CC % 4) != 0;
   constexpr bool QV = VEC || kPad;
+  // compile-time c % 4 != 0 without the repack: the scan reads the staged rows as masked
+  // scalars, but writes each finished piece's quads as 16-byte vectors into an aligned
+  // per-warp fold buffer (class stride cs4), which the epilogue reads back as vectors --
+  // half the shared-memory wavefronts of scalar words on those two passes
+  constexpr bool kFold = !VEC && !kPad && TFB_FUSE_FOLDBUF && CC != 0 && (CC % 4) != 0;
+  constexpr int cs4 = (CC + 3) & ~3;
   const int cs = kPad ? ((CC + 3) & ~3) : c;  // class stride of the working rows
   const Geo geo = geo_of(c);
-  const FastSmem L = fast_layout(c, NS, kPad ? cs : 0);
+  const FastSmem L = fast_layout(c, NS, (kPad || kFold) ? cs4 : 0);
   unsigned char *ws = smem + (size_t)warp * L.total;
   float *stages = reinterpret_cast<float *>(ws);
   float *padrows = reinterpret_cast<float *>(ws + L.o_pad);
@@ -833,7 +842,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
     }
     if (valid) {
       const float wv = kProd ? w * 0.693147180559945f : w;
-      shead[__popc(vmask & (upto >> 1))] = make_int4(r_cur * (int)p.stride, __float_as_int(wv), lane * cs, 0);
+      shead[__popc(vmask & (upto >> 1))] = make_int4(r_cur * (int)p.stride, __float_as_int(wv), lane * (kFold ? cs4 : cs), 0);
     }
     const int npv = __popc(vmask);
 
@@ -887,7 +896,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
       if (scan_lane && q < geo.nq && vmask != 0u && n > 0) {
         const unsigned sm = smask >> i0;  // bit j: a piece starts at pixel i0 + j (bit 0 always set)
         float *pp = wst + (size_t)i0 * cs + 4 * q;
-        float *ps = pp;
+        // where finished pieces go: in place over the piece's first pixel, or its fold-buffer row
+        float *pf = kFold ? padrows + (size_t)i0 * cs4 + 4 * q : pp;
+        float *ps = pf;
         float4 v = lds4<QV, TFB_QUAD_CC>(pp, nv, one);
         if (AGG == TFB_AGG_MAXSUM) {
           const float mx = smax[i0];
@@ -901,11 +912,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
 #pragma unroll 2
         for (int j = 1; j < n; ++j) {
           pp += cs;
+          if (kFold) pf += cs4;
           v = lds4<QV, TFB_QUAD_CC>(pp, nv, one);
           const bool start = smr & 1u;
           smr >>= 1;
-          if (start) sts4<QV, TFB_QUAD_CC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
-          ps = start ? pp : ps;
+          if (start) sts4<QV || kFold, TFB_QUAD_CC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
+          ps = start ? (kFold ? pf : pp) : ps;
           a01.x = start ? one : a01.x; a01.y = start ? one : a01.y;
           a23.x = start ? one : a23.x; a23.y = start ? one : a23.y;
           if (kProd) {
@@ -925,20 +937,20 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
             a23 = add2(a23, make_float2(v.z, v.w));
           }
         }
-        sts4<QV, TFB_QUAD_CC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
+        sts4<QV || kFold, TFB_QUAD_CC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
         if (kProd && (fminf(mn01, mn23) < kMulClampF || fmaxf(mx01, mx23) > 1.0f)) {
           // rare: a value outside [1e-7, 1] in this group -> redo its pieces with
           // np.clip(p, 1e-7, 1) (fusion.py:177) from the global copy (the staged
           // first-pixel slots are already overwritten)
           const float *g4 = p.probs[cur.f] + ((size_t)cur.ch * kChunk + i0) * c + 4 * q;
-          pp = wst + (size_t)i0 * cs + 4 * q;
+          pp = kFold ? padrows + (size_t)i0 * cs4 + 4 * q : wst + (size_t)i0 * cs + 4 * q;
           ps = pp;
           a01 = make_float2(1.f, 1.f);
           a23 = a01;
-          for (int j = 0; j < n; ++j, pp += cs, g4 += c) {
+          for (int j = 0; j < n; ++j, pp += (kFold ? cs4 : cs), g4 += c) {
             const bool start = (sm >> j) & 1u;
             if (start && j > 0) {
-              sts4<QV, TFB_QUAD_CC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
+              sts4<QV || kFold, TFB_QUAD_CC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
               ps = pp;
               a01 = make_float2(1.f, 1.f);
               a23 = a01;
@@ -947,13 +959,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
             a01 = mul2(a01, make_float2(clip_mul(u.x), clip_mul(u.y)));
             a23 = mul2(a23, make_float2(clip_mul(u.z), clip_mul(u.w)));
           }
-          sts4<QV, TFB_QUAD_CC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
+          sts4<QV || kFold, TFB_QUAD_CC>(ps, make_float4(a01.x, a01.y, a23.x, a23.y), nv);
         }
       }
       __syncwarp();
       // ---- epilogue (converged): lanes = (piece, quad), one red.v4 per pair (fusion.py:180-181)
       float *accq = reinterpret_cast<float *>(p.accum) + 4 * q;
-      const float *stq = wst + 4 * q;
+      const float *stq = (kFold ? padrows : wst) + 4 * q;
       const bool lane_ok = scan_lane && q < geo.nq;
       for (int P = g; P - g < npv; P += geo.G) {
         const bool ok = lane_ok && P < npv;
@@ -961,7 +973,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
         float4 m = make_float4(0.5f, 0.5f, 0.5f, 0.5f);  // idle lanes must not trip the near-1 vote
         if (ok) {
           h = shead[P];
-          m = lds4<QV, TFB_QUAD_CC>(stq + h.z, nv, one);
+          m = lds4<QV || kFold, TFB_QUAD_CC>(stq + h.z, nv, one);
         }
         float b0 = m.x, b1 = m.y, b2 = m.z, b3 = m.w;
         if (kProd) {
@@ -1085,7 +1097,7 @@ int launch_fuse(const FuseParams &p, cudaStream_t st) {
 template <int AGG, bool VEC, int CC = 0>
 int launch_fuse_fast(const FuseParams &p, cudaStream_t st, bool fix) {
   // the padded working rows of k_fuse_fast's compile-time c % 4 != 0 repack
-  constexpr int kPadCs = (!VEC && TFB_FUSE_REPACK && CC != 0 && CC % 4 != 0) ? ((CC + 3) & ~3) : 0;
+  constexpr int kPadCs = (!VEC && (TFB_FUSE_REPACK || TFB_FUSE_FOLDBUF) && CC != 0 && CC % 4 != 0) ? ((CC + 3) & ~3) : 0;
   const size_t bytes = fast_layout(p.c, p.NS, kPadCs).total;
   if (fix) {
     static LaunchCache lcf;
