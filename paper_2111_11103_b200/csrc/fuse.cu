@@ -62,6 +62,9 @@ constexpr int kWarps = TFB_FUSE_WARPS;  // warps per CTA (independent pipelines)
 #ifndef TFB_FUSE_FOLDBUF
 #define TFB_FUSE_FOLDBUF 1  // k_fuse_fast, compile-time c % 4 != 0: folded pieces through an aligned buffer (16-byte STS / LDS)
 #endif
+#ifndef TFB_FIX_TRANSPOSE
+#define TFB_FIX_TRANSPOSE 1  // k_fuse_fast fixed-point epilogue: lanes take classes qi0 + k*QW (coalesced 64-bit adds)
+#endif
 #ifndef TFB_QUAD_CSPEC
 #define TFB_QUAD_CSPEC 1  // k_fuse_fast: masked quads of a compile-time c % 4 != 0 read as 4 words + selects
 #endif
@@ -967,13 +970,27 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
       float *accq = reinterpret_cast<float *>(p.accum) + 4 * q;
       const float *stq = (kFold ? padrows : wst) + 4 * q;
       const bool lane_ok = scan_lane && q < geo.nq;
+      // fixed-point accumulator, one quad pass (c <= 128): the epilogue lane of quad slot qi0
+      // takes the piece's classes qi0 + k*QW (k < 4) instead of 4*q .. 4*q + 3, so each of its
+      // four scalar 64-bit adds has the QW lanes of a piece on consecutive words (3 sectors
+      // for c = 40, not one sector per lane); every class still lands exactly once
+      const bool kT = FIX && TFB_FIX_TRANSPOSE && geo.nq <= 32;
+      int cl[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cl[k] = qi0 + k * geo.QW;
       for (int P = g; P - g < npv; P += geo.G) {
         const bool ok = lane_ok && P < npv;
         int4 h = make_int4(0, 0, 0, 0);
         float4 m = make_float4(0.5f, 0.5f, 0.5f, 0.5f);  // idle lanes must not trip the near-1 vote
         if (ok) {
           h = shead[P];
-          m = lds4<QV || kFold, TFB_QUAD_CC>(stq + h.z, nv, one);
+          if (kT) {
+            const float *row = (kFold ? padrows : wst) + h.z;
+            m = make_float4(row[cl[0]], cl[1] < c ? row[cl[1]] : one, cl[2] < c ? row[cl[2]] : one,
+                            cl[3] < c ? row[cl[3]] : one);
+          } else {
+            m = lds4<QV || kFold, TFB_QUAD_CC>(stq + h.z, nv, one);
+          }
         }
         float b0 = m.x, b1 = m.y, b2 = m.z, b3 = m.w;
         if (kProd) {
@@ -1000,7 +1017,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
         const float2 o01 = mul2(make_float2(b0, b1), make_float2(wv, wv));
         const float2 o23 = mul2(make_float2(b2, b3), make_float2(wv, wv));
         if (ok) {
-          if (FIX) {
+          if (FIX && kT) {
+            unsigned long long *dr = reinterpret_cast<unsigned long long *>(p.accum) + h.x;
+            atomicAdd(dr + cl[0], to_fixed(o01.x));
+            if (cl[1] < c) atomicAdd(dr + cl[1], to_fixed(o01.y));
+            if (cl[2] < c) atomicAdd(dr + cl[2], to_fixed(o23.x));
+            if (cl[3] < c) atomicAdd(dr + cl[3], to_fixed(o23.y));
+          } else if (FIX) {
             // fixed-point accumulator (TFB_ACCUM_FIXED): the piece's float32 value, rounded
             // once to 2^-32 units; integer adds make the sum independent of their order
             unsigned long long *dq = reinterpret_cast<unsigned long long *>(p.accum) + h.x + 4 * q;

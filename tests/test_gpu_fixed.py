@@ -94,3 +94,31 @@ def test_fixed_accumulator_library_path_explicit_weights():
         finalize(t)
     np.testing.assert_allclose(a.rows, ref.rows, atol=1e-6)
     assert (texel_argmax(a) == texel_argmax(ref)).mean() > 0.999
+
+
+@pytest.mark.parametrize("c", [13, 19, 20, 40, 41, 132])
+@pytest.mark.parametrize("agg", ["sum", "mul"])
+def test_fixed_accumulator_class_counts(c, agg):
+    """The fixed-point epilogue's class mapping (quad slot qi0 takes classes qi0 + k*QW when
+    c <= 128, the per-quad mapping above) over the compile-time class counts (13, 19, 20,
+    40), runtime ones with and without a partial last quad (41) and two quad passes (132):
+    every class lands exactly once, equal to the float64 fold within the float32 contract,
+    and bit-identical under a different batching."""
+    import torch
+
+    from paper_2111_11103_b200 import MeshAnnotation
+
+    mesh, layout, frames, probs = _scene(n=5, c=c)
+    ref = MeshAnnotation(mesh, layout, num_classes=c, aggregator=agg, accum_dtype="float64")
+    ref.add_batch(probs, frames)
+    runs = []
+    for mb in (5, 2):
+        a = MeshAnnotation(mesh, layout, num_classes=c, aggregator=agg, accum_dtype="fixed64", max_batch=mb)
+        a.add_batch(probs, frames)
+        runs.append(a)
+    assert torch.equal(runs[0].texture._accum, runs[1].texture._accum)
+    np.testing.assert_array_equal(runs[0].texture.counts, ref.texture.counts)
+    got, want = runs[0].texture.accum, ref.texture.accum
+    assert got.shape == want.shape == (layout.total_texels, c)
+    err = np.abs(got - want) / np.maximum(np.abs(want), 1e-3)
+    assert err.max() < 1e-5, err.max()
