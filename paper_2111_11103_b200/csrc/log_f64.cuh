@@ -17,10 +17,22 @@
 
 namespace tfb_log {
 
+#ifndef TFB_LOG_SLOW_NOINLINE
+#define TFB_LOG_SLOW_NOINLINE 1
+#endif
+// the rare arguments' libdevice log, kept out of line so the call sites stay small
+// (the scatter-add inlines several log_f64 per piece; inlined, the libdevice body made
+// instruction fetch its top stall)
+#if TFB_LOG_SLOW_NOINLINE
+__device__ __noinline__ double log_slow(double x) { return log(x); }
+#else
+__device__ __forceinline__ double log_slow(double x) { return log(x); }
+#endif
+
 __device__ __forceinline__ double log_f64(double x, const double2 *__restrict__ tab) {
   const unsigned long long ix = (unsigned long long)__double_as_longlong(x);
   // positive normal and finite: 0x0010... <= ix < 0x7ff0...
-  if (ix - 0x0010000000000000ULL >= 0x7fe0000000000000ULL) return log(x);
+  if (ix - 0x0010000000000000ULL >= 0x7fe0000000000000ULL) return log_slow(x);
   const unsigned long long tmp = ix - 0x3FE6000000000000ULL;
   const int i = (int)((tmp >> 45) & 127u);
   const long long k = (long long)tmp >> 52;
