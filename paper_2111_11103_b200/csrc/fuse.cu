@@ -62,6 +62,9 @@ constexpr int kWarps = TFB_FUSE_WARPS;  // warps per CTA (independent pipelines)
 #ifndef TFB_FUSE_FOLDBUF
 #define TFB_FUSE_FOLDBUF 1  // k_fuse_fast, compile-time c % 4 != 0: folded pieces through an aligned buffer (16-byte STS / LDS)
 #endif
+#ifndef TFB_FUSE_D64
+#define TFB_FUSE_D64 1  // float64-accumulator product rule through k_fuse_fast's D64 mode (else k_fuse<double>)
+#endif
 #ifndef TFB_FIX_TRANSPOSE
 #define TFB_FIX_TRANSPOSE 1  // k_fuse_fast fixed-point epilogue: lanes take classes qi0 + k*QW (coalesced 64-bit adds)
 #endif
@@ -732,9 +735,18 @@ __device__ __forceinline__ void sts4(float *p, float4 v, int nv) {
   if (nv > 3) p[3] = v.w;
 }
 
-template <int AGG, bool VEC, int CC, bool ORD = false, bool FIX = false>
+template <int AGG, bool VEC, int CC, bool ORD = false, bool FIX = false, bool D64 = false>
 __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant__ FuseParams p) {
+  // D64: the float64 parity accumulator for the product rule (fusion.py:177 in double): no
+  // scan; converged epilogue lanes = (piece, class set) multiply the piece's clipped values
+  // in double straight from the staged rows and land w * log(prod) with float64 adds
+  static_assert(!D64 || (AGG == TFB_AGG_MUL && !FIX && !ORD), "D64: product rule, float64 accumulator");
   constexpr bool kProd = AGG == TFB_AGG_MUL;
+  __shared__ double2 s_logtab[D64 ? 128 : 1];
+  if (D64) {
+    for (int t = threadIdx.x; t < 128; t += blockDim.x) s_logtab[t] = tfb_log::kTable[t];
+    __syncthreads();
+  }
   // compile-time c below TFB_NEAR1_PACKED_C: the near-1 log series without the warp vote
   constexpr bool kNear1Packed = CC != 0 && CC < TFB_NEAR1_PACKED_C;
 #define TFB_QUAD_CC (TFB_QUAD_CSPEC ? CC : 0)
@@ -746,13 +758,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
   // compile-time c % 4 != 0: each landed stage is repacked into a working copy with the
   // class stride padded to a multiple of 4 (pad lanes = the fold identity), so the scan
   // and the epilogue move 16-byte quads as for c % 4 == 0 (QV) instead of masked scalars
-  constexpr bool kPad = !VEC && TFB_FUSE_REPACK && CC != 0 && (CC % 4) != 0;
+  constexpr bool kPad = !VEC && !D64 && TFB_FUSE_REPACK && CC != 0 && (CC % 4) != 0;
   constexpr bool QV = VEC || kPad;
   // compile-time c % 4 != 0 without the repack: the scan reads the staged rows as masked
   // scalars, but writes each finished piece's quads as 16-byte vectors into an aligned
   // per-warp fold buffer (class stride cs4), which the epilogue reads back as vectors --
   // half the shared-memory wavefronts of scalar words on those two passes
-  constexpr bool kFold = !VEC && !kPad && TFB_FUSE_FOLDBUF && CC != 0 && (CC % 4) != 0;
+  constexpr bool kFold = !VEC && !kPad && !D64 && TFB_FUSE_FOLDBUF && CC != 0 && (CC % 4) != 0;
   constexpr int cs4 = (CC + 3) & ~3;
   const int cs = kPad ? ((CC + 3) & ~3) : c;  // class stride of the working rows
   const Geo geo = geo_of(c);
@@ -828,7 +840,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
     const bool chg = lane == 0 || prev != r_cur || grp_start;
     const unsigned cmask = __ballot_sync(0xffffffffu, chg);
     bool pstart = chg;
-    if (kProd) {
+    if (kProd && !D64) {  // float64 products of <= 32 values >= 1e-7 stay normal: no cut
       const int rs = 31 - __clz(cmask & upto);
       pstart = (lane - rs) % TFB_PIECE == 0;
     }
@@ -844,8 +856,21 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
       atomicAdd(p.counts + r_cur, (uint32_t)((above ? __ffs(above) - 1 : kChunk) - lane));
     }
     if (valid) {
-      const float wv = kProd ? w * 0.693147180559945f : w;
-      shead[__popc(vmask & (upto >> 1))] = make_int4(r_cur * (int)p.stride, __float_as_int(wv), lane * (kFold ? cs4 : cs), 0);
+      if (D64) {
+        // float64 weight exactly as weight_from<double> (fusion.py:132-141); the piece's
+        // first pixel and length (up to the next piece start)
+        const double per_image = 1.0 / (double)n_cur;
+        const double w64 = p.wmode == TFB_W_IMAGES_IID ? per_image
+                           : p.wmode == TFB_W_BLEND    ? (1.0 - p.alpha) + p.alpha * per_image
+                                                       : 1.0;
+        const unsigned after = smask & ~upto;
+        const int len = (after ? __ffs(after) - 1 : kChunk) - lane;
+        shead[__popc(vmask & (upto >> 1))] =
+            make_int4(r_cur * (int)p.stride, __double2loint(w64), lane | (len << 8), __double2hiint(w64));
+      } else {
+        const float wv = kProd ? w * 0.693147180559945f : w;
+        shead[__popc(vmask & (upto >> 1))] = make_int4(r_cur * (int)p.stride, __float_as_int(wv), lane * (kFold ? cs4 : cs), 0);
+      }
     }
     const int npv = __popc(vmask);
 
@@ -896,7 +921,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
       // is stored (one predicated STS.128) and reset by selects.
       // pixels past npix (a frame's partial last chunk) hold stale stage data: not scanned
       const int n = min(i1, npix) - i0;
-      if (scan_lane && q < geo.nq && vmask != 0u && n > 0) {
+      if (!D64 && scan_lane && q < geo.nq && vmask != 0u && n > 0) {
         const unsigned sm = smask >> i0;  // bit j: a piece starts at pixel i0 + j (bit 0 always set)
         float *pp = wst + (size_t)i0 * cs + 4 * q;
         // where finished pieces go: in place over the piece's first pixel, or its fold-buffer row
@@ -978,65 +1003,90 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
       int cl[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) cl[k] = qi0 + k * geo.QW;
-      for (int P = g; P - g < npv; P += geo.G) {
-        const bool ok = lane_ok && P < npv;
-        int4 h = make_int4(0, 0, 0, 0);
-        float4 m = make_float4(0.5f, 0.5f, 0.5f, 0.5f);  // idle lanes must not trip the near-1 vote
-        if (ok) {
-          h = shead[P];
-          if (kT) {
-            const float *row = (kFold ? padrows : wst) + h.z;
-            m = make_float4(row[cl[0]], cl[1] < c ? row[cl[1]] : one, cl[2] < c ? row[cl[2]] : one,
-                            cl[3] < c ? row[cl[3]] : one);
-          } else {
-            m = lds4<QV || kFold, TFB_QUAD_CC>(stq + h.z, nv, one);
+      if (D64) {
+        // lanes = (piece, classes qi0 + k*QW): the piece's clipped values multiply in double in
+        // pixel order (as k_fuse's float64 mode), one table-driven log per piece and class
+        // (fusion.py:177), the adds coalesced over a piece's consecutive classes (c <= 128)
+        for (int P = g; P - g < npv; P += geo.G) {
+          if (lane_ok && P < npv) {
+            const int4 h = shead[P];
+            const float *row = wst + (size_t)(h.z & 0xff) * cs;
+            double d0 = 1.0, d1 = 1.0, d2 = 1.0, d3 = 1.0;
+            for (int j = h.z >> 8; j > 0; --j, row += cs) {
+              d0 *= clip_mul64(row[cl[0]]);
+              if (cl[1] < c) d1 *= clip_mul64(row[cl[1]]);
+              if (cl[2] < c) d2 *= clip_mul64(row[cl[2]]);
+              if (cl[3] < c) d3 *= clip_mul64(row[cl[3]]);
+            }
+            const double wv = __hiloint2double(h.w, h.y);
+            double *dr = reinterpret_cast<double *>(p.accum) + h.x;
+            atomicAdd(dr + cl[0], wv * tfb_log::log_f64(d0, s_logtab));
+            if (cl[1] < c) atomicAdd(dr + cl[1], wv * tfb_log::log_f64(d1, s_logtab));
+            if (cl[2] < c) atomicAdd(dr + cl[2], wv * tfb_log::log_f64(d2, s_logtab));
+            if (cl[3] < c) atomicAdd(dr + cl[3], wv * tfb_log::log_f64(d3, s_logtab));
           }
         }
-        float b0 = m.x, b1 = m.y, b2 = m.z, b3 = m.w;
-        if (kProd) {
-          b0 = lg2_approx(m.x);
-          b1 = lg2_approx(m.y);
-          b2 = lg2_approx(m.z);
-          b3 = lg2_approx(m.w);
-          if (kNear1Packed) {
-            // small c and short pieces: some lane of nearly every warp holds a value above
-            // kNear1, so the series runs branch-free, two values per instruction
-            const float2 s01 = log2_series2(make_float2(m.x, m.y)), s23 = log2_series2(make_float2(m.z, m.w));
-            b0 = m.x > kNear1 ? s01.x : b0;
-            b1 = m.y > kNear1 ? s01.y : b1;
-            b2 = m.z > kNear1 ? s23.x : b2;
-            b3 = m.w > kNear1 ? s23.y : b3;
-          } else if (__any_sync(0xffffffffu, fmaxf(fmaxf(m.x, m.y), fmaxf(m.z, m.w)) > kNear1)) {
-            if (m.x > kNear1) b0 = log2_series(m.x);
-            if (m.y > kNear1) b1 = log2_series(m.y);
-            if (m.z > kNear1) b2 = log2_series(m.z);
-            if (m.w > kNear1) b3 = log2_series(m.w);
+      } else {
+        for (int P = g; P - g < npv; P += geo.G) {
+          const bool ok = lane_ok && P < npv;
+          int4 h = make_int4(0, 0, 0, 0);
+          float4 m = make_float4(0.5f, 0.5f, 0.5f, 0.5f);  // idle lanes must not trip the near-1 vote
+          if (ok) {
+            h = shead[P];
+            if (kT) {
+              const float *row = (kFold ? padrows : wst) + h.z;
+              m = make_float4(row[cl[0]], cl[1] < c ? row[cl[1]] : one, cl[2] < c ? row[cl[2]] : one,
+                              cl[3] < c ? row[cl[3]] : one);
+            } else {
+              m = lds4<QV || kFold, TFB_QUAD_CC>(stq + h.z, nv, one);
+            }
+          }
+          float b0 = m.x, b1 = m.y, b2 = m.z, b3 = m.w;
+          if (kProd) {
+            b0 = lg2_approx(m.x);
+            b1 = lg2_approx(m.y);
+            b2 = lg2_approx(m.z);
+            b3 = lg2_approx(m.w);
+            if (kNear1Packed) {
+              // small c and short pieces: some lane of nearly every warp holds a value above
+              // kNear1, so the series runs branch-free, two values per instruction
+              const float2 s01 = log2_series2(make_float2(m.x, m.y)), s23 = log2_series2(make_float2(m.z, m.w));
+              b0 = m.x > kNear1 ? s01.x : b0;
+              b1 = m.y > kNear1 ? s01.y : b1;
+              b2 = m.z > kNear1 ? s23.x : b2;
+              b3 = m.w > kNear1 ? s23.y : b3;
+            } else if (__any_sync(0xffffffffu, fmaxf(fmaxf(m.x, m.y), fmaxf(m.z, m.w)) > kNear1)) {
+              if (m.x > kNear1) b0 = log2_series(m.x);
+              if (m.y > kNear1) b1 = log2_series(m.y);
+              if (m.z > kNear1) b2 = log2_series(m.z);
+              if (m.w > kNear1) b3 = log2_series(m.w);
+            }
+          }
+          const float wv = __int_as_float(h.y);
+          const float2 o01 = mul2(make_float2(b0, b1), make_float2(wv, wv));
+          const float2 o23 = mul2(make_float2(b2, b3), make_float2(wv, wv));
+          if (ok) {
+            if (FIX && kT) {
+              unsigned long long *dr = reinterpret_cast<unsigned long long *>(p.accum) + h.x;
+              atomicAdd(dr + cl[0], to_fixed(o01.x));
+              if (cl[1] < c) atomicAdd(dr + cl[1], to_fixed(o01.y));
+              if (cl[2] < c) atomicAdd(dr + cl[2], to_fixed(o23.x));
+              if (cl[3] < c) atomicAdd(dr + cl[3], to_fixed(o23.y));
+            } else if (FIX) {
+              // fixed-point accumulator (TFB_ACCUM_FIXED): the piece's float32 value, rounded
+              // once to 2^-32 units; integer adds make the sum independent of their order
+              unsigned long long *dq = reinterpret_cast<unsigned long long *>(p.accum) + h.x + 4 * q;
+              atomicAdd(dq, to_fixed(o01.x));
+              if (nv > 1) atomicAdd(dq + 1, to_fixed(o01.y));
+              if (nv > 2) atomicAdd(dq + 2, to_fixed(o23.x));
+              if (nv > 3) atomicAdd(dq + 3, to_fixed(o23.y));
+            } else {
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(accq + h.x), "f"(o01.x), "f"(o01.y),
+                           "f"(o23.x), "f"(o23.y));
+            }
           }
         }
-        const float wv = __int_as_float(h.y);
-        const float2 o01 = mul2(make_float2(b0, b1), make_float2(wv, wv));
-        const float2 o23 = mul2(make_float2(b2, b3), make_float2(wv, wv));
-        if (ok) {
-          if (FIX && kT) {
-            unsigned long long *dr = reinterpret_cast<unsigned long long *>(p.accum) + h.x;
-            atomicAdd(dr + cl[0], to_fixed(o01.x));
-            if (cl[1] < c) atomicAdd(dr + cl[1], to_fixed(o01.y));
-            if (cl[2] < c) atomicAdd(dr + cl[2], to_fixed(o23.x));
-            if (cl[3] < c) atomicAdd(dr + cl[3], to_fixed(o23.y));
-          } else if (FIX) {
-            // fixed-point accumulator (TFB_ACCUM_FIXED): the piece's float32 value, rounded
-            // once to 2^-32 units; integer adds make the sum independent of their order
-            unsigned long long *dq = reinterpret_cast<unsigned long long *>(p.accum) + h.x + 4 * q;
-            atomicAdd(dq, to_fixed(o01.x));
-            if (nv > 1) atomicAdd(dq + 1, to_fixed(o01.y));
-            if (nv > 2) atomicAdd(dq + 2, to_fixed(o23.x));
-            if (nv > 3) atomicAdd(dq + 3, to_fixed(o23.y));
-          } else {
-            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(accq + h.x), "f"(o01.x), "f"(o01.y),
-                         "f"(o23.x), "f"(o23.y));
-          }
-        }
-      }
+      }  // D64 / float32 and fixed-point epilogues
       __syncwarp();
     }
     // stage s is free again.  Every lane read it and wrote folded quads into it through the
@@ -1118,7 +1168,14 @@ int launch_fuse(const FuseParams &p, cudaStream_t st) {
 }
 
 template <int AGG, bool VEC, int CC = 0>
-int launch_fuse_fast(const FuseParams &p, cudaStream_t st, bool fix) {
+int launch_fuse_fast(const FuseParams &p, cudaStream_t st, bool fix, bool d64 = false) {
+  if constexpr (AGG == TFB_AGG_MUL) {
+    if (d64) {  // float64 accumulator, product rule: no scan, no padded rows
+      static LaunchCache lcd;
+      return launch_persistent(k_fuse_fast<AGG, VEC, CC, false, false, true>, lcd, fast_layout(p.c, p.NS, 0).total,
+                               p, st);
+    }
+  }
   // the padded working rows of k_fuse_fast's compile-time c % 4 != 0 repack
   constexpr int kPadCs = (!VEC && (TFB_FUSE_REPACK || TFB_FUSE_FOLDBUF) && CC != 0 && CC % 4 != 0) ? ((CC + 3) & ~3) : 0;
   const size_t bytes = fast_layout(p.c, p.NS, kPadCs).total;
@@ -1137,17 +1194,17 @@ int launch_fuse_fast(const FuseParams &p, cudaStream_t st, bool fix) {
 // Common class counts get their own instantiation (NYU40, ScanNet 20,
 // Cityscapes 19, NYU13): 3-4 % faster than the runtime-c kernel at c = 40.
 template <int AGG>
-int launch_fuse_fast_c(const FuseParams &p, bool vec, cudaStream_t st, bool fix) {
+int launch_fuse_fast_c(const FuseParams &p, bool vec, cudaStream_t st, bool fix, bool d64 = false) {
 #if TFB_FUSE_CSPEC
   switch (p.c) {
-    case 40: return launch_fuse_fast<AGG, true, 40>(p, st, fix);
-    case 20: return launch_fuse_fast<AGG, true, 20>(p, st, fix);
-    case 19: return launch_fuse_fast<AGG, false, 19>(p, st, fix);
-    case 13: return launch_fuse_fast<AGG, false, 13>(p, st, fix);
+    case 40: return launch_fuse_fast<AGG, true, 40>(p, st, fix, d64);
+    case 20: return launch_fuse_fast<AGG, true, 20>(p, st, fix, d64);
+    case 19: return launch_fuse_fast<AGG, false, 19>(p, st, fix, d64);
+    case 13: return launch_fuse_fast<AGG, false, 13>(p, st, fix, d64);
     default: break;
   }
 #endif
-  return vec ? launch_fuse_fast<AGG, true>(p, st, fix) : launch_fuse_fast<AGG, false>(p, st, fix);
+  return vec ? launch_fuse_fast<AGG, true>(p, st, fix, d64) : launch_fuse_fast<AGG, false>(p, st, fix, d64);
 }
 
 template <typename AccT, int AGG, bool FIX = false>
@@ -1405,7 +1462,12 @@ extern "C" int tfb_fuse_ordered(const int32_t *rows, int64_t hw, int nframes, co
     // float32 piece arithmetic); float64 keeps the reference's per-pixel double arithmetic
     const bool fix = accum_kind == TFB_ACCUM_FIXED;
     bool fast = (!wide || fix) && weight_mode != TFB_W_EXPLICIT && g_fuse_fast;
-    for (int i = 0; i < nf && fast; ++i) fast = ((uintptr_t)p.probs[i] & 15) == 0;
+    // float64 accumulator, product rule, count-derived weights, one class pass: k_fuse_fast's
+    // D64 mode (the reference's float64 arithmetic per piece, converged epilogue)
+    bool d64 = TFB_FUSE_D64 && accum_kind == TFB_ACCUM_F64 && aggregator == TFB_AGG_MUL &&
+               weight_mode != TFB_W_EXPLICIT && num_classes <= 128 && g_fuse_fast;
+    for (int i = 0; i < nf && (fast || d64); ++i)
+      if (((uintptr_t)p.probs[i] & 15) != 0) fast = d64 = false;
     const bool vec = num_classes % 4 == 0;
     int rc;
     if (fast) {
@@ -1420,6 +1482,8 @@ extern "C" int tfb_fuse_ordered(const int32_t *rows, int64_t hw, int nframes, co
           rc = launch_fuse_fast_c<TFB_AGG_MUL>(p, vec, st, fix);
           break;
       }
+    } else if (d64) {
+      rc = launch_fuse_fast_c<TFB_AGG_MUL>(p, vec, st, false, true);
     } else if (accum_kind == TFB_ACCUM_FIXED) {
       switch (aggregator) {
         case TFB_AGG_SUM: rc = launch_fuse_w<double, TFB_AGG_SUM, true>(p, st); break;
