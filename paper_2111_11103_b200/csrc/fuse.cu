@@ -1011,12 +1011,32 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
           if (lane_ok && P < npv) {
             const int4 h = shead[P];
             const float *row = wst + (size_t)(h.z & 0xff) * cs;
+            // np.clip(p, 1e-7, 1) is lazy, as in the float32 scan: the raw values multiply
+            // and their min / max are tracked; a piece holding a value outside [1e-7, 1]
+            // is redone with clipping (NaN is ignored by fminf / fmaxf and passes through
+            // the product exactly as through clip + log)
             double d0 = 1.0, d1 = 1.0, d2 = 1.0, d3 = 1.0;
+            float mn = 1.0f, mx = 0.0f;
+            const float pad1 = 1.0f;
             for (int j = h.z >> 8; j > 0; --j, row += cs) {
-              d0 *= clip_mul64(row[cl[0]]);
-              if (cl[1] < c) d1 *= clip_mul64(row[cl[1]]);
-              if (cl[2] < c) d2 *= clip_mul64(row[cl[2]]);
-              if (cl[3] < c) d3 *= clip_mul64(row[cl[3]]);
+              const float x0 = row[cl[0]], x1 = cl[1] < c ? row[cl[1]] : pad1, x2 = cl[2] < c ? row[cl[2]] : pad1,
+                          x3 = cl[3] < c ? row[cl[3]] : pad1;
+              d0 *= (double)x0;
+              d1 *= (double)x1;
+              d2 *= (double)x2;
+              d3 *= (double)x3;
+              mn = fminf(fminf(mn, x0), fminf(x1, fminf(x2, x3)));
+              mx = fmaxf(fmaxf(mx, x0), fmaxf(x1, fmaxf(x2, x3)));
+            }
+            if (mn < kMulClampF || mx > 1.0f) {
+              row = wst + (size_t)(h.z & 0xff) * cs;
+              d0 = d1 = d2 = d3 = 1.0;
+              for (int j = h.z >> 8; j > 0; --j, row += cs) {
+                d0 *= clip_mul64(row[cl[0]]);
+                if (cl[1] < c) d1 *= clip_mul64(row[cl[1]]);
+                if (cl[2] < c) d2 *= clip_mul64(row[cl[2]]);
+                if (cl[3] < c) d3 *= clip_mul64(row[cl[3]]);
+              }
             }
             const double wv = __hiloint2double(h.w, h.y);
             double *dr = reinterpret_cast<double *>(p.accum) + h.x;
