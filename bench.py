@@ -79,6 +79,7 @@ def _config(args, n):
             "frames_total": total, "frames_per_gpu": _frames_per_rank(args, n), "scaling": args.scaling,
             "triangles": 299568, "texels": 299568, "classes": C,
             "aggregator": AGG, "weights": WMODE, "accum": "float32", "batch": args.batch, "overlap": bool(args.overlap),
+            "split_raster": args.split_raster != 0,
             "parallelism": "frame-sharded dp%d" % n,
             "l2": "inputs larger than L2: 8-map pool per GPU (393 MB) cycled, accumulator 47.9 MB"}
 
@@ -273,7 +274,8 @@ def run_ours(args):
     probs_list = [pool[(lo + i) % POOL] for i in range(nf)]
     ann = MeshAnnotation(mesh, layout, num_classes=C, aggregator=AGG, weight_mode=WMODE, accum_dtype="float32",
                          max_batch=args.batch, device=dev, overlap=args.overlap,
-                         fuse_ctas_per_sm=args.fuse_ctas if args.fuse_ctas >= 0 else None)
+                         fuse_ctas_per_sm=args.fuse_ctas if args.fuse_ctas >= 0 else None,
+                         split_raster=None if args.split_raster < 0 else bool(args.split_raster))
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -503,6 +505,9 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--overlap", type=int, default=0)
+    ap.add_argument("--split-raster", type=int, default=-1,
+                    help="1: batch k+1's cull/setup/binning on a side stream under batch k's scatter-add "
+                         "(-1: MeshAnnotation's default, on unless TFB_SPLIT_RASTER=0)")
     ap.add_argument("--fuse-ctas", type=int, default=-1, help="cap on resident scatter-add CTAs per SM (-1: auto)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")

@@ -118,6 +118,16 @@ int tfb_rasterize(const tfb_scene *scene, const double *cams, int nframes, int w
                   uint32_t *texel_hits, int32_t *tri_out, int32_t *texel_out, double *depth_out,
                   double *u_out, double *v_out, void *stream);
 
+/* tfb_rasterize in two stream-ordered phases (phases = 1, 2 or 3 = both):
+ * 1 = cull, record setup and tile binning into the workspace; 2 = the tile
+ * kernels that read it and write the outputs.  Both calls take the same
+ * arguments; between them the workspace must not be reused.  Lets a caller
+ * run batch k+1's phase 1 on a second stream under batch k's scatter-add. */
+int tfb_rasterize_phases(const tfb_scene *scene, const double *cams, int nframes, int width, int height,
+                         void *workspace, size_t workspace_bytes, int64_t pair_capacity, int32_t *rows_out,
+                         uint32_t *texel_hits, int32_t *tri_out, int32_t *texel_out, double *depth_out,
+                         double *u_out, double *v_out, int phases, void *stream);
+
 /* rows = offsets[tri] + texel for host-built IdImages (fusion.py:167);
  * -1 where tri == -1.  Out-of-range ids set *bad_flag (device int) to 1. */
 int tfb_rows_from_ids(const int32_t *tri, const int32_t *texel, int64_t npix, const tfb_scene *scene,

@@ -40,6 +40,7 @@ _SIGNATURES = {
     "tfb_set_option": ([_I, _I], _I),
     "tfb_raster_workspace_bytes": ([_I64, _I64, _I, _I, _I, _I64], _SZ),
     "tfb_rasterize": ([_P, _P, _I, _I, _I, _P, _SZ, _I64, _P, _P, _P, _P, _P, _P, _P, _P], _I),
+    "tfb_rasterize_phases": ([_P, _P, _I, _I, _I, _P, _SZ, _I64, _P, _P, _P, _P, _P, _P, _P, _I, _P], _I),
     "tfb_rows_from_ids": ([_P, _P, _I64, _P, _P, _P, _P], _I),
     "tfb_count_hits": ([_P, _I64, _I, _I64, _P, _P], _I),
     "tfb_clear_hits": ([_P, _I64, _I, _I64, _P, _P], _I),

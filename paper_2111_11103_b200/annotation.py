@@ -28,6 +28,7 @@ It is a thin layer over the same ProbabilityTexture the reference-compatible
 functions use (fusion.py / session.py), so textures and results interchange.
 """
 
+import os
 import weakref
 
 import numpy as np
@@ -242,7 +243,7 @@ class MeshAnnotation:
 
     def __init__(self, mesh, layout=None, num_classes=None, aggregator="mul", weight_mode="images_iid",
                  accum_dtype="float32", max_batch=None, device=None, memory_budget=None, overlap=False,
-                 fuse_ctas_per_sm=None, texture=None, order_items=None):
+                 fuse_ctas_per_sm=None, texture=None, order_items=None, split_raster=None):
         if texture is None and num_classes is None:
             raise ValueError("num_classes is required")
         self.mesh = mesh
@@ -280,6 +281,15 @@ class MeshAnnotation:
         self.overlap = bool(overlap)
         self._side = torch.cuda.Stream(self.device) if self.overlap else None
         self._free = [None, None]
+        # Split mode: the rasterizer's first phase (cull, record setup, tile binning: latency
+        # bound, little issue) of batch k+1 runs on a side stream under batch k's scatter-add
+        # (bandwidth bound); its second phase (the tile kernels) stays in stream order.  One
+        # workspace and one row / hit image suffice (tfb_rasterize_phases).
+        if split_raster is None:  # default on (measured +1.5 % at cfg2); TFB_SPLIT_RASTER=0 turns it off
+            split_raster = os.environ.get("TFB_SPLIT_RASTER", "1") != "0"
+        self.split_raster = bool(split_raster) and not self.overlap
+        self._split_side = (torch.cuda.Stream(self.device, priority=int(os.environ.get("TFB_SPLIT_PRIO", "0")))
+                            if self.split_raster else None)
         if fuse_ctas_per_sm is None:
             fuse_ctas_per_sm = 2 if self.overlap else 0
         N.call("tfb_set_option", 1, int(fuse_ctas_per_sm))
@@ -469,6 +479,13 @@ class MeshAnnotation:
         if self.overlap:
             side.wait_stream(cur)  # cameras and anything queued before this call
             cams_all.record_stream(side)
+        split = self.split_raster and B > mb
+        if split:
+            sside = self._split_side
+            sside.wait_stream(cur)
+            cams_all.record_stream(sside)
+            self.scene.workspace(W, H, mb)  # sized once: never regrown while the side stream uses it
+            setup_done = None
         for i, b0 in enumerate(range(0, B, mb)):
             b = min(mb, B - b0)
             slot = i % nslots
@@ -480,7 +497,16 @@ class MeshAnnotation:
                 side.wait_event(self._free[slot])  # the scatter that last read this slot is done
             prof = self.profile
             r0 = self._event(side) if prof is not None else None
-            self.scene.rasterize(cams_all[b0:b0 + b], W, H, rows, hits=hits, stream=side)
+            if split:
+                if setup_done is None:
+                    self.scene.rasterize(cams_all[b0:b0 + b], W, H, rows, hits=hits, stream=cur, phases=1)
+                else:
+                    cur.wait_event(setup_done)
+                self.scene.rasterize(cams_all[b0:b0 + b], W, H, rows, hits=hits, stream=cur, phases=2)
+                drawn = torch.cuda.Event()
+                drawn.record(cur)  # this batch's tile kernels are done with the workspace
+            else:
+                self.scene.rasterize(cams_all[b0:b0 + b], W, H, rows, hits=hits, stream=side)
             r1 = self._event(side) if prof is not None else None
             if self.overlap:
                 ev = torch.cuda.Event()
@@ -496,6 +522,15 @@ class MeshAnnotation:
                    tex.total_texels, N.AGG_IDS[tex.aggregator], N.WMODE_IDS[self.weight_mode],
                    float(self.alpha or 0.0), N.ptr(tex._accum), tex.accum_kind, tex.stride, N.ptr(tex._counts),
                    N.ptr(fb), N.ptr(order), N.ptr(n_order), N.stream_handle(cur))
+            if split and b0 + mb < B:
+                # the next batch's first phase under this batch's scatter-add, enqueued after it
+                # so the scatter-add's persistent CTAs are placed first
+                nb0, nb = b0 + mb, min(mb, B - b0 - mb)
+                sside.wait_event(drawn)
+                with torch.cuda.stream(sside):
+                    self.scene.rasterize(cams_all[nb0:nb0 + nb], W, H, rows[:nb], stream=sside, phases=1)
+                setup_done = torch.cuda.Event()
+                setup_done.record(sside)
             if prof is not None:
                 prof.append((b, r0, r1, f0, self._event(cur)))
             if sslot is not None:

@@ -1843,10 +1843,11 @@ extern "C" size_t tfb_raster_workspace_bytes(int64_t num_vertices, int64_t num_t
   return need;
 }
 
-extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nframes, int width, int height,
-                             void *workspace, size_t workspace_bytes, int64_t pair_capacity, int32_t *rows_out,
-                             uint32_t *texel_hits, int32_t *tri_out, int32_t *texel_out, double *depth_out,
-                             double *u_out, double *v_out, void *stream) {
+extern "C" int tfb_rasterize_phases(const tfb_scene *scene, const double *cams, int nframes, int width, int height,
+                                    void *workspace, size_t workspace_bytes, int64_t pair_capacity, int32_t *rows_out,
+                                    uint32_t *texel_hits, int32_t *tri_out, int32_t *texel_out, double *depth_out,
+                                    double *u_out, double *v_out, int phases, void *stream) {
+  TFB_REQUIRE(phases >= 1 && phases <= 3, TFB_ERR_VALUE, "tfb_rasterize: phases %d outside 1..3", phases);
   TFB_REQUIRE(scene && cams && rows_out, TFB_ERR_DATA, "tfb_rasterize: null scene, cameras or output");
   TFB_REQUIRE(width > 0 && height > 0 && width < 32768 && height < 32768, TFB_ERR_DATA,
               "tfb_rasterize: image size %dx%d outside 1..32767", width, height);
@@ -1871,13 +1872,14 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
     set_error("tfb_rasterize: workspace of %zu bytes is smaller than the %zu required", workspace_bytes, need);
     return TFB_ERR_CAPACITY;
   }
-  cudaMemsetAsync(w.fcnt, 0, sizeof(uint32_t) * 4 * (nframes + 1), st);
-  cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ntiles * nframes, st);
   tfb_scene sc = *scene;
   const bool clustered = sc.num_clusters > 0 && sc.clusters;
   TFB_REQUIRE(!clustered || sc.num_clusters <= w.ncl, TFB_ERR_DATA,
               "tfb_rasterize: %lld clusters for %lld triangles (at most %lld accepted)", (long long)sc.num_clusters,
               (long long)m, (long long)w.ncl);
+  if (phases & 1) {  // phase 1: cull, record setup, tile binning (workspace only)
+  cudaMemsetAsync(w.fcnt, 0, sizeof(uint32_t) * 4 * (nframes + 1), st);
+  cudaMemsetAsync(w.tile_count, 0, sizeof(uint32_t) * ntiles * nframes, st);
   if (m > 0 && clustered) {
     dim3 g0((unsigned)((sc.num_clusters + kThreads - 1) / kThreads), nframes);
     k_ccull<<<g0, kThreads, 0, st>>>(sc, cams, width, height, w);
@@ -1903,6 +1905,9 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
     dim3 g2((unsigned)(sb < 1 ? 1 : sb), nframes);
     k_setup<<<g2, kThreads, 0, st>>>(sc, cams, width, height, TX, ntiles, w);
   }
+  }
+  if (!(phases & 2)) return check_launch("tfb_rasterize");
+  // phase 2: the tile kernels over the binned records (reads the workspace phase 1 wrote)
   Outs o{rows_out, texel_hits, tri_out, texel_out, depth_out, u_out, v_out};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -1938,6 +1943,14 @@ extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nfr
                                                                                     ntiles, w, o);
   k_raster_big<<<sms * (256 / kTP), kTP, 0, st>>>(sc, cams, width, height, TX, ntiles, w, o);
   return check_launch("tfb_rasterize");
+}
+
+extern "C" int tfb_rasterize(const tfb_scene *scene, const double *cams, int nframes, int width, int height,
+                             void *workspace, size_t workspace_bytes, int64_t pair_capacity, int32_t *rows_out,
+                             uint32_t *texel_hits, int32_t *tri_out, int32_t *texel_out, double *depth_out,
+                             double *u_out, double *v_out, void *stream) {
+  return tfb_rasterize_phases(scene, cams, nframes, width, height, workspace, workspace_bytes, pair_capacity,
+                              rows_out, texel_hits, tri_out, texel_out, depth_out, u_out, v_out, 3, stream);
 }
 
 #ifdef TFB_RASTER_STATS

@@ -187,8 +187,10 @@ class DeviceScene:
 
     # -- launches --------------------------------------------------------------
     def rasterize(self, cams, width, height, rows, hits=None, tri=None, texel=None, depth=None, u=None, v=None,
-                  stream=None):
-        """cams: (B, 16) float64 device tensor; rows: (B, H*W) int32 device tensor."""
+                  stream=None, phases=3):
+        """cams: (B, 16) float64 device tensor; rows: (B, H*W) int32 device tensor.
+        phases: 1 = cull + setup + binning, 2 = the tile kernels, 3 = both
+        (tfb_rasterize_phases; the two halves of one batch take the same arguments)."""
         B = int(cams.shape[0])
         if B == 0:
             return
@@ -198,9 +200,9 @@ class DeviceScene:
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
         with torch.cuda.device(self.device):  # launches go to this scene's GPU, whatever is current
-            N.call("tfb_rasterize", self.sref, N.ptr(cams), B, int(width), int(height), N.ptr(ws), ws.numel(), 0,
-                   N.ptr(rows), N.ptr(hits), N.ptr(tri), N.ptr(texel), N.ptr(depth), N.ptr(u), N.ptr(v),
-                   N.stream_handle(stream))
+            N.call("tfb_rasterize_phases", self.sref, N.ptr(cams), B, int(width), int(height), N.ptr(ws),
+                   ws.numel(), 0, N.ptr(rows), N.ptr(hits), N.ptr(tri), N.ptr(texel), N.ptr(depth), N.ptr(u),
+                   N.ptr(v), int(phases), N.stream_handle(stream))
 
     def cams_tensor(self, frames):
         arr = np.stack([pack_camera(f) for f in frames]) if frames else np.zeros((0, 16))
