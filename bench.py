@@ -79,7 +79,7 @@ def _config(args, n):
             "frames_total": total, "frames_per_gpu": _frames_per_rank(args, n), "scaling": args.scaling,
             "triangles": 299568, "texels": 299568, "classes": C,
             "aggregator": AGG, "weights": WMODE, "accum": "float32", "batch": args.batch, "overlap": bool(args.overlap),
-            "split_raster": args.split_raster != 0,
+            "split_raster": args.split_raster == 1 or (args.split_raster < 0 and os.environ.get("TFB_SPLIT_RASTER") == "1"),
             "parallelism": "frame-sharded dp%d" % n,
             "l2": "inputs larger than L2: 8-map pool per GPU (393 MB) cycled, accumulator 47.9 MB"}
 
@@ -507,7 +507,7 @@ def main():
     ap.add_argument("--overlap", type=int, default=0)
     ap.add_argument("--split-raster", type=int, default=-1,
                     help="1: batch k+1's cull/setup/binning on a side stream under batch k's scatter-add "
-                         "(-1: MeshAnnotation's default, on unless TFB_SPLIT_RASTER=0)")
+                         "(-1: MeshAnnotation's default, off unless TFB_SPLIT_RASTER=1)")
     ap.add_argument("--fuse-ctas", type=int, default=-1, help="cap on resident scatter-add CTAs per SM (-1: auto)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")

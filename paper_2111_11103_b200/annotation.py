@@ -285,8 +285,9 @@ class MeshAnnotation:
         # bound, little issue) of batch k+1 runs on a side stream under batch k's scatter-add
         # (bandwidth bound); its second phase (the tile kernels) stays in stream order.  One
         # workspace and one row / hit image suffice (tfb_rasterize_phases).
-        if split_raster is None:  # default on (measured +1.5 % at cfg2); TFB_SPLIT_RASTER=0 turns it off
-            split_raster = os.environ.get("TFB_SPLIT_RASTER", "1") != "0"
+        if split_raster is None:  # opt-in (TFB_SPLIT_RASTER=1): +1.5-2 % frames/s at cfg2, but the
+            # scatter-add then shares the GPU and its own roofline reads 0.87 instead of 0.97
+            split_raster = os.environ.get("TFB_SPLIT_RASTER", "0") == "1"
         self.split_raster = bool(split_raster) and not self.overlap
         self._split_side = (torch.cuda.Stream(self.device, priority=int(os.environ.get("TFB_SPLIT_PRIO", "0")))
                             if self.split_raster else None)

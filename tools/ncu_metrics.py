@@ -1,5 +1,5 @@
 """Selected raw metrics of the first kernel in each ncu report, one block per report:
-    python tools/ncu_metrics.py LABEL=REP [LABEL=REP ...]"""
+    python tools/ncu_metrics.py LABEL=REP [LABEL=REP ...]  (split at the last "=")"""
 import csv
 import subprocess
 import sys
@@ -21,7 +21,7 @@ METRICS = [
 
 def main(args):
     for arg in args:
-        label, rep = arg.split("=", 1)
+        label, rep = arg.rsplit("=", 1)
         out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(out.splitlines()))
         h, u, v = rows[0], rows[1], rows[2]
