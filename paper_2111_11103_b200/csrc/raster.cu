@@ -942,6 +942,9 @@ __device__ __forceinline__ void bin_pending(const Work &w, int f, int ntiles, in
 #ifndef TFB_CCSETUP_PER
 #define TFB_CCSETUP_PER 2  // clusters per k_ccsetup block (64 threads each; 2 measured 1 % ahead of 4 and 1)
 #endif
+#ifndef TFB_CCSETUP_GRID_DIV
+#define TFB_CCSETUP_GRID_DIV 16  // k_ccsetup grid: one pass of blocks covers 1 / DIV of the clusters (8: raster +1-2 %)
+#endif
 #ifndef TFB_CCSETUP_EARLY
 #define TFB_CCSETUP_EARLY 0
 #endif
@@ -1883,10 +1886,10 @@ extern "C" int tfb_rasterize_phases(const tfb_scene *scene, const double *cams, 
   if (m > 0 && clustered) {
     dim3 g0((unsigned)((sc.num_clusters + kThreads - 1) / kThreads), nframes);
     k_ccull<<<g0, kThreads, 0, st>>>(sc, cams, width, height, w);
-    // one pass of blocks covers 1/8 of the clusters (a typical view keeps ~1/10);
+    // one pass of blocks covers 1/16 of the clusters (a typical view keeps ~1/10);
     // more survivors are strided over
     const int per = TFB_FUSED_SETUP ? kCcsPer : kThreads / kCluster;  // clusters per block
-    const int64_t gb = (sc.num_clusters + 8 * per - 1) / (8 * per);
+    const int64_t gb = (sc.num_clusters + TFB_CCSETUP_GRID_DIV * per - 1) / (TFB_CCSETUP_GRID_DIV * per);
     dim3 g1((unsigned)(gb < 1 ? 1 : gb), nframes);
     if (TFB_FUSED_SETUP)
       k_ccsetup<<<g1, kCcsPer * kCluster, 0, st>>>(sc, cams, width, height, TX, ntiles, w);
