@@ -210,7 +210,7 @@ def _run64(rows, probs, n_x, agg, wm, alpha, weights=None):
     return acc.cpu().numpy(), cnt.cpu().numpy()
 
 
-@pytest.mark.parametrize("c", [5, 19, 40])
+@pytest.mark.parametrize("c", [5, 13, 19, 40, 41, 132])
 def test_float64_accumulator_log_within_1e12(c):
     """The float64 accumulator's per-piece log and float-domain clip (fuse.cu clip_mul64)
     against NumPy's log(clip(p, 1e-7, 1)) (fusion.py:177): 1e-12 relative, with values at and
@@ -224,7 +224,7 @@ def test_float64_accumulator_log_within_1e12(c):
     flat[rng.choice(flat.size, size=flat.size // 40, replace=False)] = np.float32(1e-7)
     flat[rng.choice(flat.size, size=flat.size // 40, replace=False)] = np.float32(0.99999994)
     flat[rng.choice(flat.size, size=flat.size // 40, replace=False)] = np.nextafter(np.float32(1e-7), np.float32(0))
-    for wm, alpha in (("images_iid", 0.0), ("blend", 0.25)):
+    for wm, alpha in (("images_iid", 0.0), ("blend", 0.25), ("pixels_iid", 0.0)):
         got, cnt = _run64(rows, probs, n_x, "mul", wm, alpha)
         ref, cref = _oracle(rows, probs, n_x, "mul", wm, alpha)
         np.testing.assert_array_equal(cnt, cref)
@@ -237,6 +237,27 @@ def test_float64_accumulator_log_within_1e12(c):
         O.accumulate_frame(ref, cref, np.arange(n_x, dtype=np.int64), rows[f], np.zeros_like(rows[f]), probs[f],
                            w[f], "mul")
     np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("c", [13, 40, 41])
+def test_float64_accumulator_long_runs(c):
+    """The float64 product rule (k_fuse_fast D64 mode: no 5-pixel cut, a piece runs to the next
+    row change or pixel-group start) over runs of 20-70 pixels crossing chunk boundaries, values
+    near the clip floor and near 1 (products of up to 32 values in double), and a partial last
+    chunk: 1e-12 relative to NumPy's per-pixel log."""
+    rng = np.random.default_rng(1300 + c)
+    hw, n_x = 32 * 30 + 7, 40
+    runs = np.repeat(np.arange(n_x, dtype=np.int32), 25)[:hw]
+    rows = np.stack([runs, runs[::-1].copy()])
+    rows[:, 100:130] = -1
+    probs = _probs(rng, 2, hw, c, special=False)
+    probs[0, :, 0] = np.float32(1.5e-7)
+    probs[1, ::3, 1] = np.float32(0.999999)
+    for wm, alpha in (("images_iid", 0.0), ("blend", 0.4)):
+        got, cnt = _run64(rows, probs, n_x, "mul", wm, alpha)
+        ref, cref = _oracle(rows, probs, n_x, "mul", wm, alpha)
+        np.testing.assert_array_equal(cnt, cref)
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
 
 
 @pytest.mark.parametrize("c", [7, 19, 40, 41])
