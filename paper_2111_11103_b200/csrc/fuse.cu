@@ -62,6 +62,9 @@ constexpr int kWarps = TFB_FUSE_WARPS;  // warps per CTA (independent pipelines)
 #ifndef TFB_FUSE_FOLDBUF
 #define TFB_FUSE_FOLDBUF 1  // k_fuse_fast, compile-time c % 4 != 0: folded pieces through an aligned buffer (16-byte STS / LDS)
 #endif
+#ifndef TFB_ARGMAX_FAST
+#define TFB_ARGMAX_FAST 1  // network argmax / pixel max: strict-greater pass, exact NaN pass only when needed
+#endif
 #ifndef TFB_FUSE_D64
 #define TFB_FUSE_D64 1  // float64-accumulator product rule through k_fuse_fast's D64 mode (else k_fuse<double>)
 #endif
@@ -308,8 +311,26 @@ __device__ __forceinline__ unsigned long long to_fixed(double x) {
 // words apart: with c % 4 == 0 the classes move as 16-byte quads (the 4c-byte pixel
 // stride puts the quads of 8 lanes on at most 2-way conflicting banks, where scalar
 // reads at a stride of 40 words would be 8-way); an odd c is conflict-free as scalars.
+__device__ __forceinline__ float2 add2(float2 a, float2 b);
 template <bool VEC>
 __device__ __forceinline__ void pixel_argmax(const float *pp, int c, float &best, int &bi) {
+  if (VEC && TFB_ARGMAX_FAST) {
+    // one strict-greater pass (the first maximum wins) with a float32x2 running sum that
+    // turns NaN if any class is NaN (or for inf - inf); only then the exact pass below
+    best = pp[0];
+    bi = 0;
+    float2 sum = make_float2(0.f, 0.f);
+    for (int k = 0; k < c; k += 4) {
+      const float4 v = *reinterpret_cast<const float4 *>(pp + k);
+      sum = add2(sum, make_float2(v.x, v.y));
+      sum = add2(sum, make_float2(v.z, v.w));
+      if (v.x > best) { best = v.x; bi = k; }
+      if (v.y > best) { best = v.y; bi = k + 1; }
+      if (v.z > best) { best = v.z; bi = k + 2; }
+      if (v.w > best) { best = v.w; bi = k + 3; }
+    }
+    if (!isnan(sum.x + sum.y)) return;
+  }
   best = pp[0];
   bi = 0;
   auto take = [&](float v, int k) {
