@@ -187,6 +187,25 @@ def test_fused_argmax_ties_and_nan(fast, c):
         _check(got, ref, _scale(rows, probs, n_x, agg, "pixels_iid", 0.0))
 
 
+@pytest.mark.parametrize("c", [8, 40])
+def test_fused_argmax_infinities(c):
+    """The strict-greater argmax pass with its NaN-detecting running sum: +inf / -inf classes
+    (inf is a maximum, -inf never; +inf and -inf in one pixel make the sum NaN and take the
+    exact pass), NaN, and all-equal pixels -- NumPy's argmax either way."""
+    rng = np.random.default_rng(31 + c)
+    nframes, hw, n_x = 1, 32 * 12 + 5, 20
+    rows = _rows(rng, nframes, hw, n_x)
+    probs = rng.random((nframes, hw, c)).astype(np.float32)
+    flat = probs.reshape(-1)
+    flat[rng.choice(flat.size, size=flat.size // 30, replace=False)] = np.inf
+    flat[rng.choice(flat.size, size=flat.size // 30, replace=False)] = -np.inf
+    flat[rng.choice(flat.size, size=flat.size // 200, replace=False)] = np.nan
+    probs[0, :7] = 0.5  # all-equal pixels: index 0
+    for fast in (True, False):
+        _, _, fb = _run(rows, probs, n_x, "sum", "pixels_iid", 0.0, fast)
+        np.testing.assert_array_equal(fb, probs.argmax(axis=2))
+
+
 def _run64(rows, probs, n_x, agg, wm, alpha, weights=None):
     """tfb_fuse into a float64 accumulator (the reference's precision, fusion.py:145-183)."""
     lib = N.load()
