@@ -360,9 +360,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse(const __grid_constant__ Fu
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // the float64 log's reduction table, per CTA in shared memory (lanes index it divergently)
-  __shared__ double2 s_logtab[sizeof(AccT) == 8 && TFB_LOG_F64 ? 128 : 1];
+  __shared__ double2 s_logtab[sizeof(AccT) == 8 && TFB_LOG_F64 ? (1 << tfb_log::kLogBits) : 1];
   if (sizeof(AccT) == 8 && TFB_LOG_F64) {
-    for (int t = threadIdx.x; t < 128; t += blockDim.x) s_logtab[t] = tfb_log::kTable[t];
+    for (int t = threadIdx.x; t < (1 << tfb_log::kLogBits); t += blockDim.x) s_logtab[t] = tfb_log::kTable[t];
     __syncthreads();
   }
   auto log64 = [&](double x) -> double { return TFB_LOG_F64 ? tfb_log::log_f64(x, s_logtab) : log(x); };
@@ -763,9 +763,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
   // in double straight from the staged rows and land w * log(prod) with float64 adds
   static_assert(!D64 || (AGG == TFB_AGG_MUL && !FIX && !ORD), "D64: product rule, float64 accumulator");
   constexpr bool kProd = AGG == TFB_AGG_MUL;
-  __shared__ double2 s_logtab[D64 ? 128 : 1];
+  __shared__ double2 s_logtab[D64 ? (1 << tfb_log::kLogBits) : 1];
   if (D64) {
-    for (int t = threadIdx.x; t < 128; t += blockDim.x) s_logtab[t] = tfb_log::kTable[t];
+    for (int t = threadIdx.x; t < (1 << tfb_log::kLogBits); t += blockDim.x) s_logtab[t] = tfb_log::kTable[t];
     __syncthreads();
   }
   // compile-time c below TFB_NEAR1_PACKED_C: the near-1 log series without the warp vote
@@ -1604,8 +1604,8 @@ extern "C" int tfb_pixel_weights(const int32_t *rows, int64_t hw, int nframes, c
 namespace tfb {
 namespace {
 __global__ void k_test_log_f64(const double *x, double *y, int64_t n) {
-  __shared__ double2 tab[128];
-  for (int t = threadIdx.x; t < 128; t += blockDim.x) tab[t] = tfb_log::kTable[t];
+  __shared__ double2 tab[1 << tfb_log::kLogBits];
+  for (int t = threadIdx.x; t < (1 << tfb_log::kLogBits); t += blockDim.x) tab[t] = tfb_log::kTable[t];
   __syncthreads();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = tfb_log::log_f64(x[i], tab);
