@@ -1024,6 +1024,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
       int cl[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) cl[k] = qi0 + k * geo.QW;
+      // with c % 4 == 0 (VEC) and one quad pass, QW = c / 4: all four classes exist
+      auto has = [&](int k) { return VEC || cl[k] < c; };
       if (D64) {
         // lanes = (piece, classes qi0 + k*QW): the piece's clipped values multiply in double in
         // pixel order (as k_fuse's float64 mode), one table-driven log per piece and class
@@ -1040,8 +1042,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
             float mn = 1.0f, mx = 0.0f;
             const float pad1 = 1.0f;
             for (int j = h.z >> 8; j > 0; --j, row += cs) {
-              const float x0 = row[cl[0]], x1 = cl[1] < c ? row[cl[1]] : pad1, x2 = cl[2] < c ? row[cl[2]] : pad1,
-                          x3 = cl[3] < c ? row[cl[3]] : pad1;
+              const float x0 = row[cl[0]], x1 = has(1) ? row[cl[1]] : pad1, x2 = has(2) ? row[cl[2]] : pad1,
+                          x3 = has(3) ? row[cl[3]] : pad1;
               d0 *= (double)x0;
               d1 *= (double)x1;
               d2 *= (double)x2;
@@ -1054,17 +1056,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
               d0 = d1 = d2 = d3 = 1.0;
               for (int j = h.z >> 8; j > 0; --j, row += cs) {
                 d0 *= clip_mul64(row[cl[0]]);
-                if (cl[1] < c) d1 *= clip_mul64(row[cl[1]]);
-                if (cl[2] < c) d2 *= clip_mul64(row[cl[2]]);
-                if (cl[3] < c) d3 *= clip_mul64(row[cl[3]]);
+                if (has(1)) d1 *= clip_mul64(row[cl[1]]);
+                if (has(2)) d2 *= clip_mul64(row[cl[2]]);
+                if (has(3)) d3 *= clip_mul64(row[cl[3]]);
               }
             }
             const double wv = __hiloint2double(h.w, h.y);
             double *dr = reinterpret_cast<double *>(p.accum) + h.x;
             atomicAdd(dr + cl[0], wv * tfb_log::log_f64(d0, s_logtab));
-            if (cl[1] < c) atomicAdd(dr + cl[1], wv * tfb_log::log_f64(d1, s_logtab));
-            if (cl[2] < c) atomicAdd(dr + cl[2], wv * tfb_log::log_f64(d2, s_logtab));
-            if (cl[3] < c) atomicAdd(dr + cl[3], wv * tfb_log::log_f64(d3, s_logtab));
+            if (has(1)) atomicAdd(dr + cl[1], wv * tfb_log::log_f64(d1, s_logtab));
+            if (has(2)) atomicAdd(dr + cl[2], wv * tfb_log::log_f64(d2, s_logtab));
+            if (has(3)) atomicAdd(dr + cl[3], wv * tfb_log::log_f64(d3, s_logtab));
           }
         }
       } else {
@@ -1076,8 +1078,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
             h = shead[P];
             if (kT) {
               const float *row = (kFold ? padrows : wst) + h.z;
-              m = make_float4(row[cl[0]], cl[1] < c ? row[cl[1]] : one, cl[2] < c ? row[cl[2]] : one,
-                              cl[3] < c ? row[cl[3]] : one);
+              m = make_float4(row[cl[0]], has(1) ? row[cl[1]] : one, has(2) ? row[cl[2]] : one,
+                              has(3) ? row[cl[3]] : one);
             } else {
               m = lds4<QV || kFold, TFB_QUAD_CC>(stq + h.z, nv, one);
             }
@@ -1110,9 +1112,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
             if (FIX && kT) {
               unsigned long long *dr = reinterpret_cast<unsigned long long *>(p.accum) + h.x;
               atomicAdd(dr + cl[0], to_fixed(o01.x));
-              if (cl[1] < c) atomicAdd(dr + cl[1], to_fixed(o01.y));
-              if (cl[2] < c) atomicAdd(dr + cl[2], to_fixed(o23.x));
-              if (cl[3] < c) atomicAdd(dr + cl[3], to_fixed(o23.y));
+              if (has(1)) atomicAdd(dr + cl[1], to_fixed(o01.y));
+              if (has(2)) atomicAdd(dr + cl[2], to_fixed(o23.x));
+              if (has(3)) atomicAdd(dr + cl[3], to_fixed(o23.y));
             } else if (FIX) {
               // fixed-point accumulator (TFB_ACCUM_FIXED): the piece's float32 value, rounded
               // once to 2^-32 units; integer adds make the sum independent of their order
