@@ -66,7 +66,7 @@ constexpr int kWarps = TFB_FUSE_WARPS;  // warps per CTA (independent pipelines)
 #define TFB_ARGMAX_FAST 1  // network argmax / pixel max: strict-greater pass, exact NaN pass only when needed
 #endif
 #ifndef TFB_FUSE_D64
-#define TFB_FUSE_D64 1  // float64-accumulator product rule through k_fuse_fast's D64 mode (else k_fuse<double>)
+#define TFB_FUSE_D64 1  // float64 accumulator (count-derived weights, c <= 128) through k_fuse_fast's D64 mode (else k_fuse<double>)
 #endif
 #ifndef TFB_FIX_TRANSPOSE
 #define TFB_FIX_TRANSPOSE 1  // k_fuse_fast fixed-point epilogue: lanes take classes qi0 + k*QW (coalesced 64-bit adds)
@@ -758,13 +758,14 @@ __device__ __forceinline__ void sts4(float *p, float4 v, int nv) {
 
 template <int AGG, bool VEC, int CC, bool ORD = false, bool FIX = false, bool D64 = false>
 __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant__ FuseParams p) {
-  // D64: the float64 parity accumulator for the product rule (fusion.py:177 in double): no
-  // scan; converged epilogue lanes = (piece, class set) multiply the piece's clipped values
-  // in double straight from the staged rows and land w * log(prod) with float64 adds
-  static_assert(!D64 || (AGG == TFB_AGG_MUL && !FIX && !ORD), "D64: product rule, float64 accumulator");
+  // D64: the float64 parity accumulator (fusion.py:171-177 in double): no scan; converged
+  // epilogue lanes = (piece, class set) fold the piece's values in double straight from the
+  // staged rows -- product of clipped values then w * log (mul), or the sum of w * p (sum;
+  // maxsum keeps p only where it equals the pixel's max) -- and land them with float64 adds
+  static_assert(!D64 || (!FIX && !ORD), "D64: float64 accumulator, frame-major walk");
   constexpr bool kProd = AGG == TFB_AGG_MUL;
-  __shared__ double2 s_logtab[D64 ? (1 << tfb_log::kLogBits) : 1];
-  if (D64) {
+  __shared__ double2 s_logtab[D64 && kProd ? (1 << tfb_log::kLogBits) : 1];
+  if (D64 && kProd) {
     for (int t = threadIdx.x; t < (1 << tfb_log::kLogBits); t += blockDim.x) s_logtab[t] = tfb_log::kTable[t];
     __syncthreads();
   }
@@ -1031,7 +1032,32 @@ __global__ void __launch_bounds__(kWarps * 32) k_fuse_fast(const __grid_constant
         // pixel order (as k_fuse's float64 mode), one table-driven log per piece and class
         // (fusion.py:177), the adds coalesced over a piece's consecutive classes (c <= 128)
         for (int P = g; P - g < npv; P += geo.G) {
-          if (lane_ok && P < npv) {
+          if (lane_ok && P < npv && !kProd) {
+            // sum / maxsum: the reference's per-pixel w * f(p) summed in double (fusion.py:171-175)
+            const int4 h = shead[P];
+            const int p0 = h.z & 0xff;
+            const float *row = wst + (size_t)p0 * cs;
+            const double wv = __hiloint2double(h.w, h.y);
+            double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+            for (int j = 0; j < (h.z >> 8); ++j, row += cs) {
+              float x0 = row[cl[0]], x1 = has(1) ? row[cl[1]] : 0.f, x2 = has(2) ? row[cl[2]] : 0.f,
+                    x3 = has(3) ? row[cl[3]] : 0.f;
+              if (AGG == TFB_AGG_MAXSUM) {  // fusion.py:174: p where p equals the pixel's max
+                const float mxp = smax[p0 + j];
+                x0 = x0 == mxp ? x0 : 0.f; x1 = x1 == mxp ? x1 : 0.f;
+                x2 = x2 == mxp ? x2 : 0.f; x3 = x3 == mxp ? x3 : 0.f;
+              }
+              d0 += wv * (double)x0;
+              d1 += wv * (double)x1;
+              d2 += wv * (double)x2;
+              d3 += wv * (double)x3;
+            }
+            double *dr = reinterpret_cast<double *>(p.accum) + h.x;
+            atomicAdd(dr + cl[0], d0);
+            if (has(1)) atomicAdd(dr + cl[1], d1);
+            if (has(2)) atomicAdd(dr + cl[2], d2);
+            if (has(3)) atomicAdd(dr + cl[3], d3);
+          } else if (lane_ok && P < npv) {
             const int4 h = shead[P];
             const float *row = wst + (size_t)(h.z & 0xff) * cs;
             // np.clip(p, 1e-7, 1) is lazy, as in the float32 scan: the raw values multiply
@@ -1212,12 +1238,10 @@ int launch_fuse(const FuseParams &p, cudaStream_t st) {
 
 template <int AGG, bool VEC, int CC = 0>
 int launch_fuse_fast(const FuseParams &p, cudaStream_t st, bool fix, bool d64 = false) {
-  if constexpr (AGG == TFB_AGG_MUL) {
-    if (d64) {  // float64 accumulator, product rule: no scan, no padded rows
-      static LaunchCache lcd;
-      return launch_persistent(k_fuse_fast<AGG, VEC, CC, false, false, true>, lcd, fast_layout(p.c, p.NS, 0).total,
-                               p, st);
-    }
+  if (d64) {  // float64 accumulator: no scan, no padded rows
+    static LaunchCache lcd;
+    return launch_persistent(k_fuse_fast<AGG, VEC, CC, false, false, true>, lcd, fast_layout(p.c, p.NS, 0).total, p,
+                             st);
   }
   // the padded working rows of k_fuse_fast's compile-time c % 4 != 0 repack
   constexpr int kPadCs = (!VEC && (TFB_FUSE_REPACK || TFB_FUSE_FOLDBUF) && CC != 0 && CC % 4 != 0) ? ((CC + 3) & ~3) : 0;
@@ -1507,8 +1531,8 @@ extern "C" int tfb_fuse_ordered(const int32_t *rows, int64_t hw, int nframes, co
     bool fast = (!wide || fix) && weight_mode != TFB_W_EXPLICIT && g_fuse_fast;
     // float64 accumulator, product rule, count-derived weights, one class pass: k_fuse_fast's
     // D64 mode (the reference's float64 arithmetic per piece, converged epilogue)
-    bool d64 = TFB_FUSE_D64 && accum_kind == TFB_ACCUM_F64 && aggregator == TFB_AGG_MUL &&
-               weight_mode != TFB_W_EXPLICIT && num_classes <= 128 && g_fuse_fast;
+    bool d64 = TFB_FUSE_D64 && accum_kind == TFB_ACCUM_F64 && weight_mode != TFB_W_EXPLICIT &&
+               num_classes <= 128 && g_fuse_fast;
     for (int i = 0; i < nf && (fast || d64); ++i)
       if (((uintptr_t)p.probs[i] & 15) != 0) fast = d64 = false;
     const bool vec = num_classes % 4 == 0;
@@ -1526,7 +1550,11 @@ extern "C" int tfb_fuse_ordered(const int32_t *rows, int64_t hw, int nframes, co
           break;
       }
     } else if (d64) {
-      rc = launch_fuse_fast_c<TFB_AGG_MUL>(p, vec, st, false, true);
+      switch (aggregator) {
+        case TFB_AGG_SUM: rc = launch_fuse_fast_c<TFB_AGG_SUM>(p, vec, st, false, true); break;
+        case TFB_AGG_MAXSUM: rc = launch_fuse_fast_c<TFB_AGG_MAXSUM>(p, vec, st, false, true); break;
+        default: rc = launch_fuse_fast_c<TFB_AGG_MUL>(p, vec, st, false, true); break;
+      }
     } else if (accum_kind == TFB_ACCUM_FIXED) {
       switch (aggregator) {
         case TFB_AGG_SUM: rc = launch_fuse_w<double, TFB_AGG_SUM, true>(p, st); break;

@@ -258,8 +258,28 @@ def test_float64_accumulator_log_within_1e12(c):
     np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("agg", ["sum", "maxsum"])
+@pytest.mark.parametrize("c", [7, 19, 40, 41, 132])
+def test_float64_accumulator_sum_rules(c, agg):
+    """float64 accumulators for sum / maxsum (k_fuse_fast D64 mode for c <= 128, k_fuse above):
+    the reference's per-pixel w * p (maxsum: p where it equals the pixel's max, ties kept)
+    summed in double, at 1e-12 relative, special values and NaN included."""
+    rng = np.random.default_rng(1700 + c)
+    nframes, hw, n_x = 2, 32 * 37 + 11, 150
+    rows = _rows(rng, nframes, hw, n_x)
+    probs = _probs(rng, nframes, hw, c, special=True)
+    flat = probs.reshape(-1)
+    flat[rng.choice(flat.size, size=flat.size // 20, replace=False)] = 0.25  # max ties
+    for wm, alpha in (("images_iid", 0.0), ("blend", 0.3), ("pixels_iid", 0.0)):
+        got, cnt = _run64(rows, probs, n_x, agg, wm, alpha)
+        ref, cref = _oracle(rows, probs, n_x, agg, wm, alpha)
+        np.testing.assert_array_equal(cnt, cref)
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("agg", ["mul", "sum", "maxsum"])
 @pytest.mark.parametrize("c", [13, 40, 41])
-def test_float64_accumulator_long_runs(c):
+def test_float64_accumulator_long_runs(c, agg):
     """The float64 product rule (k_fuse_fast D64 mode: no 5-pixel cut, a piece runs to the next
     row change or pixel-group start) over runs of 20-70 pixels crossing chunk boundaries, values
     near the clip floor and near 1 (products of up to 32 values in double), and a partial last
@@ -273,8 +293,8 @@ def test_float64_accumulator_long_runs(c):
     probs[0, :, 0] = np.float32(1.5e-7)
     probs[1, ::3, 1] = np.float32(0.999999)
     for wm, alpha in (("images_iid", 0.0), ("blend", 0.4)):
-        got, cnt = _run64(rows, probs, n_x, "mul", wm, alpha)
-        ref, cref = _oracle(rows, probs, n_x, "mul", wm, alpha)
+        got, cnt = _run64(rows, probs, n_x, agg, wm, alpha)
+        ref, cref = _oracle(rows, probs, n_x, agg, wm, alpha)
         np.testing.assert_array_equal(cnt, cref)
         np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
 

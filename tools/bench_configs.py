@@ -33,6 +33,8 @@ CONFIGS = {
     "cfg2f64": (158, 640, 480, 577.87, 40, 2000, "mul", 1, 256, 8),
     # cfg2 with the fixed-point accumulator (the session default and deterministic=true)
     "cfg2fix": (158, 640, 480, 577.87, 40, 2000, "mul", 1, 256, 8),
+    # cfg2, sum aggregator (configs[0]'s rule) with the float64 accumulator (the library default)
+    "cfg2sumf64": (158, 640, 480, 577.87, 40, 2000, "sum", 1, 256, 8),
 }
 
 
@@ -89,7 +91,8 @@ def run(name):
         "accum_rmw_bytes_per_frame": int(t_frame * ann.texture.stride * (8 if ann.texture.accum_kind else 4) * 2),
         "accum_bytes": int(layout.total_texels * ann.texture.stride * (8 if ann.texture.accum_kind else 4)),
         "order_items": ann._use_order(),
-        "fuse_kernel": ("k_fuse<double> (general)" if name.endswith(("f64", "fix")) else
+        "fuse_kernel": ("k_fuse_fast D64 (float64)" if name.endswith("f64") else
+                        "k_fuse_fast fixed64" if name.endswith("fix") else
                         "k_fuse_fast<VEC>" if c % 4 == 0 else "k_fuse_fast<scalar quads>"),
     }), flush=True)
     del ann, maps, probs
